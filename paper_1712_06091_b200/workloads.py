@@ -1,0 +1,155 @@
+"""Seeded synthetic workloads with BASELINE.json's shapes.
+
+BASELINE.json names no public dataset; these builders generate the configs'
+media, sources, attenuation layers and analytic travel times.  Decisions that
+are not facts of the reference are marked.
+
+* cfg1 : 129^2 on [0,1]^2, kappa = 1, 10 ppw, source at the centre, 16-cell layer,
+         tau = kappa*r (tau1 = 1), all-Sommerfeld.
+* cfg2 : 1025^2, v = 1.5 + 2.5 x2, 12 ppw at v_min, source (0.5, 0.05),
+         20-cell layer, analytic linear-gradient tau, all-Sommerfeld.
+Both accept ``n=`` for down-scaled parity cases (same physics, ppw kept).
+
+The coefficient fields grad(tau), lap(tau) follow the reference's
+``tau_derivatives`` (helmadr/eikonal.py:180-226) applied to the analytic tau1.
+This is setup (the travel time is an input of the solve, north_star) and is
+not timed.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .fields import AnalyticBase, GridSpec, Medium, SourceSpec, TravelTime
+
+ALL_SOMMERFELD = ("sommerfeld", "sommerfeld", "sommerfeld", "sommerfeld")  # (top, bottom, left, right)
+
+
+@dataclass
+class Workload:
+    name: str
+    grid: GridSpec
+    medium: Medium
+    source: SourceSpec
+    tt: TravelTime
+    bc: tuple  # (top, bottom, left, right)
+
+    @property
+    def omega(self) -> float:
+        return self.source.omega
+
+    @property
+    def n_dof(self) -> int:
+        return self.grid.n_nodes
+
+
+def cell_layer_gamma(grid: GridSpec, omega: float, cells: int, sides) -> np.ndarray:
+    """gamma = omega*(d/W)^2 ramp of helmadr/grid.py:158-171 with the band width W
+    given in cells instead of one wavelength (decision)."""
+    x1, x2 = grid.coords()
+    w1, w2 = cells * grid.h1, cells * grid.h2
+    g = np.zeros(grid.shape)
+    ramps = []
+    if "left" in sides:
+        ramps.append((w1 - x1, w1))
+    if "right" in sides:
+        ramps.append((x1 - (grid.L1 - w1), w1))
+    if "top" in sides:
+        ramps.append((w2 - x2, w2))
+    if "bottom" in sides:
+        ramps.append((x2 - (grid.L2 - w2), w2))
+    for depth, width in ramps:
+        d = np.clip(depth, 0.0, width)
+        g = np.maximum(g, omega * (d / width) ** 2)
+    return g
+
+
+def _d1(t, h, ax):
+    out = np.empty_like(t)
+    a, o = np.moveaxis(t, ax, 0), np.moveaxis(out, ax, 0)
+    o[1:-1] = (a[2:] - a[:-2]) / (2.0 * h)
+    o[0] = (a[1] - a[0]) / h
+    o[-1] = (a[-1] - a[-2]) / h
+    return out
+
+
+def _d2(t, h, ax):
+    out = np.empty_like(t)
+    a, o = np.moveaxis(t, ax, 0), np.moveaxis(out, ax, 0)
+    hh = h * h
+    o[1:-1] = (a[2:] - 2.0 * a[1:-1] + a[:-2]) / hh
+    o[0] = (2.0 * a[0] - 5.0 * a[1] + 4.0 * a[2] - a[3]) / hh
+    o[-1] = (2.0 * a[-1] - 5.0 * a[-2] + 4.0 * a[-3] - a[-4]) / hh
+    return out
+
+
+def travel_time_from_tau1(grid: GridSpec, source: SourceSpec, tau1: np.ndarray) -> TravelTime:
+    """Chain rule on tau = tau0*tau1 (helmadr/eikonal.py:204-226, 236-239): central
+    first differences, 3-/4-point second differences, grad = 0 and lap = 2 tau1
+    at the source node."""
+    base = AnalyticBase(grid, source)
+    a1 = _d1(tau1, grid.h1, 0)
+    a2 = _d1(tau1, grid.h2, 1)
+    lap1 = _d2(tau1, grid.h1, 0) + _d2(tau1, grid.h2, 1)
+    grad1 = base.tau0 * a1 + tau1 * base.grad1
+    grad2 = base.tau0 * a2 + tau1 * base.grad2
+    lap = tau1 * base.lap + 2.0 * (base.grad1 * a1 + base.grad2 * a2) + base.tau0 * lap1
+    i1, i2 = source.i1, source.i2
+    grad1[i1, i2] = 0.0
+    grad2[i1, i2] = 0.0
+    lap[i1, i2] = 2.0 * tau1[i1, i2]
+    return TravelTime(grid, tau1, base.tau0 * tau1, grad1, grad2, lap, base)
+
+
+def linear_gradient_tau1(grid: GridSpec, source: SourceSpec, v0: float, g: float) -> np.ndarray:
+    """tau1 = tau/tau0 for v(x2) = v0 + g*x2, tau = arccosh(1 + g^2 r^2/(2 v v_s))/g,
+    with tau1(x0) := kappa(x0) = 1/v(x0) (the limit)  (SURVEY.md §8(d) cfg 2)."""
+    x1, x2 = grid.coords()
+    p1, p2 = source.position(grid)
+    v = v0 + g * x2
+    vs = v0 + g * p2
+    r = np.hypot(x1 - p1, x2 - p2)
+    tau = np.arccosh(1.0 + (g * r) ** 2 / (2.0 * v * vs)) / g
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t1 = np.where(r > 0, tau / r, 1.0 / vs)
+    t1[source.i1, source.i2] = 1.0 / vs
+    return t1
+
+
+def cfg1(n: int = 129, ppw: float = 10.0, layer: int | None = None) -> Workload:
+    """BASELINE config 1 (n=129): constant kappa, centre source."""
+    grid = GridSpec(n, n, 1.0, 1.0)
+    omega = 2.0 * np.pi / (ppw * grid.h1)
+    layer = layer if layer is not None else max(2, round(16 * (n - 1) / 128))
+    src = SourceSpec((n - 1) // 2, (n - 1) // 2, omega)
+    ksq = np.ones(grid.shape)
+    gam = cell_layer_gamma(grid, omega, layer, ("top", "bottom", "left", "right"))
+    med = Medium(grid, ksq, gam)
+    tt = travel_time_from_tau1(grid, src, np.ones(grid.shape))
+    return Workload(f"cfg1_{n}", grid, med, src, tt, ALL_SOMMERFELD)
+
+
+def cfg2(n: int = 1025, ppw: float = 12.0, layer: int | None = None) -> Workload:
+    """BASELINE config 2 (n=1025): linear-gradient velocity 1.5 + 2.5 x2."""
+    grid = GridSpec(n, n, 1.0, 1.0)
+    vmin, g = 1.5, 2.5
+    omega = 2.0 * np.pi * vmin / (ppw * grid.h1)
+    layer = layer if layer is not None else max(3, round(20 * (n - 1) / 1024))
+    i2 = max(layer + 2, round(0.05 * (n - 1)))
+    src = SourceSpec((n - 1) // 2, i2, omega)
+    x1, x2 = grid.coords()
+    v = vmin + g * x2
+    ksq = 1.0 / v**2
+    gam = cell_layer_gamma(grid, omega, layer, ("top", "bottom", "left", "right"))
+    med = Medium(grid, ksq, gam)
+    tt = travel_time_from_tau1(grid, src, linear_gradient_tau1(grid, src, vmin, g))
+    return Workload(f"cfg2_{n}", grid, med, src, tt, ALL_SOMMERFELD)
+
+
+def by_name(name: str, n: int | None = None) -> Workload:
+    builders = {"cfg1": cfg1, "cfg2": cfg2}
+    if name not in builders:
+        raise ValueError(f"unknown workload {name!r}; known: {sorted(builders)}")
+    return builders[name]() if n is None else builders[name](n)
