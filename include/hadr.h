@@ -1,0 +1,116 @@
+/*
+ * hadr.h — C ABI of the B200-native amplitude solve (libhadr.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `helmadr`
+ * (arXiv 1712.06091; /root/reference/pkg/src/helmadr).  The reference is pure
+ * Python and has no FFI of its own: these entry points are what its duck-typed
+ * solver API binds to through the Python shim in
+ * paper_1712_06091_b200/ (ctypes).  Each function cites
+ * the reference callable it replaces.
+ *
+ * Conventions
+ *   - complex vectors are interleaved (re, im) doubles, numpy complex128 layout,
+ *     flattened row-major over (n1, n2): k = i1*n2 + i2 (helmadr/grid.py:5-9);
+ *   - `on_device` = 0: pointers are host memory (copied in/out inside the call);
+ *     `on_device` = 1: pointers are device memory on the current CUDA device;
+ *   - inputs are never modified (helmadr/krylov.py:93, 138);
+ *   - return 0 on success; HADR_EVALUE maps to Python ValueError,
+ *     HADR_ERUNTIME / HADR_ECUDA to RuntimeError; hadr_last_error() has the text.
+ *   - levels are 1-based, level 1 = finest (helmadr/multigrid.py:132).
+ */
+#ifndef HADR_H
+#define HADR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HADR_OK 0
+#define HADR_EVALUE 1
+#define HADR_ERUNTIME 2
+#define HADR_ECUDA 3
+
+typedef struct hadr_op_s* hadr_op;     /* structured 2D stencil operator (device) */
+typedef struct hadr_hier_s* hadr_hier; /* multigrid hierarchy + K-cycle workspace (device) */
+
+/* Mirrors helmadr/krylov.py:34-53 SolveReport (history returned separately). */
+typedef struct {
+  int iterations;
+  int converged;
+  int note;          /* 0 = "", 1 = "numerical breakdown: non-finite Arnoldi vector" */
+  int history_len;   /* entries written to the caller's history buffer */
+  double bnorm;
+  double final_relres;
+  double wall_time;   /* seconds, host clock around the device solve */
+  double device_time; /* seconds, CUDA events on the library stream around the solve */
+} hadr_report;
+
+const char* hadr_last_error(void);
+int hadr_init(int device);
+int hadr_device_sync(void);
+int hadr_device_malloc(void** ptr, size_t bytes);
+int hadr_device_free(void* ptr);
+/* kind: 1 host->device, 2 device->host, 3 device->device */
+int hadr_memcpy(void* dst, const void* src, size_t bytes, int kind);
+
+/* ---- operators (helmadr/operators.py CSR matrices, as structured stencils) ---- */
+/* From a canonical CSR matrix on the (n1, n2) grid; replaces the scipy CSR consumed by
+ * helmadr/krylov.py:60-65 spmv and helmadr/multigrid.py:113 build_hierarchy. */
+int hadr_op_from_csr(int n1, int n2, int64_t nnz, const int64_t* indptr, const int32_t* indices,
+                     const double* data, hadr_op* out);
+/* From coefficient planes coef[o*N + k] for offsets (d1, d2) strictly ascending. */
+int hadr_op_from_planes(int n1, int n2, int n_offsets, const int* offsets, const double* coef, hadr_op* out);
+int hadr_op_info(hadr_op op, int* n1, int* n2, int* n_offsets, int* offsets /* 2*25 */);
+int hadr_op_export(hadr_op op, double* coef /* n_offsets*N complex */);
+/* y = A x  (helmadr/krylov.py:60-65 spmv; scipy csr_matvec order, bit-exact) */
+int hadr_op_apply(hadr_op op, const double* x, double* y, int on_device);
+/* z = r / diag(A)  (helmadr/krylov.py:68-73 jacobi_apply) */
+int hadr_op_jacobi(hadr_op op, const double* r, double* z, int on_device);
+/* alpha*A + beta*B on the union pattern (helmadr/drivers.py:156 blend) */
+int hadr_op_axpby(double ar, double ai, hadr_op A, double br, double bi, hadr_op B, hadr_op* out);
+/* A + diag(s * field), field real (helmadr/operators.py:237-244 shift_operator) */
+int hadr_op_add_diag(hadr_op A, double sr, double si, const double* field, hadr_op* out);
+/* diag(left) A diag(right) (helmadr/operators.py:252-266 similarity_conjugate) */
+int hadr_op_similarity(hadr_op A, const double* left, const double* right, hadr_op* out);
+/* P^T A P for bilinear P (helmadr/multigrid.py:49-55 galerkin_coarsen) */
+int hadr_op_galerkin(hadr_op A, hadr_op* out);
+void hadr_op_destroy(hadr_op op);
+
+/* ---- transfer operators (helmadr/multigrid.py:19-46) ---- */
+/* rc = P^T r (direction 0) or y = P e (direction 1) for the fine grid (n1, n2). */
+int hadr_transfer(int n1, int n2, int direction, const double* in, double* out, int on_device);
+
+/* ---- multigrid (helmadr/multigrid.py) ---- */
+/* build_hierarchy(A0, grid, max_levels) with Galerkin coarse operators built on the device.
+ * The hierarchy keeps a reference to `fine` (do not destroy it first). */
+int hadr_hier_create(hadr_op fine, int max_levels, int coarse_steps, double coarse_tol, hadr_hier* out);
+/* MGHierarchy(ops=...) from given per-level operators (finest first; borrowed). */
+int hadr_hier_from_ops(int n_levels, const hadr_op* ops, int coarse_steps, double coarse_tol, hadr_hier* out);
+int hadr_hier_info(hadr_hier h, int* n_levels, int* shapes /* 2*n_levels */);
+/* borrowed handle to level `level` (1-based) operator */
+int hadr_hier_level_op(hadr_hier h, int level, hadr_op* out);
+/* k_cycle(hier, level, b, x) (helmadr/multigrid.py:132-171); x may be NULL (zero);
+ * visits (nullable, n_levels ints) mirrors the `stats` dict */
+int hadr_kcycle(hadr_hier h, int level, const double* b, const double* x, double* x_out, int* visits,
+                int on_device);
+/* make_kcycle_preconditioner(hier)(r) (helmadr/multigrid.py:174-184): graph-captured K-cycle */
+int hadr_precond_apply(hadr_hier h, const double* r, double* z, int on_device);
+void hadr_hier_destroy(hadr_hier h);
+/* number of kernels this library has launched so far (graph launches add their kernel nodes) */
+long long hadr_launch_count(void);
+
+/* ---- Krylov (helmadr/krylov.py) ---- */
+/* _gmres_relax_pre / gmres_relax (helmadr/krylov.py:82-119) */
+int hadr_gmres_relax(hadr_op A, const double* b, const double* x, int steps, double* x_out, int on_device);
+/* fgmres(A, b, x0, precond=make_kcycle_preconditioner(M) or None, cfg) (helmadr/krylov.py:122-242).
+ * M may be NULL (identity preconditioner); x0 may be NULL (zero). */
+int hadr_fgmres(hadr_op A, hadr_hier M, const double* b, const double* x0, int restart, int maxiter, double tol,
+                double* x_out, hadr_report* rep, double* history, int history_cap, int on_device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HADR_H */

@@ -1,0 +1,317 @@
+// extern "C" boundary (include/hadr.h).  Plain pointers and sizes only.
+#include <cstring>
+#include <string>
+
+#include "../../include/hadr.h"
+#include "engine.h"
+
+using namespace hadr;
+
+struct hadr_op_s {
+  Op* op;
+  bool own;
+};
+struct hadr_hier_s {
+  Hier* h;
+  std::vector<hadr_op_s> level_handles;
+};
+
+static thread_local std::string g_err;
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return HADR_OK;
+  } catch (const ValueError& e) {
+    g_err = e.what();
+    return HADR_EVALUE;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return HADR_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HADR_ERUNTIME;
+  } catch (...) {
+    g_err = "unknown error";
+    return HADR_ERUNTIME;
+  }
+}
+
+// Device view of a complex vector: borrowed (on_device) or a staged copy.
+struct DevVec {
+  cplx* p = nullptr;
+  bool owned = false;
+  long n = 0;
+  DevVec(const double* src, long n_, int on_device, bool copy_in) : n(n_) {
+    if (on_device || (copy_in && !src)) {
+      p = (cplx*)src;
+    } else {
+      p = dalloc<cplx>(n);
+      owned = true;
+      if (copy_in && src) {
+        Ctx& c = Ctx::get();
+        HADR_CUDA(cudaMemcpyAsync(p, src, n * sizeof(cplx), cudaMemcpyHostToDevice, c.stream));
+      }
+    }
+  }
+  void copy_out(double* dst) {
+    if (!owned) return;
+    Ctx& c = Ctx::get();
+    HADR_CUDA(cudaMemcpyAsync(dst, p, n * sizeof(cplx), cudaMemcpyDeviceToHost, c.stream));
+  }
+  ~DevVec() {
+    if (owned) dfree(p);
+  }
+};
+
+static hadr_op wrap(Op* op, bool own = true) { return new hadr_op_s{op, own}; }
+
+extern "C" {
+
+const char* hadr_last_error(void) { return g_err.c_str(); }
+
+int hadr_init(int device) {
+  return guarded([&] {
+    int n = 0;
+    HADR_CUDA(cudaGetDeviceCount(&n));
+    if (n <= 0) throw std::runtime_error("no CUDA device");
+    HADR_CUDA(cudaSetDevice(device));
+    Ctx::get();
+  });
+}
+
+int hadr_device_sync(void) { return guarded([&] { Ctx::get().sync(); }); }
+
+int hadr_device_malloc(void** ptr, size_t bytes) {
+  return guarded([&] { HADR_CUDA(cudaMalloc(ptr, bytes)); });
+}
+int hadr_device_free(void* ptr) {
+  return guarded([&] { HADR_CUDA(cudaFree(ptr)); });
+}
+int hadr_memcpy(void* dst, const void* src, size_t bytes, int kind) {
+  return guarded([&] {
+    Ctx& c = Ctx::get();
+    cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice : kind == 2 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    HADR_CUDA(cudaMemcpyAsync(dst, src, bytes, k, c.stream));
+    c.sync();
+  });
+}
+
+int hadr_op_from_csr(int n1, int n2, int64_t nnz, const int64_t* indptr, const int32_t* indices, const double* data,
+                     hadr_op* out) {
+  return guarded([&] {
+    if (n1 < 1 || n2 < 1) throw ValueError("grid dimensions must be positive");
+    *out = wrap(op_from_csr(n1, n2, nnz, indptr, indices, (const cplx*)data));
+  });
+}
+
+int hadr_op_from_planes(int n1, int n2, int n_offsets, const int* offsets, const double* coef, hadr_op* out) {
+  return guarded([&] { *out = wrap(op_from_planes(n1, n2, n_offsets, offsets, (const cplx*)coef)); });
+}
+
+int hadr_op_info(hadr_op h, int* n1, int* n2, int* n_offsets, int* offsets) {
+  return guarded([&] {
+    const Op* op = h->op;
+    *n1 = op->n1;
+    *n2 = op->n2;
+    *n_offsets = op->nofs;
+    for (int o = 0; o < op->nofs; ++o) {
+      offsets[2 * o] = op->d1[o];
+      offsets[2 * o + 1] = op->d2[o];
+    }
+  });
+}
+
+int hadr_op_export(hadr_op h, double* coef) {
+  return guarded([&] {
+    Ctx& c = Ctx::get();
+    const Op* op = h->op;
+    HADR_CUDA(cudaMemcpyAsync(coef, op->coef, (size_t)op->nofs * op->N * sizeof(cplx), cudaMemcpyDeviceToHost,
+                              c.stream));
+    c.sync();
+  });
+}
+
+int hadr_op_apply(hadr_op h, const double* x, double* y, int on_device) {
+  return guarded([&] {
+    const Op* op = h->op;
+    DevVec dx(x, op->N, on_device, true), dy(y, op->N, on_device, false);
+    op_apply(*op, dx.p, dy.p);
+    HADR_CUDA(cudaGetLastError());
+    dy.copy_out(y);
+    Ctx::get().sync();
+  });
+}
+
+int hadr_op_jacobi(hadr_op h, const double* r, double* z, int on_device) {
+  return guarded([&] {
+    Op* op = h->op;
+    const int ce = op->center();
+    if (ce < 0) throw ValueError("jacobi_apply: operator has zero diagonal entries");
+    op->inv_diag();  // raises on a zero diagonal (helmadr/krylov.py:71-72)
+    DevVec dr(r, op->N, on_device, true), dz(z, op->N, on_device, false);
+    launch_cdiv(Ctx::get().stream, op->N, dr.p, op->coef + (long)ce * op->N, dz.p);
+    HADR_CUDA(cudaGetLastError());
+    dz.copy_out(z);
+    Ctx::get().sync();
+  });
+}
+
+int hadr_op_axpby(double ar, double ai, hadr_op A, double br, double bi, hadr_op B, hadr_op* out) {
+  return guarded([&] { *out = wrap(op_axpby(mk(ar, ai), *A->op, mk(br, bi), *B->op)); });
+}
+
+int hadr_op_add_diag(hadr_op A, double sr, double si, const double* field, hadr_op* out) {
+  return guarded([&] { *out = wrap(op_add_diag_real(*A->op, mk(sr, si), field)); });
+}
+
+int hadr_op_similarity(hadr_op A, const double* left, const double* right, hadr_op* out) {
+  return guarded([&] { *out = wrap(op_similarity(*A->op, (const cplx*)left, (const cplx*)right)); });
+}
+
+int hadr_op_galerkin(hadr_op A, hadr_op* out) {
+  return guarded([&] { *out = wrap(op_galerkin(*A->op)); });
+}
+
+void hadr_op_destroy(hadr_op h) {
+  if (!h) return;
+  if (h->own) delete h->op;
+  delete h;
+}
+
+int hadr_transfer(int n1, int n2, int direction, const double* in, double* out, int on_device) {
+  return guarded([&] {
+    if ((n1 - 1) % 2 || (n2 - 1) % 2) throw ValueError("cannot coarsen: interval count is odd");
+    Ctx& c = Ctx::get();
+    const long Nf = (long)n1 * n2, Nc = (long)((n1 - 1) / 2 + 1) * ((n2 - 1) / 2 + 1);
+    if (direction == 0) {
+      DevVec di(in, Nf, on_device, true), dout(out, Nc, on_device, false);
+      launch_restrict(c.lc, n1, n2, di.p, dout.p, gate_always());
+      HADR_CUDA(cudaGetLastError());
+      dout.copy_out(out);
+    } else {
+      DevVec di(in, Nc, on_device, true), dout(out, Nf, on_device, false);
+      HADR_CUDA(cudaMemsetAsync(dout.p, 0, Nf * sizeof(cplx), c.stream));
+      launch_prolong_add(c.lc, n1, n2, di.p, dout.p, gate_always());
+      HADR_CUDA(cudaGetLastError());
+      dout.copy_out(out);
+    }
+    c.sync();
+  });
+}
+
+static hadr_hier wrap_hier(Hier* h) {
+  hadr_hier_s* s = new hadr_hier_s();
+  s->h = h;
+  for (auto& L : h->lv) s->level_handles.push_back(hadr_op_s{L.A, false});
+  return s;
+}
+
+int hadr_hier_create(hadr_op fine, int max_levels, int coarse_steps, double coarse_tol, hadr_hier* out) {
+  return guarded([&] { *out = wrap_hier(hier_build(fine->op, max_levels, coarse_steps, coarse_tol)); });
+}
+
+int hadr_hier_from_ops(int n_levels, const hadr_op* ops, int coarse_steps, double coarse_tol, hadr_hier* out) {
+  return guarded([&] {
+    std::vector<Op*> v;
+    for (int i = 0; i < n_levels; ++i) v.push_back(ops[i]->op);
+    *out = wrap_hier(hier_from_ops(n_levels, v.data(), coarse_steps, coarse_tol));
+  });
+}
+
+int hadr_hier_info(hadr_hier h, int* n_levels, int* shapes) {
+  return guarded([&] {
+    *n_levels = (int)h->h->lv.size();
+    if (shapes)
+      for (size_t i = 0; i < h->h->lv.size(); ++i) {
+        shapes[2 * i] = h->h->lv[i].n1;
+        shapes[2 * i + 1] = h->h->lv[i].n2;
+      }
+  });
+}
+
+int hadr_hier_level_op(hadr_hier h, int level, hadr_op* out) {
+  return guarded([&] {
+    if (level < 1 || level > (int)h->level_handles.size()) throw ValueError("level out of range");
+    *out = &h->level_handles[level - 1];
+  });
+}
+
+int hadr_kcycle(hadr_hier hh, int level, const double* b, const double* x, double* x_out, int* visits,
+                int on_device) {
+  return guarded([&] {
+    Hier* h = hh->h;
+    const int nl = (int)h->lv.size();
+    if (level < 1 || level > nl) throw ValueError("level outside 1.." + std::to_string(nl));
+    if (level == nl) throw ValueError("k_cycle at the coarsest level has no coarse grid");
+    const long n = h->lv[level - 1].N;
+    DevVec db(b, n, on_device, true), dxo(x_out, n, on_device, false);
+    DevVec dx(x, n, on_device, true);
+    h->kcycle_direct(level - 1, db.p, x ? dx.p : nullptr, dxo.p, visits);
+    dxo.copy_out(x_out);
+    Ctx::get().sync();
+  });
+}
+
+int hadr_precond_apply(hadr_hier hh, const double* r, double* z, int on_device) {
+  return guarded([&] {
+    Hier* h = hh->h;
+    const long n = h->lv[0].N;
+    DevVec dr(r, n, on_device, true), dz(z, n, on_device, false);
+    h->apply(dr.p, dz.p);
+    HADR_CUDA(cudaGetLastError());
+    dz.copy_out(z);
+    Ctx::get().sync();
+    if (!on_device) {  // staged buffers die with this call: drop their graph
+      auto it = h->graphs.find(std::make_pair((const void*)dr.p, (void*)dz.p));
+      if (it != h->graphs.end()) {
+        cudaGraphExecDestroy(it->second);
+        h->graphs.erase(it);
+      }
+    }
+  });
+}
+
+long long hadr_launch_count(void) { return g_launch_count; }
+
+void hadr_hier_destroy(hadr_hier h) {
+  if (!h) return;
+  delete h->h;
+  delete h;
+}
+
+int hadr_gmres_relax(hadr_op A, const double* b, const double* x, int steps, double* x_out, int on_device) {
+  return guarded([&] {
+    Op* op = A->op;
+    DevVec db(b, op->N, on_device, true), dx(x, op->N, on_device, true), dxo(x_out, op->N, on_device, false);
+    gmres_relax(*op, db.p, dx.p, dxo.p, steps);
+    dxo.copy_out(x_out);
+    Ctx::get().sync();
+  });
+}
+
+int hadr_fgmres(hadr_op A, hadr_hier M, const double* b, const double* x0, int restart, int maxiter, double tol,
+                double* x_out, hadr_report* rep, double* history, int history_cap, int on_device) {
+  return guarded([&] {
+    Op* op = A->op;
+    DevVec db(b, op->N, on_device, true), dx0(x0, op->N, on_device, true), dx(x_out, op->N, on_device, false);
+    Report r;
+    fgmres(*op, M ? M->h : nullptr, db.p, x0 ? dx0.p : nullptr, dx.p, restart, maxiter, tol, r);
+    dx.copy_out(x_out);
+    Ctx::get().sync();
+    rep->iterations = r.iterations;
+    rep->converged = r.converged;
+    rep->note = r.note;
+    rep->bnorm = r.bnorm;
+    rep->final_relres = r.final_relres;
+    rep->wall_time = r.wall_time;
+    rep->device_time = r.device_time;
+    const int nh = (int)r.history.size();
+    rep->history_len = nh;
+    if (history)
+      for (int i = 0; i < nh && i < history_cap; ++i) history[i] = r.history[i];
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,874 @@
+// Host engine of the amplitude solve.  Mirrors helmadr/multigrid.py and
+// helmadr/krylov.py control flow; the device does every vector operation and
+// every data-dependent branch of the preconditioner, the host only drives the
+// outer FGMRES (one small read-back per outer iteration).
+#include "engine.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+namespace hadr {
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+Ctx& Ctx::get() {
+  static Ctx* c = nullptr;
+  if (!c) {
+    Ctx* n = new Ctx();
+    HADR_CUDA(cudaGetDevice(&n->device));
+    HADR_CUDA(cudaDeviceGetAttribute(&n->nsm, cudaDevAttrMultiProcessorCount, n->device));
+    HADR_CUDA(cudaStreamCreateWithFlags(&n->stream, cudaStreamNonBlocking));
+    n->rs.partials = dalloc<double>(4 * 8192);
+    n->rs.ticket = dalloc<unsigned>(4);
+    HADR_CUDA(cudaMemset(n->rs.ticket, 0, 4 * sizeof(unsigned)));
+    n->dscal = dalloc<double>(64);
+    HADR_CUDA(cudaMallocHost(&n->hscal, 64 * sizeof(double)));
+    n->lc.stream = n->stream;
+    n->lc.max_blocks = n->nsm * 8;  // 8 resident 256-thread CTAs per SM
+    c = n;
+  }
+  return *c;
+}
+
+// ---------------------------------------------------------------------------
+// operators
+// ---------------------------------------------------------------------------
+Op::~Op() {
+  dfree(coef);
+  dfree(dinv);
+}
+
+StencilDev Op::dev() const {
+  StencilDev s{};
+  s.n1 = n1;
+  s.n2 = n2;
+  s.nofs = nofs;
+  for (int o = 0; o < nofs; ++o) {
+    s.d1[o] = d1[o];
+    s.d2[o] = d2[o];
+  }
+  s.coef = coef;
+  return s;
+}
+
+int Op::center() const {
+  for (int o = 0; o < nofs; ++o)
+    if (d1[o] == 0 && d2[o] == 0) return o;
+  return -1;
+}
+
+const cplx* Op::inv_diag() {
+  if (dinv) return dinv;
+  Ctx& c = Ctx::get();
+  const int ce = center();
+  dinv = dalloc<cplx>(N);
+  int* flag = dalloc<int>(1);
+  HADR_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), c.stream));
+  launch_inv_diag(c.stream, N, ce >= 0 ? coef + (long)ce * N : nullptr, dinv, flag);
+  int hflag = 0;
+  HADR_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  dfree(flag);
+  if (hflag || ce < 0) {
+    dfree(dinv);
+    dinv = nullptr;
+    throw ValueError("hierarchy operator has zero diagonal entries");
+  }
+  return dinv;
+}
+
+static void set_offsets_from_mask(Op* op, unsigned mask, int* slot_of /*25*/) {
+  op->nofs = 0;
+  for (int q = 0; q < 25; ++q) slot_of[q] = -1;
+  for (int q = 0; q < 25; ++q) {  // q = (d1+2)*5 + (d2+2): ascending (d1, d2) == ascending column
+    if (mask & (1u << q)) {
+      slot_of[q] = op->nofs;
+      op->d1[op->nofs] = (int8_t)(q / 5 - 2);
+      op->d2[op->nofs] = (int8_t)(q % 5 - 2);
+      op->nofs++;
+    }
+  }
+}
+
+Op* op_from_csr(int n1, int n2, long nnz, const int64_t* indptr, const int32_t* indices, const cplx* data) {
+  Ctx& c = Ctx::get();
+  const long N = (long)n1 * n2;
+  int64_t* dptr = dalloc<int64_t>(N + 1);
+  int32_t* dind = dalloc<int32_t>(nnz);
+  cplx* ddat = dalloc<cplx>(nnz);
+  unsigned* dmask = dalloc<unsigned>(2);
+  int* dslot = dalloc<int>(25);
+  Op* op = new Op();
+  op->n1 = n1;
+  op->n2 = n2;
+  op->N = N;
+  try {
+    HADR_CUDA(cudaMemcpyAsync(dptr, indptr, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
+    HADR_CUDA(cudaMemcpyAsync(dind, indices, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, c.stream));
+    HADR_CUDA(cudaMemcpyAsync(ddat, data, nnz * sizeof(cplx), cudaMemcpyHostToDevice, c.stream));
+    HADR_CUDA(cudaMemsetAsync(dmask, 0, 2 * sizeof(unsigned), c.stream));
+    launch_csr_mask(c.stream, n1, n2, dptr, dind, dmask);
+    unsigned hm[2];
+    HADR_CUDA(cudaMemcpyAsync(hm, dmask, sizeof(hm), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (hm[1]) throw ValueError("operator reaches beyond the 5x5 stencil box; not a structured 2D stencil");
+    int slot[25];
+    set_offsets_from_mask(op, hm[0], slot);
+    if (op->nofs == 0) {  // all-zero matrix: keep a centre plane of zeros
+      op->nofs = 1;
+      op->d1[0] = op->d2[0] = 0;
+      slot[12] = 0;
+    }
+    HADR_CUDA(cudaMemcpyAsync(dslot, slot, sizeof(slot), cudaMemcpyHostToDevice, c.stream));
+    op->coef = dalloc<cplx>((size_t)op->nofs * N);
+    HADR_CUDA(cudaMemsetAsync(op->coef, 0, (size_t)op->nofs * N * sizeof(cplx), c.stream));
+    launch_csr_scatter(c.stream, n1, n2, dptr, dind, ddat, dslot, op->coef);
+    HADR_CUDA(cudaGetLastError());
+    c.sync();
+  } catch (...) {
+    dfree(dptr), dfree(dind), dfree(ddat), dfree(dmask), dfree(dslot);
+    delete op;
+    throw;
+  }
+  dfree(dptr), dfree(dind), dfree(ddat), dfree(dmask), dfree(dslot);
+  return op;
+}
+
+Op* op_from_planes(int n1, int n2, int nofs, const int* offsets, const cplx* coef_host) {
+  if (nofs < 1 || nofs > HADR_MAX_OFS) throw ValueError("n_offsets out of range");
+  Ctx& c = Ctx::get();
+  Op* op = new Op();
+  op->n1 = n1;
+  op->n2 = n2;
+  op->N = (long)n1 * n2;
+  op->nofs = nofs;
+  for (int o = 0; o < nofs; ++o) {
+    if (std::abs(offsets[2 * o]) > 2 || std::abs(offsets[2 * o + 1]) > 2) {
+      delete op;
+      throw ValueError("offsets must lie in the 5x5 box");
+    }
+    op->d1[o] = (int8_t)offsets[2 * o];
+    op->d2[o] = (int8_t)offsets[2 * o + 1];
+  }
+  for (int o = 1; o < nofs; ++o) {
+    if (op->d1[o] * 5 + op->d2[o] <= op->d1[o - 1] * 5 + op->d2[o - 1]) {
+      delete op;
+      throw ValueError("offsets must be strictly ascending in (d1, d2)");
+    }
+  }
+  op->coef = dalloc<cplx>((size_t)nofs * op->N);
+  HADR_CUDA(cudaMemcpyAsync(op->coef, coef_host, (size_t)nofs * op->N * sizeof(cplx), cudaMemcpyHostToDevice,
+                            c.stream));
+  c.sync();
+  return op;
+}
+
+Op* op_axpby(cplx alpha, const Op& A, cplx beta, const Op& B) {
+  if (A.n1 != B.n1 || A.n2 != B.n2) throw ValueError("dimension mismatch");
+  Ctx& c = Ctx::get();
+  unsigned mask = 0;
+  for (int o = 0; o < A.nofs; ++o) mask |= 1u << ((A.d1[o] + 2) * 5 + A.d2[o] + 2);
+  for (int o = 0; o < B.nofs; ++o) mask |= 1u << ((B.d1[o] + 2) * 5 + B.d2[o] + 2);
+  Op* op = new Op();
+  op->n1 = A.n1;
+  op->n2 = A.n2;
+  op->N = A.N;
+  int slot[25];
+  set_offsets_from_mask(op, mask, slot);
+  int ma[HADR_MAX_OFS], mb[HADR_MAX_OFS];
+  for (int o = 0; o < A.nofs; ++o) ma[o] = slot[(A.d1[o] + 2) * 5 + A.d2[o] + 2];
+  for (int o = 0; o < B.nofs; ++o) mb[o] = slot[(B.d1[o] + 2) * 5 + B.d2[o] + 2];
+  int* dm = dalloc<int>(2 * HADR_MAX_OFS);
+  HADR_CUDA(cudaMemcpyAsync(dm, ma, sizeof(ma), cudaMemcpyHostToDevice, c.stream));
+  HADR_CUDA(cudaMemcpyAsync(dm + HADR_MAX_OFS, mb, sizeof(mb), cudaMemcpyHostToDevice, c.stream));
+  op->coef = dalloc<cplx>((size_t)op->nofs * op->N);
+  HADR_CUDA(cudaMemsetAsync(op->coef, 0, (size_t)op->nofs * op->N * sizeof(cplx), c.stream));
+  // (alpha*A).data then (beta*B).data, then CSR + CSR: a + b on the union (helmadr/drivers.py:156)
+  launch_remap_planes(c.stream, A.N, A.coef, A.nofs, dm, op->coef, alpha, 1);
+  launch_remap_planes(c.stream, B.N, B.coef, B.nofs, dm + HADR_MAX_OFS, op->coef, beta, 1);
+  HADR_CUDA(cudaGetLastError());
+  c.sync();
+  dfree(dm);
+  return op;
+}
+
+static Op* op_clone_with_center(const Op& A) {
+  Ctx& c = Ctx::get();
+  unsigned mask = 1u << 12;
+  for (int o = 0; o < A.nofs; ++o) mask |= 1u << ((A.d1[o] + 2) * 5 + A.d2[o] + 2);
+  Op* op = new Op();
+  op->n1 = A.n1;
+  op->n2 = A.n2;
+  op->N = A.N;
+  int slot[25];
+  set_offsets_from_mask(op, mask, slot);
+  int ma[HADR_MAX_OFS];
+  for (int o = 0; o < A.nofs; ++o) ma[o] = slot[(A.d1[o] + 2) * 5 + A.d2[o] + 2];
+  int* dm = dalloc<int>(HADR_MAX_OFS);
+  HADR_CUDA(cudaMemcpyAsync(dm, ma, sizeof(ma), cudaMemcpyHostToDevice, c.stream));
+  op->coef = dalloc<cplx>((size_t)op->nofs * op->N);
+  HADR_CUDA(cudaMemsetAsync(op->coef, 0, (size_t)op->nofs * op->N * sizeof(cplx), c.stream));
+  launch_remap_planes(c.stream, A.N, A.coef, A.nofs, dm, op->coef, mk(1.0, 0.0), 0);
+  c.sync();
+  dfree(dm);
+  return op;
+}
+
+Op* op_add_diag_real(const Op& A, cplx sc, const double* field_host) {
+  Ctx& c = Ctx::get();
+  Op* op = op_clone_with_center(A);
+  double* df = dalloc<double>(A.N);
+  HADR_CUDA(cudaMemcpyAsync(df, field_host, A.N * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  launch_add_diag_real(c.stream, A.N, op->coef + (long)op->center() * op->N, sc, df);
+  HADR_CUDA(cudaGetLastError());
+  c.sync();
+  dfree(df);
+  return op;
+}
+
+Op* op_similarity(const Op& A, const cplx* left_host, const cplx* right_host) {
+  Ctx& c = Ctx::get();
+  Op* op = new Op();
+  *op = A;  // copies geometry (and pointers, reset below)
+  op->coef = nullptr;
+  op->dinv = nullptr;
+  cplx* dl = dalloc<cplx>(A.N);
+  cplx* dr = dalloc<cplx>(A.N);
+  HADR_CUDA(cudaMemcpyAsync(dl, left_host, A.N * sizeof(cplx), cudaMemcpyHostToDevice, c.stream));
+  HADR_CUDA(cudaMemcpyAsync(dr, right_host, A.N * sizeof(cplx), cudaMemcpyHostToDevice, c.stream));
+  op->coef = dalloc<cplx>((size_t)A.nofs * A.N);
+  launch_similarity(c.stream, A.dev(), op->coef, dl, dr);
+  HADR_CUDA(cudaGetLastError());
+  c.sync();
+  dfree(dl);
+  dfree(dr);
+  return op;
+}
+
+Op* op_galerkin(const Op& A) {
+  if ((A.n1 - 1) % 2 || (A.n2 - 1) % 2) throw ValueError("cannot coarsen: interval count is odd");
+  Ctx& c = Ctx::get();
+  const int n1c = (A.n1 - 1) / 2 + 1, n2c = (A.n2 - 1) / 2 + 1;
+  unsigned* dmask = dalloc<unsigned>(1);
+  int* dslot = dalloc<int>(25);
+  HADR_CUDA(cudaMemsetAsync(dmask, 0, sizeof(unsigned), c.stream));
+  launch_galerkin(c.stream, A.dev(), n1c, n2c, dmask, nullptr, nullptr);
+  unsigned hm = 0;
+  HADR_CUDA(cudaMemcpyAsync(&hm, dmask, sizeof(unsigned), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  Op* op = new Op();
+  op->n1 = n1c;
+  op->n2 = n2c;
+  op->N = (long)n1c * n2c;
+  int slot[25];
+  set_offsets_from_mask(op, hm | (1u << 12), slot);
+  HADR_CUDA(cudaMemcpyAsync(dslot, slot, sizeof(slot), cudaMemcpyHostToDevice, c.stream));
+  op->coef = dalloc<cplx>((size_t)op->nofs * op->N);
+  launch_galerkin(c.stream, A.dev(), n1c, n2c, nullptr, dslot, op->coef);
+  HADR_CUDA(cudaGetLastError());
+  c.sync();
+  dfree(dmask);
+  dfree(dslot);
+  return op;
+}
+
+void op_apply(const Op& A, const cplx* x, cplx* y) {
+  Ctx& c = Ctx::get();
+  StencilArgs a{};
+  a.A = A.dev();
+  a.x = x;
+  a.y = y;
+  a.gate = gate_always();
+  a.rs = c.rs;
+  a.epi = epi_none();
+  launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_NONE, a);
+}
+
+// ---------------------------------------------------------------------------
+// hierarchy
+// ---------------------------------------------------------------------------
+std::vector<std::pair<int, int>> coarsenable_levels(int n1, int n2, int max_levels) {
+  // helmadr/multigrid.py:98-110
+  std::vector<std::pair<int, int>> s{{n1, n2}};
+  while ((int)s.size() < max_levels) {
+    int m1 = s.back().first, m2 = s.back().second;
+    if ((m1 - 1) % 2 || (m2 - 1) % 2) break;
+    int c1 = (m1 - 1) / 2 + 1, c2 = (m2 - 1) / 2 + 1;
+    if (c1 < 3 || c2 < 3) break;
+    s.push_back({c1, c2});
+  }
+  return s;
+}
+
+Hier::~Hier() {
+  for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& L : lv) {
+    if (L.own) delete L.A;
+    dfree(L.r);
+    for (auto* v : L.V) dfree(v);
+    dfree(L.w[0]);
+    dfree(L.w[1]);
+    dfree(L.rctl);
+    dfree(L.fb), dfree(L.fx), dfree(L.fV0), dfree(L.fu), dfree(L.fZ0), dfree(L.fZ1), dfree(L.fw), dfree(L.fr);
+    dfree(L.fctl);
+  }
+  dfree(kact);
+  dfree(visits);
+}
+
+void Hier::alloc_workspace() {
+  const int nl = (int)lv.size();
+  for (int i = 0; i < nl; ++i) {
+    Level& L = lv[i];
+    L.n1 = L.A->n1;
+    L.n2 = L.A->n2;
+    L.N = L.A->N;
+    L.dinv = L.A->inv_diag();
+    L.s = (i == nl - 1) ? coarse_steps : (i + 2);  // relax_steps(l) = l + 1 (helmadr/multigrid.py:87-88)
+    if (L.s > RMAX) throw ValueError("relaxation length exceeds the device limit (16)");
+    L.s = (int)std::min<long>(L.s, L.N);
+    for (int j = 0; j <= L.s; ++j) L.V[j] = dalloc<cplx>(L.N);
+    L.w[0] = dalloc<cplx>(L.N);
+    L.w[1] = dalloc<cplx>(L.N);
+    L.r = dalloc<cplx>(L.N);
+    L.rctl = dalloc<RelaxCtl>(1);
+    HADR_CUDA(cudaMemset(L.rctl, 0, sizeof(RelaxCtl)));
+    if (i >= 1) {
+      L.fb = dalloc<cplx>(L.N);
+      L.fx = dalloc<cplx>(L.N);
+      L.fV0 = dalloc<cplx>(L.N);
+      L.fu = dalloc<cplx>(L.N);
+      L.fZ0 = dalloc<cplx>(L.N);
+      L.fZ1 = dalloc<cplx>(L.N);
+      L.fw = dalloc<cplx>(L.N);
+      L.fr = dalloc<cplx>(L.N);
+      L.fctl = dalloc<FgCtl>(1);
+      HADR_CUDA(cudaMemset(L.fctl, 0, sizeof(FgCtl)));
+    }
+  }
+  kact = dalloc<int>(nl + 1);
+  visits = dalloc<int>(nl + 1);
+  HADR_CUDA(cudaMemset(kact, 0, (nl + 1) * sizeof(int)));
+  HADR_CUDA(cudaMemset(visits, 0, (nl + 1) * sizeof(int)));
+}
+
+Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol) {
+  auto shapes = coarsenable_levels(fine->n1, fine->n2, max_levels);
+  if (shapes.size() < 2)
+    throw ValueError("grid cannot support two multigrid levels ((n_d - 1) must be even with at least 3 coarse nodes)");
+  Hier* h = new Hier();
+  h->coarse_steps = coarse_steps;
+  h->coarse_tol = coarse_tol;
+  try {
+    Level L0;
+    L0.A = fine;
+    h->lv.push_back(L0);
+    for (size_t i = 1; i < shapes.size(); ++i) {
+      Level L;
+      L.A = op_galerkin(*h->lv.back().A);
+      L.own = true;
+      h->lv.push_back(L);
+    }
+    h->alloc_workspace();
+  } catch (...) {
+    delete h;
+    throw;
+  }
+  return h;
+}
+
+Hier* hier_from_ops(int nlev, Op** ops, int coarse_steps, double coarse_tol) {
+  if (nlev < 2) throw ValueError("need at least two levels");
+  Hier* h = new Hier();
+  h->coarse_steps = coarse_steps;
+  h->coarse_tol = coarse_tol;
+  try {
+    for (int i = 0; i < nlev; ++i) {
+      Level L;
+      L.A = ops[i];
+      if (i > 0 && (ops[i]->n1 != (ops[i - 1]->n1 - 1) / 2 + 1 || ops[i]->n2 != (ops[i - 1]->n2 - 1) / 2 + 1))
+        throw ValueError("level shapes must halve: (n-1)/2+1");
+      h->lv.push_back(L);
+    }
+    h->alloc_workspace();
+  } catch (...) {
+    delete h;
+    throw;
+  }
+  return h;
+}
+
+__global__ void k_count(int* visits, int idx, Gate g) {
+  if (gate_open(g)) visits[idx] += 1;
+}
+
+void Hier::emit_relax(Level& L, const cplx* b, const cplx* x, cplx* xo, int s, Gate g) {
+  // helmadr/krylov.py:91-119 ; r = b - A x (skipped for x == 0: r = b exactly)
+  Ctx& c = Ctx::get();
+  const StencilDev A = L.A->dev();
+  launch_relax_init(c.stream, L.rctl, s, g);
+  const cplx* r = b;
+  if (x) {
+    StencilArgs a{};
+    a.A = A;
+    a.x = x;
+    a.b = b;
+    a.y = L.w[1];
+    a.gate = g;
+    a.rs = c.rs;
+    a.epi = epi(EPI_RELAX_BETA, L.rctl);
+    launch_stencil(c.lc, IN_PLAIN, OUT_RESID, RED_NORM, a);
+    r = L.w[1];
+  } else {
+    launch_scale(c.lc, L.N, b, nullptr, nullptr, RED_NORM, g, c.rs, epi(EPI_RELAX_BETA, L.rctl));
+  }
+  RelaxCtl* rc = L.rctl;
+  for (int j = 0; j < s; ++j) {
+    Gate gj = gate_var(g.active, &rc->cur, 1u << j);
+    cplx* w = L.w[j % 2];
+    StencilArgs a{};
+    a.A = A;
+    a.x = (j == 0) ? r : L.w[(j - 1) % 2];
+    a.scale = (j == 0) ? &rc->inv_beta : &rc->inv_hn;
+    a.dinv = L.dinv;
+    a.vout = L.V[j];
+    a.y = w;
+    a.u = L.V[0];
+    a.gate = gj;
+    a.rs = c.rs;
+    a.epi = epi(EPI_RELAX_H, rc, 0, j);
+    launch_stencil(c.lc, IN_SCALE | IN_JAC | IN_WRITEV, OUT_APPLY, j == 0 ? RED_DOT_CENTER : RED_DOT, a);
+    for (int i = 0; i < j; ++i)
+      launch_axpy_red(c.lc, L.N, w, &rc->H[i * RMAX + j], L.V[i], RED_DOT, L.V[i + 1], gj, c.rs,
+                      epi(EPI_RELAX_H, rc, i + 1, j));
+    launch_axpy_red(c.lc, L.N, w, &rc->H[j * RMAX + j], L.V[j], RED_NORM, nullptr, gj, c.rs,
+                    epi(EPI_RELAX_STEP, rc, 0, j));
+  }
+  LinComb lc{};
+  for (int j = 0; j < s; ++j) lc.v[j] = L.V[j];
+  lc.y = rc->y;
+  lc.kptr = &rc->k;
+  lc.base = x;
+  lc.dinv = L.dinv;
+  lc.out = xo;
+  launch_lincomb(c.lc, L.N, lc, g);
+}
+
+void Hier::emit_kcycle(int li, const cplx* b, const cplx* x0, cplx* xo, Gate g, bool count) {
+  // helmadr/multigrid.py:132-171
+  Ctx& c = Ctx::get();
+  const int nl = (int)lv.size();
+  if (li < 0 || li >= nl - 1) throw ValueError("level outside 1..n_levels-1");
+  Level& L = lv[li];
+  Level& C = lv[li + 1];
+  if (count) k_count<<<1, 1, 0, c.stream>>>(visits, li, g);
+  emit_relax(L, b, x0, xo, L.s, g);
+  StencilArgs a{};
+  a.A = L.A->dev();
+  a.x = xo;
+  a.b = b;
+  a.y = L.r;
+  a.gate = g;
+  a.rs = c.rs;
+  a.epi = epi_none();
+  launch_stencil(c.lc, IN_PLAIN, OUT_RESID, RED_NONE, a);
+  launch_restrict(c.lc, L.n1, L.n2, L.r, C.fb, g);
+  if (li + 1 == nl - 1) {
+    if (count) k_count<<<1, 1, 0, c.stream>>>(visits, li + 1, g);
+    emit_relax(C, C.fb, nullptr, C.fx, C.s, g);
+  } else {
+    emit_inner(li + 1, g, count);
+  }
+  launch_prolong_add(c.lc, L.n1, L.n2, C.fx, xo, g);
+  emit_relax(L, b, xo, xo, L.s, g);
+}
+
+void Hier::emit_inner(int ci, Gate g, bool count) {
+  // FGMRES(restart=2, maxiter=2, tol=coarse_tol) on level ci, preconditioned by
+  // k_cycle(ci) (helmadr/multigrid.py:159-167, helmadr/krylov.py:122-242)
+  Ctx& c = Ctx::get();
+  Level& C = lv[ci];
+  FgCtl* f = C.fctl;
+  const StencilDev A = C.A->dev();
+  const long n = C.N;
+  int* act = kact + ci;
+  const unsigned bA = 1u << FG_A, bC = 1u << FG_CONT, bB = 1u << FG_BRK, bR = 1u << FG_RST;
+  launch_fg_setup(c.stream, f, coarse_tol, g);
+  launch_scale(c.lc, n, C.fb, nullptr, nullptr, RED_NORM, g, c.rs, epi(EPI_FG_INIT, f));
+  const Gate gA = gate_var(g.active, &f->path, bA);
+  launch_scale(c.lc, n, C.fb, &f->inv_r, C.fV0, 0, gA, c.rs, epi_none());
+  // ---- iteration 1 ----
+  launch_set_gate(c.stream, act, gA);
+  emit_kcycle(ci, C.fV0, nullptr, C.fZ0, gate_on(act), count);
+  {
+    StencilArgs a{};
+    a.A = A;
+    a.x = C.fZ0;
+    a.y = C.fw;
+    a.u = C.fV0;
+    a.gate = gA;
+    a.rs = c.rs;
+    a.epi = epi(EPI_FG_S, f, 0, 0);
+    launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT, a);
+    launch_axpy_red(c.lc, n, C.fw, &f->H[0], C.fV0, RED_NORM, nullptr, gA, c.rs, epi(EPI_FG_N, f, 0, 0, 1));
+    const Gate gAr = gate_var2(g.active, &f->path, bA, &f->reo, 2u);
+    launch_dot(c.lc, n, C.fV0, C.fw, gAr, c.rs, epi(EPI_FG_CORR, f, 0, 0));
+    launch_axpy_red(c.lc, n, C.fw, &f->corr[0], C.fV0, RED_NORM, nullptr, gAr, c.rs, epi(EPI_FG_N2, f, 0, 0, 1));
+  }
+  // ---- early exit after iteration 1: x = Z0 y0, r = b - A x, restart decision ----
+  {
+    const Gate gB = gate_var(g.active, &f->path, bB);
+    launch_fg_finalize(c.lc, n, f, C.fZ0, C.fZ1, C.fx, gB, 1);
+    StencilArgs a{};
+    a.A = A;
+    a.x = C.fx;
+    a.b = C.fb;
+    a.y = C.fr;
+    a.gate = gB;
+    a.rs = c.rs;
+    a.epi = epi(EPI_FG_RES, f);
+    launch_stencil(c.lc, IN_PLAIN, OUT_RESID, RED_NORM, a);
+  }
+  // ---- iteration 2: u = V1 (continue) or u = r/||r|| (restart cycle) ----
+  launch_scale(c.lc, n, C.fw, &f->inv_w, C.fu, 0, gate_var(g.active, &f->path, bC), c.rs, epi_none());
+  launch_scale(c.lc, n, C.fr, &f->inv_r, C.fu, 0, gate_var(g.active, &f->path, bR), c.rs, epi_none());
+  const Gate gCR = gate_var(g.active, &f->path, bC | bR);
+  launch_set_gate(c.stream, act, gCR);
+  emit_kcycle(ci, C.fu, nullptr, C.fZ1, gate_on(act), count);
+  {  // continue: j = 1 against basis (V0, u)
+    const Gate gC = gate_var(g.active, &f->path, bC);
+    StencilArgs a{};
+    a.A = A;
+    a.x = C.fZ1;
+    a.y = C.fw;
+    a.u = C.fV0;
+    a.gate = gC;
+    a.rs = c.rs;
+    a.epi = epi(EPI_FG_S, f, 0, 1);
+    launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT, a);
+    launch_axpy_red(c.lc, n, C.fw, &f->H[0 * MMAX + 1], C.fV0, RED_DOT, C.fu, gC, c.rs, epi(EPI_FG_H, f, 1, 1));
+    launch_axpy_red(c.lc, n, C.fw, &f->H[1 * MMAX + 1], C.fu, RED_NORM, nullptr, gC, c.rs,
+                    epi(EPI_FG_N, f, 0, 1, 1));
+    const Gate gCr = gate_var2(g.active, &f->path, bC, &f->reo, 2u);
+    launch_dot(c.lc, n, C.fV0, C.fw, gCr, c.rs, epi(EPI_FG_CORR, f, 0, 1));
+    launch_axpy_red(c.lc, n, C.fw, &f->corr[0], C.fV0, RED_DOT, C.fu, gCr, c.rs, epi(EPI_FG_CORR, f, 1, 1));
+    launch_axpy_red(c.lc, n, C.fw, &f->corr[1], C.fu, RED_NORM, nullptr, gCr, c.rs, epi(EPI_FG_N2, f, 0, 1, 1));
+  }
+  {  // restart cycle: j = 0 against basis (u)
+    const Gate gR = gate_var(g.active, &f->path, bR);
+    StencilArgs a{};
+    a.A = A;
+    a.x = C.fZ1;
+    a.y = C.fw;
+    a.u = C.fu;
+    a.gate = gR;
+    a.rs = c.rs;
+    a.epi = epi(EPI_FG_S, f, 0, 0);
+    launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT, a);
+    launch_axpy_red(c.lc, n, C.fw, &f->H[0], C.fu, RED_NORM, nullptr, gR, c.rs, epi(EPI_FG_N, f, 0, 0, 1));
+    const Gate gRr = gate_var2(g.active, &f->path, bR, &f->reo, 2u);
+    launch_dot(c.lc, n, C.fu, C.fw, gRr, c.rs, epi(EPI_FG_CORR, f, 0, 0));
+    launch_axpy_red(c.lc, n, C.fw, &f->corr[0], C.fu, RED_NORM, nullptr, gRr, c.rs, epi(EPI_FG_N2, f, 0, 0, 1));
+  }
+  launch_fg_finalize(c.lc, n, f, C.fZ0, C.fZ1, C.fx, gate_var(g.active, &f->path, (1u << FG_FIN) | (1u << FG_ZERO)),
+                     0);
+}
+
+void Hier::apply(const cplx* v, cplx* z) {
+  Ctx& c = Ctx::get();
+  auto key = std::make_pair((const void*)v, (void*)z);
+  auto it = graphs.find(key);
+  if (it == graphs.end()) {
+    cudaGraph_t graph;
+    const long long before = g_launch_count;
+    HADR_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      launch_set_gate(c.stream, kact, gate_always());
+      emit_kcycle(0, v, nullptr, z, gate_on(kact), false);
+    } catch (...) {
+      cudaStreamEndCapture(c.stream, &graph);
+      g_launch_count = before;
+      throw;
+    }
+    HADR_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    graph_kernels[key] = g_launch_count - before;  // captured, not launched
+    g_launch_count = before;
+    cudaGraphExec_t exec;
+    HADR_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    HADR_CUDA(cudaGraphDestroy(graph));
+    it = graphs.emplace(key, exec).first;
+  }
+  HADR_CUDA(cudaGraphLaunch(it->second, c.stream));
+  g_launch_count += graph_kernels[key];
+}
+
+void Hier::kcycle_direct(int li, const cplx* b, const cplx* x0, cplx* xo, int* visits_host) {
+  Ctx& c = Ctx::get();
+  const int nl = (int)lv.size();
+  HADR_CUDA(cudaMemsetAsync(visits, 0, (nl + 1) * sizeof(int), c.stream));
+  launch_set_gate(c.stream, kact + li, gate_always());
+  emit_kcycle(li, b, x0, xo, gate_on(kact + li), visits_host != nullptr);
+  HADR_CUDA(cudaGetLastError());
+  if (visits_host) HADR_CUDA(cudaMemcpyAsync(visits_host, visits, nl * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+}
+
+// ---------------------------------------------------------------------------
+// public gmres_relax (helmadr/krylov.py:82-88)
+// ---------------------------------------------------------------------------
+void gmres_relax(Op& A, const cplx* b, const cplx* x, cplx* xo, int steps) {
+  Ctx& c = Ctx::get();
+  if (steps > RMAX) throw ValueError("gmres_relax: steps exceeds the device limit (16)");
+  Hier h;  // scratch holder for one level's relaxation workspace
+  Level L;
+  L.A = &A;
+  L.n1 = A.n1;
+  L.n2 = A.n2;
+  L.N = A.N;
+  L.dinv = A.inv_diag();
+  L.s = (int)std::min<long>(std::max(steps, 0), A.N);
+  for (int j = 0; j <= L.s; ++j) L.V[j] = dalloc<cplx>(L.N);
+  L.w[0] = dalloc<cplx>(L.N);
+  L.w[1] = dalloc<cplx>(L.N);
+  L.rctl = dalloc<RelaxCtl>(1);
+  HADR_CUDA(cudaMemsetAsync(L.rctl, 0, sizeof(RelaxCtl), c.stream));
+  h.lv.push_back(L);
+  h.emit_relax(h.lv[0], b, x, xo, L.s, gate_always());
+  HADR_CUDA(cudaGetLastError());
+  c.sync();
+  h.lv[0].A = nullptr;  // borrowed
+}
+
+// ---------------------------------------------------------------------------
+// outer FGMRES (helmadr/krylov.py:122-242); Givens / history / stopping on the
+// host exactly as the reference, vector work on the device
+// ---------------------------------------------------------------------------
+static inline cplx hmul(cplx a, cplx b) { return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+static inline cplx hadd(cplx a, cplx b) { return mk(a.x + b.x, a.y + b.y); }
+static inline cplx hsub(cplx a, cplx b) { return mk(a.x - b.x, a.y - b.y); }
+static inline cplx hconj(cplx a) { return mk(a.x, -a.y); }
+static inline cplx hneg(cplx a) { return mk(-a.x, -a.y); }
+static inline double habs(cplx a) { return std::hypot(a.x, a.y); }
+
+struct OuterWS {
+  long N = 0;
+  int m = 0;
+  std::vector<cplx*> V, Z;
+  cplx *w = nullptr, *r = nullptr;
+  FgCtl* f = nullptr;
+  FgCtl* hf = nullptr;  // pinned
+  double* inv = nullptr;  // device scalar(s)
+  ~OuterWS() {
+    for (auto p : V) dfree(p);
+    for (auto p : Z) dfree(p);
+    dfree(w), dfree(r), dfree(f), dfree(inv);
+    if (hf) cudaFreeHost(hf);
+  }
+};
+
+static OuterWS* outer_ws(long N, int m) {
+  static OuterWS* ws = nullptr;
+  if (ws && ws->N == N && ws->m >= m) return ws;
+  delete ws;
+  ws = new OuterWS();
+  ws->N = N;
+  ws->m = m;
+  for (int j = 0; j <= m; ++j) ws->V.push_back(dalloc<cplx>(N));
+  for (int j = 0; j < m; ++j) ws->Z.push_back(dalloc<cplx>(N));
+  ws->w = dalloc<cplx>(N);
+  ws->r = dalloc<cplx>(N);
+  ws->f = dalloc<FgCtl>(1);
+  HADR_CUDA(cudaMemset(ws->f, 0, sizeof(FgCtl)));
+  HADR_CUDA(cudaMallocHost(&ws->hf, sizeof(FgCtl)));
+  ws->inv = dalloc<double>(4);
+  return ws;
+}
+
+void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart, int maxiter, double tol,
+            Report& rep) {
+  if (restart < 1) throw ValueError("restart must be >= 1");
+  if (tol <= 0) throw ValueError("tol must be positive");
+  if (restart > MMAX) throw ValueError("restart exceeds the device limit (16)");
+  if (M && (M->lv[0].N != A.N)) throw ValueError("preconditioner dimension mismatch");
+  Ctx& c = Ctx::get();
+  auto t0 = std::chrono::steady_clock::now();
+  const long N = A.N;
+  OuterWS* ws = outer_ws(N, restart);
+  const StencilDev Ad = A.dev();
+  auto norm2 = [&](const cplx* v) -> double {
+    launch_scale(c.lc, N, v, nullptr, nullptr, RED_NORM, gate_always(), c.rs, epi_store(c.dscal));
+    HADR_CUDA(cudaMemcpyAsync(c.hscal, c.dscal, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    return std::sqrt(c.hscal[0]);
+  };
+  auto resid_norm = [&](const cplx* xx, cplx* rr) -> double {  // rr = b - A xx, ||rr||
+    StencilArgs a{};
+    a.A = Ad;
+    a.x = xx;
+    a.b = b;
+    a.y = rr;
+    a.gate = gate_always();
+    a.rs = c.rs;
+    a.epi = epi_store(c.dscal);
+    launch_stencil(c.lc, IN_PLAIN, OUT_RESID, RED_NORM, a);
+    HADR_CUDA(cudaMemcpyAsync(c.hscal, c.dscal, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    return std::sqrt(c.hscal[0]);
+  };
+  rep = Report();
+  cudaEvent_t ev0, ev1;
+  HADR_CUDA(cudaEventCreate(&ev0));
+  HADR_CUDA(cudaEventCreate(&ev1));
+  HADR_CUDA(cudaEventRecord(ev0, c.stream));
+  auto finish_timing = [&]() {
+    HADR_CUDA(cudaEventRecord(ev1, c.stream));
+    HADR_CUDA(cudaEventSynchronize(ev1));
+    float ms = 0.f;
+    HADR_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    rep.device_time = ms * 1e-3;
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    rep.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+  const double bnorm = norm2(b);
+  rep.bnorm = bnorm;
+  if (bnorm == 0.0) {
+    HADR_CUDA(cudaMemsetAsync(x, 0, N * sizeof(cplx), c.stream));
+    c.sync();
+    rep.history = {0.0};
+    rep.converged = 1;
+    finish_timing();
+    return;
+  }
+  double rnorm;
+  if (x0) {
+    if (x0 != x) HADR_CUDA(cudaMemcpyAsync(x, x0, N * sizeof(cplx), cudaMemcpyDeviceToDevice, c.stream));
+    rnorm = resid_norm(x, ws->r);
+  } else {
+    HADR_CUDA(cudaMemsetAsync(x, 0, N * sizeof(cplx), c.stream));
+    HADR_CUDA(cudaMemcpyAsync(ws->r, b, N * sizeof(cplx), cudaMemcpyDeviceToDevice, c.stream));
+    rnorm = bnorm;  // r = b - A*0 = b
+  }
+  rep.history.push_back(rnorm);
+  const double target = tol * bnorm;
+  int it = 0;
+  int note = 0;
+  std::vector<cplx> H, cs, sn, g;
+  FgCtl* f = ws->f;
+  FgCtl* hf = ws->hf;
+  while (it < maxiter && rnorm > target) {
+    const int m = std::min(restart, maxiter - it);
+    H.assign((m + 1) * m, mk(0, 0));
+    cs.assign(m, mk(0, 0));
+    sn.assign(m, mk(0, 0));
+    g.assign(m + 1, mk(0, 0));
+    g[0] = mk(rnorm, 0);
+    auto Hm = [&](int i, int j) -> cplx& { return H[i * m + j]; };
+    // V[0] = r / rnorm
+    c.hscal[1] = 1.0 / rnorm;  // r / rnorm == r * (1/rnorm) in numpy (Smith division by a real)
+    HADR_CUDA(cudaMemcpyAsync(ws->inv, &c.hscal[1], sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    launch_scale(c.lc, N, ws->r, ws->inv, ws->V[0], 0, gate_always(), c.rs, epi_none());
+    int k = 0;
+    bool broke = false;
+    for (int j = 0; j < m; ++j) {
+      const cplx* z = ws->V[j];
+      if (M) {
+        M->apply(ws->V[j], ws->Z[j]);
+        z = ws->Z[j];
+      }
+      // w = A z ; w0 = ||w|| ; H[0,j] = <V0, w>
+      StencilArgs a{};
+      a.A = Ad;
+      a.x = z;
+      a.y = ws->w;
+      a.u = ws->V[0];
+      a.gate = gate_always();
+      a.rs = c.rs;
+      a.epi = epi(EPI_FG_S, f, 0, j);
+      launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT, a);
+      for (int i = 0; i < j; ++i)
+        launch_axpy_red(c.lc, N, ws->w, &f->H[i * MMAX + j], ws->V[i], RED_DOT, ws->V[i + 1], gate_always(), c.rs,
+                        epi(EPI_FG_H, f, i + 1, j));
+      launch_axpy_red(c.lc, N, ws->w, &f->H[j * MMAX + j], ws->V[j], RED_NORM, nullptr, gate_always(), c.rs,
+                      epi(EPI_FG_N, f, 0, j, 0));
+      const Gate gr = gate_var(nullptr, &f->reo, 2u);
+      launch_dot(c.lc, N, ws->V[0], ws->w, gr, c.rs, epi(EPI_FG_CORR, f, 0, j));
+      for (int i = 0; i < j; ++i)
+        launch_axpy_red(c.lc, N, ws->w, &f->corr[i], ws->V[i], RED_DOT, ws->V[i + 1], gr, c.rs,
+                        epi(EPI_FG_CORR, f, i + 1, j));
+      launch_axpy_red(c.lc, N, ws->w, &f->corr[j], ws->V[j], RED_NORM, nullptr, gr, c.rs, epi(EPI_FG_N2, f, 0, j, 0));
+      HADR_CUDA(cudaGetLastError());
+      HADR_CUDA(cudaMemcpyAsync(hf, f, sizeof(FgCtl), cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      for (int i = 0; i <= j; ++i) Hm(i, j) = hf->H[i * MMAX + j];
+      const double wnorm = hf->wn;
+      Hm(j + 1, j) = mk(wnorm, 0);
+      if (!std::isfinite(wnorm)) {
+        note = 1;
+        broke = true;
+        k = j;
+        break;
+      }
+      const bool lucky = wnorm <= kBreakdownEps * std::max(bnorm, 1e-300);
+      if (!lucky) {
+        c.hscal[2] = 1.0 / wnorm;
+        HADR_CUDA(cudaMemcpyAsync(ws->inv + 1, &c.hscal[2], sizeof(double), cudaMemcpyHostToDevice, c.stream));
+        launch_scale(c.lc, N, ws->w, ws->inv + 1, ws->V[j + 1], 0, gate_always(), c.rs, epi_none());
+      }
+      for (int i = 0; i < j; ++i) {
+        cplx t = hadd(hmul(cs[i], Hm(i, j)), hmul(sn[i], Hm(i + 1, j)));
+        Hm(i + 1, j) = hadd(hmul(hneg(hconj(sn[i])), Hm(i, j)), hmul(hconj(cs[i]), Hm(i + 1, j)));
+        Hm(i, j) = t;
+      }
+      const double aa = habs(Hm(j, j)), bb = habs(Hm(j + 1, j));
+      const double den = std::sqrt(aa * aa + bb * bb);
+      if (den == 0.0) {
+        cs[j] = mk(1, 0);
+        sn[j] = mk(0, 0);
+      } else {
+        cs[j] = cdiv_np(hconj(Hm(j, j)), mk(den, 0));
+        sn[j] = cdiv_np(hconj(Hm(j + 1, j)), mk(den, 0));
+      }
+      Hm(j, j) = hadd(hmul(cs[j], Hm(j, j)), hmul(sn[j], Hm(j + 1, j)));
+      Hm(j + 1, j) = mk(0, 0);
+      g[j + 1] = hmul(hneg(hconj(sn[j])), g[j]);
+      g[j] = hmul(cs[j], g[j]);
+      it += 1;
+      k = j + 1;
+      rep.history.push_back(habs(g[j + 1]));
+      if (lucky || rep.history.back() <= target) break;
+    }
+    if (k > 0) {
+      std::vector<cplx> y(g.begin(), g.begin() + k);
+      if (k == 1) {
+        y[0] = cdiv_np(g[0], Hm(0, 0));
+      } else {
+        for (int jj = k - 1; jj >= 0; --jj) {
+          y[jj] = cdiv_np(y[jj], Hm(jj, jj));
+          for (int i = 0; i < jj; ++i) y[i] = hsub(y[i], hmul(y[jj], Hm(i, jj)));
+        }
+      }
+      LinComb lcb{};
+      for (int i = 0; i < k; ++i) {
+        lcb.v[i] = M ? ws->Z[i] : ws->V[i];
+        lcb.yv[i] = y[i];
+      }
+      lcb.kfix = k;
+      lcb.base = x;
+      lcb.out = x;
+      launch_lincomb(c.lc, N, lcb, gate_always());
+    }
+    rnorm = resid_norm(x, ws->r);
+    if (broke) break;
+  }
+  rep.iterations = it;
+  rep.note = note;
+  rep.final_relres = rnorm / bnorm;
+  rep.converged = (rnorm <= target * (1.0 + 1e-12)) && !note;
+  finish_timing();
+}
+
+}  // namespace hadr

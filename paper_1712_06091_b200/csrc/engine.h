@@ -1,0 +1,127 @@
+// Host-side engine: device operators, multigrid hierarchy, K-cycle emission
+// (captured once as a CUDA graph per input/output pair) and the outer FGMRES.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace hadr {
+
+struct CudaError : std::runtime_error {
+  CudaError(cudaError_t e, const char* what, const char* file, int line)
+      : std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " at " + file + ":" +
+                           std::to_string(line) + " (" + what + ")") {}
+};
+struct ValueError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Process-wide device context: one stream, one reduction scratch.
+struct Ctx {
+  int device = 0;
+  int nsm = 148;
+  cudaStream_t stream = nullptr;
+  RedScratch rs{};
+  double* dscal = nullptr;   // device scalars for host readback
+  double* hscal = nullptr;   // pinned mirror
+  LaunchCfg lc{};
+  static Ctx& get();
+  void sync() { HADR_CUDA(cudaStreamSynchronize(stream)); }
+};
+
+template <class T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  HADR_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  return (T*)p;
+}
+inline void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+// Structured 2D operator (owns its coefficient planes).
+struct Op {
+  int n1 = 0, n2 = 0;
+  long N = 0;
+  int nofs = 0;
+  int8_t d1[HADR_MAX_OFS] = {0}, d2[HADR_MAX_OFS] = {0};
+  cplx* coef = nullptr;
+  cplx* dinv = nullptr;  // lazily computed inverse diagonal
+  ~Op();
+  StencilDev dev() const;
+  int center() const;
+  const cplx* inv_diag();  // computes on first use; throws ValueError on a zero diagonal
+};
+
+Op* op_from_csr(int n1, int n2, long nnz, const int64_t* indptr, const int32_t* indices, const cplx* data);
+Op* op_from_planes(int n1, int n2, int nofs, const int* offsets, const cplx* coef_host);
+Op* op_axpby(cplx alpha, const Op& A, cplx beta, const Op& B);       // alpha*A + beta*B on the union pattern
+Op* op_add_diag_real(const Op& A, cplx sc, const double* field_host);  // A + diag(sc*field)
+Op* op_similarity(const Op& A, const cplx* left_host, const cplx* right_host);
+Op* op_galerkin(const Op& A);                                          // P^T A P
+void op_apply(const Op& A, const cplx* x, cplx* y);                    // device pointers, async
+
+struct Level {
+  Op* A = nullptr;
+  bool own = false;
+  int n1 = 0, n2 = 0;
+  long N = 0;
+  const cplx* dinv = nullptr;
+  int s = 0;                 // relaxation length at this level
+  // K-cycle workspace
+  cplx* r = nullptr;
+  cplx* V[RMAX + 1] = {nullptr};
+  cplx* w[2] = {nullptr, nullptr};
+  RelaxCtl* rctl = nullptr;
+  // inner-FGMRES workspace (levels >= 2)
+  cplx *fb = nullptr, *fx = nullptr, *fV0 = nullptr, *fu = nullptr, *fZ0 = nullptr, *fZ1 = nullptr,
+       *fw = nullptr, *fr = nullptr;
+  FgCtl* fctl = nullptr;
+};
+
+struct Hier {
+  std::vector<Level> lv;
+  int coarse_steps = 10;
+  double coarse_tol = 0.1;
+  int* kact = nullptr;      // device: K-cycle-active flag per level
+  int* visits = nullptr;    // device: visit counters (stats mode)
+  std::map<std::pair<const void*, void*>, cudaGraphExec_t> graphs;
+  std::map<std::pair<const void*, void*>, long long> graph_kernels;  // kernel nodes per graph
+  ~Hier();
+  void alloc_workspace();
+  // emit the kernels of k_cycle(level li, b, x0 -> xo) onto the context stream
+  void emit_kcycle(int li, const cplx* b, const cplx* x0, cplx* xo, Gate g, bool count);
+  void emit_relax(Level& L, const cplx* b, const cplx* x, cplx* xo, int s, Gate g);
+  void emit_inner(int ci, Gate g, bool count);
+  // precond application z = K(v) from level 1 with x = 0, via a cached CUDA graph
+  void apply(const cplx* v, cplx* z);
+  void kcycle_direct(int li, const cplx* b, const cplx* x0, cplx* xo, int* visits_host);
+};
+
+Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol);
+Hier* hier_from_ops(int nlev, Op** ops, int coarse_steps, double coarse_tol);
+std::vector<std::pair<int, int>> coarsenable_levels(int n1, int n2, int max_levels);
+
+struct Report {
+  int iterations = 0;
+  int converged = 0;
+  int note = 0;
+  double bnorm = 0, final_relres = 0, wall_time = 0;
+  double device_time = 0;  // CUDA events on the library stream around the solve
+  std::vector<double> history;
+};
+
+// x = fgmres(A, b, x0, M) on device pointers (x0 may be null)
+void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart, int maxiter, double tol,
+            Report& rep);
+// Jacobi-GMRES relaxation of arbitrary length on one operator (public gmres_relax)
+void gmres_relax(Op& A, const cplx* b, const cplx* x, cplx* xo, int steps);
+
+}  // namespace hadr

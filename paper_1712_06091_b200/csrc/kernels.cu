@@ -1,0 +1,760 @@
+// sm_100a kernels of the amplitude solve (FGMRES + multigrid K-cycle).
+//
+// Memory-bound complex128 stencil / BLAS-1 work: no tensor cores (nothing is a
+// dense contraction).  Every streaming kernel is a grid-stride loop over a grid
+// capped at a multiple of the SM count; reductions finish in the last block
+// (deterministic order) which also runs the scalar control epilogue, so no
+// separate "small" kernel and no host round trip is needed per Krylov step.
+#include "kernels.cuh"
+
+#include <stdexcept>
+
+namespace hadr {
+
+long long g_launch_count = 0;  // kernels launched directly on the stream (graphs add their node count)
+
+// ---------------------------------------------------------------------------
+// scalar helpers for the control epilogues (numpy *scalar* arithmetic is plain,
+// non-contracted C: use the no-FMA product)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ cplx cneg(cplx a) { return mk(-a.x, -a.y); }
+__device__ __forceinline__ double cabs_d(cplx a) { return hypot(a.x, a.y); }
+
+template <int LD>
+__device__ void givens_step(cplx* H, cplx* cs, cplx* sn, cplx* g, int j) {
+  // helmadr/krylov.py:195-208
+  for (int i = 0; i < j; ++i) {
+    cplx hij = H[i * LD + j], hi1 = H[(i + 1) * LD + j];
+    cplx t = cadd(cmul_sp(cs[i], hij), cmul_sp(sn[i], hi1));
+    H[(i + 1) * LD + j] = cadd(cmul_sp(cneg(cconj(sn[i])), hij), cmul_sp(cconj(cs[i]), hi1));
+    H[i * LD + j] = t;
+  }
+  cplx a = H[j * LD + j], b = H[(j + 1) * LD + j];
+  double aa = cabs_d(a), bb = cabs_d(b);
+  double den = sqrt(aa * aa + bb * bb);
+  if (den == 0.0) {
+    cs[j] = mk(1.0, 0.0);
+    sn[j] = mk(0.0, 0.0);
+  } else {
+    cs[j] = cdiv_np(cconj(a), mk(den, 0.0));
+    sn[j] = cdiv_np(cconj(b), mk(den, 0.0));
+  }
+  H[j * LD + j] = cadd(cmul_sp(cs[j], a), cmul_sp(sn[j], b));
+  H[(j + 1) * LD + j] = mk(0.0, 0.0);
+  cplx gj = g[j];
+  g[j + 1] = cmul_sp(cneg(cconj(sn[j])), gj);
+  g[j] = cmul_sp(cs[j], gj);
+}
+
+// Upper-triangular solve R[:k,:k] y = g[:k], column-oriented like LAPACK ?trsm.
+template <int LD>
+__device__ void backsolve(const cplx* R, const cplx* g, cplx* y, int k) {
+  for (int i = 0; i < k; ++i) y[i] = g[i];
+  for (int j = k - 1; j >= 0; --j) {
+    y[j] = cdiv_np(y[j], R[j * LD + j]);
+    for (int i = 0; i < j; ++i) y[i] = csub(y[i], cmul_sp(y[j], R[i * LD + j]));
+  }
+}
+
+// ---- Jacobi-GMRES relaxation control (helmadr/krylov.py:91-119) ----
+__device__ void relax_beta(RelaxCtl* c, double ss) {
+  double beta = sqrt(ss);
+  c->beta = beta;
+  c->k = 0;
+  for (int i = 0; i <= RMAX; ++i) c->g[i] = mk(0.0, 0.0);
+  if (beta == 0.0 || c->steps < 1) {  // helmadr/krylov.py:96-97
+    c->cur = kStopped;
+    return;
+  }
+  c->inv_beta = 1.0 / beta;
+  c->g[0] = mk(beta, 0.0);
+  c->cur = 0;
+}
+
+__device__ void relax_step(RelaxCtl* c, int j, double ss) {
+  double hn = sqrt(ss);
+  c->H[(j + 1) * RMAX + j] = mk(hn, 0.0);
+  c->k = j + 1;
+  for (int i = 0; i <= j + 1; ++i) c->R[i * RMAX + j] = c->H[i * RMAX + j];
+  givens_step<RMAX>(c->R, c->cs, c->sn, c->g, j);
+  bool stop = (hn <= kBreakdownEps * c->beta) || (j + 1 >= c->steps);  // helmadr/krylov.py:113-114
+  if (!stop) {
+    c->inv_hn = 1.0 / hn;
+    c->cur = j + 1;
+    return;
+  }
+  c->cur = kStopped;
+  backsolve<RMAX>(c->R, c->g, c->y, c->k);
+}
+
+// ---- inner FGMRES(2) control (helmadr/krylov.py:142-231, helmadr/multigrid.py:159-167) ----
+__device__ void fg_init(FgCtl* f, double ss) {
+  double bn = sqrt(ss);
+  f->bnorm = bn;
+  f->it = 0;
+  f->k = 0;
+  f->cycle = 0;
+  f->broke = 0;
+  f->note = 0;
+  f->reo = 0;
+  f->nhist = 0;
+  for (int i = 0; i < (MMAX + 1) * MMAX; ++i) f->H[i] = mk(0.0, 0.0);
+  for (int i = 0; i <= MMAX; ++i) f->g[i] = mk(0.0, 0.0);
+  if (bn == 0.0) {  // helmadr/krylov.py:143-145
+    f->path = FG_ZERO;
+    return;
+  }
+  f->rnorm = bn;  // r = b - A*0 = b
+  f->target = f->tol * bn;
+  f->g[0] = mk(bn, 0.0);
+  f->inv_r = 1.0 / bn;
+  f->path = FG_A;
+}
+
+__device__ void fg_solve_y(FgCtl* f) {
+  int k = f->k;
+  if (k == 1) {
+    f->y[0] = cdiv_np(f->g[0], f->H[0]);  // g[:1] / H[0, 0]
+  } else if (k > 1) {
+    backsolve<MMAX>(f->H, f->g, f->y, k);  // np.linalg.solve on the rotated (triangular) H
+  }
+}
+
+__device__ void fg_post(FgCtl* f, int j) {
+  f->reo = 0;
+  double wn = f->wn;
+  f->H[(j + 1) * MMAX + j] = mk(wn, 0.0);
+  if (!isfinite(wn)) {  // helmadr/krylov.py:186-190
+    f->note = 1;
+    f->broke = 1;
+    f->k = j;
+  } else {
+    bool lucky = wn <= kBreakdownEps * fmax(f->bnorm, 1e-300);
+    if (!lucky) f->inv_w = 1.0 / wn;
+    givens_step<MMAX>(f->H, f->cs, f->sn, f->g, j);
+    f->it += 1;
+    f->k = j + 1;
+    double h = cabs_d(f->g[j + 1]);
+    if (f->nhist < 8) f->hist[f->nhist++] = h;
+    bool stop = lucky || h <= f->target;
+    if (f->cycle == 0 && j == 0 && !stop) {  // m = 2: second iteration of the first cycle
+      f->path = FG_CONT;
+      return;
+    }
+  }
+  fg_solve_y(f);
+  f->path = (f->cycle == 0 && j == 0) ? FG_BRK : FG_FIN;
+}
+
+__device__ void fg_res(FgCtl* f, double ss) {
+  double rn = sqrt(ss);
+  f->rnorm = rn;
+  if (f->broke) {
+    f->path = FG_DONE;
+    return;
+  }
+  if (f->it < 2 && rn > f->target) {  // while it < maxiter and rnorm > target: restart with m = 1
+    f->path = FG_RST;
+    f->cycle = 1;
+    f->k = 0;
+    for (int i = 0; i < (MMAX + 1) * MMAX; ++i) f->H[i] = mk(0.0, 0.0);
+    for (int i = 0; i <= MMAX; ++i) f->g[i] = mk(0.0, 0.0);
+    f->g[0] = mk(rn, 0.0);
+    f->inv_r = 1.0 / rn;
+  } else {
+    f->path = FG_DONE;
+  }
+}
+
+__device__ __noinline__ void run_epi(const Epi& e, const double* t, int nv) {
+  switch (e.code) {
+    case EPI_STORE:
+      for (int q = 0; q < nv; ++q) e.out[q] = t[q];
+      break;
+    case EPI_RELAX_BETA:
+      relax_beta((RelaxCtl*)e.ctl, t[0]);
+      break;
+    case EPI_RELAX_H:
+      ((RelaxCtl*)e.ctl)->H[e.i * RMAX + e.j] = mk(t[0], t[1]);
+      break;
+    case EPI_RELAX_STEP:
+      relax_step((RelaxCtl*)e.ctl, e.j, t[0]);
+      break;
+    case EPI_FG_INIT:
+      fg_init((FgCtl*)e.ctl, t[0]);
+      break;
+    case EPI_FG_S: {
+      FgCtl* f = (FgCtl*)e.ctl;
+      f->w0 = sqrt(t[0]);
+      f->H[0 * MMAX + e.j] = mk(t[1], t[2]);
+      break;
+    }
+    case EPI_FG_H:
+      ((FgCtl*)e.ctl)->H[e.i * MMAX + e.j] = mk(t[0], t[1]);
+      break;
+    case EPI_FG_CORR: {
+      FgCtl* f = (FgCtl*)e.ctl;
+      f->corr[e.i] = mk(t[0], t[1]);
+      f->H[e.i * MMAX + e.j] = cadd(f->H[e.i * MMAX + e.j], f->corr[e.i]);
+      break;
+    }
+    case EPI_FG_N: {
+      FgCtl* f = (FgCtl*)e.ctl;
+      f->wn = sqrt(t[0]);
+      f->reo = (f->wn < kReorthRatio * f->w0) ? 1 : 0;  // helmadr/krylov.py:178-179
+      if (!f->reo && e.inner) fg_post(f, e.j);
+      break;
+    }
+    case EPI_FG_N2: {
+      FgCtl* f = (FgCtl*)e.ctl;
+      f->wn = sqrt(t[0]);
+      if (e.inner) fg_post(f, e.j);
+      break;
+    }
+    case EPI_FG_RES:
+      fg_res((FgCtl*)e.ctl, t[0]);
+      break;
+    default:
+      break;
+  }
+}
+
+template <int NV>
+__device__ __forceinline__ void finish(double (&v)[NV], const RedScratch& rs, const Epi& e) {
+  double tot[NV];
+  if (grid_sum<NV>(v, rs, tot)) {
+    if (threadIdx.x == 0) run_epi(e, tot, NV);
+  }
+}
+
+__device__ __forceinline__ cplx ldc(const cplx* p, long i) { return __ldg(p + i); }
+
+// ---------------------------------------------------------------------------
+// K1: stencil apply   y = A x   |   y = b - A x
+//   input transform per neighbour: v = x*s (IN_SCALE), v = dinv (.) v (IN_JAC)
+//   IN_WRITEV stores the centre's scaled input (the new Krylov basis vector).
+//   reductions: ||y||^2, <u, y> (u = array, or the centre input with RED_DOT_CENTER)
+// ---------------------------------------------------------------------------
+template <int INM, int OUTM, int RED, int NO>
+__global__ void __launch_bounds__(kThreads) k_stencil(StencilArgs a) {
+  if (!gate_open(a.gate)) return;
+  const int n1 = a.A.n1, n2 = a.A.n2, nofs = a.A.nofs;
+  const long N = (long)n1 * n2;
+  const double s = (INM & IN_SCALE) ? *a.scale : 1.0;
+  constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & (RED_DOT | RED_DOT_CENTER)) ? 2 : 0);
+  double red[NV > 0 ? NV : 1];
+#pragma unroll
+  for (int q = 0; q < (NV > 0 ? NV : 1); ++q) red[q] = 0.0;
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += stride) {
+    const int i1 = (int)(k / n2);
+    const int i2 = (int)(k - (long)i1 * n2);
+    cplx acc = mk(0.0, 0.0);
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      if (o < nofs) {
+        const int j1 = i1 + a.A.d1[o], j2 = i2 + a.A.d2[o];
+        if (j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2) {
+          const long jj = (long)j1 * n2 + j2;
+          cplx v = ldc(a.x, jj);
+          if (INM & IN_SCALE) v = cscale(v, s);
+          if (INM & IN_JAC) v = cmul_np(ldc(a.dinv, jj), v);
+          acc = cadd(acc, cmul_sp(ldc(a.A.coef, (long)o * N + k), v));
+        }
+      }
+    }
+    cplx vc = mk(0.0, 0.0);
+    if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) {
+      vc = ldc(a.x, k);
+      if (INM & IN_SCALE) vc = cscale(vc, s);
+      if (INM & IN_WRITEV) a.vout[k] = vc;
+    }
+    cplx y = (OUTM == OUT_RESID) ? csub(ldc(a.b, k), acc) : acc;
+    a.y[k] = y;
+    if (RED & RED_NORM) red[0] += y.x * y.x + y.y * y.y;
+    if (RED & (RED_DOT | RED_DOT_CENTER)) {
+      const cplx u = (RED & RED_DOT_CENTER) ? vc : ldc(a.u, k);
+      constexpr int o = (RED & RED_NORM) ? 1 : 0;
+      red[o] += u.x * y.x + u.y * y.y;
+      red[o + 1] += u.x * y.y - u.y * y.x;
+    }
+  }
+  if constexpr (NV > 0) {
+    double v[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v[q] = red[q];
+    finish<NV>(v, a.rs, a.epi);
+  }
+}
+
+template <int INM, int OUTM, int RED>
+static void dispatch_no(const LaunchCfg& lc, const StencilArgs& a, int blocks) {
+  const int n = a.A.nofs;
+  if (n <= 5)
+    k_stencil<INM, OUTM, RED, 5><<<blocks, kThreads, 0, lc.stream>>>(a);
+  else if (n <= 9)
+    k_stencil<INM, OUTM, RED, 9><<<blocks, kThreads, 0, lc.stream>>>(a);
+  else if (n <= 13)
+    k_stencil<INM, OUTM, RED, 13><<<blocks, kThreads, 0, lc.stream>>>(a);
+  else if (n <= 21)
+    k_stencil<INM, OUTM, RED, 21><<<blocks, kThreads, 0, lc.stream>>>(a);
+  else
+    k_stencil<INM, OUTM, RED, 25><<<blocks, kThreads, 0, lc.stream>>>(a);
+}
+
+static int blocks_for(const LaunchCfg& lc, long n) {
+  long b = (n + kThreads - 1) / kThreads;
+  if (b > lc.max_blocks) b = lc.max_blocks;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const StencilArgs& a) {
+  ++g_launch_count;
+  const long N = (long)a.A.n1 * a.A.n2;
+  const int blocks = blocks_for(lc, N);
+  constexpr int J = IN_SCALE | IN_JAC | IN_WRITEV;
+#define HADR_CASE(I, O, R)                       \
+  if (inm == (I) && outm == (O) && red == (R)) { \
+    dispatch_no<I, O, R>(lc, a, blocks);         \
+    return;                                      \
+  }
+  HADR_CASE(IN_PLAIN, OUT_APPLY, RED_NONE)
+  HADR_CASE(IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT)
+  HADR_CASE(IN_PLAIN, OUT_RESID, RED_NONE)
+  HADR_CASE(IN_PLAIN, OUT_RESID, RED_NORM)
+  HADR_CASE(J, OUT_APPLY, RED_DOT_CENTER)
+  HADR_CASE(J, OUT_APPLY, RED_DOT)
+  HADR_CASE(IN_JAC, OUT_APPLY, RED_NONE)
+#undef HADR_CASE
+  throw std::runtime_error("launch_stencil: unsupported variant");
+}
+
+// ---------------------------------------------------------------------------
+// K2/K3: MGS building blocks.  w -= h v (numpy: tmp = h*v; w = w - tmp) fused
+// with the next inner product / norm of the updated w.
+// ---------------------------------------------------------------------------
+template <int RED>
+__global__ void __launch_bounds__(kThreads) k_axpy_red(long n, cplx* __restrict__ w, const cplx* h,
+                                                         const cplx* __restrict__ v, const cplx* __restrict__ u,
+                                                         Gate g, RedScratch rs, Epi e) {
+  if (!gate_open(g)) return;
+  const cplx hh = *h;
+  constexpr int NV = (RED == RED_NORM) ? 1 : 2;
+  double red[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) red[q] = 0.0;
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    cplx y = csub(w[k], cmul_np(hh, ldc(v, k)));
+    w[k] = y;
+    if (RED == RED_NORM) {
+      red[0] += y.x * y.x + y.y * y.y;
+    } else {
+      const cplx uu = ldc(u, k);
+      red[0] += uu.x * y.x + uu.y * y.y;
+      red[NV - 1] += uu.x * y.y - uu.y * y.x;
+    }
+  }
+  finish<NV>(red, rs, e);
+}
+
+void launch_axpy_red(const LaunchCfg& lc, long n, cplx* w, const cplx* h, const cplx* v, int red, const cplx* u,
+                     Gate g, RedScratch rs, Epi e) {
+  ++g_launch_count;
+  const int blocks = blocks_for(lc, n);
+  if (red == RED_NORM)
+    k_axpy_red<RED_NORM><<<blocks, kThreads, 0, lc.stream>>>(n, w, h, v, u, g, rs, e);
+  else
+    k_axpy_red<RED_DOT><<<blocks, kThreads, 0, lc.stream>>>(n, w, h, v, u, g, rs, e);
+}
+
+__global__ void __launch_bounds__(kThreads) k_dot(long n, const cplx* __restrict__ u, const cplx* __restrict__ w,
+                                                    Gate g, RedScratch rs, Epi e) {
+  if (!gate_open(g)) return;
+  double red[2] = {0.0, 0.0};
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    const cplx uu = ldc(u, k), y = ldc(w, k);
+    red[0] += uu.x * y.x + uu.y * y.y;
+    red[1] += uu.x * y.y - uu.y * y.x;
+  }
+  finish<2>(red, rs, e);
+}
+
+void launch_dot(const LaunchCfg& lc, long n, const cplx* u, const cplx* w, Gate g, RedScratch rs, Epi e) {
+  ++g_launch_count;
+  k_dot<<<blocks_for(lc, n), kThreads, 0, lc.stream>>>(n, u, w, g, rs, e);
+}
+
+template <int RED>
+__global__ void __launch_bounds__(kThreads) k_scale(long n, const cplx* __restrict__ in, const double* s,
+                                                      cplx* __restrict__ out, Gate g, RedScratch rs, Epi e) {
+  if (!gate_open(g)) return;
+  const double sc = s ? *s : 1.0;
+  double red[1] = {0.0};
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    cplx y = ldc(in, k);
+    if (s) y = cscale(y, sc);
+    if (out) out[k] = y;
+    if (RED) red[0] += y.x * y.x + y.y * y.y;
+  }
+  if (RED) finish<1>(red, rs, e);
+}
+
+void launch_scale(const LaunchCfg& lc, long n, const cplx* in, const double* s, cplx* out, int red, Gate g,
+                  RedScratch rs, Epi e) {
+  ++g_launch_count;
+  const int blocks = blocks_for(lc, n);
+  if (red)
+    k_scale<1><<<blocks, kThreads, 0, lc.stream>>>(n, in, s, out, g, rs, e);
+  else
+    k_scale<0><<<blocks, kThreads, 0, lc.stream>>>(n, in, s, out, g, rs, e);
+}
+
+__global__ void k_zero(long n, cplx* out, Gate g) {
+  if (!gate_open(g)) return;
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) out[k] = mk(0.0, 0.0);
+}
+void launch_zero(const LaunchCfg& lc, long n, cplx* out, Gate g) {
+  ++g_launch_count;
+  k_zero<<<blocks_for(lc, n), kThreads, 0, lc.stream>>>(n, out, g);
+}
+
+// K5: out = base + [dinv (.)] sum_i v_i y_i
+__global__ void __launch_bounds__(kThreads) k_lincomb(long n, LinComb c, Gate g) {
+  if (!gate_open(g)) return;
+  const int k = c.kptr ? *c.kptr : c.kfix;
+  cplx y[MMAX];
+#pragma unroll
+  for (int i = 0; i < MMAX; ++i) y[i] = (i < k) ? (c.y ? c.y[i] : c.yv[i]) : mk(0.0, 0.0);
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long p = (long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+    cplx t = mk(0.0, 0.0);
+    for (int i = 0; i < k; ++i) t = cadd(t, cmul_np(ldc(c.v[i], p), y[i]));
+    if (c.dinv) t = cmul_np(ldc(c.dinv, p), t);
+    c.out[p] = c.base ? cadd(ldc(c.base, p), t) : cadd(mk(0.0, 0.0), t);
+  }
+}
+void launch_lincomb(const LaunchCfg& lc, long n, const LinComb& c, Gate g) {
+  ++g_launch_count;
+  k_lincomb<<<blocks_for(lc, n), kThreads, 0, lc.stream>>>(n, c, g);
+}
+
+// brk_stage 1: first-cycle early exit, x = 0 + Z0*y0 (k<=1)
+// brk_stage 0: final: ZERO -> 0 ; FIN/cycle0 -> x = Z0 y0 + Z1 y1 ; FIN/cycle1 -> x += Z1 y0
+__global__ void __launch_bounds__(kThreads) k_fg_finalize(long n, FgCtl* f, const cplx* __restrict__ Z0,
+                                                            const cplx* __restrict__ Z1, cplx* x, Gate g,
+                                                            int brk_stage) {
+  if (!gate_open(g)) return;
+  const int path = f->path, k = f->k, cyc = f->cycle;
+  const cplx y0 = f->y[0], y1 = f->y[1];
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long p = (long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+    cplx out;
+    if (brk_stage) {
+      out = (k >= 1) ? cadd(mk(0.0, 0.0), cmul_np(ldc(Z0, p), y0)) : mk(0.0, 0.0);
+    } else if (path == FG_ZERO) {
+      out = mk(0.0, 0.0);
+    } else if (cyc == 0) {
+      cplx t = mk(0.0, 0.0);
+      if (k >= 1) t = cadd(t, cmul_np(ldc(Z0, p), y0));
+      if (k >= 2) t = cadd(t, cmul_np(ldc(Z1, p), y1));
+      out = cadd(mk(0.0, 0.0), t);
+    } else {
+      out = (k >= 1) ? cadd(x[p], cmul_np(ldc(Z1, p), y0)) : x[p];
+    }
+    x[p] = out;
+  }
+}
+void launch_fg_finalize(const LaunchCfg& lc, long n, FgCtl* f, const cplx* Z0, const cplx* Z1, cplx* x, Gate g,
+                        int brk_stage) {
+  ++g_launch_count;
+  k_fg_finalize<<<blocks_for(lc, n), kThreads, 0, lc.stream>>>(n, f, Z0, Z1, x, g, brk_stage);
+}
+
+// ---------------------------------------------------------------------------
+// K6/K7: transfer operators for the bilinear P = kron(P1(n1), P1(n2)).
+// Restriction rc = P^T r follows scipy csc_matvec: contributions added in
+// ascending fine index, i.e. lexicographic (a, b) over the 3x3 fine patch.
+// Prolongation follows csr_matvec: parents in ascending coarse index.
+// Weights are powers of two, so each product is exact and the sums match
+// the reference bit for bit.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_restrict(int n1f, int n2f, const cplx* __restrict__ r,
+                                                         cplx* __restrict__ rc, Gate g) {
+  if (!gate_open(g)) return;
+  const int n1c = (n1f - 1) / 2 + 1, n2c = (n2f - 1) / 2 + 1;
+  const long Nc = (long)n1c * n2c;
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long c = (long)blockIdx.x * blockDim.x + threadIdx.x; c < Nc; c += stride) {
+    const int I1 = (int)(c / n2c), I2 = (int)(c - (long)I1 * n2c);
+    cplx acc = mk(0.0, 0.0);
+#pragma unroll
+    for (int a = -1; a <= 1; ++a) {
+      const int f1 = 2 * I1 + a;
+      if (f1 < 0 || f1 >= n1f) continue;
+      const double w1 = a == 0 ? 1.0 : 0.5;
+#pragma unroll
+      for (int b = -1; b <= 1; ++b) {
+        const int f2 = 2 * I2 + b;
+        if (f2 < 0 || f2 >= n2f) continue;
+        const double w = w1 * (b == 0 ? 1.0 : 0.5);
+        acc = cadd(acc, cmul_sp(mk(w, 0.0), ldc(r, (long)f1 * n2f + f2)));
+      }
+    }
+    rc[c] = acc;
+  }
+}
+void launch_restrict(const LaunchCfg& lc, int n1f, int n2f, const cplx* r, cplx* rc, Gate g) {
+  ++g_launch_count;
+  const long Nc = (long)((n1f - 1) / 2 + 1) * ((n2f - 1) / 2 + 1);
+  k_restrict<<<blocks_for(lc, Nc), kThreads, 0, lc.stream>>>(n1f, n2f, r, rc, g);
+}
+
+__global__ void __launch_bounds__(kThreads) k_prolong_add(int n1f, int n2f, const cplx* __restrict__ ec,
+                                                            cplx* __restrict__ x, Gate g) {
+  if (!gate_open(g)) return;
+  const int n2c = (n2f - 1) / 2 + 1;
+  const long Nf = (long)n1f * n2f;
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long f = (long)blockIdx.x * blockDim.x + threadIdx.x; f < Nf; f += stride) {
+    const int f1 = (int)(f / n2f), f2 = (int)(f - (long)f1 * n2f);
+    int c1[2], c2[2], m1, m2;
+    double w1, w2;
+    if (f1 & 1) { c1[0] = f1 >> 1; c1[1] = (f1 >> 1) + 1; m1 = 2; w1 = 0.5; } else { c1[0] = f1 >> 1; m1 = 1; w1 = 1.0; }
+    if (f2 & 1) { c2[0] = f2 >> 1; c2[1] = (f2 >> 1) + 1; m2 = 2; w2 = 0.5; } else { c2[0] = f2 >> 1; m2 = 1; w2 = 1.0; }
+    cplx p = mk(0.0, 0.0);
+    for (int a = 0; a < m1; ++a)
+      for (int b = 0; b < m2; ++b)
+        p = cadd(p, cmul_sp(mk(w1 * w2, 0.0), ldc(ec, (long)c1[a] * n2c + c2[b])));
+    x[f] = cadd(x[f], p);
+  }
+}
+void launch_prolong_add(const LaunchCfg& lc, int n1f, int n2f, const cplx* ec, cplx* x, Gate g) {
+  ++g_launch_count;
+  k_prolong_add<<<blocks_for(lc, (long)n1f * n2f), kThreads, 0, lc.stream>>>(n1f, n2f, ec, x, g);
+}
+
+// ---------------------------------------------------------------------------
+// gates and control initialisation (single thread)
+// ---------------------------------------------------------------------------
+__global__ void k_set_gate(int* dst, Gate g) { *dst = gate_open(g) ? 1 : 0; }
+void launch_set_gate(cudaStream_t s, int* dst, Gate g) {
+  ++g_launch_count; k_set_gate<<<1, 1, 0, s>>>(dst, g); }
+
+__global__ void k_relax_init(RelaxCtl* c, int steps, Gate g) {
+  if (!gate_open(g)) return;
+  c->steps = steps;
+  c->k = 0;
+  c->cur = kStopped;
+}
+void launch_relax_init(cudaStream_t s, RelaxCtl* c, int steps, Gate g) {
+  ++g_launch_count; k_relax_init<<<1, 1, 0, s>>>(c, steps, g); }
+
+__global__ void k_fg_setup(FgCtl* f, double tol, Gate g) {
+  if (!gate_open(g)) return;
+  f->tol = tol;
+  f->reo = 0;
+}
+void launch_fg_setup(cudaStream_t s, FgCtl* f, double tol, Gate g) {
+  ++g_launch_count; k_fg_setup<<<1, 1, 0, s>>>(f, tol, g); }
+
+// ---------------------------------------------------------------------------
+// operator construction (setup; not on the solve's inner loop)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int slot25(int d1, int d2) { return (d1 + 2) * 5 + (d2 + 2); }
+
+__global__ void k_csr_mask(int n1, int n2, const int64_t* indptr, const int32_t* indices, unsigned* mask) {
+  const long N = (long)n1 * n2;
+  unsigned m = 0u, bad = 0u;
+  for (long row = (long)blockIdx.x * blockDim.x + threadIdx.x; row < N; row += (long)gridDim.x * blockDim.x) {
+    const int i1 = (int)(row / n2), i2 = (int)(row - (long)i1 * n2);
+    for (int64_t p = indptr[row]; p < indptr[row + 1]; ++p) {
+      const long col = indices[p];
+      const int j1 = (int)(col / n2), j2 = (int)(col - (long)j1 * n2);
+      const int d1 = j1 - i1, d2 = j2 - i2;
+      if (d1 < -2 || d1 > 2 || d2 < -2 || d2 > 2)
+        bad = 1u;
+      else
+        m |= 1u << slot25(d1, d2);
+    }
+  }
+  if (m) atomicOr(mask, m);
+  if (bad) atomicOr(mask + 1, 1u);
+}
+void launch_csr_mask(cudaStream_t s, int n1, int n2, const int64_t* indptr, const int32_t* indices, unsigned* mask) {
+  ++g_launch_count;
+  long N = (long)n1 * n2;
+  int blocks = (int)((N + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  k_csr_mask<<<blocks, 256, 0, s>>>(n1, n2, indptr, indices, mask);
+}
+
+__global__ void k_csr_scatter(int n1, int n2, const int64_t* indptr, const int32_t* indices, const cplx* data,
+                              const int* slot_of, cplx* coef) {
+  const long N = (long)n1 * n2;
+  for (long row = (long)blockIdx.x * blockDim.x + threadIdx.x; row < N; row += (long)gridDim.x * blockDim.x) {
+    const int i1 = (int)(row / n2), i2 = (int)(row - (long)i1 * n2);
+    for (int64_t p = indptr[row]; p < indptr[row + 1]; ++p) {
+      const long col = indices[p];
+      const int j1 = (int)(col / n2), j2 = (int)(col - (long)j1 * n2);
+      const int sl = slot_of[slot25(j1 - i1, j2 - i2)];
+      cplx* dst = coef + (long)sl * N + row;
+      *dst = cadd(*dst, data[p]);
+    }
+  }
+}
+void launch_csr_scatter(cudaStream_t s, int n1, int n2, const int64_t* indptr, const int32_t* indices,
+                        const cplx* data, const int* slot_of, cplx* coef) {
+  ++g_launch_count;
+  long N = (long)n1 * n2;
+  int blocks = (int)((N + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  k_csr_scatter<<<blocks, 256, 0, s>>>(n1, n2, indptr, indices, data, slot_of, coef);
+}
+
+// z = r / d elementwise (numpy complex division), helmadr/krylov.py:68-73
+__global__ void k_cdiv(long n, const cplx* r, const cplx* d, cplx* z) {
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x)
+    z[k] = cdiv_np(r[k], d[k]);
+}
+void launch_cdiv(cudaStream_t s, long n, const cplx* r, const cplx* d, cplx* z) {
+  ++g_launch_count;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  k_cdiv<<<blocks, 256, 0, s>>>(n, r, d, z);
+}
+
+// dinv = 1.0 / diag (numpy complex division), helmadr/multigrid.py:74-81
+__global__ void k_inv_diag(long n, const cplx* diag, cplx* dinv, int* zero_flag) {
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    const cplx d = diag ? diag[k] : mk(0.0, 0.0);
+    if (d.x == 0.0 && d.y == 0.0) atomicOr(zero_flag, 1);
+    dinv[k] = cdiv_np(mk(1.0, 0.0), d);
+  }
+}
+void launch_inv_diag(cudaStream_t s, long n, const cplx* diag, cplx* dinv, int* zero_flag) {
+  ++g_launch_count;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  k_inv_diag<<<blocks, 256, 0, s>>>(n, diag, dinv, zero_flag);
+}
+
+// dst[dst_slot[o]] (+)= alpha * src[o]   (scalar * CSR data, then CSR + CSR)
+__global__ void k_remap_planes(long n, const cplx* src, int nsrc, const int* dst_slot, cplx* dst, cplx alpha,
+                               int accumulate, int scaled) {
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    for (int o = 0; o < nsrc; ++o) {
+      cplx v = src[(long)o * n + k];
+      if (scaled) v = cmul_np(v, alpha);
+      cplx* d = dst + (long)dst_slot[o] * n + k;
+      *d = accumulate ? cadd(*d, v) : v;
+    }
+  }
+}
+void launch_remap_planes(cudaStream_t s, long n, const cplx* src, int nsrc, const int* dst_slot, cplx* dst,
+                         cplx alpha, int accumulate) {
+  ++g_launch_count;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  const int scaled = !(alpha.x == 1.0 && alpha.y == 0.0);
+  k_remap_planes<<<blocks, 256, 0, s>>>(n, src, nsrc, dst_slot, dst, alpha, accumulate, scaled);
+}
+
+// center += sc * field  (complex scalar times real field, numpy product; then CSR add)
+__global__ void k_add_diag_real(long n, cplx* center, cplx sc, const double* field) {
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x)
+    center[k] = cadd(center[k], cmul_np(sc, mk(field[k], 0.0)));
+}
+void launch_add_diag_real(cudaStream_t s, long n, cplx* center, cplx sc, const double* field) {
+  ++g_launch_count;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  k_add_diag_real<<<blocks, 256, 0, s>>>(n, center, sc, field);
+}
+
+// diag(left) @ A @ diag(right): scipy csr_matmat products, left first (helmadr/operators.py:264)
+__global__ void k_similarity(StencilDev A, cplx* out, const cplx* left, const cplx* right) {
+  const int n1 = A.n1, n2 = A.n2;
+  const long N = (long)n1 * n2;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (long)gridDim.x * blockDim.x) {
+    const int i1 = (int)(k / n2), i2 = (int)(k - (long)i1 * n2);
+    for (int o = 0; o < A.nofs; ++o) {
+      const int j1 = i1 + A.d1[o], j2 = i2 + A.d2[o];
+      cplx v = mk(0.0, 0.0);
+      if (j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2) {
+        const cplx c = A.coef[(long)o * N + k];
+        v = cmul_sp(cmul_sp(left[k], c), right[(long)j1 * n2 + j2]);
+      }
+      out[(long)o * N + k] = v;
+    }
+  }
+}
+void launch_similarity(cudaStream_t s, const StencilDev& A, cplx* out, const cplx* left, const cplx* right) {
+  ++g_launch_count;
+  long N = (long)A.n1 * A.n2;
+  int blocks = (int)((N + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  k_similarity<<<blocks, 256, 0, s>>>(A, out, left, right);
+}
+
+// K8: Galerkin coarse operator A_c = P^T A P on the stencil representation.
+// Pass 1 (coef_c == null): OR the mask of non-zero coarse offsets (5x5 box).
+// Pass 2: write the compacted planes (slot_of maps box slot -> plane).
+__global__ void k_galerkin(StencilDev Af, int n1c, int n2c, unsigned* mask, const int* slot_of, cplx* coef_c) {
+  const int n1f = Af.n1, n2f = Af.n2;
+  const long Nf = (long)n1f * n2f, Nc = (long)n1c * n2c;
+  unsigned m = 0u;
+  for (long c = (long)blockIdx.x * blockDim.x + threadIdx.x; c < Nc; c += (long)gridDim.x * blockDim.x) {
+    const int I1 = (int)(c / n2c), I2 = (int)(c - (long)I1 * n2c);
+    cplx acc[25];
+#pragma unroll
+    for (int q = 0; q < 25; ++q) acc[q] = mk(0.0, 0.0);
+    for (int a = -1; a <= 1; ++a) {
+      const int f1 = 2 * I1 + a;
+      if (f1 < 0 || f1 >= n1f) continue;
+      for (int b = -1; b <= 1; ++b) {
+        const int f2 = 2 * I2 + b;
+        if (f2 < 0 || f2 >= n2f) continue;
+        const double wf = (a == 0 ? 1.0 : 0.5) * (b == 0 ? 1.0 : 0.5);
+        const long f = (long)f1 * n2f + f2;
+        for (int o = 0; o < Af.nofs; ++o) {
+          const int g1 = f1 + Af.d1[o], g2 = f2 + Af.d2[o];
+          if (g1 < 0 || g1 >= n1f || g2 < 0 || g2 >= n2f) continue;
+          const cplx cf = Af.coef[(long)o * Nf + f];
+          if (cf.x == 0.0 && cf.y == 0.0) continue;
+          const cplx wc = mk(wf * cf.x, wf * cf.y);
+          int p1[2], p2[2], m1, m2;
+          double v1, v2;
+          if (g1 & 1) { p1[0] = g1 >> 1; p1[1] = (g1 >> 1) + 1; m1 = 2; v1 = 0.5; } else { p1[0] = g1 >> 1; m1 = 1; v1 = 1.0; }
+          if (g2 & 1) { p2[0] = g2 >> 1; p2[1] = (g2 >> 1) + 1; m2 = 2; v2 = 0.5; } else { p2[0] = g2 >> 1; m2 = 1; v2 = 1.0; }
+          for (int x = 0; x < m1; ++x)
+            for (int y = 0; y < m2; ++y) {
+              const int D1 = p1[x] - I1, D2 = p2[y] - I2;
+              const double pw = v1 * v2;
+              const int sl = slot25(D1, D2);
+              acc[sl] = cadd(acc[sl], mk(pw * wc.x, pw * wc.y));
+            }
+        }
+      }
+    }
+    for (int q = 0; q < 25; ++q) {
+      if (acc[q].x != 0.0 || acc[q].y != 0.0) m |= 1u << q;
+      if (coef_c && slot_of[q] >= 0) coef_c[(long)slot_of[q] * Nc + c] = acc[q];
+    }
+  }
+  if (mask && m) atomicOr(mask, m);
+}
+void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, unsigned* mask, const int* slot_of,
+                     cplx* coef_c) {
+  ++g_launch_count;
+  long Nc = (long)n1c * n2c;
+  int blocks = (int)((Nc + 127) / 128);
+  if (blocks > 4096) blocks = 4096;
+  k_galerkin<<<blocks, 128, 0, s>>>(Af, n1c, n2c, mask, slot_of, coef_c);
+}
+
+}  // namespace hadr

@@ -1,0 +1,121 @@
+// Launch interface of the sm_100a kernels (kernels.cu) used by the host engine.
+#pragma once
+#include "ctl.cuh"
+
+namespace hadr {
+
+extern long long g_launch_count;
+
+// Structured 2D stencil in union-offset, plane-major layout:
+//   coef[o*N + k] multiplies x[k + d1[o]*n2 + d2[o]],  offsets sorted by (d1, d2)
+//   == ascending column index of the reference CSR row, so the accumulation
+//   order equals scipy csr_matvec's.
+struct StencilDev {
+  int n1, n2;
+  int nofs;
+  int pad_;
+  int8_t d1[HADR_MAX_OFS];
+  int8_t d2[HADR_MAX_OFS];
+  const cplx* coef;
+};
+
+enum : int { IN_PLAIN = 0, IN_SCALE = 1, IN_JAC = 2, IN_WRITEV = 4 };
+enum : int { OUT_APPLY = 0, OUT_RESID = 1 };
+enum : int { RED_NONE = 0, RED_NORM = 1, RED_DOT = 2, RED_DOT_CENTER = 4 };
+
+enum EpiCode : int {
+  EPI_NONE = 0,
+  EPI_STORE,        // out[0..nv) = totals
+  EPI_RELAX_BETA,   // beta = sqrt(t0)
+  EPI_RELAX_H,      // H[i][j] = dot
+  EPI_RELAX_STEP,   // H[j+1][j] = sqrt(t0); Givens; stop/continue
+  EPI_FG_INIT,      // bnorm
+  EPI_FG_S,         // w0 = sqrt(t0), H[0][j] = (t1, t2)
+  EPI_FG_H,         // H[i][j] = dot
+  EPI_FG_CORR,      // corr[i] = dot; H[i][j] += corr
+  EPI_FG_N,         // wn; reo decision; inner: post if no reorth
+  EPI_FG_N2,        // wn after reorth; inner: post
+  EPI_FG_RES,       // inner early-exit residual -> restart decision
+};
+
+struct Epi {
+  int code;
+  int i, j;
+  int inner;   // FG_N / FG_N2: run the device-side FGMRES post-step
+  void* ctl;
+  double* out;
+};
+inline Epi epi_none() { return Epi{EPI_NONE, 0, 0, 0, nullptr, nullptr}; }
+inline Epi epi_store(double* out) { return Epi{EPI_STORE, 0, 0, 0, nullptr, out}; }
+inline Epi epi(int code, void* ctl, int i = 0, int j = 0, int inner = 0) { return Epi{code, i, j, inner, ctl, nullptr}; }
+
+struct StencilArgs {
+  StencilDev A;
+  const cplx* x;       // input vector (neighbours read)
+  const double* scale; // IN_SCALE: x*(*scale)
+  const cplx* dinv;    // IN_JAC: dinv (.) x
+  cplx* vout;          // IN_WRITEV: transformed-but-unjacobied centre value
+  const cplx* b;       // OUT_RESID
+  cplx* y;             // output
+  const cplx* u;       // RED_DOT partner (conjugated)
+  Gate gate;
+  RedScratch rs;
+  Epi epi;
+};
+
+struct LaunchCfg {
+  cudaStream_t stream;
+  int max_blocks;  // grid cap (multiple of the SM count)
+};
+
+void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const StencilArgs& a);
+
+// w -= (*h) * v ; then reduce: RED_DOT -> <u, w>, RED_NORM -> ||w||^2
+void launch_axpy_red(const LaunchCfg& lc, long n, cplx* w, const cplx* h, const cplx* v, int red, const cplx* u,
+                     Gate g, RedScratch rs, Epi e);
+// reduce <u, w>
+void launch_dot(const LaunchCfg& lc, long n, const cplx* u, const cplx* w, Gate g, RedScratch rs, Epi e);
+// out = in * (*s) (s may be null: copy); red: RED_NORM of out ; out may be null (reduction only)
+void launch_scale(const LaunchCfg& lc, long n, const cplx* in, const double* s, cplx* out, int red, Gate g,
+                  RedScratch rs, Epi e);
+void launch_zero(const LaunchCfg& lc, long n, cplx* out, Gate g);
+
+// out = base + [dinv (.)] sum_{i<k} v_i * y_i ; k = *kptr if kptr else kfix ; base may be null (zero)
+struct LinComb {
+  const cplx* v[MMAX];
+  const cplx* y;       // device coefficients (ctl) or null -> yv
+  cplx yv[MMAX];       // by-value coefficients
+  const int* kptr;
+  int kfix;
+  const cplx* base;
+  const cplx* dinv;    // optional Jacobi on the sum
+  cplx* out;
+};
+void launch_lincomb(const LaunchCfg& lc, long n, const LinComb& c, Gate g);
+
+// Inner FGMRES finalisation, branches on the device path/cycle (helmadr/krylov.py:218-223).
+void launch_fg_finalize(const LaunchCfg& lc, long n, FgCtl* f, const cplx* Z0, const cplx* Z1, cplx* x, Gate g,
+                        int brk_stage);
+
+// Restriction rc = P^T r and prolongation x += P e (bilinear P, helmadr/multigrid.py:19-46).
+void launch_restrict(const LaunchCfg& lc, int n1f, int n2f, const cplx* r, cplx* rc, Gate g);
+void launch_prolong_add(const LaunchCfg& lc, int n1f, int n2f, const cplx* ec, cplx* x, Gate g);
+
+void launch_set_gate(cudaStream_t s, int* dst, Gate g);
+void launch_relax_init(cudaStream_t s, RelaxCtl* c, int steps, Gate g);
+void launch_fg_setup(cudaStream_t s, FgCtl* f, double tol, Gate g);
+
+// ---- operator construction (setup) ----
+void launch_csr_mask(cudaStream_t s, int n1, int n2, const int64_t* indptr, const int32_t* indices, unsigned* mask);
+void launch_csr_scatter(cudaStream_t s, int n1, int n2, const int64_t* indptr, const int32_t* indices,
+                        const cplx* data, const int* slot_of, cplx* coef);
+void launch_cdiv(cudaStream_t s, long n, const cplx* r, const cplx* d, cplx* z);
+void launch_inv_diag(cudaStream_t s, long n, const cplx* diag, cplx* dinv, int* zero_flag);
+void launch_remap_planes(cudaStream_t s, long n, const cplx* src, int nsrc, const int* dst_slot, cplx* dst,
+                         cplx alpha, int accumulate);
+void launch_add_diag_real(cudaStream_t s, long n, cplx* center, cplx sc, const double* field);
+void launch_similarity(cudaStream_t s, const StencilDev& A, cplx* out, const cplx* left, const cplx* right);
+void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, unsigned* mask, const int* slot_of,
+                     cplx* coef_c);
+
+}  // namespace hadr

@@ -1,0 +1,161 @@
+"""Krylov solvers on the B200 — drop-in mirror of helmadr/krylov.py.
+
+Same names, arguments, defaults, error behaviour and report fields as the
+reference (helmadr/krylov.py:16-242); the arithmetic runs in libhadr.so.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import HadrReport, as_c128, cbuf, check
+from .stencil import StencilOperator, as_operator
+
+
+@dataclass
+class KrylovConfig:
+    """helmadr/krylov.py:16-31."""
+
+    restart: int = 5
+    maxiter: int = 200
+    tol: float = 1e-5
+    flexible: bool = True
+    collect_diagnostics: bool = False
+
+    def __post_init__(self):
+        if self.restart < 1:
+            raise ValueError("restart must be >= 1")
+        if self.tol <= 0:
+            raise ValueError("tol must be positive")
+
+
+@dataclass
+class SolveReport:
+    """helmadr/krylov.py:34-57, plus the device timing of the solve."""
+
+    iterations: int
+    history: np.ndarray
+    converged: bool
+    wall_time: float
+    bnorm: float
+    final_relres: float
+    note: str = ""
+    ortho_max: float = 0.0
+    stage1: "SolveReport | None" = None
+    stage2: "SolveReport | None" = None
+    fm_time: float = 0.0
+    device_time: float = 0.0
+
+    def history_csv_lines(self) -> list[str]:
+        scale = self.bnorm if self.bnorm > 0 else 1.0
+        return [f"{i},{r / scale:.16e}" for i, r in enumerate(self.history)]
+
+
+_NOTES = {0: "", 1: "numerical breakdown: non-finite Arnoldi vector"}
+
+
+def _grid_of(A, b=None):
+    if isinstance(A, StencilOperator):
+        return A.grid_shape
+    raise TypeError("a scipy matrix has no grid; wrap it with StencilOperator.from_csr(A, (n1, n2))")
+
+
+def spmv(A, x) -> np.ndarray:
+    """y = A x with an explicit dimension check (helmadr/krylov.py:60-65)."""
+    x = np.asarray(x)
+    if A.shape[1] != x.shape[0]:
+        raise ValueError(f"dimension mismatch: operator {A.shape}, vector {x.shape}")
+    op = as_operator(A, getattr(A, "grid_shape", None))
+    return op.matvec(x)
+
+
+def jacobi_apply(A, r) -> np.ndarray:
+    """z_j = r_j / A_jj (helmadr/krylov.py:68-73)."""
+    op = as_operator(A, getattr(A, "grid_shape", None))
+    r = as_c128(r, op.shape[0])
+    z = np.empty_like(r)
+    check(_lib.lib().hadr_op_jacobi(op.handle, cbuf(r), cbuf(z), 0))
+    return z
+
+
+def gmres_relax(A, b, x, steps: int) -> np.ndarray:
+    """Fixed-length Jacobi-preconditioned GMRES from x (helmadr/krylov.py:82-119)."""
+    op = as_operator(A, getattr(A, "grid_shape", None))
+    n = op.shape[0]
+    b = as_c128(b, n)
+    x = as_c128(x, n)
+    out = np.empty_like(b)
+    check(_lib.lib().hadr_gmres_relax(op.handle, cbuf(b), cbuf(x), int(steps), cbuf(out), 0))
+    return out
+
+
+def _report_from(rep: HadrReport, hist: np.ndarray) -> SolveReport:
+    return SolveReport(
+        iterations=int(rep.iterations),
+        history=np.array(hist[: rep.history_len], copy=True),
+        converged=bool(rep.converged),
+        wall_time=float(rep.wall_time),
+        bnorm=float(rep.bnorm),
+        final_relres=float(rep.final_relres),
+        note=_NOTES.get(int(rep.note), "breakdown"),
+        device_time=float(rep.device_time),
+    )
+
+
+def fgmres(A, b, x0=None, precond=None, cfg: KrylovConfig | None = None):
+    """Restarted flexible GMRES (helmadr/krylov.py:122-242) on the device.
+
+    ``A``: StencilOperator (or scipy matrix already wrapped); ``precond``: None
+    or a K-cycle preconditioner from ``make_kcycle_preconditioner``.  Returns
+    ``(x, SolveReport)``; inputs are not modified.
+    """
+    from .multigrid import KCyclePreconditioner  # local: multigrid imports krylov
+
+    cfg = cfg or KrylovConfig()
+    if not cfg.flexible:
+        raise ValueError("the K-cycle is a varying preconditioner: only flexible GMRES is supported")
+    op = as_operator(A, getattr(A, "grid_shape", None))
+    n = op.shape[0]
+    b = as_c128(b, n)
+    x0a = None if x0 is None else as_c128(x0, n)
+    if precond is None:
+        hh = None
+    elif isinstance(precond, KCyclePreconditioner):
+        hh = precond.hier.handle
+    else:
+        raise TypeError("precond must be None or make_kcycle_preconditioner(hier) (device K-cycle)")
+    x = np.empty_like(b)
+    rep = HadrReport()
+    cap = cfg.maxiter + 2
+    hist = np.zeros(cap)
+    check(
+        _lib.lib().hadr_fgmres(op.handle, hh, cbuf(b), None if x0a is None else cbuf(x0a), int(cfg.restart),
+                               int(cfg.maxiter), float(cfg.tol), cbuf(x), C.byref(rep), cbuf(hist), cap, 0)
+    )
+    return x, _report_from(rep, hist)
+
+
+def fgmres_device(A, b_ptr: int, x_ptr: int, precond=None, cfg: KrylovConfig | None = None, x0_ptr: int | None = None):
+    """fgmres on device-resident vectors (raw CUDA pointers, e.g. torch ``data_ptr()``).
+    Returns the SolveReport; x is written in place."""
+    cfg = cfg or KrylovConfig()
+    op = as_operator(A, getattr(A, "grid_shape", None))
+    hh = None if precond is None else precond.hier.handle
+    rep = HadrReport()
+    cap = cfg.maxiter + 2
+    hist = np.zeros(cap)
+    check(
+        _lib.lib().hadr_fgmres(op.handle, hh, C.c_void_p(b_ptr), None if x0_ptr is None else C.c_void_p(x0_ptr),
+                               int(cfg.restart), int(cfg.maxiter), float(cfg.tol), C.c_void_p(x_ptr), C.byref(rep),
+                               cbuf(hist), cap, 1)
+    )
+    return _report_from(rep, hist)
+
+
+def launch_count() -> int:
+    """Kernels libhadr.so has launched so far in this process."""
+    return int(_lib.load().hadr_launch_count())

@@ -1,0 +1,208 @@
+"""Device-resident structured operators — the B200 replacement for the scipy CSR
+matrices the reference's solver consumes (helmadr/operators.py,
+helmadr/multigrid.py:19-55).
+
+``StencilOperator`` keeps an operator as union-offset coefficient planes in HBM
+(complex128, plane-major: coef[o, k] multiplies x[k + d1*n2 + d2]).  It
+supports the duck-typed surface the reference's solver uses on its matrices
+(``@``, ``.shape``, ``.nnz``, ``.diagonal()``, ``.tocsr()``) so it can stand in
+for the scipy objects in ``MGHierarchy.ops`` (helmadr/multigrid.py:58-72).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from ._lib import as_c128, cbuf, check
+
+
+class StencilOperator:
+    """Complex128 2D stencil operator on an (n1, n2) nodal grid, on the GPU."""
+
+    def __init__(self, handle, owner=None, keepalive=()):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+        self._owner = owner            # hierarchy that owns a borrowed handle
+        self._keep = tuple(keepalive)  # operators a derived handle depends on
+        n1, n2, no = C.c_int(), C.c_int(), C.c_int()
+        offs = (C.c_int * 50)()
+        check(_lib.lib().hadr_op_info(self._h, C.byref(n1), C.byref(n2), C.byref(no), offs))
+        self.grid_shape = (n1.value, n2.value)
+        self.offsets = [(offs[2 * i], offs[2 * i + 1]) for i in range(no.value)]
+
+    # ---- construction ----
+    @classmethod
+    def from_csr(cls, A, grid_shape) -> "StencilOperator":
+        """Convert a square CSR matrix on the (n1, n2) grid (bit-exact value copy)."""
+        n1, n2 = int(grid_shape[0]), int(grid_shape[1])
+        A = sp.csr_matrix(A)
+        if A.shape != (n1 * n2, n1 * n2):
+            raise ValueError(f"operator {A.shape} does not match grid {n1}x{n2}")
+        if not A.has_canonical_format:
+            A = A.copy()
+            A.sum_duplicates()
+        indptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
+        indices = np.ascontiguousarray(A.indices, dtype=np.int32)
+        data = np.ascontiguousarray(A.data, dtype=np.complex128)
+        h = C.c_void_p()
+        check(_lib.lib().hadr_op_from_csr(n1, n2, int(A.nnz), cbuf(indptr), cbuf(indices), cbuf(data), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_planes(cls, grid_shape, offsets, coef) -> "StencilOperator":
+        n1, n2 = int(grid_shape[0]), int(grid_shape[1])
+        offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.int32).reshape(-1))
+        coef = np.ascontiguousarray(np.asarray(coef, dtype=np.complex128).reshape(len(offsets), n1 * n2))
+        h = C.c_void_p()
+        check(_lib.lib().hadr_op_from_planes(n1, n2, len(offsets), cbuf(offs), cbuf(coef), C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        try:
+            if self._owner is None and self._h:
+                _lib._lib.hadr_op_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ---- duck-typed matrix surface ----
+    @property
+    def shape(self):
+        n = self.grid_shape[0] * self.grid_shape[1]
+        return (n, n)
+
+    @property
+    def dtype(self):
+        return np.dtype(np.complex128)
+
+    def planes(self) -> np.ndarray:
+        n = self.shape[0]
+        out = np.empty((len(self.offsets), n), dtype=np.complex128)
+        check(_lib.lib().hadr_op_export(self._h, cbuf(out)))
+        return out
+
+    def tocsr(self) -> sp.csr_matrix:
+        """Export to canonical scipy CSR (structural zeros dropped)."""
+        n1, n2 = self.grid_shape
+        n = n1 * n2
+        P = self.planes()
+        k = np.arange(n)
+        i1, i2 = k // n2, k % n2
+        rows, cols, vals = [], [], []
+        for o, (d1, d2) in enumerate(self.offsets):
+            j1, j2 = i1 + d1, i2 + d2
+            ok = (j1 >= 0) & (j1 < n1) & (j2 >= 0) & (j2 < n2) & (P[o] != 0)
+            rows.append(k[ok])
+            cols.append((j1 * n2 + j2)[ok])
+            vals.append(P[o][ok])
+        A = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(n, n))
+        A.sort_indices()
+        return A
+
+    @property
+    def nnz(self) -> int:
+        return int(np.count_nonzero(self.planes()))
+
+    def diagonal(self) -> np.ndarray:
+        try:
+            o = self.offsets.index((0, 0))
+        except ValueError:
+            return np.zeros(self.shape[0], dtype=np.complex128)
+        return self.planes()[o].copy()
+
+    def matvec(self, x) -> np.ndarray:
+        """y = A x on the GPU (scipy csr_matvec accumulation order: bit-exact)."""
+        x = as_c128(x, self.shape[1])
+        y = np.empty_like(x)
+        check(_lib.lib().hadr_op_apply(self._h, cbuf(x), cbuf(y), 0))
+        return y
+
+    def __matmul__(self, x):
+        if isinstance(x, np.ndarray) and x.ndim == 1:
+            return self.matvec(x)
+        return NotImplemented
+
+    def __call__(self, x):
+        return self.matvec(x)
+
+    def __repr__(self):
+        return f"<StencilOperator {self.grid_shape[0]}x{self.grid_shape[1]}, {len(self.offsets)} offsets, device>"
+
+
+def as_operator(A, grid_shape=None) -> StencilOperator:
+    """A StencilOperator for A (StencilOperator or scipy sparse on a known grid)."""
+    if isinstance(A, StencilOperator):
+        return A
+    if sp.issparse(A):
+        if grid_shape is None:
+            raise ValueError("a scipy operator needs its grid shape to become a device stencil")
+        return StencilOperator.from_csr(A, grid_shape)
+    raise TypeError(
+        f"unsupported operator type {type(A).__name__}: the B200 path needs a StencilOperator or a scipy sparse "
+        "matrix on a structured grid (no CPU fallback for arbitrary callables)"
+    )
+
+
+class _TransposedProlongation:
+    def __init__(self, P):
+        self.P = P
+
+    @property
+    def shape(self):
+        return (self.P.shape[1], self.P.shape[0])
+
+    def __matmul__(self, r):
+        r = as_c128(r, self.shape[1])
+        out = np.empty(self.shape[0], dtype=np.complex128)
+        check(_lib.lib().hadr_transfer(self.P.fine_shape[0], self.P.fine_shape[1], 0, cbuf(r), cbuf(out), 0))
+        return out
+
+
+class Prolongation:
+    """Bilinear P = kron(P1(n1), P1(n2)) applied matrix-free on the device
+    (helmadr/multigrid.py:19-46).  ``P @ e`` prolongs, ``P.T @ r`` restricts."""
+
+    def __init__(self, fine_shape):
+        n1, n2 = int(fine_shape[0]), int(fine_shape[1])
+        if (n1 - 1) % 2 or (n2 - 1) % 2:
+            raise ValueError(f"cannot coarsen {fine_shape}: interval count is odd")
+        self.fine_shape = (n1, n2)
+        self.coarse_shape = ((n1 - 1) // 2 + 1, (n2 - 1) // 2 + 1)
+
+    @property
+    def shape(self):
+        return (self.fine_shape[0] * self.fine_shape[1], self.coarse_shape[0] * self.coarse_shape[1])
+
+    @property
+    def T(self):
+        return _TransposedProlongation(self)
+
+    def __matmul__(self, e):
+        e = as_c128(e, self.shape[1])
+        out = np.empty(self.shape[0], dtype=np.complex128)
+        check(_lib.lib().hadr_transfer(self.fine_shape[0], self.fine_shape[1], 1, cbuf(e), cbuf(out), 0))
+        return out
+
+    def tocsr(self) -> sp.csr_matrix:
+        def p1(nf):
+            nc = (nf - 1) // 2 + 1
+            r, c, v = [], [], []
+            for i in range(nf):
+                if i % 2 == 0:
+                    r.append(i), c.append(i // 2), v.append(1.0)
+                else:
+                    r += [i, i]
+                    c += [i // 2, i // 2 + 1]
+                    v += [0.5, 0.5]
+            return sp.csr_matrix((v, (r, c)), shape=(nf, nc))
+
+        P = sp.kron(p1(self.fine_shape[0]), p1(self.fine_shape[1])).tocsr()
+        P.sort_indices()
+        return P
