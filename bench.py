@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark: amplitude solve (FGMRES(5) + multigrid K-cycle) — Mdof*iter/s.
+
+Workload (BASELINE.json configs[1]): 1025^2 grid, v = 1.5 + 2.5 x2, 12 ppw,
+source (0.5, 0.05), 20-cell layer, analytic linear-gradient tau, complex128,
+ADR upwind-blend strategy (helmadr/drivers.py:136-168), tol 1e-6, 5 levels.
+
+One step = one full amplitude solve as the reference times it
+(helmadr/drivers.py:153-165): device assembly of H2up/H1up, blend, Galerkin
+hierarchy, FGMRES to 1e-6.
+  value : inputs (medium, tau fields, transformed source) resident in HBM;
+          CUDA events on the library stream around the K steps.
+  e2e   : the public API drivers.solve_adr_upwind(...) with numpy inputs in
+          pinned host memory: host phase transform, H2D of the fields, the
+          solve, D2H of the amplitude, compose_waveform — wall clock.
+Metric: Mdof*iter/s = N * outer_iterations / t / 1e6.
+
+--impl reference: the CPU oracle (oracle/hadr_oracle.py, a restatement of
+the Python reference) on the host cores, bounded sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+HBM_FALLBACK = 6650.0
+B_OP_2D_UPWIND_C128 = 7726.0   # algorithmic bytes / dof / outer iteration
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+        return ws, rank, local, dist
+    return 1, 0, local, None
+
+
+def max_over_ranks(x, dist):
+    if dist is None:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, dist):
+    if dist is None:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        try:
+            self.f.flush()
+            rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        sm = [float(r[1]) for r in rows if len(r) >= 9]
+        mx = max([float(r[2]) for r in rows if len(r) >= 9] or [0.0])
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) >= 9:
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def pinned(a):
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    return t.pin_memory().numpy()
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def run_ours(args, ws, rank, local, dist):
+    import ctypes as C
+
+    import torch
+
+    os.environ["HADR_DEVICE"] = str(local)
+    torch.cuda.set_device(local)
+    import paper_1712_06091_b200 as H
+    from paper_1712_06091_b200 import _lib, drivers, workloads
+    from paper_1712_06091_b200.fields import point_source
+    from paper_1712_06091_b200.operators import rhs_transform
+
+    L = _lib.lib()
+    wl = workloads.by_name(args.workload, args.n)
+    g = wl.grid
+    n1, n2 = g.shape
+    N = n1 * n2
+    cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=args.tol, max_iter=args.maxiter)
+    qhat = rhs_transform(point_source(g, wl.source), wl.tt, wl.omega, "to_adr").reshape(-1)
+    codes = np.array([0 if k == "neumann" else 1 for k in wl.bc], dtype=np.int32)
+    # ---- device-resident inputs ----
+    dev = torch.device("cuda", local)
+    fields = [torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
+              for x in (wl.medium.kappa_sq, wl.medium.gamma, wl.tt.grad1, wl.tt.grad2, wl.tt.lap)]
+    q_d = torch.from_numpy(qhat).to(dev)
+    a_d = torch.empty(N, dtype=torch.complex128, device=dev)
+    torch.cuda.synchronize()
+    rep = _lib.HadrReport()
+    cap = cfg.max_iter + 2
+    hist = np.zeros(cap)
+    tset = C.c_double()
+
+    def step_device():
+        _lib.check(L.hadr_solve_adr_upwind(
+            n1, n2, float(g.h1), float(g.h2), float(wl.omega), _lib.cbuf(codes), wl.source.i1, wl.source.i2,
+            *[C.c_void_p(f.data_ptr()) for f in fields], C.c_void_p(q_d.data_ptr()), float(cfg.beta),
+            int(cfg.levels), int(cfg.restart), int(cfg.max_iter), float(cfg.tol), C.c_void_p(a_d.data_ptr()),
+            C.byref(rep), _lib.cbuf(hist), cap, C.byref(tset), 1))
+        return rep.iterations, tset.value, rep.device_time
+
+    for _ in range(args.warmup):
+        step_device()
+    its_list, t_setup, t_kry = [], [], []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n_launch0 = L.hadr_launch_count()
+    with Clocks(local) as clk:
+        L.hadr_stream_timer(1)
+        for _ in range(args.steps):
+            its, ts, tk = step_device()
+            its_list.append(its)
+            t_setup.append(ts)
+            t_kry.append(tk)
+        t_dev = L.hadr_stream_timer(0) * 1e-3
+    torch.cuda.synchronize()
+    launches = L.hadr_launch_count() - n_launch0
+    if dist:
+        dist.barrier()
+    t_max = max_over_ranks(t_dev, dist)
+    mdof_its = sum_over_ranks(N * sum(its_list) / 1e6, dist)
+    value = mdof_its / t_max
+    a_dev = a_d.cpu().numpy()
+
+    # ---- e2e through the public API (host numpy inputs, pinned) ----
+    med = type(wl.medium)(g, pinned(wl.medium.kappa_sq), pinned(wl.medium.gamma))
+    tt = wl.tt
+    tt_p = type(tt)(g, tt.tau1, pinned(tt.tau), pinned(tt.grad1), pinned(tt.grad2), pinned(tt.lap), tt.base)
+    e2e_its = 0
+    u = a = None
+    for _ in range(max(1, min(args.warmup, 2))):
+        drivers.solve_adr_upwind(med, g, wl.source, tt_p, cfg, wl.bc)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        u, a, r = drivers.solve_adr_upwind(med, g, wl.source, tt_p, cfg, wl.bc)
+        e2e_its += r.iterations
+    t_e2e = max_over_ranks(time.perf_counter() - t0, dist)
+    e2e_value = sum_over_ranks(N * e2e_its / 1e6, dist) / t_e2e
+    h2d = 5 * 8 * N  # kappa^2, gamma, grad1, grad2, lap(tau)  (+ qhat below)
+    h2d += 16 * N
+    d2h = 16 * N
+    agree = float(np.linalg.norm(a.reshape(-1) - a_dev) / np.linalg.norm(a_dev))
+
+    # ---- dominant-kernel roofline: fine-level relaxation stencil (K1), live CUDA events ----
+    roof = kernel_roofline(H, L, wl, cfg, args)
+    hbm, src = peaks()
+    its_mean = sum(its_list) / len(its_list)
+    solve_bw = B_OP_2D_UPWIND_C128 * N * its_mean / (sum(t_kry) / len(t_kry)) / 1e9
+    out = {
+        "metric": "amplitude solve Mdof*iter/s (FGMRES(5) + K-cycle, ADR upwind blend)",
+        "value": value,
+        "unit": "Mdof*iter/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128",
+        "data": "synthetic (seeded config builder: linear-gradient velocity, analytic tau)",
+        "config": {"workload": f"{wl.name} (BASELINE configs[1], 2D 1025x1025, c128)", "grid": [n1, n2],
+                   "strategy": "adr_upwind_blend", "tol": args.tol, "restart": 5, "levels": 5,
+                   "outer_iterations": its_list, "t_setup_ms": [x * 1e3 for x in t_setup],
+                   "t_krylov_ms": [x * 1e3 for x in t_kry], "parallelism": f"replicas x{ws}",
+                   "l2": "working set (~1.3 GB) > 126 MB L2; no flush needed"},
+        "e2e": {"value": e2e_value, "unit": "Mdof*iter/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": t_e2e / args.steps * 1e3, "rel_l2_vs_device_path": agree},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "solve_roofline": {"bound": "hbm", "model_bytes_per_dof_iter": B_OP_2D_UPWIND_C128,
+                           "achieved": solve_bw, "peak": hbm, "unit": "GB/s", "frac": solve_bw / hbm,
+                           "peak_source": src, "note": "B_op (SURVEY.md §8(d)) over the FGMRES time"},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(wl, args, sample_its=args.cpu_its, threads_one=True)
+    return out
+
+
+def kernel_roofline(H, L, wl, cfg, args):
+    """Time the fine-level stencil apply of the K-cycle (the most frequent full-grid
+    sweep) with CUDA events on the library stream and compare its algorithmic bytes."""
+    import ctypes as C
+
+    from paper_1712_06091_b200 import _lib, operators
+    from paper_1712_06091_b200.operators import blend_operator
+
+    g = wl.grid
+    H2 = operators.assemble_adr(wl.medium, g, wl.omega, wl.tt, "upwind2", wl.bc)
+    H1 = operators.assemble_adr(wl.medium, g, wl.omega, wl.tt, "upwind1", wl.bc)
+    B = blend_operator(H2, H1, 0.25)
+    N = g.n_nodes
+    import torch
+
+    x = torch.randn(N, dtype=torch.complex128, device="cuda")
+    y = torch.empty_like(x)
+    torch.cuda.synchronize()
+    reps = 50
+    for _ in range(5):
+        L.hadr_op_apply(B.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), 1)
+    L.hadr_stream_timer(1)
+    for _ in range(reps):
+        L.hadr_op_apply(B.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), 1)
+    ms = L.hadr_stream_timer(0) / reps
+    nnz = B.nnz
+    planes = len(B.offsets)
+    alg = (nnz + 2 * N) * 16  # coefficients (non-zeros) + x read + y write
+    moved = (planes * N + 2 * N) * 16
+    hbm, src = peaks()
+    ach = alg / (ms * 1e-3) / 1e9
+    return {"kernel": "k_stencil (fine level, blend operator, y = A x)", "bound": "hbm", "achieved": ach,
+            "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None, "peak_source": src,
+            "algorithmic_bytes_per_launch": alg, "layout_bytes_per_launch": moved,
+            "avg_launch_ms": ms, "note": "host API sync per launch included in the event window"}
+
+
+# --------------------------------------------------------------------------
+# CPU oracle (baseline / reference arm)
+# --------------------------------------------------------------------------
+def _oracle_step(wl, its, tol):
+    from oracle import hadr_oracle as O
+
+    g = wl.grid
+    p = O.Problem(g.n1, g.n2, g.h1, g.h2, wl.omega, (wl.source.i1, wl.source.i2), wl.medium.kappa_sq,
+                  wl.medium.gamma, wl.tt.tau, wl.tt.grad1, wl.tt.grad2, wl.tt.lap, wl.bc)
+    t0 = time.perf_counter()
+    u, a, rep = O.solve_upwind(p, tol=tol, maxiter=its)
+    return time.perf_counter() - t0, rep.iterations
+
+
+def cpu_baseline(wl, args, sample_its, threads_one):
+    """The oracle (numpy/scipy restatement of the reference) on this host: one
+    bounded sample = assembly + hierarchy + `sample_its` outer iterations."""
+    from threadpoolctl import threadpool_limits
+
+    if threads_one:
+        with threadpool_limits(1):
+            t, its = _oracle_step(wl, sample_its, args.tol)
+    else:
+        t, its = _oracle_step(wl, sample_its, args.tol)
+    N = wl.grid.n_nodes
+    return {"value": N * its / t / 1e6, "unit": "Mdof*iter/s", "cores": 1, "kind": "port",
+            "sample": f"oracle solve_upwind on {wl.name}: assembly + hierarchy + {its} outer FGMRES iterations "
+                      f"({t:.1f} s); host cpu_count={os.cpu_count()}, scipy sparse kernels single-threaded"}
+
+
+def run_reference(args, ws, rank, local, dist):
+    if rank != 0:
+        return None
+    from paper_1712_06091_b200 import workloads
+
+    wl = workloads.by_name(args.workload, args.n)
+    N = wl.grid.n_nodes
+    for _ in range(args.warmup):
+        _oracle_step(wl, 1, args.tol)
+    tot_t, tot_its = 0.0, 0
+    for _ in range(args.steps):
+        t, its = _oracle_step(wl, args.ref_its, args.tol)
+        tot_t += t
+        tot_its += its
+    value = N * tot_its / tot_t / 1e6
+    cores = os.cpu_count()
+    return {
+        "impl": "reference",
+        "metric": "amplitude solve Mdof*iter/s (FGMRES(5) + K-cycle, ADR upwind blend)",
+        "value": value,
+        "unit": "Mdof*iter/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": tot_t / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128",
+        "data": "synthetic (seeded config builder)",
+        "config": {"workload": f"{wl.name} (BASELINE configs[1])", "grid": list(wl.grid.shape),
+                   "strategy": "adr_upwind_blend", "tol": args.tol},
+        "cpu_baseline": {"value": value, "unit": "Mdof*iter/s", "cores": cores, "kind": "port",
+                         "sample": f"per step: oracle assembly + hierarchy + {args.ref_its} outer iterations "
+                                   f"(all BLAS threads; scipy sparse kernels single-threaded)"},
+        "e2e": {"value": value, "unit": "Mdof*iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--n", type=int, default=None, help="override grid size (parity/debug)")
+    ap.add_argument("--tol", type=float, default=1e-6)
+    ap.add_argument("--maxiter", type=int, default=1000)
+    ap.add_argument("--cpu-its", type=int, default=6, help="outer iterations in the cpu_baseline sample")
+    ap.add_argument("--ref-its", type=int, default=4, help="outer iterations per reference-arm step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local, dist = dist_init()
+    if args.impl == "reference":
+        out = run_reference(args, ws, rank, local, dist)
+    else:
+        out = run_ours(args, ws, rank, local, dist)
+    if rank == 0 and out is not None:
+        print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -77,6 +77,24 @@ int hadr_op_add_diag(hadr_op A, double sr, double si, const double* field, hadr_
 int hadr_op_similarity(hadr_op A, const double* left, const double* right, hadr_op* out);
 /* P^T A P for bilinear P (helmadr/multigrid.py:49-55 galerkin_coarsen) */
 int hadr_op_galerkin(hadr_op A, hadr_op* out);
+/* On-device assembly (helmadr/operators.py:190-234): scheme 0 central, 1 upwind1, 2 upwind2 ADR
+ * (assemble_adr), 3 Helmholtz (assemble_helmholtz; grad/lap ignored).  bc = (top, bottom, left,
+ * right), 0 neumann / 1 sommerfeld.  src = node of the point source (near-source central
+ * stencil), (-1, -1) for none.  Fields are host arrays of n1*n2 doubles. */
+int hadr_assemble(int n1, int n2, double h1, double h2, double omega, int scheme, const int* bc, int src1, int src2,
+                  const double* kappa_sq, const double* gamma, const double* grad1, const double* grad2,
+                  const double* lap_tau, int on_device, hadr_op* out);
+/* solve_adr_upwind (helmadr/drivers.py:136-168) minus the host-side phase transforms:
+ * assemble H2up, H1up, blend (1-beta)H2up + beta H1up, build the hierarchy, FGMRES on H2up
+ * with the K-cycle on the blend.  qhat is the transformed source (to_adr).  *t_setup gets the
+ * device time of assembly + hierarchy; rep->device_time the FGMRES time. */
+int hadr_solve_adr_upwind(int n1, int n2, double h1, double h2, double omega, const int* bc, int src1, int src2,
+                          const double* kappa_sq, const double* gamma, const double* grad1, const double* grad2,
+                          const double* lap_tau, const double* qhat, double beta, int levels, int restart,
+                          int maxiter, double tol, double* a_out, hadr_report* rep, double* history, int history_cap,
+                          double* t_setup, int on_device);
+/* release recycled hierarchies and cached device blocks */
+int hadr_pool_trim(void);
 void hadr_op_destroy(hadr_op op);
 
 /* ---- transfer operators (helmadr/multigrid.py:19-46) ---- */
@@ -101,6 +119,9 @@ int hadr_precond_apply(hadr_hier h, const double* r, double* z, int on_device);
 void hadr_hier_destroy(hadr_hier h);
 /* number of kernels this library has launched so far (graph launches add their kernel nodes) */
 long long hadr_launch_count(void);
+/* CUDA-event timer on the library stream: start=1 records the start event (returns 0);
+ * start=0 records the stop event, waits for it and returns the elapsed milliseconds (-1 on error) */
+double hadr_stream_timer(int start);
 
 /* ---- Krylov (helmadr/krylov.py) ---- */
 /* _gmres_relax_pre / gmres_relax (helmadr/krylov.py:82-119) */

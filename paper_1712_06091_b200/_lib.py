@@ -24,7 +24,8 @@ EXPORTS = (
     "hadr_op_jacobi", "hadr_op_axpby", "hadr_op_add_diag", "hadr_op_similarity", "hadr_op_galerkin",
     "hadr_op_destroy", "hadr_transfer", "hadr_hier_create", "hadr_hier_from_ops", "hadr_hier_info",
     "hadr_hier_level_op", "hadr_kcycle", "hadr_precond_apply", "hadr_hier_destroy", "hadr_gmres_relax",
-    "hadr_fgmres", "hadr_launch_count",
+    "hadr_fgmres", "hadr_launch_count", "hadr_assemble", "hadr_solve_adr_upwind", "hadr_pool_trim",
+    "hadr_stream_timer",
 )
 
 
@@ -60,6 +61,11 @@ _SIGS = {
     "hadr_op_similarity": (_i, [_vp, _vp, _vp, C.POINTER(_vp)]),
     "hadr_op_galerkin": (_i, [_vp, C.POINTER(_vp)]),
     "hadr_op_destroy": (None, [_vp]),
+    "hadr_assemble": (_i, [_i, _i, _d, _d, _d, _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, C.POINTER(_vp)]),
+    "hadr_solve_adr_upwind": (_i, [_i, _i, _d, _d, _d, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _d, _i, _i, _i,
+                                   _d, _vp, C.POINTER(HadrReport), _vp, _i, C.POINTER(_d), _i]),
+    "hadr_pool_trim": (_i, []),
+    "hadr_stream_timer": (_d, [_i]),
     "hadr_transfer": (_i, [_i, _i, _i, _vp, _vp, _i]),
     "hadr_hier_create": (_i, [_vp, _i, _i, _d, C.POINTER(_vp)]),
     "hadr_hier_from_ops": (_i, [_i, _vp, _i, _d, C.POINTER(_vp)]),

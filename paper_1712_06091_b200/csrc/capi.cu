@@ -174,6 +174,77 @@ int hadr_op_galerkin(hadr_op A, hadr_op* out) {
   return guarded([&] { *out = wrap(op_galerkin(*A->op)); });
 }
 
+int hadr_assemble(int n1, int n2, double h1, double h2, double omega, int scheme, const int* bc, int src1, int src2,
+                  const double* kappa_sq, const double* gamma, const double* grad1, const double* grad2,
+                  const double* lap_tau, int on_device, hadr_op* out) {
+  return guarded([&] {
+    *out = wrap(op_assemble(n1, n2, h1, h2, omega, scheme, bc, src1, src2, kappa_sq, gamma, grad1, grad2, lap_tau,
+                            on_device != 0));
+  });
+}
+
+int hadr_solve_adr_upwind(int n1, int n2, double h1, double h2, double omega, const int* bc, int src1, int src2,
+                          const double* kappa_sq, const double* gamma, const double* grad1, const double* grad2,
+                          const double* lap_tau, const double* qhat, double beta, int levels, int restart,
+                          int maxiter, double tol, double* a_out, hadr_report* rep, double* history, int history_cap,
+                          double* t_setup, int on_device) {
+  return guarded([&] {
+    Ctx& c = Ctx::get();
+    const long N = (long)n1 * n2;
+    cudaEvent_t e0, e1;
+    HADR_CUDA(cudaEventCreate(&e0));
+    HADR_CUDA(cudaEventCreate(&e1));
+    HADR_CUDA(cudaEventRecord(e0, c.stream));
+    // helmadr/drivers.py:153-157: assemble H2up, H1up, blend, hierarchy
+    Op* H2 = op_assemble(n1, n2, h1, h2, omega, 2, bc, src1, src2, kappa_sq, gamma, grad1, grad2, lap_tau, on_device);
+    Op* H1 = nullptr;
+    Op* B = nullptr;
+    Hier* hier = nullptr;
+    try {
+      H1 = op_assemble(n1, n2, h1, h2, omega, 1, bc, src1, src2, kappa_sq, gamma, grad1, grad2, lap_tau, on_device);
+      B = op_axpby(mk(1.0 - beta, 0.0), *H2, mk(beta, 0.0), *H1);
+      delete H1;
+      H1 = nullptr;
+      hier = hier_build(B, levels, 10, 0.1);
+      delete B;
+      B = nullptr;
+      HADR_CUDA(cudaEventRecord(e1, c.stream));
+      HADR_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      HADR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      if (t_setup) *t_setup = ms * 1e-3;
+      DevVec dq(qhat, N, on_device, true), da(a_out, N, on_device, false);
+      Report r;
+      fgmres(*H2, hier, dq.p, nullptr, da.p, restart, maxiter, tol, r);
+      da.copy_out(a_out);
+      c.sync();
+      rep->iterations = r.iterations;
+      rep->converged = r.converged;
+      rep->note = r.note;
+      rep->bnorm = r.bnorm;
+      rep->final_relres = r.final_relres;
+      rep->wall_time = r.wall_time;
+      rep->device_time = r.device_time;
+      const int nh = (int)r.history.size();
+      rep->history_len = nh;
+      if (history)
+        for (int i = 0; i < nh && i < history_cap; ++i) history[i] = r.history[i];
+    } catch (...) {
+      delete H1;
+      delete B;
+      hier_release(hier);
+      delete H2;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      throw;
+    }
+    hier_release(hier);
+    delete H2;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
 void hadr_op_destroy(hadr_op h) {
   if (!h) return;
   if (h->own) delete h->op;
@@ -275,10 +346,44 @@ int hadr_precond_apply(hadr_hier hh, const double* r, double* z, int on_device) 
 
 long long hadr_launch_count(void) { return g_launch_count; }
 
+double hadr_stream_timer(int start) {
+  static cudaEvent_t ev[2] = {nullptr, nullptr};
+  try {
+    Ctx& c = Ctx::get();
+    if (!ev[0]) {
+      HADR_CUDA(cudaEventCreate(&ev[0]));
+      HADR_CUDA(cudaEventCreate(&ev[1]));
+    }
+    if (start) {
+      HADR_CUDA(cudaEventRecord(ev[0], c.stream));
+      return 0.0;
+    }
+    HADR_CUDA(cudaEventRecord(ev[1], c.stream));
+    HADR_CUDA(cudaEventSynchronize(ev[1]));
+    float ms = 0.f;
+    HADR_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    return ms;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
+}
+
 void hadr_hier_destroy(hadr_hier h) {
   if (!h) return;
-  delete h->h;
+  hier_release(h->h);
   delete h;
+}
+
+int hadr_pool_trim(void) {
+  return guarded([&] {
+    for (;;) {  // drop recycled hierarchies, then cached blocks
+      Hier* h = hier_pool_pop();
+      if (!h) break;
+      delete h;
+    }
+    pool_trim();
+  });
 }
 
 int hadr_gmres_relax(hadr_op A, const double* b, const double* x, int steps, double* x_out, int on_device) {

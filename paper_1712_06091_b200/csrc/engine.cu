@@ -12,6 +12,56 @@
 namespace hadr {
 
 // ---------------------------------------------------------------------------
+// caching allocator
+// ---------------------------------------------------------------------------
+static std::map<void*, size_t>& live_blocks() {
+  static std::map<void*, size_t> m;
+  return m;
+}
+static std::multimap<size_t, void*>& free_blocks() {
+  static std::multimap<size_t, void*> m;
+  return m;
+}
+
+void* pool_alloc(size_t bytes) {
+  bytes = (bytes + 511) & ~size_t(511);
+  auto& fb = free_blocks();
+  auto it = fb.find(bytes);
+  void* p = nullptr;
+  if (it != fb.end()) {
+    p = it->second;
+    fb.erase(it);
+  } else {
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {  // out of memory: drop the cache and retry once
+      cudaGetLastError();
+      pool_trim();
+      HADR_CUDA(cudaMalloc(&p, bytes));
+    }
+  }
+  live_blocks()[p] = bytes;
+  return p;
+}
+
+void pool_free(void* p) {
+  auto& lb = live_blocks();
+  auto it = lb.find(p);
+  if (it == lb.end()) return;
+  free_blocks().emplace(it->second, p);
+  lb.erase(it);
+}
+
+size_t pool_trim() {
+  size_t n = 0;
+  for (auto& kv : free_blocks()) {
+    cudaFree(kv.second);
+    n += kv.first;
+  }
+  free_blocks().clear();
+  return n;
+}
+
+// ---------------------------------------------------------------------------
 // context
 // ---------------------------------------------------------------------------
 Ctx& Ctx::get() {
@@ -78,6 +128,39 @@ const cplx* Op::inv_diag() {
     throw ValueError("hierarchy operator has zero diagonal entries");
   }
   return dinv;
+}
+
+void Op::refresh_inv_diag() {
+  if (!dinv) {
+    inv_diag();
+    return;
+  }
+  Ctx& c = Ctx::get();
+  const int ce = center();
+  int* flag = (int*)c.dscal + 32;
+  HADR_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), c.stream));
+  launch_inv_diag(c.stream, N, ce >= 0 ? coef + (long)ce * N : nullptr, dinv, flag);
+  int hflag = 0;
+  HADR_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  if (hflag || ce < 0) throw ValueError("hierarchy operator has zero diagonal entries");
+}
+
+Op* op_copy(const Op& A) {
+  Ctx& c = Ctx::get();
+  Op* op = new Op();
+  op->n1 = A.n1;
+  op->n2 = A.n2;
+  op->N = A.N;
+  op->nofs = A.nofs;
+  for (int o = 0; o < A.nofs; ++o) {
+    op->d1[o] = A.d1[o];
+    op->d2[o] = A.d2[o];
+  }
+  op->coef = dalloc<cplx>((size_t)A.nofs * A.N);
+  HADR_CUDA(cudaMemcpyAsync(op->coef, A.coef, (size_t)A.nofs * A.N * sizeof(cplx), cudaMemcpyDeviceToDevice,
+                            c.stream));
+  return op;
 }
 
 static void set_offsets_from_mask(Op* op, unsigned mask, int* slot_of /*25*/) {
@@ -248,30 +331,103 @@ Op* op_similarity(const Op& A, const cplx* left_host, const cplx* right_host) {
   return op;
 }
 
-Op* op_galerkin(const Op& A) {
-  if ((A.n1 - 1) % 2 || (A.n2 - 1) % 2) throw ValueError("cannot coarsen: interval count is odd");
+static unsigned galerkin_mask(const Op& A) {
   Ctx& c = Ctx::get();
   const int n1c = (A.n1 - 1) / 2 + 1, n2c = (A.n2 - 1) / 2 + 1;
-  unsigned* dmask = dalloc<unsigned>(1);
-  int* dslot = dalloc<int>(25);
+  unsigned* dmask = (unsigned*)(c.dscal + 40);
   HADR_CUDA(cudaMemsetAsync(dmask, 0, sizeof(unsigned), c.stream));
   launch_galerkin(c.stream, A.dev(), n1c, n2c, dmask, nullptr, nullptr);
   unsigned hm = 0;
   HADR_CUDA(cudaMemcpyAsync(&hm, dmask, sizeof(unsigned), cudaMemcpyDeviceToHost, c.stream));
   c.sync();
-  Op* op = new Op();
-  op->n1 = n1c;
-  op->n2 = n2c;
-  op->N = (long)n1c * n2c;
+  return hm | (1u << 12);  // the diagonal is always kept
+}
+
+static unsigned layout_mask(const Op& A) {
+  unsigned m = 0;
+  for (int o = 0; o < A.nofs; ++o) m |= 1u << ((A.d1[o] + 2) * 5 + A.d2[o] + 2);
+  return m;
+}
+
+static void galerkin_write(const Op& A, Op& C) {  // C's offsets define the planes
+  Ctx& c = Ctx::get();
   int slot[25];
-  set_offsets_from_mask(op, hm | (1u << 12), slot);
+  for (int q = 0; q < 25; ++q) slot[q] = -1;
+  for (int o = 0; o < C.nofs; ++o) slot[(C.d1[o] + 2) * 5 + C.d2[o] + 2] = o;
+  int* dslot = (int*)(c.dscal + 48);
   HADR_CUDA(cudaMemcpyAsync(dslot, slot, sizeof(slot), cudaMemcpyHostToDevice, c.stream));
+  launch_galerkin(c.stream, A.dev(), C.n1, C.n2, nullptr, dslot, C.coef);
+  HADR_CUDA(cudaGetLastError());
+  c.sync();  // slot table lives in shared scratch
+}
+
+Op* op_galerkin(const Op& A) {
+  if ((A.n1 - 1) % 2 || (A.n2 - 1) % 2) throw ValueError("cannot coarsen: interval count is odd");
+  const unsigned hm = galerkin_mask(A);
+  Op* op = new Op();
+  op->n1 = (A.n1 - 1) / 2 + 1;
+  op->n2 = (A.n2 - 1) / 2 + 1;
+  op->N = (long)op->n1 * op->n2;
+  int slot[25];
+  set_offsets_from_mask(op, hm, slot);
   op->coef = dalloc<cplx>((size_t)op->nofs * op->N);
-  launch_galerkin(c.stream, A.dev(), n1c, n2c, nullptr, dslot, op->coef);
+  galerkin_write(A, *op);
+  return op;
+}
+
+Op* op_assemble(int n1, int n2, double h1, double h2, double omega, int scheme, const int* bc, int src1, int src2,
+                const double* ksq, const double* gam, const double* g1, const double* g2, const double* lap,
+                bool fields_on_device) {
+  if (n1 < 5 || n2 < 5) throw ValueError("grid needs at least 5 nodes per dimension");
+  if (scheme < 0 || scheme > 3) throw ValueError("scheme must be central/upwind1/upwind2/helmholtz");
+  Ctx& c = Ctx::get();
+  const long N = (long)n1 * n2;
+  const int nf = scheme == 3 ? 2 : 5;
+  const double* src[5] = {ksq, gam, g1, g2, lap};
+  const double* fld[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  double* df = nullptr;
+  if (fields_on_device) {
+    for (int i = 0; i < nf; ++i) fld[i] = src[i];
+  } else {
+    df = dalloc<double>(nf * N);
+    for (int i = 0; i < nf; ++i) {
+      HADR_CUDA(cudaMemcpyAsync(df + i * N, src[i], N * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+      fld[i] = df + i * N;
+    }
+  }
+  cplx* c9 = dalloc<cplx>(9 * N);
+  unsigned* dmask = dalloc<unsigned>(1);
+  HADR_CUDA(cudaMemsetAsync(dmask, 0, sizeof(unsigned), c.stream));
+  launch_assemble(c.stream, n1, n2, h1, h2, omega, scheme, bc, src1, src2, fld[0], fld[1], fld[2], fld[3], fld[4], c9,
+                  dmask);
+  unsigned hm = 0;
+  HADR_CUDA(cudaMemcpyAsync(&hm, dmask, sizeof(unsigned), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  static const int d9[9][2] = {{-2, 0}, {-1, 0}, {0, -2}, {0, -1}, {0, 0}, {0, 1}, {0, 2}, {1, 0}, {2, 0}};
+  hm |= 1u << 4;  // keep the centre plane
+  Op* op = new Op();
+  op->n1 = n1;
+  op->n2 = n2;
+  op->N = N;
+  int dst[9];
+  int used[9], nu = 0;
+  for (int q = 0; q < 9; ++q)
+    if (hm & (1u << q)) {
+      op->d1[nu] = (int8_t)d9[q][0];
+      op->d2[nu] = (int8_t)d9[q][1];
+      used[nu++] = q;
+    }
+  op->nofs = nu;
+  op->coef = dalloc<cplx>((size_t)nu * N);
+  for (int o = 0; o < nu; ++o)
+    HADR_CUDA(cudaMemcpyAsync(op->coef + (long)o * N, c9 + (long)used[o] * N, N * sizeof(cplx),
+                              cudaMemcpyDeviceToDevice, c.stream));
+  (void)dst;
   HADR_CUDA(cudaGetLastError());
   c.sync();
+  dfree(df);
+  dfree(c9);
   dfree(dmask);
-  dfree(dslot);
   return op;
 }
 
@@ -355,16 +511,72 @@ void Hier::alloc_workspace() {
   HADR_CUDA(cudaMemset(visits, 0, (nl + 1) * sizeof(int)));
 }
 
+static std::vector<Hier*>& hier_pool() {
+  static std::vector<Hier*> p;
+  return p;
+}
+
+Hier* hier_pool_pop() {
+  auto& pool = hier_pool();
+  if (pool.empty()) return nullptr;
+  Hier* h = pool.back();
+  pool.pop_back();
+  return h;
+}
+
+void hier_release(Hier* h) {
+  if (!h) return;
+  auto& pool = hier_pool();
+  if (h->poolable && pool.size() < 4) {
+    pool.push_back(h);
+    return;
+  }
+  delete h;
+}
+
+// Refresh a recycled hierarchy in place: same shapes and offset layouts, so the
+// captured K-cycle graphs (which reference its buffers) stay valid.
+static bool hier_refresh(Hier* h, const Op& fine) {
+  Ctx& c = Ctx::get();
+  Op& L0 = *h->lv[0].A;
+  if (L0.n1 != fine.n1 || L0.n2 != fine.n2 || layout_mask(L0) != layout_mask(fine)) return false;
+  HADR_CUDA(cudaMemcpyAsync(L0.coef, fine.coef, (size_t)fine.nofs * fine.N * sizeof(cplx), cudaMemcpyDeviceToDevice,
+                            c.stream));
+  for (size_t l = 1; l < h->lv.size(); ++l) {
+    Op& F = *h->lv[l - 1].A;
+    Op& C = *h->lv[l].A;
+    if (galerkin_mask(F) != layout_mask(C)) return false;
+    galerkin_write(F, C);
+  }
+  for (auto& L : h->lv) L.A->refresh_inv_diag();
+  return true;
+}
+
 Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol) {
   auto shapes = coarsenable_levels(fine->n1, fine->n2, max_levels);
   if (shapes.size() < 2)
     throw ValueError("grid cannot support two multigrid levels ((n_d - 1) must be even with at least 3 coarse nodes)");
+  auto& pool = hier_pool();
+  for (size_t i = 0; i < pool.size(); ++i) {
+    Hier* h = pool[i];
+    if (h->lv.size() != shapes.size() || h->coarse_steps != coarse_steps || h->coarse_tol != coarse_tol) continue;
+    bool same = true;
+    for (size_t l = 0; l < shapes.size(); ++l)
+      same = same && h->lv[l].n1 == shapes[l].first && h->lv[l].n2 == shapes[l].second;
+    if (!same) continue;
+    pool.erase(pool.begin() + i);
+    if (hier_refresh(h, *fine)) return h;
+    delete h;  // layout changed: rebuild from scratch
+    break;
+  }
   Hier* h = new Hier();
   h->coarse_steps = coarse_steps;
   h->coarse_tol = coarse_tol;
+  h->poolable = true;
   try {
     Level L0;
-    L0.A = fine;
+    L0.A = op_copy(*fine);  // own a copy: the graphs then never depend on the caller's buffers
+    L0.own = true;
     h->lv.push_back(L0);
     for (size_t i = 1; i < shapes.size(); ++i) {
       Level L;

@@ -35,15 +35,17 @@ struct Ctx {
   void sync() { HADR_CUDA(cudaStreamSynchronize(stream)); }
 };
 
+// Caching device allocator (exact-size free lists): repeated solves of one
+// configuration reuse their buffers instead of cudaMalloc/cudaFree per solve.
+void* pool_alloc(size_t bytes);
+void pool_free(void* p);
+size_t pool_trim();  // release cached blocks; returns bytes freed
 template <class T>
 T* dalloc(size_t n) {
-  void* p = nullptr;
-  if (n == 0) n = 1;
-  HADR_CUDA(cudaMalloc(&p, n * sizeof(T)));
-  return (T*)p;
+  return (T*)pool_alloc((n == 0 ? 1 : n) * sizeof(T));
 }
 inline void dfree(void* p) {
-  if (p) cudaFree(p);
+  if (p) pool_free(p);
 }
 
 // Structured 2D operator (owns its coefficient planes).
@@ -58,7 +60,9 @@ struct Op {
   StencilDev dev() const;
   int center() const;
   const cplx* inv_diag();  // computes on first use; throws ValueError on a zero diagonal
+  void refresh_inv_diag();  // recompute into the existing buffer (coefficients changed)
 };
+Op* op_copy(const Op& A);
 
 Op* op_from_csr(int n1, int n2, long nnz, const int64_t* indptr, const int32_t* indices, const cplx* data);
 Op* op_from_planes(int n1, int n2, int nofs, const int* offsets, const cplx* coef_host);
@@ -66,6 +70,10 @@ Op* op_axpby(cplx alpha, const Op& A, cplx beta, const Op& B);       // alpha*A 
 Op* op_add_diag_real(const Op& A, cplx sc, const double* field_host);  // A + diag(sc*field)
 Op* op_similarity(const Op& A, const cplx* left_host, const cplx* right_host);
 Op* op_galerkin(const Op& A);                                          // P^T A P
+// ADR (scheme 0 central, 1 upwind1, 2 upwind2) or Helmholtz (scheme 3) operator, fields host (n1*n2)
+Op* op_assemble(int n1, int n2, double h1, double h2, double omega, int scheme, const int* bc, int src1, int src2,
+                const double* ksq, const double* gam, const double* g1, const double* g2, const double* lap,
+                bool fields_on_device = false);
 void op_apply(const Op& A, const cplx* x, cplx* y);                    // device pointers, async
 
 struct Level {
@@ -88,6 +96,7 @@ struct Level {
 
 struct Hier {
   std::vector<Level> lv;
+  bool poolable = false;     // owns copies of every level operator: may be recycled
   int coarse_steps = 10;
   double coarse_tol = 0.1;
   int* kact = nullptr;      // device: K-cycle-active flag per level
@@ -106,6 +115,8 @@ struct Hier {
 };
 
 Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol);
+void hier_release(Hier* h);  // recycle (workspace + captured graphs) or delete
+Hier* hier_pool_pop();       // take one recycled hierarchy (or null)
 Hier* hier_from_ops(int nlev, Op** ops, int coarse_steps, double coarse_tol);
 std::vector<std::pair<int, int>> coarsenable_levels(int n1, int n2, int max_levels);
 

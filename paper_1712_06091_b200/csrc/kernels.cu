@@ -758,3 +758,168 @@ void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, uns
 }
 
 }  // namespace hadr
+
+namespace hadr {
+
+// ---------------------------------------------------------------------------
+// On-device assembly of the ADR / Helmholtz operators (helmadr/operators.py:85-234)
+// into the 9 plus-radius-2 planes, ordered (d1, d2) ascending:
+//   0:(-2,0) 1:(-1,0) 2:(0,-2) 3:(0,-1) 4:(0,0) 5:(0,1) 6:(0,2) 7:(1,0) 8:(2,0)
+// Each term is formed with the reference's numpy expression semantics; the
+// duplicates of a row are summed in the order the reference appends them.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int p9(int ax, int d) {  // plane of offset d along axis ax
+  if (d == 0) return 4;
+  if (ax == 0) return d == -2 ? 0 : d == -1 ? 1 : d == 1 ? 7 : 8;
+  return d == -2 ? 2 : d == -1 ? 3 : d == 1 ? 5 : 6;
+}
+
+// complex scalar (python complex) times real array element, numpy complex multiply
+__device__ __forceinline__ cplx cs_times_real(cplx s, double v) { return cmul_np(s, mk(v, 0.0)); }
+// complex / real, numpy Smith division by (d, 0)
+__device__ __forceinline__ cplx cdiv_real(cplx a, double d) { return cdiv_np(a, mk(d, 0.0)); }
+
+struct AsmArgs {
+  int n1, n2;
+  double h1, h2, omega;
+  int scheme;       // 0 central, 1 upwind1, 2 upwind2, 3 helmholtz
+  int bc[4];        // top, bottom, left, right: 0 neumann, 1 sommerfeld
+  int src1, src2;   // source node (near-source set), -1 = none
+  const double *ksq, *gam, *g1, *g2, *lap;
+  cplx* coef;       // 9 planes
+  unsigned* mask;   // OR of non-zero planes
+};
+
+__global__ void k_assemble(AsmArgs a) {
+  const long N = (long)a.n1 * a.n2;
+  unsigned m = 0u;
+  const double om = a.omega;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (long)gridDim.x * blockDim.x) {
+    const int i1 = (int)(k / a.n2), i2 = (int)(k - (long)i1 * a.n2);
+    cplx acc[9];
+    bool has[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      acc[q] = mk(0.0, 0.0);
+      has[q] = false;
+    }
+    auto put = [&](int q, cplx v) {
+      acc[q] = has[q] ? cadd(acc[q], v) : v;
+      has[q] = true;
+    };
+    const bool helm = a.scheme == 3;
+    const double gr[2] = {helm ? 0.0 : a.g1[k], helm ? 0.0 : a.g2[k]};
+    const double kap = sqrt(a.ksq[k]);
+    // ---- Laplacian + ghost-eliminated BC (helmadr/operators.py:85-120) ----
+    for (int ax = 0; ax < 2; ++ax) {
+      const double h = ax == 0 ? a.h1 : a.h2;
+      const int idx = ax == 0 ? i1 : i2, size = ax == 0 ? a.n1 : a.n2;
+      const double ih2 = 1.0 / (h * h);
+      if (idx >= 1) put(p9(ax, -1), mk(ih2, 0.0));
+      if (idx <= size - 2) put(p9(ax, 1), mk(ih2, 0.0));
+      put(4, mk(-2.0 * ih2, 0.0));
+      for (int lo = 1; lo >= 0; --lo) {
+        if (lo ? idx != 0 : idx != size - 1) continue;
+        const double nd = lo ? -gr[ax] : gr[ax];
+        const int kind = ax == 0 ? a.bc[lo ? 2 : 3] : a.bc[lo ? 0 : 1];
+        if (kind == 0) {
+          put(p9(ax, lo ? 1 : -1), mk(ih2, 0.0));
+          // 2j * omega * nd / h
+          const cplx c2 = mk(0.0 * om, 2.0 * om);
+          put(4, cdiv_real(cs_times_real(c2, nd), h));
+        } else {
+          // (1.0 + 1j * omega * h * (nd - kappa)) * ih2
+          const cplx c1 = mk(0.0 * om * h, 1.0 * om * h);
+          const cplx t = cs_times_real(c1, nd - kap);
+          const cplx u = mk(1.0 + t.x, t.y);
+          put(4, cmul_np(u, mk(ih2, 0.0)));
+        }
+      }
+    }
+    if (!helm) {
+      // ---- advection (helmadr/operators.py:123-170) ----
+      const bool near = a.src1 >= 0 && abs(i1 - a.src1) <= 1 && abs(i2 - a.src2) <= 1;
+      for (int ax = 0; ax < 2; ++ax) {
+        const double h = ax == 0 ? a.h1 : a.h2;
+        const int idx = ax == 0 ? i1 : i2, size = ax == 0 ? a.n1 : a.n2;
+        const double c = gr[ax];
+        const cplx F = cs_times_real(mk(-0.0 * om, -2.0 * om), c);  // -2j * omega * c
+        const bool inner = idx >= 1 && idx <= size - 2;
+        const bool cen = a.scheme == 0 ? inner : (inner && near);
+        if (cen) {
+          put(p9(ax, 1), cdiv_real(F, 2.0 * h));
+          put(p9(ax, -1), cdiv_real(cneg(F), 2.0 * h));
+        } else if (c != 0.0) {
+          const int sg = c > 0 ? 1 : -1;
+          const bool ok2 = sg == 1 ? idx >= 2 : idx <= size - 3;
+          const bool ok1 = sg == 1 ? idx >= 1 : idx <= size - 2;
+          if (a.scheme != 1 && ok2) {
+            put(4, cdiv_real(cs_times_real(F, sg * 3.0), 2.0 * h));
+            put(p9(ax, -sg), cdiv_real(cs_times_real(F, -sg * 4.0), 2.0 * h));
+            put(p9(ax, -2 * sg), cdiv_real(cs_times_real(F, (double)sg), 2.0 * h));
+          } else if (ok1) {
+            put(4, cdiv_real(cs_times_real(F, (double)sg), h));
+            put(p9(ax, -sg), cdiv_real(cs_times_real(F, (double)-sg), h));
+          } else {
+            put(4, cdiv_real(cs_times_real(F, (double)-sg), h));
+            put(p9(ax, sg), cdiv_real(cs_times_real(F, (double)sg), h));
+          }
+        }
+      }
+      // ---- neighbour-averaged mass term (helmadr/operators.py:173-187) ----
+      const cplx G = cs_times_real(mk(-0.0 * om, -0.25 * om), a.lap[k]);  // -0.25j * omega * lap
+      for (int ax = 0; ax < 2; ++ax) {
+        const int idx = ax == 0 ? i1 : i2, size = ax == 0 ? a.n1 : a.n2;
+        for (int sg = 1; sg >= -1; sg -= 2) {
+          const bool ins = sg == 1 ? idx <= size - 2 : idx >= 1;
+          put(ins ? p9(ax, sg) : 4, G);
+        }
+      }
+      // ---- reaction + attenuation (helmadr/operators.py:230-233) ----
+      const double gsq = gr[0] * gr[0] + gr[1] * gr[1];
+      const double react = -(om * om) * (gsq - a.ksq[k]);
+      const cplx att = cs_times_real(cs_times_real(mk(-0.0 * om, -1.0 * om), a.gam[k]), a.ksq[k]);
+      put(4, mk(react + att.x, att.y));
+    } else {
+      // omega**2 * kappa_sq - 1j * omega * gamma * kappa_sq (helmadr/operators.py:198)
+      const double w2k = (om * om) * a.ksq[k];
+      const cplx t = cs_times_real(cs_times_real(mk(0.0 * om, 1.0 * om), a.gam[k]), a.ksq[k]);
+      put(4, mk(w2k - t.x, 0.0 - t.y));
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      a.coef[(long)q * N + k] = acc[q];
+      if (acc[q].x != 0.0 || acc[q].y != 0.0) m |= 1u << q;
+    }
+  }
+  if (m) atomicOr(a.mask, m);
+}
+
+void launch_assemble(cudaStream_t s, int n1, int n2, double h1, double h2, double omega, int scheme, const int* bc,
+                     int src1, int src2, const double* ksq, const double* gam, const double* g1, const double* g2,
+                     const double* lap, cplx* coef9, unsigned* mask) {
+  ++g_launch_count;
+  AsmArgs a{};
+  a.n1 = n1;
+  a.n2 = n2;
+  a.h1 = h1;
+  a.h2 = h2;
+  a.omega = omega;
+  a.scheme = scheme;
+  for (int i = 0; i < 4; ++i) a.bc[i] = bc[i];
+  a.src1 = src1;
+  a.src2 = src2;
+  a.ksq = ksq;
+  a.gam = gam;
+  a.g1 = g1;
+  a.g2 = g2;
+  a.lap = lap;
+  a.coef = coef9;
+  a.mask = mask;
+  long N = (long)n1 * n2;
+  int blocks = (int)((N + 127) / 128);
+  if (blocks > 4096) blocks = 4096;
+  k_assemble<<<blocks, 128, 0, s>>>(a);
+}
+
+}  // namespace hadr

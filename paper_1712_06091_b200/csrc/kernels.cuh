@@ -115,6 +115,9 @@ void launch_remap_planes(cudaStream_t s, long n, const cplx* src, int nsrc, cons
                          cplx alpha, int accumulate);
 void launch_add_diag_real(cudaStream_t s, long n, cplx* center, cplx sc, const double* field);
 void launch_similarity(cudaStream_t s, const StencilDev& A, cplx* out, const cplx* left, const cplx* right);
+void launch_assemble(cudaStream_t s, int n1, int n2, double h1, double h2, double omega, int scheme, const int* bc,
+                     int src1, int src2, const double* ksq, const double* gam, const double* g1, const double* g2,
+                     const double* lap, cplx* coef9, unsigned* mask);
 void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, unsigned* mask, const int* slot_of,
                      cplx* coef_c);
 

@@ -48,7 +48,8 @@ class SolveReport:
     stage1: "SolveReport | None" = None
     stage2: "SolveReport | None" = None
     fm_time: float = 0.0
-    device_time: float = 0.0
+    device_time: float = 0.0   # CUDA-event time of the FGMRES solve
+    setup_time: float = 0.0    # CUDA-event time of assembly + hierarchy (ADR drivers)
 
     def history_csv_lines(self) -> list[str]:
         scale = self.bnorm if self.bnorm > 0 else 1.0
