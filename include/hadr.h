@@ -117,6 +117,12 @@ int hadr_kcycle(hadr_hier h, int level, const double* b, const double* x, double
 /* make_kcycle_preconditioner(hier)(r) (helmadr/multigrid.py:174-184): graph-captured K-cycle */
 int hadr_precond_apply(hadr_hier h, const double* r, double* z, int on_device);
 void hadr_hier_destroy(hadr_hier h);
+/* runtime options: "ce_max_n" = levels with at most this many points run their coarse part inside
+ * the single-cluster engine (default 32768; 0 = every operation is its own kernel) */
+int hadr_set_option(const char* name, double value);
+/* cluster-engine phase counters (enable with hadr_set_option("ce_profile", 1)): cycles seen by CTA 0
+ * [total, allreduce, n_allreduce, scalar epilogue, n_epilogue, stencil, n_stencil, launches] */
+int hadr_ce_profile(unsigned long long* out8, int reset);
 /* number of kernels this library has launched so far (graph launches add their kernel nodes) */
 long long hadr_launch_count(void);
 /* CUDA-event timer on the library stream: start=1 records the start event (returns 0);

@@ -25,7 +25,7 @@ EXPORTS = (
     "hadr_op_destroy", "hadr_transfer", "hadr_hier_create", "hadr_hier_from_ops", "hadr_hier_info",
     "hadr_hier_level_op", "hadr_kcycle", "hadr_precond_apply", "hadr_hier_destroy", "hadr_gmres_relax",
     "hadr_fgmres", "hadr_launch_count", "hadr_assemble", "hadr_solve_adr_upwind", "hadr_pool_trim",
-    "hadr_stream_timer",
+    "hadr_stream_timer", "hadr_set_option", "hadr_ce_profile",
 )
 
 
@@ -66,6 +66,8 @@ _SIGS = {
                                    _d, _vp, C.POINTER(HadrReport), _vp, _i, C.POINTER(_d), _i]),
     "hadr_pool_trim": (_i, []),
     "hadr_stream_timer": (_d, [_i]),
+    "hadr_set_option": (_i, [C.c_char_p, _d]),
+    "hadr_ce_profile": (_i, [_vp, _i]),
     "hadr_transfer": (_i, [_i, _i, _i, _vp, _vp, _i]),
     "hadr_hier_create": (_i, [_vp, _i, _i, _d, C.POINTER(_vp)]),
     "hadr_hier_from_ops": (_i, [_i, _vp, _i, _d, C.POINTER(_vp)]),
@@ -111,6 +113,11 @@ def lib():
         check(L.hadr_init(dev))
         _initialised = True
     return L
+
+
+def set_option(name: str, value: float) -> None:
+    """Runtime switches of libhadr.so, e.g. set_option("ce_max_n", 0) disables the cluster engine."""
+    check(lib().hadr_set_option(name.encode(), float(value)))
 
 
 def check(code: int) -> None:

@@ -346,6 +346,32 @@ int hadr_precond_apply(hadr_hier hh, const double* r, double* z, int on_device) 
 
 long long hadr_launch_count(void) { return g_launch_count; }
 
+int hadr_ce_profile(unsigned long long* out8, int reset) {
+  return guarded([&] {
+    Ctx::get().sync();
+    if (ce_profile_read(out8, reset)) throw std::runtime_error("ce_profile_read failed");
+  });
+}
+
+int hadr_set_option(const char* name, double value) {
+  return guarded([&] {
+    std::string n(name ? name : "");
+    if (n == "ce_profile") {
+      g_ce_prof_on = value != 0.0;
+    } else if (n == "ce_max_n") {
+      g_ce_max_n = (long)value;
+      // recycled hierarchies hold graphs captured under the old setting
+      for (;;) {
+        Hier* h = hier_pool_pop();
+        if (!h) break;
+        delete h;
+      }
+    } else {
+      throw ValueError("unknown option " + n);
+    }
+  });
+}
+
 double hadr_stream_timer(int start) {
   static cudaEvent_t ev[2] = {nullptr, nullptr};
   try {

@@ -1,0 +1,604 @@
+// Cluster engine: the coarse part of the K-cycle as ONE persistent kernel on
+// one thread-block cluster (16 CTAs x 512 threads, non-portable cluster size).
+//
+// Why: on the coarse grids (<= ~32k points) every Krylov/multigrid operation
+// is latency-bound.  As separate kernels each op costs ~5 us (launch + a chain
+// of dependent global-memory round trips for gates, scalars and the reduction
+// epilogue).  Inside one cluster an op costs one DSMEM all-reduce (~0.55 us
+// measured) or one cluster barrier (~0.34 us): the Krylov control state (the
+// Hessenberg matrices, Givens rotations, branch decisions of
+// helmadr/krylov.py:91-242 and helmadr/multigrid.py:132-171) lives in shared
+// memory, computed redundantly and identically by every CTA from the same
+// deterministic all-reduced values, so control flow is uniform with no
+// global-memory round trip.
+//
+// Arithmetic is exactly the graph path's (same element formulas, same
+// reduction algebra), so the two paths agree to rounding in the reductions'
+// association only.
+#include "cluster_engine.h"
+#include "krylov_ctl.cuh"
+
+#include <set>
+
+namespace hadr {
+
+struct CEShared {
+  double slot[2][4];  // DSMEM all-reduce slots (double-buffered)
+  double tot[4];
+  double bsum[4 * 32];
+  RelaxCtl rc;            // the (single) live relaxation
+  FgCtl2 fg[CE_MAXLEV];   // one inner FGMRES(2) per level (nested)
+  CELevel lv[CE_MAXLEV];
+  int nlev, coarse_steps;
+  double coarse_tol;
+};
+
+struct CEC {
+  unsigned rank, C;
+  long gtid, gstride;
+  int ph;
+  CEShared* S;
+  unsigned long long* prof;  // CTA 0 / thread 0 phase counters (null = off)
+};
+
+// Phase profile of the engine (hadr_ce_profile): cycles seen by CTA 0 thread 0.
+__device__ unsigned long long g_ce_prof[8];
+struct CEProfScope {
+  unsigned long long* p;
+  int slot;
+  long long t0;
+  __device__ CEProfScope(const CEC& c, int s) : p(c.prof), slot(s), t0(0) {
+    if (p) t0 = clock64();
+  }
+  __device__ ~CEProfScope() {
+    if (p) {
+      p[slot] += clock64() - t0;
+      p[slot + 1] += 1;
+    }
+  }
+};
+
+__device__ __forceinline__ void ce_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ double ce_remote(const double* p, unsigned rank) {
+  unsigned long long in = reinterpret_cast<unsigned long long>(p), out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(in), "r"(rank));
+  return *reinterpret_cast<const double*>(out);
+}
+// mutable vectors are read through L2 (written by other CTAs of the cluster)
+__device__ __forceinline__ cplx ldm(const cplx* p, long i) { return __ldcg(p + i); }
+__device__ __forceinline__ cplx ldk(const cplx* p, long i) { return __ldg(p + i); }
+
+// Cluster all-reduce of NV doubles: every CTA ends with bit-identical totals.
+template <int NV>
+__device__ void ce_allreduce(CEC& c, double (&v)[NV]) {
+  CEProfScope prof_(c, 1);
+  CEShared* S = c.S;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) S->bsum[q * 32 + wid] = v[q];
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double t = lane < nw ? S->bsum[q * 32 + lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) S->slot[c.ph][q] = t;
+    }
+  }
+  ce_sync();
+  if (wid == 0) {
+    double t[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) t[q] = lane < (int)c.C ? ce_remote(&S->slot[c.ph][q], lane) : 0.0;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t[q] += __shfl_xor_sync(0xffffffffu, t[q], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) S->tot[q] = t[q];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = S->tot[q];
+  c.ph ^= 1;
+}
+
+// ---------------------------------------------------------------------------
+// vector operations (same element formulas as kernels.cu)
+// ---------------------------------------------------------------------------
+// Stencil on a row-slab partition: CTA r owns rows [r0, r1) of the level grid.
+// The (transformed) input rows [r0-2, r1+2) are staged once in shared memory,
+// so every neighbour is an LDS instead of an L2 round trip; D^-1 and the scale
+// are applied once per point (same values as applying them per neighbour).
+extern __shared__ cplx ce_tile[];
+
+template <int NO, int INM, int OUTM, int RED>
+__device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double s, const cplx* dinv, cplx* vout,
+                              const cplx* b, cplx* y, const cplx* u, double (&red)[3]) {
+  const int n1 = A.n1, n2 = A.n2, nofs = A.nofs;
+  const long N = (long)n1 * n2;
+  const int R = (n1 + (int)c.C - 1) / (int)c.C;
+  const int r0 = min(n1, (int)c.rank * R), r1 = min(n1, r0 + R);
+  const int t0 = max(0, r0 - 2), t1 = min(n1, r1 + 2);
+  const long base = (long)t0 * n2, tn = (long)(t1 - t0) * n2;
+  for (long p = threadIdx.x; p < tn; p += blockDim.x) {
+    cplx v = ldm(x, base + p);
+    if (INM & IN_SCALE) v = cscale(v, s);
+    if (INM & IN_JAC) v = cmul_np(ldk(dinv, base + p), v);
+    ce_tile[p] = v;
+  }
+  __syncthreads();
+  const long own1 = (long)r1 * n2;
+  for (long k = (long)r0 * n2 + threadIdx.x; k < own1; k += blockDim.x) {
+    const int i1 = (int)(k / n2);
+    const int i2 = (int)(k - (long)i1 * n2);
+    cplx cv[NO];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) cv[o] = ldk(A.coef, o < nofs ? (long)o * N + k : k);
+    cplx acc = mk(0.0, 0.0);
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      const int j1 = i1 + A.d1[o], j2 = i2 + A.d2[o];
+      const bool ok = o < nofs && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2;
+      const cplx v = ce_tile[ok ? (long)(j1 - t0) * n2 + j2 : 0];
+      const cplx t = cadd(acc, cmul_sp(cv[o], v));
+      acc = ok ? t : acc;
+    }
+    cplx vc = mk(0.0, 0.0);
+    if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) {
+      vc = ldm(x, k);
+      if (INM & IN_SCALE) vc = cscale(vc, s);
+      if (INM & IN_WRITEV) vout[k] = vc;
+    }
+    const cplx yy = (OUTM == OUT_RESID) ? csub(ldm(b, k), acc) : acc;
+    y[k] = yy;
+    if (RED & RED_NORM) red[0] += yy.x * yy.x + yy.y * yy.y;
+    if (RED & (RED_DOT | RED_DOT_CENTER)) {
+      const cplx uu = (RED & RED_DOT_CENTER) ? vc : ldm(u, k);
+      constexpr int o = (RED & RED_NORM) ? 1 : 0;
+      red[o] += uu.x * yy.x + uu.y * yy.y;
+      red[o + 1] += uu.x * yy.y - uu.y * yy.x;
+    }
+  }
+  __syncthreads();  // the tile is reused by the next stencil
+}
+
+template <int INM, int OUTM, int RED>
+__device__ __noinline__ void ce_stencil(CEC& c, const StencilDev& A, const cplx* x, double s, const cplx* dinv, cplx* vout,
+                           const cplx* b, cplx* y, const cplx* u, double (&red)[3]) {
+  CEProfScope prof_(c, 5);
+  red[0] = red[1] = red[2] = 0.0;
+  switch (A.nofs) {
+    case 5: ce_stencil_no<5, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
+    case 9: ce_stencil_no<9, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
+    case 21: ce_stencil_no<21, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
+    default: ce_stencil_no<25, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
+  }
+}
+
+// w -= h*v ; RED_DOT: <u, w> ; RED_NORM: ||w||^2
+template <int RED>
+__device__ void ce_axpy(CEC& c, long n, cplx* w, cplx h, const cplx* v, const cplx* u, double (&red)[2]) {
+  red[0] = red[1] = 0.0;
+  for (long k = c.gtid; k < n; k += c.gstride) {
+    const cplx y = csub(ldm(w, k), cmul_np(h, ldm(v, k)));
+    w[k] = y;
+    if (RED == RED_NORM) {
+      red[0] += y.x * y.x + y.y * y.y;
+    } else {
+      const cplx uu = ldm(u, k);
+      red[0] += uu.x * y.x + uu.y * y.y;
+      red[1] += uu.x * y.y - uu.y * y.x;
+    }
+  }
+}
+
+__device__ void ce_dot(CEC& c, long n, const cplx* u, const cplx* w, double (&red)[2]) {
+  red[0] = red[1] = 0.0;
+  for (long k = c.gtid; k < n; k += c.gstride) {
+    const cplx uu = ldm(u, k), y = ldm(w, k);
+    red[0] += uu.x * y.x + uu.y * y.y;
+    red[1] += uu.x * y.y - uu.y * y.x;
+  }
+}
+
+// out = in * s (s < 0: copy) ; returns ||out||^2 partial
+__device__ double ce_scale(CEC& c, long n, const cplx* in, double s, bool scaled, cplx* out) {
+  double r = 0.0;
+  for (long k = c.gtid; k < n; k += c.gstride) {
+    cplx y = ldm(in, k);
+    if (scaled) y = cscale(y, s);
+    if (out) out[k] = y;
+    r += y.x * y.x + y.y * y.y;
+  }
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Jacobi-GMRES(s) relaxation (helmadr/krylov.py:91-119)
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, const cplx* x, cplx* xo, int s) {
+  RelaxCtl* R = &c.S->rc;
+  const long n = L.N;
+  if (threadIdx.x == 0) {
+    R->steps = s;
+    R->k = 0;
+    R->cur = kStopped;
+  }
+  const cplx* r = b;
+  {
+    double v[1];
+    if (x) {
+      double red[3];
+      ce_stencil<IN_PLAIN, OUT_RESID, RED_NORM>(c, L.A, x, 1.0, nullptr, nullptr, b, L.w[1], nullptr, red);
+      v[0] = red[0];
+      r = L.w[1];
+    } else {
+      v[0] = ce_scale(c, n, b, 1.0, false, nullptr);
+    }
+    ce_allreduce<1>(c, v);
+    if (threadIdx.x == 0) relax_beta(R, v[0]);
+    __syncthreads();
+  }
+  for (int j = 0; j < s; ++j) {
+    if (R->cur != j) break;
+    cplx* w = L.w[j % 2];
+    const cplx* src = (j == 0) ? r : L.w[(j - 1) % 2];
+    const double sc = (j == 0) ? R->inv_beta : R->inv_hn;
+    {
+      double red[3];
+      if (j == 0)
+        ce_stencil<IN_SCALE | IN_JAC | IN_WRITEV, OUT_APPLY, RED_DOT_CENTER>(c, L.A, src, sc, L.dinv, L.V[j], nullptr,
+                                                                             w, nullptr, red);
+      else
+        ce_stencil<IN_SCALE | IN_JAC | IN_WRITEV, OUT_APPLY, RED_DOT>(c, L.A, src, sc, L.dinv, L.V[j], nullptr, w,
+                                                                      L.V[0], red);
+      double v[2] = {red[0], red[1]};
+      ce_allreduce<2>(c, v);
+      if (threadIdx.x == 0) R->H[0 * RMAX + j] = mk(v[0], v[1]);
+      __syncthreads();
+    }
+    for (int i = 0; i < j; ++i) {
+      double v[2];
+      ce_axpy<RED_DOT>(c, n, w, R->H[i * RMAX + j], L.V[i], L.V[i + 1], v);
+      ce_allreduce<2>(c, v);
+      if (threadIdx.x == 0) R->H[(i + 1) * RMAX + j] = mk(v[0], v[1]);
+      __syncthreads();
+    }
+    {
+      double v2[2];
+      ce_axpy<RED_NORM>(c, n, w, R->H[j * RMAX + j], L.V[j], nullptr, v2);
+      double v[1] = {v2[0]};
+      ce_allreduce<1>(c, v);
+      {
+        CEProfScope prof_(c, 3);
+        if (threadIdx.x == 0) relax_step(R, j, v[0]);
+        __syncthreads();
+      }
+    }
+  }
+  // xo = x + dinv (.) (V[:k]^T y)
+  const int k = R->k;
+  for (long p = c.gtid; p < n; p += c.gstride) {
+    cplx t = mk(0.0, 0.0);
+    for (int i = 0; i < k; ++i) t = cadd(t, cmul_np(ldm(L.V[i], p), R->y[i]));
+    t = cmul_np(ldk(L.dinv, p), t);
+    xo[p] = x ? cadd(ldm(x, p), t) : cadd(mk(0.0, 0.0), t);
+  }
+  ce_sync();
+}
+
+// ---------------------------------------------------------------------------
+// transfer operators (bit-exact orders, see kernels.cu)
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void ce_restrict(CEC& c, int n1f, int n2f, const cplx* r, cplx* rc) {
+  const int n1c = (n1f - 1) / 2 + 1, n2c = (n2f - 1) / 2 + 1;
+  const long Nc = (long)n1c * n2c;
+  for (long q = c.gtid; q < Nc; q += c.gstride) {
+    const int I1 = (int)(q / n2c), I2 = (int)(q - (long)I1 * n2c);
+    cplx acc = mk(0.0, 0.0);
+#pragma unroll
+    for (int a = -1; a <= 1; ++a) {
+      const int f1 = 2 * I1 + a;
+      if (f1 < 0 || f1 >= n1f) continue;
+      const double w1 = a == 0 ? 1.0 : 0.5;
+#pragma unroll
+      for (int bb = -1; bb <= 1; ++bb) {
+        const int f2 = 2 * I2 + bb;
+        if (f2 < 0 || f2 >= n2f) continue;
+        const double w = w1 * (bb == 0 ? 1.0 : 0.5);
+        acc = cadd(acc, cmul_sp(mk(w, 0.0), ldm(r, (long)f1 * n2f + f2)));
+      }
+    }
+    rc[q] = acc;
+  }
+}
+
+__device__ __noinline__ void ce_prolong_add(CEC& c, int n1f, int n2f, const cplx* ec, cplx* x) {
+  const int n2c = (n2f - 1) / 2 + 1;
+  const long Nf = (long)n1f * n2f;
+  for (long f = c.gtid; f < Nf; f += c.gstride) {
+    const int f1 = (int)(f / n2f), f2 = (int)(f - (long)f1 * n2f);
+    int c1[2], c2[2], m1, m2;
+    double w1, w2;
+    if (f1 & 1) { c1[0] = f1 >> 1; c1[1] = (f1 >> 1) + 1; m1 = 2; w1 = 0.5; } else { c1[0] = f1 >> 1; c1[1] = c1[0]; m1 = 1; w1 = 1.0; }
+    if (f2 & 1) { c2[0] = f2 >> 1; c2[1] = (f2 >> 1) + 1; m2 = 2; w2 = 0.5; } else { c2[0] = f2 >> 1; c2[1] = c2[0]; m2 = 1; w2 = 1.0; }
+    cplx p = mk(0.0, 0.0);
+    for (int a = 0; a < m1; ++a)
+      for (int bb = 0; bb < m2; ++bb) p = cadd(p, cmul_sp(mk(w1 * w2, 0.0), ldm(ec, (long)c1[a] * n2c + c2[bb])));
+    x[f] = cadd(ldm(x, f), p);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K-cycle recursion (helmadr/multigrid.py:132-171) and the inner FGMRES(2)
+// (helmadr/multigrid.py:159-167 with helmadr/krylov.py:122-242).  Templated on
+// the recursion depth so the compiler sees no runtime recursion.
+// ---------------------------------------------------------------------------
+template <int D>
+__device__ void ce_kcycle(CEC& c, int l, const cplx* b, cplx* xo);
+
+// one Arnoldi column j of the inner FGMRES: w = A z against basis B[0..j]
+__device__ __noinline__ void ce_arnoldi(CEC& c, FgCtl2* f, const CELevel& L, int j, const cplx* z, const cplx* B0,
+                           const cplx* B1) {
+  const long n = L.N;
+  const cplx* B[2] = {B0, B1};
+  {
+    double red[3];
+    ce_stencil<IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT>(c, L.A, z, 1.0, nullptr, nullptr, nullptr, L.fw, B0, red);
+    double v[3] = {red[0], red[1], red[2]};
+    ce_allreduce<3>(c, v);
+    if (threadIdx.x == 0) {
+      f->w0 = sqrt(v[0]);
+      f->H[0 * 2 + j] = mk(v[1], v[2]);
+    }
+    __syncthreads();
+  }
+  for (int i = 0; i < j; ++i) {
+    double v[2];
+    ce_axpy<RED_DOT>(c, n, L.fw, f->H[i * 2 + j], B[i], B[i + 1], v);
+    ce_allreduce<2>(c, v);
+    if (threadIdx.x == 0) f->H[(i + 1) * 2 + j] = mk(v[0], v[1]);
+    __syncthreads();
+  }
+  {
+    double v2[2];
+    ce_axpy<RED_NORM>(c, n, L.fw, f->H[j * 2 + j], B[j], nullptr, v2);
+    double v[1] = {v2[0]};
+    ce_allreduce<1>(c, v);
+    if (threadIdx.x == 0) {
+      f->wn = sqrt(v[0]);
+      f->reo = (f->wn < kReorthRatio * f->w0) ? 1 : 0;  // helmadr/krylov.py:178-179
+      if (!f->reo) {
+        CEProfScope prof_(c, 3);
+        fg_post(f, j);
+      }
+    }
+    __syncthreads();
+  }
+  if (f->reo) {  // one re-orthogonalisation pass (helmadr/krylov.py:180-184)
+    {
+      double v[2];
+      ce_dot(c, n, B0, L.fw, v);
+      ce_allreduce<2>(c, v);
+      if (threadIdx.x == 0) {
+        f->corr[0] = mk(v[0], v[1]);
+        f->H[0 * 2 + j] = cadd(f->H[0 * 2 + j], f->corr[0]);
+      }
+      __syncthreads();
+    }
+    for (int i = 0; i < j; ++i) {
+      double v[2];
+      ce_axpy<RED_DOT>(c, n, L.fw, f->corr[i], B[i], B[i + 1], v);
+      ce_allreduce<2>(c, v);
+      if (threadIdx.x == 0) {
+        f->corr[i + 1] = mk(v[0], v[1]);
+        f->H[(i + 1) * 2 + j] = cadd(f->H[(i + 1) * 2 + j], f->corr[i + 1]);
+      }
+      __syncthreads();
+    }
+    double v2[2];
+    ce_axpy<RED_NORM>(c, n, L.fw, f->corr[j], B[j], nullptr, v2);
+    double v[1] = {v2[0]};
+    ce_allreduce<1>(c, v);
+    if (threadIdx.x == 0) {
+      f->wn = sqrt(v[0]);
+      fg_post(f, j);
+    }
+    __syncthreads();
+  }
+}
+
+template <int D>
+__device__ void ce_inner(CEC& c, int ci) {
+  CEShared* S = c.S;
+  const CELevel& C = S->lv[ci];
+  FgCtl2* f = &S->fg[ci];
+  const long n = C.N;
+  if (threadIdx.x == 0) {
+    f->tol = S->coarse_tol;
+    f->reo = 0;
+  }
+  {
+    double v[1] = {ce_scale(c, n, C.fb, 1.0, false, nullptr)};
+    ce_allreduce<1>(c, v);
+    if (threadIdx.x == 0) fg_init(f, v[0]);
+    __syncthreads();
+  }
+  if (f->path == FG_ZERO) {
+    for (long p = c.gtid; p < n; p += c.gstride) C.fx[p] = mk(0.0, 0.0);
+    ce_sync();
+    return;
+  }
+  ce_scale(c, n, C.fb, f->inv_r, true, C.fV0);
+  ce_sync();
+  ce_kcycle<D>(c, ci, C.fV0, C.fZ0);
+  ce_arnoldi(c, f, C, 0, C.fZ0, C.fV0, nullptr);
+  if (f->path == FG_BRK) {  // early exit after iteration 1: x = Z0 y0, r = b - A x
+    const int k = f->k;
+    const cplx y0 = f->y[0];
+    for (long p = c.gtid; p < n; p += c.gstride)
+      C.fx[p] = (k >= 1) ? cadd(mk(0.0, 0.0), cmul_np(ldm(C.fZ0, p), y0)) : mk(0.0, 0.0);
+    ce_sync();
+    double red[3];
+    ce_stencil<IN_PLAIN, OUT_RESID, RED_NORM>(c, C.A, C.fx, 1.0, nullptr, nullptr, C.fb, C.fr, nullptr, red);
+    double v[1] = {red[0]};
+    ce_allreduce<1>(c, v);
+    if (threadIdx.x == 0) fg_res(f, v[0]);
+    __syncthreads();
+  }
+  const int path = f->path;
+  if (path == FG_CONT || path == FG_RST) {
+    if (path == FG_CONT)
+      ce_scale(c, n, C.fw, f->inv_w, true, C.fu);
+    else
+      ce_scale(c, n, C.fr, f->inv_r, true, C.fu);
+    ce_sync();
+    ce_kcycle<D>(c, ci, C.fu, C.fZ1);
+    if (path == FG_CONT)
+      ce_arnoldi(c, f, C, 1, C.fZ1, C.fV0, C.fu);
+    else
+      ce_arnoldi(c, f, C, 0, C.fZ1, C.fu, nullptr);
+  }
+  if (f->path == FG_FIN) {
+    const int k = f->k, cyc = f->cycle;
+    const cplx y0 = f->y[0], y1 = f->y[1];
+    for (long p = c.gtid; p < n; p += c.gstride) {
+      cplx out;
+      if (cyc == 0) {
+        cplx t = mk(0.0, 0.0);
+        if (k >= 1) t = cadd(t, cmul_np(ldm(C.fZ0, p), y0));
+        if (k >= 2) t = cadd(t, cmul_np(ldm(C.fZ1, p), y1));
+        out = cadd(mk(0.0, 0.0), t);
+      } else {
+        const cplx xp = ldm(C.fx, p);
+        out = (k >= 1) ? cadd(xp, cmul_np(ldm(C.fZ1, p), y0)) : xp;
+      }
+      C.fx[p] = out;
+    }
+    ce_sync();
+  }
+}
+
+template <int D>
+__device__ void ce_kcycle(CEC& c, int l, const cplx* b, cplx* xo) {
+  if constexpr (D < CE_MAXLEV) {
+    CEShared* S = c.S;
+    const CELevel& L = S->lv[l];
+    const CELevel& C = S->lv[l + 1];
+    ce_relax(c, L, b, nullptr, xo, L.s);
+    {
+      double red[3];
+      ce_stencil<IN_PLAIN, OUT_RESID, RED_NONE>(c, L.A, xo, 1.0, nullptr, nullptr, b, L.r, nullptr, red);
+      ce_sync();
+    }
+    ce_restrict(c, L.A.n1, L.A.n2, L.r, C.fb);
+    ce_sync();
+    if (l + 1 == S->nlev - 1)
+      ce_relax(c, C, C.fb, nullptr, C.fx, S->coarse_steps);
+    else
+      ce_inner<D + 1>(c, l + 1);
+    ce_prolong_add(c, L.A.n1, L.A.n2, C.fx, xo);
+    ce_sync();
+    ce_relax(c, L, b, xo, xo, L.s);
+  }
+}
+
+__global__ void __launch_bounds__(CE_THREADS, 1)
+    k_cluster_engine(const CEDesc* __restrict__ d, int mode, int l0, const cplx* b, cplx* xo, const int* active,
+                     int prof) {
+  if (active && *((volatile const int*)active) == 0) return;
+  __shared__ CEShared S;
+  // level descriptors into shared memory
+  {
+    const int nw = (int)(sizeof(CELevel) * CE_MAXLEV / sizeof(int));
+    const int* src = reinterpret_cast<const int*>(d->lv);
+    int* dst = reinterpret_cast<int*>(S.lv);
+    for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = src[i];
+    if (threadIdx.x == 0) {
+      S.nlev = d->nlev;
+      S.coarse_steps = d->coarse_steps;
+      S.coarse_tol = d->coarse_tol;
+    }
+  }
+  __syncthreads();
+  CEC c;
+  c.rank = blockIdx.x;
+  c.C = gridDim.x;
+  c.gtid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  c.gstride = (long)gridDim.x * blockDim.x;
+  c.ph = 0;
+  c.S = &S;
+  c.prof = (prof && blockIdx.x == 0 && threadIdx.x == 0) ? g_ce_prof : nullptr;
+  const long long t_start = clock64();
+  if (mode == 0) {
+    ce_kcycle<0>(c, l0, b, xo);
+  } else if (mode == 1) {
+    ce_inner<0>(c, l0);
+  } else {
+    const CELevel& C = S.lv[l0];
+    ce_relax(c, C, C.fb, nullptr, C.fx, S.coarse_steps);
+  }
+  ce_sync();  // no CTA exits while another may still read its shared memory
+  if (c.prof) {
+    c.prof[0] += clock64() - t_start;
+    c.prof[7] += 1;
+  }
+}
+
+int ce_profile_read(unsigned long long* out, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_ce_prof, sizeof(unsigned long long) * 8);
+  if (e != cudaSuccess) return (int)e;
+  if (reset) {
+    unsigned long long z[8] = {0};
+    e = cudaMemcpyToSymbol(g_ce_prof, z, sizeof(z));
+  }
+  return (int)e;
+}
+
+int g_ce_prof_on = 0;
+
+extern int g_ce_prof_on;
+void launch_cluster_engine(cudaStream_t s, const CEDesc* d, int mode, int l0, const cplx* b, cplx* xo,
+                           const int* active, int ctas, size_t tile_bytes) {
+  ++g_launch_count;
+  static bool init = false;
+  static size_t max_tile = 0;
+  if (!init) {
+    cudaFuncSetAttribute(k_cluster_engine, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    init = true;
+  }
+  if (tile_bytes > max_tile) {
+    cudaFuncSetAttribute(k_cluster_engine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_bytes);
+    max_tile = tile_bytes;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(CE_THREADS);
+  cfg.dynamicSmemBytes = tile_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = ctas;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_cluster_engine, d, mode, l0, b, xo, active, g_ce_prof_on);
+}
+
+}  // namespace hadr

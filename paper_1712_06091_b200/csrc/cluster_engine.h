@@ -1,0 +1,44 @@
+// Cluster engine interface (cluster_engine.cu).
+#pragma once
+#include "kernels.cuh"
+
+namespace hadr {
+
+constexpr int CE_MAXLEV = 6;      // levels a single engine launch may span
+constexpr int CE_THREADS = 512;   // threads per CTA
+constexpr int CE_CTAS = 16;       // CTAs in the (single, non-portable) cluster
+
+// Device-resident description of one multigrid level for the engine.
+struct CELevel {
+  StencilDev A;
+  const cplx* dinv;
+  long N;
+  int s;  // relaxation length
+  int pad_;
+  cplx* r;
+  cplx* V[RMAX + 1];
+  cplx* w[2];
+  cplx *fb, *fx, *fV0, *fu, *fZ0, *fZ1, *fw, *fr;
+};
+
+struct CEDesc {
+  int nlev;          // levels described (index 0 = the hierarchy's level `base`)
+  int coarse_steps;
+  double coarse_tol;
+  CELevel lv[CE_MAXLEV];
+};
+
+// mode 0: k_cycle(l0, b -> xo) with x = 0
+// mode 1: inner FGMRES(2) at level l0 (lv[l0].fb -> lv[l0].fx)
+// mode 2: coarsest relaxation at level l0 (lv[l0].fb -> lv[l0].fx)
+// phase counters [total cyc, allreduce cyc, n, epilogue cyc, n, stencil cyc, n, launches]
+int ce_profile_read(unsigned long long* out, int reset);
+extern int g_ce_prof_on;
+void launch_cluster_engine(cudaStream_t s, const CEDesc* d, int mode, int l0, const cplx* b, cplx* xo,
+                           const int* active, int ctas, size_t tile_bytes);
+// dynamic shared memory for the stencil row tiles of levels with n1 x n2 points
+inline size_t ce_tile_bytes(int n1, int n2, int ctas) {
+  return (size_t)((n1 + ctas - 1) / ctas + 4) * n2 * sizeof(cplx);
+}
+
+}  // namespace hadr

@@ -45,7 +45,8 @@ enum FgPath : int {
   FG_ZERO = 6,     // ||b|| == 0 -> x = 0
 };
 
-struct FgCtl {
+template <int MM>
+struct FgCtlT {
   int path;       // gate var (inner solver)
   int reo;        // gate var: 1 = re-orthogonalisation pass needed
   int it;
@@ -56,12 +57,15 @@ struct FgCtl {
   int nhist;
   double bnorm, target, rnorm, inv_r;
   double w0, wn, inv_w, tol;
-  cplx corr[MMAX + 1];
-  cplx H[(MMAX + 1) * MMAX];   // H[i*MMAX + j], rotated in place as in the reference
-  cplx cs[MMAX], sn[MMAX];
-  cplx g[MMAX + 1];
-  cplx y[MMAX];
+  cplx corr[MM + 1];
+  cplx H[(MM + 1) * MM];   // H[i*MM + j], rotated in place as in the reference
+  cplx cs[MM], sn[MM];
+  cplx g[MM + 1];
+  cplx y[MM];
   double hist[8];
+  static constexpr int LD = MM;
 };
+using FgCtl = FgCtlT<MMAX>;   // outer solver scratch / graph-path inner solver
+using FgCtl2 = FgCtlT<2>;     // inner FGMRES(2) inside the cluster engine
 
 }  // namespace hadr

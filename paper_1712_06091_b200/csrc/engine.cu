@@ -11,6 +11,8 @@
 
 namespace hadr {
 
+long g_ce_max_n = 32768;
+
 // ---------------------------------------------------------------------------
 // caching allocator
 // ---------------------------------------------------------------------------
@@ -473,6 +475,18 @@ Hier::~Hier() {
   }
   dfree(kact);
   dfree(visits);
+  dfree(ce_desc);
+}
+
+size_t Hier::ce_tile(int li) const {
+  size_t m = 0;  // the engine touches levels li .. coarsest; the finest of them is the largest
+  for (int i = li; i < (int)lv.size(); ++i) m = std::max(m, ce_tile_bytes(lv[i].n1, lv[i].n2, CE_CTAS));
+  return m;
+}
+
+bool Hier::use_ce(int li) const {
+  return ce_desc != nullptr && g_ce_max_n > 0 && li < (int)lv.size() && lv[li].N <= g_ce_max_n &&
+         (int)lv.size() <= CE_MAXLEV && ce_tile(li) <= 200 * 1024;
 }
 
 void Hier::alloc_workspace() {
@@ -509,6 +523,27 @@ void Hier::alloc_workspace() {
   visits = dalloc<int>(nl + 1);
   HADR_CUDA(cudaMemset(kact, 0, (nl + 1) * sizeof(int)));
   HADR_CUDA(cudaMemset(visits, 0, (nl + 1) * sizeof(int)));
+  if (nl <= CE_MAXLEV) {
+    CEDesc h{};
+    h.nlev = nl;
+    h.coarse_steps = coarse_steps;
+    h.coarse_tol = coarse_tol;
+    for (int i = 0; i < nl; ++i) {
+      const Level& L = lv[i];
+      CELevel& d = h.lv[i];
+      d.A = L.A->dev();
+      d.dinv = L.dinv;
+      d.N = L.N;
+      d.s = L.s;
+      d.r = L.r;
+      for (int j = 0; j <= RMAX; ++j) d.V[j] = L.V[j];
+      d.w[0] = L.w[0];
+      d.w[1] = L.w[1];
+      d.fb = L.fb, d.fx = L.fx, d.fV0 = L.fV0, d.fu = L.fu, d.fZ0 = L.fZ0, d.fZ1 = L.fZ1, d.fw = L.fw, d.fr = L.fr;
+    }
+    ce_desc = dalloc<CEDesc>(1);
+    HADR_CUDA(cudaMemcpy(ce_desc, &h, sizeof(CEDesc), cudaMemcpyHostToDevice));
+  }
 }
 
 static std::vector<Hier*>& hier_pool() {
@@ -674,6 +709,10 @@ void Hier::emit_kcycle(int li, const cplx* b, const cplx* x0, cplx* xo, Gate g, 
   Ctx& c = Ctx::get();
   const int nl = (int)lv.size();
   if (li < 0 || li >= nl - 1) throw ValueError("level outside 1..n_levels-1");
+  if (!x0 && !count && use_ce(li)) {  // the whole cycle fits one cluster
+    launch_cluster_engine(c.stream, ce_desc, 0, li, b, xo, g.active, CE_CTAS, ce_tile(li));
+    return;
+  }
   Level& L = lv[li];
   Level& C = lv[li + 1];
   if (count) k_count<<<1, 1, 0, c.stream>>>(visits, li, g);
@@ -690,7 +729,12 @@ void Hier::emit_kcycle(int li, const cplx* b, const cplx* x0, cplx* xo, Gate g, 
   launch_restrict(c.lc, L.n1, L.n2, L.r, C.fb, g);
   if (li + 1 == nl - 1) {
     if (count) k_count<<<1, 1, 0, c.stream>>>(visits, li + 1, g);
-    emit_relax(C, C.fb, nullptr, C.fx, C.s, g);
+    if (!count && use_ce(li + 1))
+      launch_cluster_engine(c.stream, ce_desc, 2, li + 1, nullptr, nullptr, g.active, CE_CTAS, ce_tile(li + 1));
+    else
+      emit_relax(C, C.fb, nullptr, C.fx, C.s, g);
+  } else if (!count && use_ce(li + 1)) {
+    launch_cluster_engine(c.stream, ce_desc, 1, li + 1, nullptr, nullptr, g.active, CE_CTAS, ce_tile(li + 1));
   } else {
     emit_inner(li + 1, g, count);
   }

@@ -9,6 +9,7 @@
 #include <utility>
 #include <vector>
 
+#include "cluster_engine.h"
 #include "kernels.cuh"
 
 namespace hadr {
@@ -100,6 +101,9 @@ struct Hier {
   int coarse_steps = 10;
   double coarse_tol = 0.1;
   int* kact = nullptr;      // device: K-cycle-active flag per level
+  CEDesc* ce_desc = nullptr;  // device: level descriptors for the cluster engine
+  bool use_ce(int li) const;  // level li's coarse part runs in the cluster engine
+  size_t ce_tile(int li) const;  // engine dynamic shared memory when entered at level li
   int* visits = nullptr;    // device: visit counters (stats mode)
   std::map<std::pair<const void*, void*>, cudaGraphExec_t> graphs;
   std::map<std::pair<const void*, void*>, long long> graph_kernels;  // kernel nodes per graph
@@ -113,6 +117,9 @@ struct Hier {
   void apply(const cplx* v, cplx* z);
   void kcycle_direct(int li, const cplx* b, const cplx* x0, cplx* xo, int* visits_host);
 };
+
+// runtime options (hadr_set_option)
+extern long g_ce_max_n;  // levels with N <= this run inside the cluster engine (0 disables)
 
 Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol);
 void hier_release(Hier* h);  // recycle (workspace + captured graphs) or delete

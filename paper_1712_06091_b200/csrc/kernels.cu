@@ -6,165 +6,15 @@
 // (deterministic order) which also runs the scalar control epilogue, so no
 // separate "small" kernel and no host round trip is needed per Krylov step.
 #include "kernels.cuh"
+#include "krylov_ctl.cuh"
 
+#include <set>
 #include <stdexcept>
+#include <utility>
 
 namespace hadr {
 
 long long g_launch_count = 0;  // kernels launched directly on the stream (graphs add their node count)
-
-// ---------------------------------------------------------------------------
-// scalar helpers for the control epilogues (numpy *scalar* arithmetic is plain,
-// non-contracted C: use the no-FMA product)
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ cplx cneg(cplx a) { return mk(-a.x, -a.y); }
-__device__ __forceinline__ double cabs_d(cplx a) { return hypot(a.x, a.y); }
-
-template <int LD>
-__device__ void givens_step(cplx* H, cplx* cs, cplx* sn, cplx* g, int j) {
-  // helmadr/krylov.py:195-208
-  for (int i = 0; i < j; ++i) {
-    cplx hij = H[i * LD + j], hi1 = H[(i + 1) * LD + j];
-    cplx t = cadd(cmul_sp(cs[i], hij), cmul_sp(sn[i], hi1));
-    H[(i + 1) * LD + j] = cadd(cmul_sp(cneg(cconj(sn[i])), hij), cmul_sp(cconj(cs[i]), hi1));
-    H[i * LD + j] = t;
-  }
-  cplx a = H[j * LD + j], b = H[(j + 1) * LD + j];
-  double aa = cabs_d(a), bb = cabs_d(b);
-  double den = sqrt(aa * aa + bb * bb);
-  if (den == 0.0) {
-    cs[j] = mk(1.0, 0.0);
-    sn[j] = mk(0.0, 0.0);
-  } else {
-    cs[j] = cdiv_np(cconj(a), mk(den, 0.0));
-    sn[j] = cdiv_np(cconj(b), mk(den, 0.0));
-  }
-  H[j * LD + j] = cadd(cmul_sp(cs[j], a), cmul_sp(sn[j], b));
-  H[(j + 1) * LD + j] = mk(0.0, 0.0);
-  cplx gj = g[j];
-  g[j + 1] = cmul_sp(cneg(cconj(sn[j])), gj);
-  g[j] = cmul_sp(cs[j], gj);
-}
-
-// Upper-triangular solve R[:k,:k] y = g[:k], column-oriented like LAPACK ?trsm.
-template <int LD>
-__device__ void backsolve(const cplx* R, const cplx* g, cplx* y, int k) {
-  for (int i = 0; i < k; ++i) y[i] = g[i];
-  for (int j = k - 1; j >= 0; --j) {
-    y[j] = cdiv_np(y[j], R[j * LD + j]);
-    for (int i = 0; i < j; ++i) y[i] = csub(y[i], cmul_sp(y[j], R[i * LD + j]));
-  }
-}
-
-// ---- Jacobi-GMRES relaxation control (helmadr/krylov.py:91-119) ----
-__device__ void relax_beta(RelaxCtl* c, double ss) {
-  double beta = sqrt(ss);
-  c->beta = beta;
-  c->k = 0;
-  for (int i = 0; i <= RMAX; ++i) c->g[i] = mk(0.0, 0.0);
-  if (beta == 0.0 || c->steps < 1) {  // helmadr/krylov.py:96-97
-    c->cur = kStopped;
-    return;
-  }
-  c->inv_beta = 1.0 / beta;
-  c->g[0] = mk(beta, 0.0);
-  c->cur = 0;
-}
-
-__device__ void relax_step(RelaxCtl* c, int j, double ss) {
-  double hn = sqrt(ss);
-  c->H[(j + 1) * RMAX + j] = mk(hn, 0.0);
-  c->k = j + 1;
-  for (int i = 0; i <= j + 1; ++i) c->R[i * RMAX + j] = c->H[i * RMAX + j];
-  givens_step<RMAX>(c->R, c->cs, c->sn, c->g, j);
-  bool stop = (hn <= kBreakdownEps * c->beta) || (j + 1 >= c->steps);  // helmadr/krylov.py:113-114
-  if (!stop) {
-    c->inv_hn = 1.0 / hn;
-    c->cur = j + 1;
-    return;
-  }
-  c->cur = kStopped;
-  backsolve<RMAX>(c->R, c->g, c->y, c->k);
-}
-
-// ---- inner FGMRES(2) control (helmadr/krylov.py:142-231, helmadr/multigrid.py:159-167) ----
-__device__ void fg_init(FgCtl* f, double ss) {
-  double bn = sqrt(ss);
-  f->bnorm = bn;
-  f->it = 0;
-  f->k = 0;
-  f->cycle = 0;
-  f->broke = 0;
-  f->note = 0;
-  f->reo = 0;
-  f->nhist = 0;
-  for (int i = 0; i < (MMAX + 1) * MMAX; ++i) f->H[i] = mk(0.0, 0.0);
-  for (int i = 0; i <= MMAX; ++i) f->g[i] = mk(0.0, 0.0);
-  if (bn == 0.0) {  // helmadr/krylov.py:143-145
-    f->path = FG_ZERO;
-    return;
-  }
-  f->rnorm = bn;  // r = b - A*0 = b
-  f->target = f->tol * bn;
-  f->g[0] = mk(bn, 0.0);
-  f->inv_r = 1.0 / bn;
-  f->path = FG_A;
-}
-
-__device__ void fg_solve_y(FgCtl* f) {
-  int k = f->k;
-  if (k == 1) {
-    f->y[0] = cdiv_np(f->g[0], f->H[0]);  // g[:1] / H[0, 0]
-  } else if (k > 1) {
-    backsolve<MMAX>(f->H, f->g, f->y, k);  // np.linalg.solve on the rotated (triangular) H
-  }
-}
-
-__device__ void fg_post(FgCtl* f, int j) {
-  f->reo = 0;
-  double wn = f->wn;
-  f->H[(j + 1) * MMAX + j] = mk(wn, 0.0);
-  if (!isfinite(wn)) {  // helmadr/krylov.py:186-190
-    f->note = 1;
-    f->broke = 1;
-    f->k = j;
-  } else {
-    bool lucky = wn <= kBreakdownEps * fmax(f->bnorm, 1e-300);
-    if (!lucky) f->inv_w = 1.0 / wn;
-    givens_step<MMAX>(f->H, f->cs, f->sn, f->g, j);
-    f->it += 1;
-    f->k = j + 1;
-    double h = cabs_d(f->g[j + 1]);
-    if (f->nhist < 8) f->hist[f->nhist++] = h;
-    bool stop = lucky || h <= f->target;
-    if (f->cycle == 0 && j == 0 && !stop) {  // m = 2: second iteration of the first cycle
-      f->path = FG_CONT;
-      return;
-    }
-  }
-  fg_solve_y(f);
-  f->path = (f->cycle == 0 && j == 0) ? FG_BRK : FG_FIN;
-}
-
-__device__ void fg_res(FgCtl* f, double ss) {
-  double rn = sqrt(ss);
-  f->rnorm = rn;
-  if (f->broke) {
-    f->path = FG_DONE;
-    return;
-  }
-  if (f->it < 2 && rn > f->target) {  // while it < maxiter and rnorm > target: restart with m = 1
-    f->path = FG_RST;
-    f->cycle = 1;
-    f->k = 0;
-    for (int i = 0; i < (MMAX + 1) * MMAX; ++i) f->H[i] = mk(0.0, 0.0);
-    for (int i = 0; i <= MMAX; ++i) f->g[i] = mk(0.0, 0.0);
-    f->g[0] = mk(rn, 0.0);
-    f->inv_r = 1.0 / rn;
-  } else {
-    f->path = FG_DONE;
-  }
-}
 
 __device__ __noinline__ void run_epi(const Epi& e, const double* t, int nv) {
   switch (e.code) {
@@ -219,15 +69,134 @@ __device__ __noinline__ void run_epi(const Epi& e, const double* t, int nv) {
   }
 }
 
-template <int NV>
+// ---------------------------------------------------------------------------
+// Reductions without same-address atomics (the last-block ticket pattern
+// serialises in L2: 31.7 us at 1184 blocks, measured in tools/sync_microbench.cu).
+//   CL = 0 : every block writes its partial sums; a 1-block k_finalize follows
+//            (fixed summation order, then the scalar epilogue).
+//   CL = 1 : the whole grid is ONE thread-block cluster (<= 16 CTAs): partials
+//            are summed through distributed shared memory and CTA 0 runs the
+//            epilogue inside the same kernel (~0.55 us, measured).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ const double* cluster_map(const double* p, unsigned rank) {
+  unsigned long long in = reinterpret_cast<unsigned long long>(p), out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(in), "r"(rank));
+  return reinterpret_cast<const double*>(out);
+}
+
+template <int NV, int CL>
 __device__ __forceinline__ void finish(double (&v)[NV], const RedScratch& rs, const Epi& e) {
-  double tot[NV];
-  if (grid_sum<NV>(v, rs, tot)) {
-    if (threadIdx.x == 0) run_epi(e, tot, NV);
+  __shared__ double sm[NV * 32];
+  block_sum<NV>(v, sm);
+  if constexpr (CL == 0) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) rs.partials[blockIdx.x * NV + q] = v[q];
+    }
+  } else {
+    __shared__ double cp[NV];
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) cp[q] = v[q];
+    }
+    cluster_sync_all();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      double tot[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) tot[q] = 0.0;
+      for (unsigned r = 0; r < gridDim.x; ++r) {
+        const double* rp = cluster_map(cp, r);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) tot[q] += rp[q];
+      }
+      run_epi(e, tot, NV);
+    }
+    cluster_sync_all();  // keep every CTA's shared memory alive until CTA 0 has read it
   }
 }
 
+template <int NV>
+__global__ void __launch_bounds__(kThreads) k_finalize(RedScratch rs, int nblocks, Gate g, Epi e) {
+  if (!gate_open(g)) return;
+  __shared__ double sm[NV * 32];
+  double acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] += rs.partials[b * NV + q];
+  }
+  block_sum<NV>(acc, sm);
+  if (threadIdx.x == 0) run_epi(e, acc, NV);
+}
+
 __device__ __forceinline__ cplx ldc(const cplx* p, long i) { return __ldg(p + i); }
+
+// Launch geometry of one vector op: a single cluster for small levels, else a
+// grid capped at a multiple of the SM count (+ a finalize kernel when reducing).
+constexpr long kClusterMaxN = 32768;
+constexpr int kClusterMaxCTAs = 16;
+
+struct Geo {
+  int blocks;
+  int cluster;  // 0: plain grid
+};
+
+static Geo geo_for(const LaunchCfg& lc, long n) {
+  long b = (n + kThreads - 1) / kThreads;
+  if (n <= kClusterMaxN) {
+    if (b > kClusterMaxCTAs) b = kClusterMaxCTAs;
+    if (b < 1) b = 1;
+    return Geo{(int)b, (int)b};
+  }
+  if (b > lc.max_blocks) b = lc.max_blocks;
+  return Geo{(int)b, 0};
+}
+
+static int blocks_for(const LaunchCfg& lc, long n) {
+  long b = (n + kThreads - 1) / kThreads;
+  if (b > lc.max_blocks) b = lc.max_blocks;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_geo(void (*kern)(KArgs...), const Geo& geo, cudaStream_t s, Args&&... args) {
+  if (!geo.cluster) {
+    kern<<<geo.blocks, kThreads, 0, s>>>(std::forward<Args>(args)...);
+    return;
+  }
+  if (geo.cluster > 8) {  // non-portable cluster sizes must be enabled per kernel
+    static std::set<const void*> enabled;
+    if (!enabled.count((const void*)kern)) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      enabled.insert((const void*)kern);
+    }
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(geo.blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = geo.cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+template <int NV>
+static void launch_finalize(const LaunchCfg& lc, const Geo& geo, Gate g, RedScratch rs, Epi e) {
+  if (geo.cluster) return;
+  ++g_launch_count;
+  k_finalize<NV><<<1, kThreads, 0, lc.stream>>>(rs, geo.blocks, g, e);
+}
 
 // ---------------------------------------------------------------------------
 // K1: stencil apply   y = A x   |   y = b - A x
@@ -235,7 +204,7 @@ __device__ __forceinline__ cplx ldc(const cplx* p, long i) { return __ldg(p + i)
 //   IN_WRITEV stores the centre's scaled input (the new Krylov basis vector).
 //   reductions: ||y||^2, <u, y> (u = array, or the centre input with RED_DOT_CENTER)
 // ---------------------------------------------------------------------------
-template <int INM, int OUTM, int RED, int NO>
+template <int INM, int OUTM, int RED, int NO, int CL>
 __global__ void __launch_bounds__(kThreads) k_stencil(StencilArgs a) {
   if (!gate_open(a.gate)) return;
   const int n1 = a.A.n1, n2 = a.A.n2, nofs = a.A.nofs;
@@ -249,19 +218,29 @@ __global__ void __launch_bounds__(kThreads) k_stencil(StencilArgs a) {
   for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += stride) {
     const int i1 = (int)(k / n2);
     const int i2 = (int)(k - (long)i1 * n2);
+    // All loads are unconditional (out-of-grid neighbours read the centre, dead
+    // offsets read plane 0) so the compiler can batch them; out-of-grid terms are
+    // then skipped, which keeps scipy csr_matvec's exact accumulation.
+    cplx cv[NO], xv[NO], dv[NO];
+    bool ok[NO];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      const bool live = o < nofs;
+      const int j1 = i1 + a.A.d1[o], j2 = i2 + a.A.d2[o];
+      ok[o] = live && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2;
+      const long jj = ok[o] ? (long)j1 * n2 + j2 : k;
+      cv[o] = ldc(a.A.coef, live ? (long)o * N + k : k);
+      xv[o] = ldc(a.x, jj);
+      if (INM & IN_JAC) dv[o] = ldc(a.dinv, jj);
+    }
     cplx acc = mk(0.0, 0.0);
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
-      if (o < nofs) {
-        const int j1 = i1 + a.A.d1[o], j2 = i2 + a.A.d2[o];
-        if (j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2) {
-          const long jj = (long)j1 * n2 + j2;
-          cplx v = ldc(a.x, jj);
-          if (INM & IN_SCALE) v = cscale(v, s);
-          if (INM & IN_JAC) v = cmul_np(ldc(a.dinv, jj), v);
-          acc = cadd(acc, cmul_sp(ldc(a.A.coef, (long)o * N + k), v));
-        }
-      }
+      cplx v = xv[o];
+      if (INM & IN_SCALE) v = cscale(v, s);
+      if (INM & IN_JAC) v = cmul_np(dv[o], v);
+      const cplx t = cadd(acc, cmul_sp(cv[o], v));
+      acc = ok[o] ? t : acc;
     }
     cplx vc = mk(0.0, 0.0);
     if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) {
@@ -283,40 +262,47 @@ __global__ void __launch_bounds__(kThreads) k_stencil(StencilArgs a) {
     double v[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) v[q] = red[q];
-    finish<NV>(v, a.rs, a.epi);
+    finish<NV, CL>(v, a.rs, a.epi);
   }
 }
 
-template <int INM, int OUTM, int RED>
-static void dispatch_no(const LaunchCfg& lc, const StencilArgs& a, int blocks) {
-  const int n = a.A.nofs;
-  if (n <= 5)
-    k_stencil<INM, OUTM, RED, 5><<<blocks, kThreads, 0, lc.stream>>>(a);
-  else if (n <= 9)
-    k_stencil<INM, OUTM, RED, 9><<<blocks, kThreads, 0, lc.stream>>>(a);
-  else if (n <= 13)
-    k_stencil<INM, OUTM, RED, 13><<<blocks, kThreads, 0, lc.stream>>>(a);
-  else if (n <= 21)
-    k_stencil<INM, OUTM, RED, 21><<<blocks, kThreads, 0, lc.stream>>>(a);
+template <int INM, int OUTM, int RED, int NO>
+static void launch_stencil_no(const LaunchCfg& lc, const StencilArgs& a, const Geo& geo) {
+  if (geo.cluster)
+    launch_geo(k_stencil<INM, OUTM, RED, NO, 1>, geo, lc.stream, a);
   else
-    k_stencil<INM, OUTM, RED, 25><<<blocks, kThreads, 0, lc.stream>>>(a);
+    launch_geo(k_stencil<INM, OUTM, RED, NO, 0>, geo, lc.stream, a);
 }
 
-static int blocks_for(const LaunchCfg& lc, long n) {
-  long b = (n + kThreads - 1) / kThreads;
-  if (b > lc.max_blocks) b = lc.max_blocks;
-  if (b < 1) b = 1;
-  return (int)b;
+template <int INM, int OUTM, int RED>
+static void dispatch_no(const LaunchCfg& lc, const StencilArgs& a, const Geo& geo) {
+  const int n = a.A.nofs;
+  if (n == 5)
+    launch_stencil_no<INM, OUTM, RED, 5>(lc, a, geo);
+  else if (n == 9)
+    launch_stencil_no<INM, OUTM, RED, 9>(lc, a, geo);
+  else if (n == 21)
+    launch_stencil_no<INM, OUTM, RED, 21>(lc, a, geo);
+  else if (n <= 7)
+    launch_stencil_no<INM, OUTM, RED, 7>(lc, a, geo);
+  else if (n <= 13)
+    launch_stencil_no<INM, OUTM, RED, 13>(lc, a, geo);
+  else if (n <= 21)
+    launch_stencil_no<INM, OUTM, RED, 21>(lc, a, geo);
+  else
+    launch_stencil_no<INM, OUTM, RED, 25>(lc, a, geo);
+  constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & (RED_DOT | RED_DOT_CENTER)) ? 2 : 0);
+  if constexpr (NV > 0) launch_finalize<NV>(lc, geo, a.gate, a.rs, a.epi);
 }
 
 void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const StencilArgs& a) {
   ++g_launch_count;
   const long N = (long)a.A.n1 * a.A.n2;
-  const int blocks = blocks_for(lc, N);
+  const Geo geo = red ? geo_for(lc, N) : Geo{blocks_for(lc, N), 0};
   constexpr int J = IN_SCALE | IN_JAC | IN_WRITEV;
 #define HADR_CASE(I, O, R)                       \
   if (inm == (I) && outm == (O) && red == (R)) { \
-    dispatch_no<I, O, R>(lc, a, blocks);         \
+    dispatch_no<I, O, R>(lc, a, geo);            \
     return;                                      \
   }
   HADR_CASE(IN_PLAIN, OUT_APPLY, RED_NONE)
@@ -334,7 +320,7 @@ void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const Stenc
 // K2/K3: MGS building blocks.  w -= h v (numpy: tmp = h*v; w = w - tmp) fused
 // with the next inner product / norm of the updated w.
 // ---------------------------------------------------------------------------
-template <int RED>
+template <int RED, int CL>
 __global__ void __launch_bounds__(kThreads) k_axpy_red(long n, cplx* __restrict__ w, const cplx* h,
                                                          const cplx* __restrict__ v, const cplx* __restrict__ u,
                                                          Gate g, RedScratch rs, Epi e) {
@@ -356,19 +342,29 @@ __global__ void __launch_bounds__(kThreads) k_axpy_red(long n, cplx* __restrict_
       red[NV - 1] += uu.x * y.y - uu.y * y.x;
     }
   }
-  finish<NV>(red, rs, e);
+  finish<NV, CL>(red, rs, e);
 }
 
 void launch_axpy_red(const LaunchCfg& lc, long n, cplx* w, const cplx* h, const cplx* v, int red, const cplx* u,
                      Gate g, RedScratch rs, Epi e) {
   ++g_launch_count;
-  const int blocks = blocks_for(lc, n);
-  if (red == RED_NORM)
-    k_axpy_red<RED_NORM><<<blocks, kThreads, 0, lc.stream>>>(n, w, h, v, u, g, rs, e);
-  else
-    k_axpy_red<RED_DOT><<<blocks, kThreads, 0, lc.stream>>>(n, w, h, v, u, g, rs, e);
+  const Geo geo = geo_for(lc, n);
+  if (red == RED_NORM) {
+    if (geo.cluster)
+      launch_geo(k_axpy_red<RED_NORM, 1>, geo, lc.stream, n, w, h, v, u, g, rs, e);
+    else
+      launch_geo(k_axpy_red<RED_NORM, 0>, geo, lc.stream, n, w, h, v, u, g, rs, e);
+    launch_finalize<1>(lc, geo, g, rs, e);
+  } else {
+    if (geo.cluster)
+      launch_geo(k_axpy_red<RED_DOT, 1>, geo, lc.stream, n, w, h, v, u, g, rs, e);
+    else
+      launch_geo(k_axpy_red<RED_DOT, 0>, geo, lc.stream, n, w, h, v, u, g, rs, e);
+    launch_finalize<2>(lc, geo, g, rs, e);
+  }
 }
 
+template <int CL>
 __global__ void __launch_bounds__(kThreads) k_dot(long n, const cplx* __restrict__ u, const cplx* __restrict__ w,
                                                     Gate g, RedScratch rs, Epi e) {
   if (!gate_open(g)) return;
@@ -379,15 +375,20 @@ __global__ void __launch_bounds__(kThreads) k_dot(long n, const cplx* __restrict
     red[0] += uu.x * y.x + uu.y * y.y;
     red[1] += uu.x * y.y - uu.y * y.x;
   }
-  finish<2>(red, rs, e);
+  finish<2, CL>(red, rs, e);
 }
 
 void launch_dot(const LaunchCfg& lc, long n, const cplx* u, const cplx* w, Gate g, RedScratch rs, Epi e) {
   ++g_launch_count;
-  k_dot<<<blocks_for(lc, n), kThreads, 0, lc.stream>>>(n, u, w, g, rs, e);
+  const Geo geo = geo_for(lc, n);
+  if (geo.cluster)
+    launch_geo(k_dot<1>, geo, lc.stream, n, u, w, g, rs, e);
+  else
+    launch_geo(k_dot<0>, geo, lc.stream, n, u, w, g, rs, e);
+  launch_finalize<2>(lc, geo, g, rs, e);
 }
 
-template <int RED>
+template <int RED, int CL>
 __global__ void __launch_bounds__(kThreads) k_scale(long n, const cplx* __restrict__ in, const double* s,
                                                       cplx* __restrict__ out, Gate g, RedScratch rs, Epi e) {
   if (!gate_open(g)) return;
@@ -400,17 +401,22 @@ __global__ void __launch_bounds__(kThreads) k_scale(long n, const cplx* __restri
     if (out) out[k] = y;
     if (RED) red[0] += y.x * y.x + y.y * y.y;
   }
-  if (RED) finish<1>(red, rs, e);
+  if constexpr (RED != 0) finish<1, CL>(red, rs, e);
 }
 
 void launch_scale(const LaunchCfg& lc, long n, const cplx* in, const double* s, cplx* out, int red, Gate g,
                   RedScratch rs, Epi e) {
   ++g_launch_count;
-  const int blocks = blocks_for(lc, n);
-  if (red)
-    k_scale<1><<<blocks, kThreads, 0, lc.stream>>>(n, in, s, out, g, rs, e);
-  else
-    k_scale<0><<<blocks, kThreads, 0, lc.stream>>>(n, in, s, out, g, rs, e);
+  if (red) {
+    const Geo geo = geo_for(lc, n);
+    if (geo.cluster)
+      launch_geo(k_scale<1, 1>, geo, lc.stream, n, in, s, out, g, rs, e);
+    else
+      launch_geo(k_scale<1, 0>, geo, lc.stream, n, in, s, out, g, rs, e);
+    launch_finalize<1>(lc, geo, g, rs, e);
+  } else {
+    k_scale<0, 0><<<blocks_for(lc, n), kThreads, 0, lc.stream>>>(n, in, s, out, g, rs, e);
+  }
 }
 
 __global__ void k_zero(long n, cplx* out, Gate g) {

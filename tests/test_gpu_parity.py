@@ -86,8 +86,17 @@ def test_galerkin_device(hadr, case, request):
         assert err <= 1e-12 * abs(ref).max(), (l, err)
 
 
+@pytest.fixture(params=["cluster", "graph"])
+def engine(request, hadr):
+    """Run a test with the coarse levels in the single-cluster engine (default)
+    and with every operation as its own kernel (ce_max_n = 0)."""
+    hadr._lib.set_option("ce_max_n", 32768 if request.param == "cluster" else 0)
+    yield request.param
+    hadr._lib.set_option("ce_max_n", 32768)
+
+
 @pytest.mark.parametrize("case", ["g33", "g65"])
-def test_relax_and_kcycle(hadr, case, request):
+def test_relax_and_kcycle(hadr, case, request, engine):
     g = request.getfixturevalue(case)
     n = int(g["n_levels"])
     shapes = [tuple(s) for s in g["shapes"]]
@@ -98,13 +107,15 @@ def test_relax_and_kcycle(hadr, case, request):
     nc = ops[-1].shape[0]
     assert rel(hadr.gmres_relax(H.ops[-1], b[:nc], np.zeros(nc, complex), 10), g["relax10_coarsest"]) <= 1e-12
     stats = {}
-    z = hadr.k_cycle(H, 1, b, np.zeros_like(b), stats)
+    z = hadr.k_cycle(H, 1, b, np.zeros_like(b), stats)  # stats mode: per-op kernels, counted visits
     assert rel(z, g["kcycle"]) <= 1e-12
     assert [stats.get(l, 0) for l in range(1, n + 1)] == g["kcycle_visits"].tolist()
+    z = hadr.k_cycle(H, 1, b, np.zeros_like(b))  # engine under test
+    assert rel(z, g["kcycle"]) <= 1e-12
     # the graph-captured preconditioner path gives the same result
     M = hadr.make_kcycle_preconditioner(H)
     assert rel(M(b), g["kcycle"]) <= 1e-12
-    assert rel(M(b), z) == 0.0  # deterministic reductions
+    assert rel(M(b), z) == 0.0  # deterministic reductions, identical op sequence
 
 
 def _floor(p, O, tol):
@@ -128,7 +139,7 @@ def _floor(p, O, tol):
 
 
 @pytest.mark.parametrize("case", ["g33", "g65", "gcfg1"])
-def test_solve_upwind_vs_oracle(hadr, case, request):
+def test_solve_upwind_vs_oracle(hadr, case, request, engine):
     from oracle import hadr_oracle as O
     from paper_1712_06091_b200 import workloads
 

@@ -1,0 +1,90 @@
+"""Small driver for ncu launch lists: one warm-up solve, then one profiled solve
+of the bench workload with a capped outer iteration count.
+
+    python tools/prof_solve.py --n 1025 --its 2
+"""
+
+import argparse
+import ctypes as C
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=1025)
+    ap.add_argument("--its", type=int, default=2)
+    ap.add_argument("--warm", type=int, default=1)
+    args = ap.parse_args()
+    from paper_1712_06091_b200 import _lib, workloads
+    from paper_1712_06091_b200.fields import point_source
+    from paper_1712_06091_b200.operators import rhs_transform
+
+    L = _lib.lib()
+    wl = workloads.cfg2(args.n)
+    g = wl.grid
+    n1, n2 = g.shape
+    qhat = rhs_transform(point_source(g, wl.source), wl.tt, wl.omega, "to_adr").reshape(-1)
+    codes = np.array([1, 1, 1, 1], dtype=np.int32)
+    f = [np.ascontiguousarray(x, dtype=np.float64) for x in
+         (wl.medium.kappa_sq, wl.medium.gamma, wl.tt.grad1, wl.tt.grad2, wl.tt.lap)]
+    a = np.empty(n1 * n2, complex)
+    rep = _lib.HadrReport()
+    hist = np.zeros(2000)
+    ts = C.c_double()
+
+    def solve(its):
+        _lib.check(L.hadr_solve_adr_upwind(n1, n2, g.h1, g.h2, wl.omega, _lib.cbuf(codes), wl.source.i1,
+                                           wl.source.i2, *[_lib.cbuf(x) for x in f], _lib.cbuf(qhat), 0.25, 5, 5,
+                                           its, 1e-6, _lib.cbuf(a), C.byref(rep), _lib.cbuf(hist), 2000,
+                                           C.byref(ts), 0))
+        return rep.device_time
+
+    for _ in range(args.warm):
+        solve(args.its)
+    k0 = L.hadr_launch_count()
+    t = solve(args.its)
+    print(f"profiled solve: its={rep.iterations} device_time={t*1e3:.3f} ms kernels={L.hadr_launch_count()-k0}")
+
+
+
+
+def ce_breakdown(n=1025, its=1000):
+    """Phase breakdown of the cluster engine over one solve."""
+    from paper_1712_06091_b200 import _lib
+
+    L = _lib.lib()
+    _lib.set_option("ce_profile", 1)
+    out = (C.c_ulonglong * 8)()
+    L.hadr_ce_profile(out, 1)
+    sys.argv = [sys.argv[0], "--n", str(n), "--its", str(its), "--warm", "0"]
+    main()
+    L.hadr_ce_profile(out, 1)
+    tot, ar, nar, ep, nep, st, nst, launches = list(out)
+    print(f"CE launches={launches} total={tot/1.9e3:.0f}us  allreduce={ar/1.9e3:.0f}us n={nar} ({ar/max(nar,1)/1.9:.0f} ns/op)  "
+          f"epilogue={ep/1.9e3:.0f}us n={nep} ({ep/max(nep,1)/1.9:.0f} ns)  stencil={st/1.9e3:.0f}us n={nst} ({st/max(nst,1)/1.9:.0f} ns)")
+
+
+def sweep_ce(n=1025, values=(0, 32768, 70000, 270000)):
+    from paper_1712_06091_b200 import _lib
+
+    for v in values:
+        _lib.set_option("ce_max_n", v)
+        sys.argv = [sys.argv[0], "--n", str(n), "--its", "1000", "--warm", "1"]
+        print(f"ce_max_n={v}: ", end="")
+        main()
+
+
+if __name__ == "__main__":
+    if "--sweep" in sys.argv:
+        sweep_ce()
+    elif "--ce" in sys.argv:
+        sys.argv.remove("--ce")
+        ce_breakdown(int(sys.argv[sys.argv.index("--n") + 1]) if "--n" in sys.argv else 1025)
+    else:
+        main()
