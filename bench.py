@@ -152,7 +152,7 @@ def run_ours(args, ws, rank, local, dist):
     from paper_1712_06091_b200.operators import rhs_transform
 
     L = _lib.lib()
-    wl = workloads.by_name(args.workload, args.n)
+    wl = workloads.by_name(args.workload, args.size)
     g = wl.grid
     n1, n2 = g.shape
     N = n1 * n2
@@ -262,40 +262,24 @@ def run_ours(args, ws, rank, local, dist):
 
 
 def kernel_roofline(H, L, wl, cfg, args):
-    """Time the fine-level stencil apply of the K-cycle (the most frequent full-grid
-    sweep) with CUDA events on the library stream and compare its algorithmic bytes."""
-    import ctypes as C
+    """K1 — the fine-level relaxation stencil y = A(D^-1 s x) with the basis write
+    and the fused <V0, y> — timed live with CUDA events on the library stream
+    (back-to-back launches, no host sync), against its algorithmic bytes."""
+    sys.path.insert(0, os.path.join(REPO, "tools"))
+    from k1_kernel import k1_measure
 
-    from paper_1712_06091_b200 import _lib, operators
-    from paper_1712_06091_b200.operators import blend_operator
-
-    g = wl.grid
-    H2 = operators.assemble_adr(wl.medium, g, wl.omega, wl.tt, "upwind2", wl.bc)
-    H1 = operators.assemble_adr(wl.medium, g, wl.omega, wl.tt, "upwind1", wl.bc)
-    B = blend_operator(H2, H1, 0.25)
-    N = g.n_nodes
-    import torch
-
-    x = torch.randn(N, dtype=torch.complex128, device="cuda")
-    y = torch.empty_like(x)
-    torch.cuda.synchronize()
-    reps = 50
-    for _ in range(5):
-        L.hadr_op_apply(B.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), 1)
-    L.hadr_stream_timer(1)
-    for _ in range(reps):
-        L.hadr_op_apply(B.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), 1)
-    ms = L.hadr_stream_timer(0) / reps
-    nnz = B.nnz
-    planes = len(B.offsets)
-    alg = (nnz + 2 * N) * 16  # coefficients (non-zeros) + x read + y write
-    moved = (planes * N + 2 * N) * 16
+    m = k1_measure(wl, reps=50, variant=1)
     hbm, src = peaks()
-    ach = alg / (ms * 1e-3) / 1e9
-    return {"kernel": "k_stencil (fine level, blend operator, y = A x)", "bound": "hbm", "achieved": ach,
-            "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None, "peak_source": src,
-            "algorithmic_bytes_per_launch": alg, "layout_bytes_per_launch": moved,
-            "avg_launch_ms": ms, "note": "host API sync per launch included in the event window"}
+    ach = m["algorithmic_bytes_per_launch"] / (m["avg_launch_ms"] * 1e-3) / 1e9
+    traffic = None
+    try:  # dram__bytes_read.sum + dram__bytes_write.sum from the committed ncu --set full capture
+        with open(os.path.join(REPO, "profiles", "k1_ncu.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return {"kernel": "k_stencil<IN_SCALE|IN_JAC|IN_WRITEV, APPLY, RED_DOT> (K1, fine level 1025^2, blend operator)",
+            "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+            "peak_source": src, **m}
 
 
 # --------------------------------------------------------------------------
@@ -333,7 +317,7 @@ def run_reference(args, ws, rank, local, dist):
         return None
     from paper_1712_06091_b200 import workloads
 
-    wl = workloads.by_name(args.workload, args.n)
+    wl = workloads.by_name(args.workload, args.size)
     N = wl.grid.n_nodes
     for _ in range(args.warmup):
         _oracle_step(wl, 1, args.tol)
@@ -374,7 +358,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2")
-    ap.add_argument("--n", type=int, default=None, help="override grid size (parity/debug)")
+    ap.add_argument("--size", type=int, default=None, help="override the grid size n (parity/debug runs)")
     ap.add_argument("--tol", type=float, default=1e-6)
     ap.add_argument("--maxiter", type=int, default=1000)
     ap.add_argument("--cpu-its", type=int, default=6, help="outer iterations in the cpu_baseline sample")

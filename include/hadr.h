@@ -123,6 +123,10 @@ int hadr_set_option(const char* name, double value);
 /* cluster-engine phase counters (enable with hadr_set_option("ce_profile", 1)): cycles seen by CTA 0
  * [total, allreduce, n_allreduce, scalar epilogue, n_epilogue, stencil, n_stencil, launches] */
 int hadr_ce_profile(unsigned long long* out8, int reset);
+/* microbenchmark of the stencil kernel K1 on device vectors x, y: `reps` back-to-back launches timed
+ * with CUDA events on the library stream; variant 0 = y = A x, 1 = the relaxation's fused
+ * y = A(D^-1 s x) + basis write + <V0, y>.  *avg_ms = mean launch duration (incl. any finalize). */
+int hadr_op_bench(hadr_op op, const double* x, double* y, int reps, int variant, double* avg_ms);
 /* number of kernels this library has launched so far (graph launches add their kernel nodes) */
 long long hadr_launch_count(void);
 /* CUDA-event timer on the library stream: start=1 records the start event (returns 0);

@@ -25,7 +25,7 @@ EXPORTS = (
     "hadr_op_destroy", "hadr_transfer", "hadr_hier_create", "hadr_hier_from_ops", "hadr_hier_info",
     "hadr_hier_level_op", "hadr_kcycle", "hadr_precond_apply", "hadr_hier_destroy", "hadr_gmres_relax",
     "hadr_fgmres", "hadr_launch_count", "hadr_assemble", "hadr_solve_adr_upwind", "hadr_pool_trim",
-    "hadr_stream_timer", "hadr_set_option", "hadr_ce_profile",
+    "hadr_stream_timer", "hadr_set_option", "hadr_ce_profile", "hadr_op_bench",
 )
 
 
@@ -68,6 +68,7 @@ _SIGS = {
     "hadr_stream_timer": (_d, [_i]),
     "hadr_set_option": (_i, [C.c_char_p, _d]),
     "hadr_ce_profile": (_i, [_vp, _i]),
+    "hadr_op_bench": (_i, [_vp, _vp, _vp, _i, _i, C.POINTER(_d)]),
     "hadr_transfer": (_i, [_i, _i, _i, _vp, _vp, _i]),
     "hadr_hier_create": (_i, [_vp, _i, _i, _d, C.POINTER(_vp)]),
     "hadr_hier_from_ops": (_i, [_i, _vp, _i, _d, C.POINTER(_vp)]),

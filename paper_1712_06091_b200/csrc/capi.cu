@@ -346,6 +346,52 @@ int hadr_precond_apply(hadr_hier hh, const double* r, double* z, int on_device) 
 
 long long hadr_launch_count(void) { return g_launch_count; }
 
+int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, double* avg_ms) {
+  return guarded([&] {
+    Ctx& c = Ctx::get();
+    Op* op = h->op;
+    const cplx* xd = (const cplx*)x;
+    cplx* yd = (cplx*)y;
+    cplx* vtmp = dalloc<cplx>(op->N);
+    double* sc = c.dscal + 56;
+    const double one = 1.0;
+    HADR_CUDA(cudaMemcpyAsync(sc, &one, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    auto once = [&]() {
+      StencilArgs a{};
+      a.A = op->dev();
+      a.x = xd;
+      a.y = yd;
+      a.gate = gate_always();
+      a.rs = c.rs;
+      if (variant == 0) {  // y = A x
+        a.epi = epi_none();
+        launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_NONE, a);
+      } else {             // relaxation Arnoldi input: y = A (D^-1 (s x)), V = s x, <V0, y>
+        a.scale = sc;
+        a.dinv = op->inv_diag();
+        a.vout = vtmp;
+        a.u = xd;
+        a.epi = epi_store(c.dscal);
+        launch_stencil(c.lc, IN_SCALE | IN_JAC | IN_WRITEV, OUT_APPLY, RED_DOT, a);
+      }
+    };
+    for (int i = 0; i < 3; ++i) once();
+    cudaEvent_t e0, e1;
+    HADR_CUDA(cudaEventCreate(&e0));
+    HADR_CUDA(cudaEventCreate(&e1));
+    HADR_CUDA(cudaEventRecord(e0, c.stream));
+    for (int i = 0; i < reps; ++i) once();
+    HADR_CUDA(cudaEventRecord(e1, c.stream));
+    HADR_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    HADR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *avg_ms = ms / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    dfree(vtmp);
+  });
+}
+
 int hadr_ce_profile(unsigned long long* out8, int reset) {
   return guarded([&] {
     Ctx::get().sync();

@@ -205,7 +205,7 @@ static void launch_finalize(const LaunchCfg& lc, const Geo& geo, Gate g, RedScra
 //   reductions: ||y||^2, <u, y> (u = array, or the centre input with RED_DOT_CENTER)
 // ---------------------------------------------------------------------------
 template <int INM, int OUTM, int RED, int NO, int CL>
-__global__ void __launch_bounds__(kThreads) k_stencil(StencilArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_stencil(StencilArgs a) {
   if (!gate_open(a.gate)) return;
   const int n1 = a.A.n1, n2 = a.A.n2, nofs = a.A.nofs;
   const long N = (long)n1 * n2;

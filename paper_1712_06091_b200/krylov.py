@@ -119,7 +119,10 @@ def fgmres(A, b, x0=None, precond=None, cfg: KrylovConfig | None = None):
     cfg = cfg or KrylovConfig()
     if not cfg.flexible:
         raise ValueError("the K-cycle is a varying preconditioner: only flexible GMRES is supported")
-    op = as_operator(A, getattr(A, "grid_shape", None))
+    grid = getattr(A, "grid_shape", None)
+    if grid is None and isinstance(precond, KCyclePreconditioner):
+        grid = precond.hier.shapes[0]  # a scipy A on the hierarchy's finest grid
+    op = as_operator(A, grid)
     n = op.shape[0]
     b = as_c128(b, n)
     x0a = None if x0 is None else as_c128(x0, n)
