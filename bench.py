@@ -154,15 +154,23 @@ def run_ours(args, ws, rank, local, dist):
     L = _lib.lib()
     wl = workloads.by_name(args.workload, args.size)
     g = wl.grid
-    n1, n2 = g.shape
+    n1, n2 = g.shape[0], g.shape[1]
     N = n1 * n2
     cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=args.tol, max_iter=args.maxiter)
     qhat = rhs_transform(point_source(g, wl.source), wl.tt, wl.omega, "to_adr").reshape(-1)
-    codes = np.array([0 if k == "neumann" else 1 for k in wl.bc], dtype=np.int32)
+    from paper_1712_06091_b200.operators import _bc
+
+    codes = _bc(wl.bc).codes()
+    dim = len(g.shape)
+    n3 = g.shape[2] if dim == 3 else 1
+    hs = tuple(g.hs) + (1.0,)
+    src = tuple(wl.source.index) + (0,)
     # ---- device-resident inputs ----
     dev = torch.device("cuda", local)
+    grads = list(wl.tt.grads) + [np.zeros(g.shape)] * (3 - dim)
     fields = [torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
-              for x in (wl.medium.kappa_sq, wl.medium.gamma, wl.tt.grad1, wl.tt.grad2, wl.tt.lap)]
+              for x in [wl.medium.kappa_sq, wl.medium.gamma] + grads + [wl.tt.lap]]
+    N = N * n3
     q_d = torch.from_numpy(qhat).to(dev)
     a_d = torch.empty(N, dtype=torch.complex128, device=dev)
     torch.cuda.synchronize()
@@ -173,8 +181,8 @@ def run_ours(args, ws, rank, local, dist):
 
     def step_device():
         _lib.check(L.hadr_solve_adr_upwind(
-            n1, n2, float(g.h1), float(g.h2), float(wl.omega), _lib.cbuf(codes), wl.source.i1, wl.source.i2,
-            *[C.c_void_p(f.data_ptr()) for f in fields], C.c_void_p(q_d.data_ptr()), float(cfg.beta),
+            dim, n1, n2, n3, float(hs[0]), float(hs[1]), float(hs[2]), float(wl.omega), _lib.cbuf(codes), src[0],
+            src[1], src[2], *[C.c_void_p(f.data_ptr()) for f in fields], C.c_void_p(q_d.data_ptr()), float(cfg.beta),
             int(cfg.levels), int(cfg.restart), int(cfg.max_iter), float(cfg.tol), C.c_void_p(a_d.data_ptr()),
             C.byref(rep), _lib.cbuf(hist), cap, C.byref(tset), 1))
         return rep.iterations, tset.value, rep.device_time
@@ -219,7 +227,7 @@ def run_ours(args, ws, rank, local, dist):
         e2e_its += r.iterations
     t_e2e = max_over_ranks(time.perf_counter() - t0, dist)
     e2e_value = sum_over_ranks(N * e2e_its / 1e6, dist) / t_e2e
-    h2d = 5 * 8 * N  # kappa^2, gamma, grad1, grad2, lap(tau)  (+ qhat below)
+    h2d = (3 + dim) * 8 * N  # kappa^2, gamma, grad(tau) per axis, lap(tau)  (+ qhat below)
     h2d += 16 * N
     d2h = 16 * N
     agree = float(np.linalg.norm(a.reshape(-1) - a_dev) / np.linalg.norm(a_dev))

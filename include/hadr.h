@@ -10,7 +10,8 @@
  *
  * Conventions
  *   - complex vectors are interleaved (re, im) doubles, numpy complex128 layout,
- *     flattened row-major over (n1, n2): k = i1*n2 + i2 (helmadr/grid.py:5-9);
+ *     flattened row-major over (n1, n2[, n3]): k = (i1*n2 + i2)*n3 + i3, the last
+ *     axis (depth) fastest (helmadr/grid.py:5-9); 2D grids pass n3 = 1;
  *   - `on_device` = 0: pointers are host memory (copied in/out inside the call);
  *     `on_device` = 1: pointers are device memory on the current CUDA device;
  *   - inputs are never modified (helmadr/krylov.py:93, 138);
@@ -59,11 +60,11 @@ int hadr_memcpy(void* dst, const void* src, size_t bytes, int kind);
 /* ---- operators (helmadr/operators.py CSR matrices, as structured stencils) ---- */
 /* From a canonical CSR matrix on the (n1, n2) grid; replaces the scipy CSR consumed by
  * helmadr/krylov.py:60-65 spmv and helmadr/multigrid.py:113 build_hierarchy. */
-int hadr_op_from_csr(int n1, int n2, int64_t nnz, const int64_t* indptr, const int32_t* indices,
+int hadr_op_from_csr(int n1, int n2, int n3, int64_t nnz, const int64_t* indptr, const int32_t* indices,
                      const double* data, hadr_op* out);
-/* From coefficient planes coef[o*N + k] for offsets (d1, d2) strictly ascending. */
-int hadr_op_from_planes(int n1, int n2, int n_offsets, const int* offsets, const double* coef, hadr_op* out);
-int hadr_op_info(hadr_op op, int* n1, int* n2, int* n_offsets, int* offsets /* 2*25 */);
+/* From coefficient planes coef[o*N + k] for offsets (d1, d2, d3) strictly ascending (2D: d3 = 0). */
+int hadr_op_from_planes(int n1, int n2, int n3, int n_offsets, const int* offsets, const double* coef, hadr_op* out);
+int hadr_op_info(hadr_op op, int* n1, int* n2, int* n3, int* n_offsets, int* offsets /* 3*125 */);
 int hadr_op_export(hadr_op op, double* coef /* n_offsets*N complex */);
 /* y = A x  (helmadr/krylov.py:60-65 spmv; scipy csr_matvec order, bit-exact) */
 int hadr_op_apply(hadr_op op, const double* x, double* y, int on_device);
@@ -77,29 +78,34 @@ int hadr_op_add_diag(hadr_op A, double sr, double si, const double* field, hadr_
 int hadr_op_similarity(hadr_op A, const double* left, const double* right, hadr_op* out);
 /* P^T A P for bilinear P (helmadr/multigrid.py:49-55 galerkin_coarsen) */
 int hadr_op_galerkin(hadr_op A, hadr_op* out);
-/* On-device assembly (helmadr/operators.py:190-234): scheme 0 central, 1 upwind1, 2 upwind2 ADR
- * (assemble_adr), 3 Helmholtz (assemble_helmholtz; grad/lap ignored).  bc = (top, bottom, left,
- * right), 0 neumann / 1 sommerfeld.  src = node of the point source (near-source central
- * stencil), (-1, -1) for none.  Fields are host arrays of n1*n2 doubles. */
-int hadr_assemble(int n1, int n2, double h1, double h2, double omega, int scheme, const int* bc, int src1, int src2,
-                  const double* kappa_sq, const double* gamma, const double* grad1, const double* grad2,
-                  const double* lap_tau, int on_device, hadr_op* out);
+/* On-device assembly (helmadr/operators.py:190-234; 3D: the per-axis restatement):
+ * scheme 0 central, 1 upwind1, 2 upwind2 ADR (assemble_adr), 3 Helmholtz (assemble_helmholtz;
+ * grad/lap ignored).  dim 2 or 3; bc = (top, bottom, left, right, front, back) face kinds,
+ * 0 neumann / 1 sommerfeld (front/back unused in 2D).  src = node of the point source
+ * (near-source central stencil), src1 = -1 for none.  Fields are arrays of n1*n2*n3 doubles
+ * (host, or device with on_device = 1); grad3 unused in 2D. */
+int hadr_assemble(int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega, int scheme,
+                  const int* bc, int src1, int src2, int src3, const double* kappa_sq, const double* gamma,
+                  const double* grad1, const double* grad2, const double* grad3, const double* lap_tau, int on_device,
+                  hadr_op* out);
 /* solve_adr_upwind (helmadr/drivers.py:136-168) minus the host-side phase transforms:
  * assemble H2up, H1up, blend (1-beta)H2up + beta H1up, build the hierarchy, FGMRES on H2up
  * with the K-cycle on the blend.  qhat is the transformed source (to_adr).  *t_setup gets the
  * device time of assembly + hierarchy; rep->device_time the FGMRES time. */
-int hadr_solve_adr_upwind(int n1, int n2, double h1, double h2, double omega, const int* bc, int src1, int src2,
-                          const double* kappa_sq, const double* gamma, const double* grad1, const double* grad2,
-                          const double* lap_tau, const double* qhat, double beta, int levels, int restart,
-                          int maxiter, double tol, double* a_out, hadr_report* rep, double* history, int history_cap,
-                          double* t_setup, int on_device);
+int hadr_solve_adr_upwind(int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega,
+                          const int* bc, int src1, int src2, int src3, const double* kappa_sq, const double* gamma,
+                          const double* grad1, const double* grad2, const double* grad3, const double* lap_tau,
+                          const double* qhat, double beta, int levels, int restart, int maxiter, double tol,
+                          double* a_out, hadr_report* rep, double* history, int history_cap, double* t_setup,
+                          int on_device);
 /* release recycled hierarchies and cached device blocks */
 int hadr_pool_trim(void);
 void hadr_op_destroy(hadr_op op);
 
 /* ---- transfer operators (helmadr/multigrid.py:19-46) ---- */
-/* rc = P^T r (direction 0) or y = P e (direction 1) for the fine grid (n1, n2). */
-int hadr_transfer(int n1, int n2, int direction, const double* in, double* out, int on_device);
+/* rc = P^T r (direction 0) or y = P e (direction 1) for the fine grid (n1, n2, n3); P is the
+ * bilinear (2D, n3 = 1) / trilinear (3D) interpolation of helmadr/multigrid.py:19-46. */
+int hadr_transfer(int n1, int n2, int n3, int direction, const double* in, double* out, int on_device);
 
 /* ---- multigrid (helmadr/multigrid.py) ---- */
 /* build_hierarchy(A0, grid, max_levels) with Galerkin coarse operators built on the device.
@@ -107,7 +113,7 @@ int hadr_transfer(int n1, int n2, int direction, const double* in, double* out, 
 int hadr_hier_create(hadr_op fine, int max_levels, int coarse_steps, double coarse_tol, hadr_hier* out);
 /* MGHierarchy(ops=...) from given per-level operators (finest first; borrowed). */
 int hadr_hier_from_ops(int n_levels, const hadr_op* ops, int coarse_steps, double coarse_tol, hadr_hier* out);
-int hadr_hier_info(hadr_hier h, int* n_levels, int* shapes /* 2*n_levels */);
+int hadr_hier_info(hadr_hier h, int* n_levels, int* shapes /* 3*n_levels */);
 /* borrowed handle to level `level` (1-based) operator */
 int hadr_hier_level_op(hadr_hier h, int level, hadr_op* out);
 /* k_cycle(hier, level, b, x) (helmadr/multigrid.py:132-171); x may be NULL (zero);

@@ -50,9 +50,9 @@ _SIGS = {
     "hadr_device_malloc": (_i, [C.POINTER(_vp), C.c_size_t]),
     "hadr_device_free": (_i, [_vp]),
     "hadr_memcpy": (_i, [_vp, _vp, C.c_size_t, _i]),
-    "hadr_op_from_csr": (_i, [_i, _i, _i64, _vp, _vp, _vp, C.POINTER(_vp)]),
-    "hadr_op_from_planes": (_i, [_i, _i, _i, _vp, _vp, C.POINTER(_vp)]),
-    "hadr_op_info": (_i, [_vp, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), _vp]),
+    "hadr_op_from_csr": (_i, [_i, _i, _i, _i64, _vp, _vp, _vp, C.POINTER(_vp)]),
+    "hadr_op_from_planes": (_i, [_i, _i, _i, _i, _vp, _vp, C.POINTER(_vp)]),
+    "hadr_op_info": (_i, [_vp, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), _vp]),
     "hadr_op_export": (_i, [_vp, _vp]),
     "hadr_op_apply": (_i, [_vp, _vp, _vp, _i]),
     "hadr_op_jacobi": (_i, [_vp, _vp, _vp, _i]),
@@ -61,15 +61,16 @@ _SIGS = {
     "hadr_op_similarity": (_i, [_vp, _vp, _vp, C.POINTER(_vp)]),
     "hadr_op_galerkin": (_i, [_vp, C.POINTER(_vp)]),
     "hadr_op_destroy": (None, [_vp]),
-    "hadr_assemble": (_i, [_i, _i, _d, _d, _d, _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, C.POINTER(_vp)]),
-    "hadr_solve_adr_upwind": (_i, [_i, _i, _d, _d, _d, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _d, _i, _i, _i,
-                                   _d, _vp, C.POINTER(HadrReport), _vp, _i, C.POINTER(_d), _i]),
+    "hadr_assemble": (_i, [_i, _i, _i, _i, _d, _d, _d, _d, _i, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i,
+                           C.POINTER(_vp)]),
+    "hadr_solve_adr_upwind": (_i, [_i, _i, _i, _i, _d, _d, _d, _d, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp,
+                                   _vp, _d, _i, _i, _i, _d, _vp, C.POINTER(HadrReport), _vp, _i, C.POINTER(_d), _i]),
     "hadr_pool_trim": (_i, []),
     "hadr_stream_timer": (_d, [_i]),
     "hadr_set_option": (_i, [C.c_char_p, _d]),
     "hadr_ce_profile": (_i, [_vp, _i]),
     "hadr_op_bench": (_i, [_vp, _vp, _vp, _i, _i, C.POINTER(_d)]),
-    "hadr_transfer": (_i, [_i, _i, _i, _vp, _vp, _i]),
+    "hadr_transfer": (_i, [_i, _i, _i, _i, _vp, _vp, _i]),
     "hadr_hier_create": (_i, [_vp, _i, _i, _d, C.POINTER(_vp)]),
     "hadr_hier_from_ops": (_i, [_i, _vp, _i, _d, C.POINTER(_vp)]),
     "hadr_hier_info": (_i, [_vp, C.POINTER(_i), _vp]),

@@ -98,27 +98,29 @@ int hadr_memcpy(void* dst, const void* src, size_t bytes, int kind) {
   });
 }
 
-int hadr_op_from_csr(int n1, int n2, int64_t nnz, const int64_t* indptr, const int32_t* indices, const double* data,
-                     hadr_op* out) {
+int hadr_op_from_csr(int n1, int n2, int n3, int64_t nnz, const int64_t* indptr, const int32_t* indices,
+                     const double* data, hadr_op* out) {
   return guarded([&] {
-    if (n1 < 1 || n2 < 1) throw ValueError("grid dimensions must be positive");
-    *out = wrap(op_from_csr(n1, n2, nnz, indptr, indices, (const cplx*)data));
+    if (n1 < 1 || n2 < 1 || n3 < 1) throw ValueError("grid dimensions must be positive");
+    *out = wrap(op_from_csr(n1, n2, n3, nnz, indptr, indices, (const cplx*)data));
   });
 }
 
-int hadr_op_from_planes(int n1, int n2, int n_offsets, const int* offsets, const double* coef, hadr_op* out) {
-  return guarded([&] { *out = wrap(op_from_planes(n1, n2, n_offsets, offsets, (const cplx*)coef)); });
+int hadr_op_from_planes(int n1, int n2, int n3, int n_offsets, const int* offsets, const double* coef, hadr_op* out) {
+  return guarded([&] { *out = wrap(op_from_planes(n1, n2, n3, n_offsets, offsets, (const cplx*)coef)); });
 }
 
-int hadr_op_info(hadr_op h, int* n1, int* n2, int* n_offsets, int* offsets) {
+int hadr_op_info(hadr_op h, int* n1, int* n2, int* n3, int* n_offsets, int* offsets) {
   return guarded([&] {
     const Op* op = h->op;
     *n1 = op->n1;
     *n2 = op->n2;
+    *n3 = op->n3;
     *n_offsets = op->nofs;
     for (int o = 0; o < op->nofs; ++o) {
-      offsets[2 * o] = op->d1[o];
-      offsets[2 * o + 1] = op->d2[o];
+      offsets[3 * o] = op->d1[o];
+      offsets[3 * o + 1] = op->d2[o];
+      offsets[3 * o + 2] = op->d3[o];
     }
   });
 }
@@ -174,34 +176,39 @@ int hadr_op_galerkin(hadr_op A, hadr_op* out) {
   return guarded([&] { *out = wrap(op_galerkin(*A->op)); });
 }
 
-int hadr_assemble(int n1, int n2, double h1, double h2, double omega, int scheme, const int* bc, int src1, int src2,
-                  const double* kappa_sq, const double* gamma, const double* grad1, const double* grad2,
-                  const double* lap_tau, int on_device, hadr_op* out) {
+int hadr_assemble(int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega, int scheme,
+                  const int* bc, int src1, int src2, int src3, const double* kappa_sq, const double* gamma,
+                  const double* grad1, const double* grad2, const double* grad3, const double* lap_tau, int on_device,
+                  hadr_op* out) {
   return guarded([&] {
-    *out = wrap(op_assemble(n1, n2, h1, h2, omega, scheme, bc, src1, src2, kappa_sq, gamma, grad1, grad2, lap_tau,
-                            on_device != 0));
+    *out = wrap(op_assemble(dim, n1, n2, n3, h1, h2, h3, omega, scheme, bc, src1, src2, src3, kappa_sq, gamma, grad1,
+                            grad2, grad3, lap_tau, on_device != 0));
   });
 }
 
-int hadr_solve_adr_upwind(int n1, int n2, double h1, double h2, double omega, const int* bc, int src1, int src2,
-                          const double* kappa_sq, const double* gamma, const double* grad1, const double* grad2,
-                          const double* lap_tau, const double* qhat, double beta, int levels, int restart,
-                          int maxiter, double tol, double* a_out, hadr_report* rep, double* history, int history_cap,
-                          double* t_setup, int on_device) {
+int hadr_solve_adr_upwind(int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega,
+                          const int* bc, int src1, int src2, int src3, const double* kappa_sq, const double* gamma,
+                          const double* grad1, const double* grad2, const double* grad3, const double* lap_tau,
+                          const double* qhat, double beta, int levels, int restart, int maxiter, double tol,
+                          double* a_out, hadr_report* rep, double* history, int history_cap, double* t_setup,
+                          int on_device) {
   return guarded([&] {
     Ctx& c = Ctx::get();
-    const long N = (long)n1 * n2;
+    if (dim == 2) n3 = 1;
+    const long N = (long)n1 * n2 * n3;
     cudaEvent_t e0, e1;
     HADR_CUDA(cudaEventCreate(&e0));
     HADR_CUDA(cudaEventCreate(&e1));
     HADR_CUDA(cudaEventRecord(e0, c.stream));
     // helmadr/drivers.py:153-157: assemble H2up, H1up, blend, hierarchy
-    Op* H2 = op_assemble(n1, n2, h1, h2, omega, 2, bc, src1, src2, kappa_sq, gamma, grad1, grad2, lap_tau, on_device);
+    Op* H2 = op_assemble(dim, n1, n2, n3, h1, h2, h3, omega, 2, bc, src1, src2, src3, kappa_sq, gamma, grad1, grad2,
+                         grad3, lap_tau, on_device);
     Op* H1 = nullptr;
     Op* B = nullptr;
     Hier* hier = nullptr;
     try {
-      H1 = op_assemble(n1, n2, h1, h2, omega, 1, bc, src1, src2, kappa_sq, gamma, grad1, grad2, lap_tau, on_device);
+      H1 = op_assemble(dim, n1, n2, n3, h1, h2, h3, omega, 1, bc, src1, src2, src3, kappa_sq, gamma, grad1, grad2,
+                       grad3, lap_tau, on_device);
       B = op_axpby(mk(1.0 - beta, 0.0), *H2, mk(beta, 0.0), *H1);
       delete H1;
       H1 = nullptr;
@@ -251,20 +258,22 @@ void hadr_op_destroy(hadr_op h) {
   delete h;
 }
 
-int hadr_transfer(int n1, int n2, int direction, const double* in, double* out, int on_device) {
+int hadr_transfer(int n1, int n2, int n3, int direction, const double* in, double* out, int on_device) {
   return guarded([&] {
-    if ((n1 - 1) % 2 || (n2 - 1) % 2) throw ValueError("cannot coarsen: interval count is odd");
+    if ((n1 - 1) % 2 || (n2 - 1) % 2 || (n3 > 1 && (n3 - 1) % 2))
+      throw ValueError("cannot coarsen: interval count is odd");
     Ctx& c = Ctx::get();
-    const long Nf = (long)n1 * n2, Nc = (long)((n1 - 1) / 2 + 1) * ((n2 - 1) / 2 + 1);
+    const long Nf = (long)n1 * n2 * n3;
+    const long Nc = (long)((n1 - 1) / 2 + 1) * ((n2 - 1) / 2 + 1) * ((n3 - 1) / 2 + 1);
     if (direction == 0) {
       DevVec di(in, Nf, on_device, true), dout(out, Nc, on_device, false);
-      launch_restrict(c.lc, n1, n2, di.p, dout.p, gate_always());
+      launch_restrict(c.lc, n1, n2, n3, di.p, dout.p, gate_always());
       HADR_CUDA(cudaGetLastError());
       dout.copy_out(out);
     } else {
       DevVec di(in, Nc, on_device, true), dout(out, Nf, on_device, false);
       HADR_CUDA(cudaMemsetAsync(dout.p, 0, Nf * sizeof(cplx), c.stream));
-      launch_prolong_add(c.lc, n1, n2, di.p, dout.p, gate_always());
+      launch_prolong_add(c.lc, n1, n2, n3, di.p, dout.p, gate_always());
       HADR_CUDA(cudaGetLastError());
       dout.copy_out(out);
     }
@@ -296,8 +305,9 @@ int hadr_hier_info(hadr_hier h, int* n_levels, int* shapes) {
     *n_levels = (int)h->h->lv.size();
     if (shapes)
       for (size_t i = 0; i < h->h->lv.size(); ++i) {
-        shapes[2 * i] = h->h->lv[i].n1;
-        shapes[2 * i + 1] = h->h->lv[i].n2;
+        shapes[3 * i] = h->h->lv[i].n1;
+        shapes[3 * i + 1] = h->h->lv[i].n2;
+        shapes[3 * i + 2] = h->h->lv[i].n3;
       }
   });
 }

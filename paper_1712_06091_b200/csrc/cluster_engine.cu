@@ -129,12 +129,13 @@ extern __shared__ cplx ce_tile[];
 template <int NO, int INM, int OUTM, int RED>
 __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double s, const cplx* dinv, cplx* vout,
                               const cplx* b, cplx* y, const cplx* u, double (&red)[3]) {
-  const int n1 = A.n1, n2 = A.n2, nofs = A.nofs;
-  const long N = (long)n1 * n2;
+  const int n1 = A.n1, n2 = A.n2, n3 = A.n3, nofs = A.nofs;
+  const int n23 = n2 * n3;
+  const long N = (long)n1 * n23;
   const int R = (n1 + (int)c.C - 1) / (int)c.C;
   const int r0 = min(n1, (int)c.rank * R), r1 = min(n1, r0 + R);
   const int t0 = max(0, r0 - 2), t1 = min(n1, r1 + 2);
-  const long base = (long)t0 * n2, tn = (long)(t1 - t0) * n2;
+  const long base = (long)t0 * n23, tn = (long)(t1 - t0) * n23;
   for (long p = threadIdx.x; p < tn; p += blockDim.x) {
     cplx v = ldm(x, base + p);
     if (INM & IN_SCALE) v = cscale(v, s);
@@ -142,21 +143,32 @@ __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double
     ce_tile[p] = v;
   }
   __syncthreads();
-  const long own1 = (long)r1 * n2;
-  for (long k = (long)r0 * n2 + threadIdx.x; k < own1; k += blockDim.x) {
-    const int i1 = (int)(k / n2);
-    const int i2 = (int)(k - (long)i1 * n2);
-    cplx cv[NO];
-#pragma unroll
-    for (int o = 0; o < NO; ++o) cv[o] = ldk(A.coef, o < nofs ? (long)o * N + k : k);
+  const long own1 = (long)r1 * n23;
+  for (long k = (long)r0 * n23 + threadIdx.x; k < own1; k += blockDim.x) {
+    const int i1 = (int)(k / n23);
+    const int rem = (int)(k - (long)i1 * n23);
+    const int i2 = rem / n3, i3 = rem - (rem / n3) * n3;
     cplx acc = mk(0.0, 0.0);
+    constexpr int CH = NO > 0 ? NO : 9;
+    const int nch = NO > 0 ? 1 : (nofs + CH - 1) / CH;
+    for (int ch = 0; ch < nch; ++ch) {
+      const int o0 = ch * CH;
+      cplx cv[CH];
 #pragma unroll
-    for (int o = 0; o < NO; ++o) {
-      const int j1 = i1 + A.d1[o], j2 = i2 + A.d2[o];
-      const bool ok = o < nofs && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2;
-      const cplx v = ce_tile[ok ? (long)(j1 - t0) * n2 + j2 : 0];
-      const cplx t = cadd(acc, cmul_sp(cv[o], v));
-      acc = ok ? t : acc;
+      for (int q = 0; q < CH; ++q) {
+        const int o = o0 + q;
+        cv[q] = ldk(A.coef, o < nofs ? (long)o * N + k : k);
+      }
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int o = o0 + q;
+        const int oo = o < nofs ? o : 0;
+        const int j1 = i1 + A.d1[oo], j2 = i2 + A.d2[oo], j3 = i3 + A.d3[oo];
+        const bool ok = o < nofs && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2 && j3 >= 0 && j3 < n3;
+        const cplx v = ce_tile[ok ? ((long)(j1 - t0) * n2 + j2) * n3 + j3 : 0];
+        const cplx t = cadd(acc, cmul_sp(cv[q], v));
+        acc = ok ? t : acc;
+      }
     }
     cplx vc = mk(0.0, 0.0);
     if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) {
@@ -178,15 +190,15 @@ __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double
 }
 
 template <int INM, int OUTM, int RED>
-__device__ __noinline__ void ce_stencil(CEC& c, const StencilDev& A, const cplx* x, double s, const cplx* dinv, cplx* vout,
-                           const cplx* b, cplx* y, const cplx* u, double (&red)[3]) {
+__device__ __noinline__ void ce_stencil(CEC& c, const StencilDev& A, const cplx* x, double s, const cplx* dinv,
+                                        cplx* vout, const cplx* b, cplx* y, const cplx* u, double (&red)[3]) {
   CEProfScope prof_(c, 5);
   red[0] = red[1] = red[2] = 0.0;
   switch (A.nofs) {
     case 5: ce_stencil_no<5, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
     case 9: ce_stencil_no<9, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
     case 21: ce_stencil_no<21, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
-    default: ce_stencil_no<25, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
+    default: ce_stencil_no<0, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
   }
 }
 
@@ -305,41 +317,64 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
 // ---------------------------------------------------------------------------
 // transfer operators (bit-exact orders, see kernels.cu)
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void ce_restrict(CEC& c, int n1f, int n2f, const cplx* r, cplx* rc) {
-  const int n1c = (n1f - 1) / 2 + 1, n2c = (n2f - 1) / 2 + 1;
-  const long Nc = (long)n1c * n2c;
+__device__ __noinline__ void ce_restrict(CEC& c, int n1f, int n2f, int n3f, const cplx* r, cplx* rc) {
+  const int n1c = (n1f - 1) / 2 + 1, n2c = (n2f - 1) / 2 + 1, n3c = (n3f - 1) / 2 + 1;
+  const long Nc = (long)n1c * n2c * n3c;
+  const int c3lo = n3f > 1 ? -1 : 0, c3hi = n3f > 1 ? 1 : 0;
   for (long q = c.gtid; q < Nc; q += c.gstride) {
-    const int I1 = (int)(q / n2c), I2 = (int)(q - (long)I1 * n2c);
+    const int I1 = (int)(q / ((long)n2c * n3c));
+    const int rem = (int)(q - (long)I1 * n2c * n3c);
+    const int I2 = rem / n3c, I3 = rem - (rem / n3c) * n3c;
     cplx acc = mk(0.0, 0.0);
-#pragma unroll
     for (int a = -1; a <= 1; ++a) {
       const int f1 = 2 * I1 + a;
       if (f1 < 0 || f1 >= n1f) continue;
       const double w1 = a == 0 ? 1.0 : 0.5;
-#pragma unroll
       for (int bb = -1; bb <= 1; ++bb) {
         const int f2 = 2 * I2 + bb;
         if (f2 < 0 || f2 >= n2f) continue;
-        const double w = w1 * (bb == 0 ? 1.0 : 0.5);
-        acc = cadd(acc, cmul_sp(mk(w, 0.0), ldm(r, (long)f1 * n2f + f2)));
+        const double w12 = w1 * (bb == 0 ? 1.0 : 0.5);
+        for (int cc = c3lo; cc <= c3hi; ++cc) {
+          const int f3 = 2 * I3 + cc;
+          if (f3 < 0 || f3 >= n3f) continue;
+          const double w = w12 * (cc == 0 ? 1.0 : 0.5);
+          acc = cadd(acc, cmul_sp(mk(w, 0.0), ldm(r, ((long)f1 * n2f + f2) * n3f + f3)));
+        }
       }
     }
     rc[q] = acc;
   }
 }
 
-__device__ __noinline__ void ce_prolong_add(CEC& c, int n1f, int n2f, const cplx* ec, cplx* x) {
-  const int n2c = (n2f - 1) / 2 + 1;
-  const long Nf = (long)n1f * n2f;
+__device__ __forceinline__ int ce_parents(int f, int* p, double& w) {
+  if (f & 1) {
+    p[0] = f >> 1;
+    p[1] = (f >> 1) + 1;
+    w = 0.5;
+    return 2;
+  }
+  p[0] = f >> 1;
+  p[1] = p[0];
+  w = 1.0;
+  return 1;
+}
+
+__device__ __noinline__ void ce_prolong_add(CEC& c, int n1f, int n2f, int n3f, const cplx* ec, cplx* x) {
+  const int n2c = (n2f - 1) / 2 + 1, n3c = (n3f - 1) / 2 + 1;
+  const int n23 = n2f * n3f;
+  const long Nf = (long)n1f * n23;
   for (long f = c.gtid; f < Nf; f += c.gstride) {
-    const int f1 = (int)(f / n2f), f2 = (int)(f - (long)f1 * n2f);
-    int c1[2], c2[2], m1, m2;
-    double w1, w2;
-    if (f1 & 1) { c1[0] = f1 >> 1; c1[1] = (f1 >> 1) + 1; m1 = 2; w1 = 0.5; } else { c1[0] = f1 >> 1; c1[1] = c1[0]; m1 = 1; w1 = 1.0; }
-    if (f2 & 1) { c2[0] = f2 >> 1; c2[1] = (f2 >> 1) + 1; m2 = 2; w2 = 0.5; } else { c2[0] = f2 >> 1; c2[1] = c2[0]; m2 = 1; w2 = 1.0; }
+    const int f1 = (int)(f / n23);
+    const int rem = (int)(f - (long)f1 * n23);
+    const int f2 = rem / n3f, f3 = rem - (rem / n3f) * n3f;
+    int c1[2], c2[2], c3[2];
+    double w1, w2, w3;
+    const int m1 = ce_parents(f1, c1, w1), m2 = ce_parents(f2, c2, w2), m3 = ce_parents(f3, c3, w3);
     cplx p = mk(0.0, 0.0);
     for (int a = 0; a < m1; ++a)
-      for (int bb = 0; bb < m2; ++bb) p = cadd(p, cmul_sp(mk(w1 * w2, 0.0), ldm(ec, (long)c1[a] * n2c + c2[bb])));
+      for (int bb = 0; bb < m2; ++bb)
+        for (int cc = 0; cc < m3; ++cc)
+          p = cadd(p, cmul_sp(mk(w1 * w2 * w3, 0.0), ldm(ec, ((long)c1[a] * n2c + c2[bb]) * n3c + c3[cc])));
     x[f] = cadd(ldm(x, f), p);
   }
 }
@@ -506,13 +541,13 @@ __device__ void ce_kcycle(CEC& c, int l, const cplx* b, cplx* xo) {
       ce_stencil<IN_PLAIN, OUT_RESID, RED_NONE>(c, L.A, xo, 1.0, nullptr, nullptr, b, L.r, nullptr, red);
       ce_sync();
     }
-    ce_restrict(c, L.A.n1, L.A.n2, L.r, C.fb);
+    ce_restrict(c, L.A.n1, L.A.n2, L.A.n3, L.r, C.fb);
     ce_sync();
     if (l + 1 == S->nlev - 1)
       ce_relax(c, C, C.fb, nullptr, C.fx, S->coarse_steps);
     else
       ce_inner<D + 1>(c, l + 1);
-    ce_prolong_add(c, L.A.n1, L.A.n2, C.fx, xo);
+    ce_prolong_add(c, L.A.n1, L.A.n2, L.A.n3, C.fx, xo);
     ce_sync();
     ce_relax(c, L, b, xo, xo, L.s);
   }

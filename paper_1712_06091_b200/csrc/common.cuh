@@ -16,7 +16,7 @@
 #include <stdint.h>
 
 #ifndef HADR_MAX_OFS
-#define HADR_MAX_OFS 25  // 2D: up to the 5x5 box (union of coarse upwind stencils is 21)
+#define HADR_MAX_OFS 125  // offsets in the 5x5(x5) box: 2D unions reach 21, 3D coarse upwind 81
 #endif
 
 typedef double2 cplx;

@@ -97,10 +97,12 @@ StencilDev Op::dev() const {
   StencilDev s{};
   s.n1 = n1;
   s.n2 = n2;
+  s.n3 = n3;
   s.nofs = nofs;
   for (int o = 0; o < nofs; ++o) {
     s.d1[o] = d1[o];
     s.d2[o] = d2[o];
+    s.d3[o] = d3[o];
   }
   s.coef = coef;
   return s;
@@ -108,7 +110,7 @@ StencilDev Op::dev() const {
 
 int Op::center() const {
   for (int o = 0; o < nofs; ++o)
-    if (d1[o] == 0 && d2[o] == 0) return o;
+    if (d1[o] == 0 && d2[o] == 0 && d3[o] == 0) return o;
   return -1;
 }
 
@@ -148,16 +150,22 @@ void Op::refresh_inv_diag() {
   if (hflag || ce < 0) throw ValueError("hierarchy operator has zero diagonal entries");
 }
 
+static void copy_geometry(Op* op, const Op& A) {
+  op->n1 = A.n1;
+  op->n2 = A.n2;
+  op->n3 = A.n3;
+  op->N = A.N;
+}
+
 Op* op_copy(const Op& A) {
   Ctx& c = Ctx::get();
   Op* op = new Op();
-  op->n1 = A.n1;
-  op->n2 = A.n2;
-  op->N = A.N;
+  copy_geometry(op, A);
   op->nofs = A.nofs;
   for (int o = 0; o < A.nofs; ++o) {
     op->d1[o] = A.d1[o];
     op->d2[o] = A.d2[o];
+    op->d3[o] = A.d3[o];
   }
   op->coef = dalloc<cplx>((size_t)A.nofs * A.N);
   HADR_CUDA(cudaMemcpyAsync(op->coef, A.coef, (size_t)A.nofs * A.N * sizeof(cplx), cudaMemcpyDeviceToDevice,
@@ -165,52 +173,62 @@ Op* op_copy(const Op& A) {
   return op;
 }
 
-static void set_offsets_from_mask(Op* op, unsigned mask, int* slot_of /*25*/) {
+static inline bool mask_has(const Mask125& m, int q) { return (m.w[q >> 6] >> (q & 63)) & 1ull; }
+static inline void mask_set(Mask125& m, int q) { m.w[q >> 6] |= 1ull << (q & 63); }
+static inline bool mask_eq(const Mask125& a, const Mask125& b) { return a.w[0] == b.w[0] && a.w[1] == b.w[1]; }
+
+// slots ascending == lexicographic (d1, d2, d3) == ascending CSR column for in-grid entries
+static void set_offsets_from_mask(Op* op, const Mask125& mask, int* slot_of /*125*/) {
   op->nofs = 0;
-  for (int q = 0; q < 25; ++q) slot_of[q] = -1;
-  for (int q = 0; q < 25; ++q) {  // q = (d1+2)*5 + (d2+2): ascending (d1, d2) == ascending column
-    if (mask & (1u << q)) {
+  for (int q = 0; q < 125; ++q) {
+    slot_of[q] = -1;
+    if (mask_has(mask, q)) {
       slot_of[q] = op->nofs;
-      op->d1[op->nofs] = (int8_t)(q / 5 - 2);
-      op->d2[op->nofs] = (int8_t)(q % 5 - 2);
+      op->d1[op->nofs] = (int8_t)(q / 25 - 2);
+      op->d2[op->nofs] = (int8_t)((q / 5) % 5 - 2);
+      op->d3[op->nofs] = (int8_t)(q % 5 - 2);
       op->nofs++;
     }
   }
 }
 
-Op* op_from_csr(int n1, int n2, long nnz, const int64_t* indptr, const int32_t* indices, const cplx* data) {
+static Mask125 layout_mask(const Op& A) {
+  Mask125 m{{0ull, 0ull}};
+  for (int o = 0; o < A.nofs; ++o) mask_set(m, slot125(A.d1[o], A.d2[o], A.d3[o]));
+  return m;
+}
+
+Op* op_from_csr(int n1, int n2, int n3, long nnz, const int64_t* indptr, const int32_t* indices, const cplx* data) {
   Ctx& c = Ctx::get();
-  const long N = (long)n1 * n2;
+  const long N = (long)n1 * n2 * n3;
   int64_t* dptr = dalloc<int64_t>(N + 1);
   int32_t* dind = dalloc<int32_t>(nnz);
   cplx* ddat = dalloc<cplx>(nnz);
-  unsigned* dmask = dalloc<unsigned>(2);
-  int* dslot = dalloc<int>(25);
+  unsigned long long* dmask = dalloc<unsigned long long>(3);
+  int* dslot = dalloc<int>(125);
   Op* op = new Op();
   op->n1 = n1;
   op->n2 = n2;
+  op->n3 = n3;
   op->N = N;
   try {
     HADR_CUDA(cudaMemcpyAsync(dptr, indptr, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
     HADR_CUDA(cudaMemcpyAsync(dind, indices, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, c.stream));
     HADR_CUDA(cudaMemcpyAsync(ddat, data, nnz * sizeof(cplx), cudaMemcpyHostToDevice, c.stream));
-    HADR_CUDA(cudaMemsetAsync(dmask, 0, 2 * sizeof(unsigned), c.stream));
-    launch_csr_mask(c.stream, n1, n2, dptr, dind, dmask);
-    unsigned hm[2];
+    HADR_CUDA(cudaMemsetAsync(dmask, 0, 3 * sizeof(unsigned long long), c.stream));
+    launch_csr_mask(c.stream, n1, n2, n3, dptr, dind, dmask);
+    unsigned long long hm[3];
     HADR_CUDA(cudaMemcpyAsync(hm, dmask, sizeof(hm), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
-    if (hm[1]) throw ValueError("operator reaches beyond the 5x5 stencil box; not a structured 2D stencil");
-    int slot[25];
-    set_offsets_from_mask(op, hm[0], slot);
-    if (op->nofs == 0) {  // all-zero matrix: keep a centre plane of zeros
-      op->nofs = 1;
-      op->d1[0] = op->d2[0] = 0;
-      slot[12] = 0;
-    }
+    if (hm[2]) throw ValueError("operator reaches beyond the 5x5x5 stencil box; not a structured grid stencil");
+    Mask125 m{{hm[0], hm[1]}};
+    if (!m.w[0] && !m.w[1]) mask_set(m, slot125(0, 0, 0));  // all-zero matrix: keep a centre plane
+    int slot[125];
+    set_offsets_from_mask(op, m, slot);
     HADR_CUDA(cudaMemcpyAsync(dslot, slot, sizeof(slot), cudaMemcpyHostToDevice, c.stream));
     op->coef = dalloc<cplx>((size_t)op->nofs * N);
     HADR_CUDA(cudaMemsetAsync(op->coef, 0, (size_t)op->nofs * N * sizeof(cplx), c.stream));
-    launch_csr_scatter(c.stream, n1, n2, dptr, dind, ddat, dslot, op->coef);
+    launch_csr_scatter(c.stream, n1, n2, n3, dptr, dind, ddat, dslot, op->coef);
     HADR_CUDA(cudaGetLastError());
     c.sync();
   } catch (...) {
@@ -222,26 +240,27 @@ Op* op_from_csr(int n1, int n2, long nnz, const int64_t* indptr, const int32_t* 
   return op;
 }
 
-Op* op_from_planes(int n1, int n2, int nofs, const int* offsets, const cplx* coef_host) {
+Op* op_from_planes(int n1, int n2, int n3, int nofs, const int* offsets, const cplx* coef_host) {
   if (nofs < 1 || nofs > HADR_MAX_OFS) throw ValueError("n_offsets out of range");
   Ctx& c = Ctx::get();
   Op* op = new Op();
   op->n1 = n1;
   op->n2 = n2;
-  op->N = (long)n1 * n2;
+  op->n3 = n3;
+  op->N = (long)n1 * n2 * n3;
   op->nofs = nofs;
   for (int o = 0; o < nofs; ++o) {
-    if (std::abs(offsets[2 * o]) > 2 || std::abs(offsets[2 * o + 1]) > 2) {
+    const int a = offsets[3 * o], b = offsets[3 * o + 1], cc = offsets[3 * o + 2];
+    if (std::abs(a) > 2 || std::abs(b) > 2 || std::abs(cc) > 2 || (n3 == 1 && cc != 0)) {
       delete op;
-      throw ValueError("offsets must lie in the 5x5 box");
+      throw ValueError("offsets must lie in the 5x5x5 box (d3 = 0 in 2D)");
     }
-    op->d1[o] = (int8_t)offsets[2 * o];
-    op->d2[o] = (int8_t)offsets[2 * o + 1];
-  }
-  for (int o = 1; o < nofs; ++o) {
-    if (op->d1[o] * 5 + op->d2[o] <= op->d1[o - 1] * 5 + op->d2[o - 1]) {
+    op->d1[o] = (int8_t)a;
+    op->d2[o] = (int8_t)b;
+    op->d3[o] = (int8_t)cc;
+    if (o > 0 && slot125(a, b, cc) <= slot125(op->d1[o - 1], op->d2[o - 1], op->d3[o - 1])) {
       delete op;
-      throw ValueError("offsets must be strictly ascending in (d1, d2)");
+      throw ValueError("offsets must be strictly ascending in (d1, d2, d3)");
     }
   }
   op->coef = dalloc<cplx>((size_t)nofs * op->N);
@@ -251,27 +270,26 @@ Op* op_from_planes(int n1, int n2, int nofs, const int* offsets, const cplx* coe
   return op;
 }
 
+// alpha*A + beta*B on the union pattern: (alpha*A).data, (beta*B).data, CSR + CSR (helmadr/drivers.py:156)
 Op* op_axpby(cplx alpha, const Op& A, cplx beta, const Op& B) {
-  if (A.n1 != B.n1 || A.n2 != B.n2) throw ValueError("dimension mismatch");
+  if (A.n1 != B.n1 || A.n2 != B.n2 || A.n3 != B.n3) throw ValueError("dimension mismatch");
   Ctx& c = Ctx::get();
-  unsigned mask = 0;
-  for (int o = 0; o < A.nofs; ++o) mask |= 1u << ((A.d1[o] + 2) * 5 + A.d2[o] + 2);
-  for (int o = 0; o < B.nofs; ++o) mask |= 1u << ((B.d1[o] + 2) * 5 + B.d2[o] + 2);
+  Mask125 m = layout_mask(A);
+  const Mask125 mb = layout_mask(B);
+  m.w[0] |= mb.w[0];
+  m.w[1] |= mb.w[1];
   Op* op = new Op();
-  op->n1 = A.n1;
-  op->n2 = A.n2;
-  op->N = A.N;
-  int slot[25];
-  set_offsets_from_mask(op, mask, slot);
-  int ma[HADR_MAX_OFS], mb[HADR_MAX_OFS];
-  for (int o = 0; o < A.nofs; ++o) ma[o] = slot[(A.d1[o] + 2) * 5 + A.d2[o] + 2];
-  for (int o = 0; o < B.nofs; ++o) mb[o] = slot[(B.d1[o] + 2) * 5 + B.d2[o] + 2];
+  copy_geometry(op, A);
+  int slot[125];
+  set_offsets_from_mask(op, m, slot);
+  int ma[HADR_MAX_OFS], mbs[HADR_MAX_OFS];
+  for (int o = 0; o < A.nofs; ++o) ma[o] = slot[slot125(A.d1[o], A.d2[o], A.d3[o])];
+  for (int o = 0; o < B.nofs; ++o) mbs[o] = slot[slot125(B.d1[o], B.d2[o], B.d3[o])];
   int* dm = dalloc<int>(2 * HADR_MAX_OFS);
   HADR_CUDA(cudaMemcpyAsync(dm, ma, sizeof(ma), cudaMemcpyHostToDevice, c.stream));
-  HADR_CUDA(cudaMemcpyAsync(dm + HADR_MAX_OFS, mb, sizeof(mb), cudaMemcpyHostToDevice, c.stream));
+  HADR_CUDA(cudaMemcpyAsync(dm + HADR_MAX_OFS, mbs, sizeof(mbs), cudaMemcpyHostToDevice, c.stream));
   op->coef = dalloc<cplx>((size_t)op->nofs * op->N);
   HADR_CUDA(cudaMemsetAsync(op->coef, 0, (size_t)op->nofs * op->N * sizeof(cplx), c.stream));
-  // (alpha*A).data then (beta*B).data, then CSR + CSR: a + b on the union (helmadr/drivers.py:156)
   launch_remap_planes(c.stream, A.N, A.coef, A.nofs, dm, op->coef, alpha, 1);
   launch_remap_planes(c.stream, B.N, B.coef, B.nofs, dm + HADR_MAX_OFS, op->coef, beta, 1);
   HADR_CUDA(cudaGetLastError());
@@ -282,16 +300,14 @@ Op* op_axpby(cplx alpha, const Op& A, cplx beta, const Op& B) {
 
 static Op* op_clone_with_center(const Op& A) {
   Ctx& c = Ctx::get();
-  unsigned mask = 1u << 12;
-  for (int o = 0; o < A.nofs; ++o) mask |= 1u << ((A.d1[o] + 2) * 5 + A.d2[o] + 2);
+  Mask125 m = layout_mask(A);
+  mask_set(m, slot125(0, 0, 0));
   Op* op = new Op();
-  op->n1 = A.n1;
-  op->n2 = A.n2;
-  op->N = A.N;
-  int slot[25];
-  set_offsets_from_mask(op, mask, slot);
+  copy_geometry(op, A);
+  int slot[125];
+  set_offsets_from_mask(op, m, slot);
   int ma[HADR_MAX_OFS];
-  for (int o = 0; o < A.nofs; ++o) ma[o] = slot[(A.d1[o] + 2) * 5 + A.d2[o] + 2];
+  for (int o = 0; o < A.nofs; ++o) ma[o] = slot[slot125(A.d1[o], A.d2[o], A.d3[o])];
   int* dm = dalloc<int>(HADR_MAX_OFS);
   HADR_CUDA(cudaMemcpyAsync(dm, ma, sizeof(ma), cudaMemcpyHostToDevice, c.stream));
   op->coef = dalloc<cplx>((size_t)op->nofs * op->N);
@@ -317,9 +333,13 @@ Op* op_add_diag_real(const Op& A, cplx sc, const double* field_host) {
 Op* op_similarity(const Op& A, const cplx* left_host, const cplx* right_host) {
   Ctx& c = Ctx::get();
   Op* op = new Op();
-  *op = A;  // copies geometry (and pointers, reset below)
-  op->coef = nullptr;
-  op->dinv = nullptr;
+  copy_geometry(op, A);
+  op->nofs = A.nofs;
+  for (int o = 0; o < A.nofs; ++o) {
+    op->d1[o] = A.d1[o];
+    op->d2[o] = A.d2[o];
+    op->d3[o] = A.d3[o];
+  }
   cplx* dl = dalloc<cplx>(A.N);
   cplx* dr = dalloc<cplx>(A.N);
   HADR_CUDA(cudaMemcpyAsync(dl, left_host, A.N * sizeof(cplx), cudaMemcpyHostToDevice, c.stream));
@@ -333,102 +353,109 @@ Op* op_similarity(const Op& A, const cplx* left_host, const cplx* right_host) {
   return op;
 }
 
-static unsigned galerkin_mask(const Op& A) {
-  Ctx& c = Ctx::get();
-  const int n1c = (A.n1 - 1) / 2 + 1, n2c = (A.n2 - 1) / 2 + 1;
-  unsigned* dmask = (unsigned*)(c.dscal + 40);
-  HADR_CUDA(cudaMemsetAsync(dmask, 0, sizeof(unsigned), c.stream));
-  launch_galerkin(c.stream, A.dev(), n1c, n2c, dmask, nullptr, nullptr);
-  unsigned hm = 0;
-  HADR_CUDA(cudaMemcpyAsync(&hm, dmask, sizeof(unsigned), cudaMemcpyDeviceToHost, c.stream));
-  c.sync();
-  return hm | (1u << 12);  // the diagonal is always kept
-}
+static inline int coarse_dim(int n) { return (n - 1) / 2 + 1; }
 
-static unsigned layout_mask(const Op& A) {
-  unsigned m = 0;
-  for (int o = 0; o < A.nofs; ++o) m |= 1u << ((A.d1[o] + 2) * 5 + A.d2[o] + 2);
+static Mask125 galerkin_mask(const Op& A) {
+  Ctx& c = Ctx::get();
+  unsigned long long* dmask = (unsigned long long*)(c.dscal + 40);
+  HADR_CUDA(cudaMemsetAsync(dmask, 0, 2 * sizeof(unsigned long long), c.stream));
+  launch_galerkin(c.stream, A.dev(), coarse_dim(A.n1), coarse_dim(A.n2), coarse_dim(A.n3), dmask, nullptr, nullptr);
+  Mask125 m{{0ull, 0ull}};
+  HADR_CUDA(cudaMemcpyAsync(m.w, dmask, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  mask_set(m, slot125(0, 0, 0));  // the diagonal is always kept
   return m;
 }
 
 static void galerkin_write(const Op& A, Op& C) {  // C's offsets define the planes
   Ctx& c = Ctx::get();
-  int slot[25];
-  for (int q = 0; q < 25; ++q) slot[q] = -1;
-  for (int o = 0; o < C.nofs; ++o) slot[(C.d1[o] + 2) * 5 + C.d2[o] + 2] = o;
-  int* dslot = (int*)(c.dscal + 48);
+  int* dslot = dalloc<int>(125);
+  int slot[125];
+  for (int q = 0; q < 125; ++q) slot[q] = -1;
+  for (int o = 0; o < C.nofs; ++o) slot[slot125(C.d1[o], C.d2[o], C.d3[o])] = o;
   HADR_CUDA(cudaMemcpyAsync(dslot, slot, sizeof(slot), cudaMemcpyHostToDevice, c.stream));
-  launch_galerkin(c.stream, A.dev(), C.n1, C.n2, nullptr, dslot, C.coef);
+  launch_galerkin(c.stream, A.dev(), C.n1, C.n2, C.n3, nullptr, dslot, C.coef);
   HADR_CUDA(cudaGetLastError());
-  c.sync();  // slot table lives in shared scratch
+  c.sync();
+  dfree(dslot);
 }
 
 Op* op_galerkin(const Op& A) {
-  if ((A.n1 - 1) % 2 || (A.n2 - 1) % 2) throw ValueError("cannot coarsen: interval count is odd");
-  const unsigned hm = galerkin_mask(A);
+  if ((A.n1 - 1) % 2 || (A.n2 - 1) % 2 || (A.n3 > 1 && (A.n3 - 1) % 2))
+    throw ValueError("cannot coarsen: interval count is odd");
+  const Mask125 m = galerkin_mask(A);
   Op* op = new Op();
-  op->n1 = (A.n1 - 1) / 2 + 1;
-  op->n2 = (A.n2 - 1) / 2 + 1;
-  op->N = (long)op->n1 * op->n2;
-  int slot[25];
-  set_offsets_from_mask(op, hm, slot);
+  op->n1 = coarse_dim(A.n1);
+  op->n2 = coarse_dim(A.n2);
+  op->n3 = coarse_dim(A.n3);
+  op->N = (long)op->n1 * op->n2 * op->n3;
+  int slot[125];
+  set_offsets_from_mask(op, m, slot);
   op->coef = dalloc<cplx>((size_t)op->nofs * op->N);
   galerkin_write(A, *op);
   return op;
 }
 
-Op* op_assemble(int n1, int n2, double h1, double h2, double omega, int scheme, const int* bc, int src1, int src2,
-                const double* ksq, const double* gam, const double* g1, const double* g2, const double* lap,
-                bool fields_on_device) {
-  if (n1 < 5 || n2 < 5) throw ValueError("grid needs at least 5 nodes per dimension");
+Op* op_assemble(int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega, int scheme,
+                const int* bc, int src1, int src2, int src3, const double* ksq, const double* gam, const double* g1,
+                const double* g2, const double* g3, const double* lap, bool fields_on_device) {
+  if (dim != 2 && dim != 3) throw ValueError("dim must be 2 or 3");
+  if (n1 < 5 || n2 < 5 || (dim == 3 && n3 < 5)) throw ValueError("grid needs at least 5 nodes per dimension");
   if (scheme < 0 || scheme > 3) throw ValueError("scheme must be central/upwind1/upwind2/helmholtz");
+  if (dim == 2) n3 = 1;
   Ctx& c = Ctx::get();
-  const long N = (long)n1 * n2;
-  const int nf = scheme == 3 ? 2 : 5;
-  const double* src[5] = {ksq, gam, g1, g2, lap};
-  const double* fld[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  const long N = (long)n1 * n2 * n3;
+  const double* src[6] = {ksq, gam, g1, g2, g3, lap};
+  const bool need[6] = {true, true, scheme != 3, scheme != 3, scheme != 3 && dim == 3, scheme != 3};
+  const double* fld[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   double* df = nullptr;
   if (fields_on_device) {
-    for (int i = 0; i < nf; ++i) fld[i] = src[i];
+    for (int i = 0; i < 6; ++i) fld[i] = need[i] ? src[i] : nullptr;
   } else {
-    df = dalloc<double>(nf * N);
-    for (int i = 0; i < nf; ++i) {
-      HADR_CUDA(cudaMemcpyAsync(df + i * N, src[i], N * sizeof(double), cudaMemcpyHostToDevice, c.stream));
-      fld[i] = df + i * N;
-    }
+    df = dalloc<double>(6 * N);
+    for (int i = 0; i < 6; ++i)
+      if (need[i]) {
+        HADR_CUDA(cudaMemcpyAsync(df + i * N, src[i], N * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+        fld[i] = df + i * N;
+      }
   }
-  cplx* c9 = dalloc<cplx>(9 * N);
+  const int NP = dim == 2 ? 9 : 13;
+  cplx* cp = dalloc<cplx>(NP * N);
   unsigned* dmask = dalloc<unsigned>(1);
   HADR_CUDA(cudaMemsetAsync(dmask, 0, sizeof(unsigned), c.stream));
-  launch_assemble(c.stream, n1, n2, h1, h2, omega, scheme, bc, src1, src2, fld[0], fld[1], fld[2], fld[3], fld[4], c9,
-                  dmask);
+  launch_assemble(c.stream, dim, n1, n2, n3, h1, h2, h3, omega, scheme, bc, src1, src2, src3, fld[0], fld[1], fld[2],
+                  fld[3], fld[4], fld[5], cp, dmask);
   unsigned hm = 0;
   HADR_CUDA(cudaMemcpyAsync(&hm, dmask, sizeof(unsigned), cudaMemcpyDeviceToHost, c.stream));
   c.sync();
-  static const int d9[9][2] = {{-2, 0}, {-1, 0}, {0, -2}, {0, -1}, {0, 0}, {0, 1}, {0, 2}, {1, 0}, {2, 0}};
-  hm |= 1u << 4;  // keep the centre plane
+  static const int d9[9][3] = {{-2, 0, 0}, {-1, 0, 0}, {0, -2, 0}, {0, -1, 0}, {0, 0, 0},
+                               {0, 1, 0},  {0, 2, 0},  {1, 0, 0},  {2, 0, 0}};
+  static const int d13[13][3] = {{-2, 0, 0}, {-1, 0, 0}, {0, -2, 0}, {0, -1, 0}, {0, 0, -2}, {0, 0, -1}, {0, 0, 0},
+                                 {0, 0, 1},  {0, 0, 2},  {0, 1, 0},  {0, 2, 0},  {1, 0, 0},  {2, 0, 0}};
+  hm |= 1u << (dim == 2 ? 4 : 6);  // keep the centre plane
   Op* op = new Op();
   op->n1 = n1;
   op->n2 = n2;
+  op->n3 = n3;
   op->N = N;
-  int dst[9];
-  int used[9], nu = 0;
-  for (int q = 0; q < 9; ++q)
+  int used[13], nu = 0;
+  for (int q = 0; q < NP; ++q)
     if (hm & (1u << q)) {
-      op->d1[nu] = (int8_t)d9[q][0];
-      op->d2[nu] = (int8_t)d9[q][1];
+      const int* d = dim == 2 ? d9[q] : d13[q];
+      op->d1[nu] = (int8_t)d[0];
+      op->d2[nu] = (int8_t)d[1];
+      op->d3[nu] = (int8_t)d[2];
       used[nu++] = q;
     }
   op->nofs = nu;
   op->coef = dalloc<cplx>((size_t)nu * N);
   for (int o = 0; o < nu; ++o)
-    HADR_CUDA(cudaMemcpyAsync(op->coef + (long)o * N, c9 + (long)used[o] * N, N * sizeof(cplx),
+    HADR_CUDA(cudaMemcpyAsync(op->coef + (long)o * N, cp + (long)used[o] * N, N * sizeof(cplx),
                               cudaMemcpyDeviceToDevice, c.stream));
-  (void)dst;
   HADR_CUDA(cudaGetLastError());
   c.sync();
   dfree(df);
-  dfree(c9);
+  dfree(cp);
   dfree(dmask);
   return op;
 }
@@ -448,15 +475,22 @@ void op_apply(const Op& A, const cplx* x, cplx* y) {
 // ---------------------------------------------------------------------------
 // hierarchy
 // ---------------------------------------------------------------------------
-std::vector<std::pair<int, int>> coarsenable_levels(int n1, int n2, int max_levels) {
-  // helmadr/multigrid.py:98-110
-  std::vector<std::pair<int, int>> s{{n1, n2}};
+std::vector<Shape3> coarsenable_levels(int n1, int n2, int n3, int max_levels) {
+  // helmadr/multigrid.py:98-110 per axis; an axis of size 1 (2D: n3 = 1) is not coarsened
+  std::vector<Shape3> s{{n1, n2, n3}};
   while ((int)s.size() < max_levels) {
-    int m1 = s.back().first, m2 = s.back().second;
-    if ((m1 - 1) % 2 || (m2 - 1) % 2) break;
-    int c1 = (m1 - 1) / 2 + 1, c2 = (m2 - 1) / 2 + 1;
-    if (c1 < 3 || c2 < 3) break;
-    s.push_back({c1, c2});
+    const Shape3 m = s.back();
+    const int dims = m.n3 > 1 ? 3 : 2;
+    const int mm[3] = {m.n1, m.n2, m.n3};
+    int cc[3] = {m.n1, m.n2, m.n3};
+    bool ok = true;
+    for (int a = 0; a < dims; ++a) {
+      if ((mm[a] - 1) % 2) ok = false;
+      cc[a] = (mm[a] - 1) / 2 + 1;
+      if (cc[a] < 3) ok = false;
+    }
+    if (!ok) break;
+    s.push_back({cc[0], cc[1], cc[2]});
   }
   return s;
 }
@@ -480,7 +514,7 @@ Hier::~Hier() {
 
 size_t Hier::ce_tile(int li) const {
   size_t m = 0;  // the engine touches levels li .. coarsest; the finest of them is the largest
-  for (int i = li; i < (int)lv.size(); ++i) m = std::max(m, ce_tile_bytes(lv[i].n1, lv[i].n2, CE_CTAS));
+  for (int i = li; i < (int)lv.size(); ++i) m = std::max(m, ce_tile_bytes(lv[i].n1, lv[i].n2 * lv[i].n3, CE_CTAS));
   return m;
 }
 
@@ -495,6 +529,7 @@ void Hier::alloc_workspace() {
     Level& L = lv[i];
     L.n1 = L.A->n1;
     L.n2 = L.A->n2;
+    L.n3 = L.A->n3;
     L.N = L.A->N;
     L.dinv = L.A->inv_diag();
     L.s = (i == nl - 1) ? coarse_steps : (i + 2);  // relax_steps(l) = l + 1 (helmadr/multigrid.py:87-88)
@@ -574,13 +609,14 @@ void hier_release(Hier* h) {
 static bool hier_refresh(Hier* h, const Op& fine) {
   Ctx& c = Ctx::get();
   Op& L0 = *h->lv[0].A;
-  if (L0.n1 != fine.n1 || L0.n2 != fine.n2 || layout_mask(L0) != layout_mask(fine)) return false;
+  if (L0.n1 != fine.n1 || L0.n2 != fine.n2 || L0.n3 != fine.n3 || !mask_eq(layout_mask(L0), layout_mask(fine)))
+    return false;
   HADR_CUDA(cudaMemcpyAsync(L0.coef, fine.coef, (size_t)fine.nofs * fine.N * sizeof(cplx), cudaMemcpyDeviceToDevice,
                             c.stream));
   for (size_t l = 1; l < h->lv.size(); ++l) {
     Op& F = *h->lv[l - 1].A;
     Op& C = *h->lv[l].A;
-    if (galerkin_mask(F) != layout_mask(C)) return false;
+    if (!mask_eq(galerkin_mask(F), layout_mask(C))) return false;
     galerkin_write(F, C);
   }
   for (auto& L : h->lv) L.A->refresh_inv_diag();
@@ -588,7 +624,7 @@ static bool hier_refresh(Hier* h, const Op& fine) {
 }
 
 Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol) {
-  auto shapes = coarsenable_levels(fine->n1, fine->n2, max_levels);
+  auto shapes = coarsenable_levels(fine->n1, fine->n2, fine->n3, max_levels);
   if (shapes.size() < 2)
     throw ValueError("grid cannot support two multigrid levels ((n_d - 1) must be even with at least 3 coarse nodes)");
   auto& pool = hier_pool();
@@ -597,7 +633,7 @@ Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol) 
     if (h->lv.size() != shapes.size() || h->coarse_steps != coarse_steps || h->coarse_tol != coarse_tol) continue;
     bool same = true;
     for (size_t l = 0; l < shapes.size(); ++l)
-      same = same && h->lv[l].n1 == shapes[l].first && h->lv[l].n2 == shapes[l].second;
+      same = same && h->lv[l].n1 == shapes[l].n1 && h->lv[l].n2 == shapes[l].n2 && h->lv[l].n3 == shapes[l].n3;
     if (!same) continue;
     pool.erase(pool.begin() + i);
     if (hier_refresh(h, *fine)) return h;
@@ -636,7 +672,8 @@ Hier* hier_from_ops(int nlev, Op** ops, int coarse_steps, double coarse_tol) {
     for (int i = 0; i < nlev; ++i) {
       Level L;
       L.A = ops[i];
-      if (i > 0 && (ops[i]->n1 != (ops[i - 1]->n1 - 1) / 2 + 1 || ops[i]->n2 != (ops[i - 1]->n2 - 1) / 2 + 1))
+      if (i > 0 && (ops[i]->n1 != (ops[i - 1]->n1 - 1) / 2 + 1 || ops[i]->n2 != (ops[i - 1]->n2 - 1) / 2 + 1 ||
+                    ops[i]->n3 != (ops[i - 1]->n3 - 1) / 2 + 1))
         throw ValueError("level shapes must halve: (n-1)/2+1");
       h->lv.push_back(L);
     }
@@ -726,7 +763,7 @@ void Hier::emit_kcycle(int li, const cplx* b, const cplx* x0, cplx* xo, Gate g, 
   a.rs = c.rs;
   a.epi = epi_none();
   launch_stencil(c.lc, IN_PLAIN, OUT_RESID, RED_NONE, a);
-  launch_restrict(c.lc, L.n1, L.n2, L.r, C.fb, g);
+  launch_restrict(c.lc, L.n1, L.n2, L.n3, L.r, C.fb, g);
   if (li + 1 == nl - 1) {
     if (count) k_count<<<1, 1, 0, c.stream>>>(visits, li + 1, g);
     if (!count && use_ce(li + 1))
@@ -738,7 +775,7 @@ void Hier::emit_kcycle(int li, const cplx* b, const cplx* x0, cplx* xo, Gate g, 
   } else {
     emit_inner(li + 1, g, count);
   }
-  launch_prolong_add(c.lc, L.n1, L.n2, C.fx, xo, g);
+  launch_prolong_add(c.lc, L.n1, L.n2, L.n3, C.fx, xo, g);
   emit_relax(L, b, xo, xo, L.s, g);
 }
 
@@ -883,6 +920,7 @@ void gmres_relax(Op& A, const cplx* b, const cplx* x, cplx* xo, int steps) {
   L.A = &A;
   L.n1 = A.n1;
   L.n2 = A.n2;
+  L.n3 = A.n3;
   L.N = A.N;
   L.dinv = A.inv_diag();
   L.s = (int)std::min<long>(std::max(steps, 0), A.N);

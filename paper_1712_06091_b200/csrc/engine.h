@@ -51,10 +51,10 @@ inline void dfree(void* p) {
 
 // Structured 2D operator (owns its coefficient planes).
 struct Op {
-  int n1 = 0, n2 = 0;
+  int n1 = 0, n2 = 0, n3 = 1;  // 2D: n3 = 1
   long N = 0;
   int nofs = 0;
-  int8_t d1[HADR_MAX_OFS] = {0}, d2[HADR_MAX_OFS] = {0};
+  int8_t d1[HADR_MAX_OFS] = {0}, d2[HADR_MAX_OFS] = {0}, d3[HADR_MAX_OFS] = {0};
   cplx* coef = nullptr;
   cplx* dinv = nullptr;  // lazily computed inverse diagonal
   ~Op();
@@ -65,22 +65,27 @@ struct Op {
 };
 Op* op_copy(const Op& A);
 
-Op* op_from_csr(int n1, int n2, long nnz, const int64_t* indptr, const int32_t* indices, const cplx* data);
-Op* op_from_planes(int n1, int n2, int nofs, const int* offsets, const cplx* coef_host);
+Op* op_from_csr(int n1, int n2, int n3, long nnz, const int64_t* indptr, const int32_t* indices, const cplx* data);
+Op* op_from_planes(int n1, int n2, int n3, int nofs, const int* offsets /* 3 per offset */, const cplx* coef_host);
 Op* op_axpby(cplx alpha, const Op& A, cplx beta, const Op& B);       // alpha*A + beta*B on the union pattern
 Op* op_add_diag_real(const Op& A, cplx sc, const double* field_host);  // A + diag(sc*field)
 Op* op_similarity(const Op& A, const cplx* left_host, const cplx* right_host);
 Op* op_galerkin(const Op& A);                                          // P^T A P
 // ADR (scheme 0 central, 1 upwind1, 2 upwind2) or Helmholtz (scheme 3) operator, fields host (n1*n2)
-Op* op_assemble(int n1, int n2, double h1, double h2, double omega, int scheme, const int* bc, int src1, int src2,
-                const double* ksq, const double* gam, const double* g1, const double* g2, const double* lap,
+Op* op_assemble(int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega, int scheme,
+                const int* bc /* top,bottom,left,right,front,back */, int src1, int src2, int src3, const double* ksq,
+                const double* gam, const double* g1, const double* g2, const double* g3, const double* lap,
                 bool fields_on_device = false);
 void op_apply(const Op& A, const cplx* x, cplx* y);                    // device pointers, async
+
+struct Shape3 {
+  int n1, n2, n3;
+};
 
 struct Level {
   Op* A = nullptr;
   bool own = false;
-  int n1 = 0, n2 = 0;
+  int n1 = 0, n2 = 0, n3 = 1;
   long N = 0;
   const cplx* dinv = nullptr;
   int s = 0;                 // relaxation length at this level
@@ -125,7 +130,7 @@ Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol);
 void hier_release(Hier* h);  // recycle (workspace + captured graphs) or delete
 Hier* hier_pool_pop();       // take one recycled hierarchy (or null)
 Hier* hier_from_ops(int nlev, Op** ops, int coarse_steps, double coarse_tol);
-std::vector<std::pair<int, int>> coarsenable_levels(int n1, int n2, int max_levels);
+std::vector<Shape3> coarsenable_levels(int n1, int n2, int n3, int max_levels);
 
 struct Report {
   int iterations = 0;

@@ -199,16 +199,49 @@ static void launch_finalize(const LaunchCfg& lc, const Geo& geo, Gate g, RedScra
 }
 
 // ---------------------------------------------------------------------------
-// K1: stencil apply   y = A x   |   y = b - A x
+// K1: stencil apply   y = A x   |   y = b - A x      (2D: n3 = 1)
 //   input transform per neighbour: v = x*s (IN_SCALE), v = dinv (.) v (IN_JAC)
 //   IN_WRITEV stores the centre's scaled input (the new Krylov basis vector).
 //   reductions: ||y||^2, <u, y> (u = array, or the centre input with RED_DOT_CENTER)
+// NO > 0: all NO offsets unrolled with batched loads; NO == 0: runtime chunks of
+// 9 offsets (3D coarse unions of 27..81 offsets).
 // ---------------------------------------------------------------------------
+template <int CH, int INM>
+__device__ __forceinline__ void stencil_chunk(const StencilArgs& a, int o0, int nofs, long k, int i1, int i2, int i3,
+                                              int n1, int n2, int n3, long N, double s, cplx& acc) {
+  // All loads are unconditional (out-of-grid neighbours read the centre, dead
+  // offsets read plane 0) so the compiler can batch them; out-of-grid terms are
+  // then skipped, which keeps scipy csr_matvec's exact accumulation.
+  cplx cv[CH], xv[CH], dv[CH];
+  bool ok[CH];
+#pragma unroll
+  for (int q = 0; q < CH; ++q) {
+    const int o = o0 + q;
+    const bool live = o < nofs;
+    const int oo = live ? o : 0;
+    const int j1 = i1 + a.A.d1[oo], j2 = i2 + a.A.d2[oo], j3 = i3 + a.A.d3[oo];
+    ok[q] = live && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2 && j3 >= 0 && j3 < n3;
+    const long jj = ok[q] ? ((long)j1 * n2 + j2) * n3 + j3 : k;
+    cv[q] = ldc(a.A.coef, live ? (long)o * N + k : k);
+    xv[q] = ldc(a.x, jj);
+    if (INM & IN_JAC) dv[q] = ldc(a.dinv, jj);
+  }
+#pragma unroll
+  for (int q = 0; q < CH; ++q) {
+    cplx v = xv[q];
+    if (INM & IN_SCALE) v = cscale(v, s);
+    if (INM & IN_JAC) v = cmul_np(dv[q], v);
+    const cplx t = cadd(acc, cmul_sp(cv[q], v));
+    acc = ok[q] ? t : acc;
+  }
+}
+
 template <int INM, int OUTM, int RED, int NO, int CL>
 __global__ void __launch_bounds__(kThreads, 4) k_stencil(StencilArgs a) {
   if (!gate_open(a.gate)) return;
-  const int n1 = a.A.n1, n2 = a.A.n2, nofs = a.A.nofs;
-  const long N = (long)n1 * n2;
+  const int n1 = a.A.n1, n2 = a.A.n2, n3 = a.A.n3, nofs = a.A.nofs;
+  const int n23 = n2 * n3;
+  const long N = (long)n1 * n23;
   const double s = (INM & IN_SCALE) ? *a.scale : 1.0;
   constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & (RED_DOT | RED_DOT_CENTER)) ? 2 : 0);
   double red[NV > 0 ? NV : 1];
@@ -216,31 +249,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(StencilArgs a) {
   for (int q = 0; q < (NV > 0 ? NV : 1); ++q) red[q] = 0.0;
   const long stride = (long)gridDim.x * blockDim.x;
   for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += stride) {
-    const int i1 = (int)(k / n2);
-    const int i2 = (int)(k - (long)i1 * n2);
-    // All loads are unconditional (out-of-grid neighbours read the centre, dead
-    // offsets read plane 0) so the compiler can batch them; out-of-grid terms are
-    // then skipped, which keeps scipy csr_matvec's exact accumulation.
-    cplx cv[NO], xv[NO], dv[NO];
-    bool ok[NO];
-#pragma unroll
-    for (int o = 0; o < NO; ++o) {
-      const bool live = o < nofs;
-      const int j1 = i1 + a.A.d1[o], j2 = i2 + a.A.d2[o];
-      ok[o] = live && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2;
-      const long jj = ok[o] ? (long)j1 * n2 + j2 : k;
-      cv[o] = ldc(a.A.coef, live ? (long)o * N + k : k);
-      xv[o] = ldc(a.x, jj);
-      if (INM & IN_JAC) dv[o] = ldc(a.dinv, jj);
-    }
+    const int i1 = (int)(k / n23);
+    const int rem = (int)(k - (long)i1 * n23);
+    const int i2 = rem / n3;
+    const int i3 = rem - i2 * n3;
     cplx acc = mk(0.0, 0.0);
-#pragma unroll
-    for (int o = 0; o < NO; ++o) {
-      cplx v = xv[o];
-      if (INM & IN_SCALE) v = cscale(v, s);
-      if (INM & IN_JAC) v = cmul_np(dv[o], v);
-      const cplx t = cadd(acc, cmul_sp(cv[o], v));
-      acc = ok[o] ? t : acc;
+    if constexpr (NO > 0) {
+      stencil_chunk<NO, INM>(a, 0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
+    } else {
+      for (int o0 = 0; o0 < nofs; o0 += 9) stencil_chunk<9, INM>(a, o0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
     }
     cplx vc = mk(0.0, 0.0);
     if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) {
@@ -287,17 +304,17 @@ static void dispatch_no(const LaunchCfg& lc, const StencilArgs& a, const Geo& ge
     launch_stencil_no<INM, OUTM, RED, 7>(lc, a, geo);
   else if (n <= 13)
     launch_stencil_no<INM, OUTM, RED, 13>(lc, a, geo);
-  else if (n <= 21)
-    launch_stencil_no<INM, OUTM, RED, 21>(lc, a, geo);
-  else
+  else if (n <= 25)
     launch_stencil_no<INM, OUTM, RED, 25>(lc, a, geo);
+  else
+    launch_stencil_no<INM, OUTM, RED, 0>(lc, a, geo);
   constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & (RED_DOT | RED_DOT_CENTER)) ? 2 : 0);
   if constexpr (NV > 0) launch_finalize<NV>(lc, geo, a.gate, a.rs, a.epi);
 }
 
 void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const StencilArgs& a) {
   ++g_launch_count;
-  const long N = (long)a.A.n1 * a.A.n2;
+  const long N = (long)a.A.n1 * a.A.n2 * a.A.n3;
   const Geo geo = red ? geo_for(lc, N) : Geo{blocks_for(lc, N), 0};
   constexpr int J = IN_SCALE | IN_JAC | IN_WRITEV;
 #define HADR_CASE(I, O, R)                       \
@@ -482,21 +499,26 @@ void launch_fg_finalize(const LaunchCfg& lc, long n, FgCtl* f, const cplx* Z0, c
 }
 
 // ---------------------------------------------------------------------------
-// K6/K7: transfer operators for the bilinear P = kron(P1(n1), P1(n2)).
+// K6/K7: transfer operators for the (tri)linear P = kron(P1(n1), P1(n2), P1(n3)).
 // Restriction rc = P^T r follows scipy csc_matvec: contributions added in
-// ascending fine index, i.e. lexicographic (a, b) over the 3x3 fine patch.
-// Prolongation follows csr_matvec: parents in ascending coarse index.
-// Weights are powers of two, so each product is exact and the sums match
-// the reference bit for bit.
+// ascending fine index, i.e. lexicographic (a, b, c) over the 3x3(x3) fine
+// patch.  Prolongation follows csr_matvec: parents in ascending coarse index.
+// Weights are powers of two, so each product is exact and the sums match the
+// reference bit for bit.  An axis of size 1 (2D: n3 = 1) is not coarsened.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_restrict(int n1f, int n2f, const cplx* __restrict__ r,
+__device__ __forceinline__ int coarse_n(int n) { return (n - 1) / 2 + 1; }
+
+__global__ void __launch_bounds__(kThreads) k_restrict(int n1f, int n2f, int n3f, const cplx* __restrict__ r,
                                                          cplx* __restrict__ rc, Gate g) {
   if (!gate_open(g)) return;
-  const int n1c = (n1f - 1) / 2 + 1, n2c = (n2f - 1) / 2 + 1;
-  const long Nc = (long)n1c * n2c;
+  const int n1c = coarse_n(n1f), n2c = coarse_n(n2f), n3c = coarse_n(n3f);
+  const long Nc = (long)n1c * n2c * n3c;
+  const int c3lo = n3f > 1 ? -1 : 0, c3hi = n3f > 1 ? 1 : 0;
   const long stride = (long)gridDim.x * blockDim.x;
   for (long c = (long)blockIdx.x * blockDim.x + threadIdx.x; c < Nc; c += stride) {
-    const int I1 = (int)(c / n2c), I2 = (int)(c - (long)I1 * n2c);
+    const int I1 = (int)(c / ((long)n2c * n3c));
+    const int rem = (int)(c - (long)I1 * n2c * n3c);
+    const int I2 = rem / n3c, I3 = rem - (rem / n3c) * n3c;
     cplx acc = mk(0.0, 0.0);
 #pragma unroll
     for (int a = -1; a <= 1; ++a) {
@@ -507,41 +529,62 @@ __global__ void __launch_bounds__(kThreads) k_restrict(int n1f, int n2f, const c
       for (int b = -1; b <= 1; ++b) {
         const int f2 = 2 * I2 + b;
         if (f2 < 0 || f2 >= n2f) continue;
-        const double w = w1 * (b == 0 ? 1.0 : 0.5);
-        acc = cadd(acc, cmul_sp(mk(w, 0.0), ldc(r, (long)f1 * n2f + f2)));
+        const double w12 = w1 * (b == 0 ? 1.0 : 0.5);
+        for (int cc = c3lo; cc <= c3hi; ++cc) {
+          const int f3 = 2 * I3 + cc;
+          if (f3 < 0 || f3 >= n3f) continue;
+          const double w = w12 * (cc == 0 ? 1.0 : 0.5);
+          acc = cadd(acc, cmul_sp(mk(w, 0.0), ldc(r, ((long)f1 * n2f + f2) * n3f + f3)));
+        }
       }
     }
     rc[c] = acc;
   }
 }
-void launch_restrict(const LaunchCfg& lc, int n1f, int n2f, const cplx* r, cplx* rc, Gate g) {
+void launch_restrict(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx* r, cplx* rc, Gate g) {
   ++g_launch_count;
-  const long Nc = (long)((n1f - 1) / 2 + 1) * ((n2f - 1) / 2 + 1);
-  k_restrict<<<blocks_for(lc, Nc), kThreads, 0, lc.stream>>>(n1f, n2f, r, rc, g);
+  const long Nc = (long)((n1f - 1) / 2 + 1) * ((n2f - 1) / 2 + 1) * ((n3f - 1) / 2 + 1);
+  k_restrict<<<blocks_for(lc, Nc), kThreads, 0, lc.stream>>>(n1f, n2f, n3f, r, rc, g);
 }
 
-__global__ void __launch_bounds__(kThreads) k_prolong_add(int n1f, int n2f, const cplx* __restrict__ ec,
+__device__ __forceinline__ int parents(int f, int* p, double& w) {
+  if (f & 1) {
+    p[0] = f >> 1;
+    p[1] = (f >> 1) + 1;
+    w = 0.5;
+    return 2;
+  }
+  p[0] = f >> 1;
+  p[1] = p[0];
+  w = 1.0;
+  return 1;
+}
+
+__global__ void __launch_bounds__(kThreads) k_prolong_add(int n1f, int n2f, int n3f, const cplx* __restrict__ ec,
                                                             cplx* __restrict__ x, Gate g) {
   if (!gate_open(g)) return;
-  const int n2c = (n2f - 1) / 2 + 1;
-  const long Nf = (long)n1f * n2f;
+  const int n2c = coarse_n(n2f), n3c = coarse_n(n3f);
+  const int n23 = n2f * n3f;
+  const long Nf = (long)n1f * n23;
   const long stride = (long)gridDim.x * blockDim.x;
   for (long f = (long)blockIdx.x * blockDim.x + threadIdx.x; f < Nf; f += stride) {
-    const int f1 = (int)(f / n2f), f2 = (int)(f - (long)f1 * n2f);
-    int c1[2], c2[2], m1, m2;
-    double w1, w2;
-    if (f1 & 1) { c1[0] = f1 >> 1; c1[1] = (f1 >> 1) + 1; m1 = 2; w1 = 0.5; } else { c1[0] = f1 >> 1; m1 = 1; w1 = 1.0; }
-    if (f2 & 1) { c2[0] = f2 >> 1; c2[1] = (f2 >> 1) + 1; m2 = 2; w2 = 0.5; } else { c2[0] = f2 >> 1; m2 = 1; w2 = 1.0; }
+    const int f1 = (int)(f / n23);
+    const int rem = (int)(f - (long)f1 * n23);
+    const int f2 = rem / n3f, f3 = rem - (rem / n3f) * n3f;
+    int c1[2], c2[2], c3[2];
+    double w1, w2, w3;
+    const int m1 = parents(f1, c1, w1), m2 = parents(f2, c2, w2), m3 = parents(f3, c3, w3);
     cplx p = mk(0.0, 0.0);
     for (int a = 0; a < m1; ++a)
       for (int b = 0; b < m2; ++b)
-        p = cadd(p, cmul_sp(mk(w1 * w2, 0.0), ldc(ec, (long)c1[a] * n2c + c2[b])));
+        for (int cc = 0; cc < m3; ++cc)
+          p = cadd(p, cmul_sp(mk(w1 * w2 * w3, 0.0), ldc(ec, ((long)c1[a] * n2c + c2[b]) * n3c + c3[cc])));
     x[f] = cadd(x[f], p);
   }
 }
-void launch_prolong_add(const LaunchCfg& lc, int n1f, int n2f, const cplx* ec, cplx* x, Gate g) {
+void launch_prolong_add(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx* ec, cplx* x, Gate g) {
   ++g_launch_count;
-  k_prolong_add<<<blocks_for(lc, (long)n1f * n2f), kThreads, 0, lc.stream>>>(n1f, n2f, ec, x, g);
+  k_prolong_add<<<blocks_for(lc, (long)n1f * n2f * n3f), kThreads, 0, lc.stream>>>(n1f, n2f, n3f, ec, x, g);
 }
 
 // ---------------------------------------------------------------------------
@@ -571,55 +614,68 @@ void launch_fg_setup(cudaStream_t s, FgCtl* f, double tol, Gate g) {
 // ---------------------------------------------------------------------------
 // operator construction (setup; not on the solve's inner loop)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int slot25(int d1, int d2) { return (d1 + 2) * 5 + (d2 + 2); }
+__device__ __forceinline__ void decomp3(long k, int n2, int n3, int& i1, int& i2, int& i3) {
+  const long n23 = (long)n2 * n3;
+  i1 = (int)(k / n23);
+  const int rem = (int)(k - (long)i1 * n23);
+  i2 = rem / n3;
+  i3 = rem - i2 * n3;
+}
 
-__global__ void k_csr_mask(int n1, int n2, const int64_t* indptr, const int32_t* indices, unsigned* mask) {
-  const long N = (long)n1 * n2;
-  unsigned m = 0u, bad = 0u;
+__global__ void k_csr_mask(int n1, int n2, int n3, const int64_t* indptr, const int32_t* indices,
+                           unsigned long long* mask) {
+  const long N = (long)n1 * n2 * n3;
+  unsigned long long m0 = 0ull, m1 = 0ull, bad = 0ull;
   for (long row = (long)blockIdx.x * blockDim.x + threadIdx.x; row < N; row += (long)gridDim.x * blockDim.x) {
-    const int i1 = (int)(row / n2), i2 = (int)(row - (long)i1 * n2);
+    int i1, i2, i3;
+    decomp3(row, n2, n3, i1, i2, i3);
     for (int64_t p = indptr[row]; p < indptr[row + 1]; ++p) {
-      const long col = indices[p];
-      const int j1 = (int)(col / n2), j2 = (int)(col - (long)j1 * n2);
-      const int d1 = j1 - i1, d2 = j2 - i2;
-      if (d1 < -2 || d1 > 2 || d2 < -2 || d2 > 2)
-        bad = 1u;
-      else
-        m |= 1u << slot25(d1, d2);
+      int j1, j2, j3;
+      decomp3(indices[p], n2, n3, j1, j2, j3);
+      const int d1 = j1 - i1, d2 = j2 - i2, d3 = j3 - i3;
+      if (d1 < -2 || d1 > 2 || d2 < -2 || d2 > 2 || d3 < -2 || d3 > 2) {
+        bad = 1ull;
+      } else {
+        const int q = slot125(d1, d2, d3);
+        if (q < 64) m0 |= 1ull << q; else m1 |= 1ull << (q - 64);
+      }
     }
   }
-  if (m) atomicOr(mask, m);
-  if (bad) atomicOr(mask + 1, 1u);
+  if (m0) atomicOr(mask, m0);
+  if (m1) atomicOr(mask + 1, m1);
+  if (bad) atomicOr(mask + 2, 1ull);
 }
-void launch_csr_mask(cudaStream_t s, int n1, int n2, const int64_t* indptr, const int32_t* indices, unsigned* mask) {
+void launch_csr_mask(cudaStream_t s, int n1, int n2, int n3, const int64_t* indptr, const int32_t* indices,
+                     unsigned long long* mask) {
   ++g_launch_count;
-  long N = (long)n1 * n2;
+  long N = (long)n1 * n2 * n3;
   int blocks = (int)((N + 255) / 256);
   if (blocks > 4096) blocks = 4096;
-  k_csr_mask<<<blocks, 256, 0, s>>>(n1, n2, indptr, indices, mask);
+  k_csr_mask<<<blocks, 256, 0, s>>>(n1, n2, n3, indptr, indices, mask);
 }
 
-__global__ void k_csr_scatter(int n1, int n2, const int64_t* indptr, const int32_t* indices, const cplx* data,
-                              const int* slot_of, cplx* coef) {
-  const long N = (long)n1 * n2;
+__global__ void k_csr_scatter(int n1, int n2, int n3, const int64_t* indptr, const int32_t* indices,
+                              const cplx* data, const int* slot_of, cplx* coef) {
+  const long N = (long)n1 * n2 * n3;
   for (long row = (long)blockIdx.x * blockDim.x + threadIdx.x; row < N; row += (long)gridDim.x * blockDim.x) {
-    const int i1 = (int)(row / n2), i2 = (int)(row - (long)i1 * n2);
+    int i1, i2, i3;
+    decomp3(row, n2, n3, i1, i2, i3);
     for (int64_t p = indptr[row]; p < indptr[row + 1]; ++p) {
-      const long col = indices[p];
-      const int j1 = (int)(col / n2), j2 = (int)(col - (long)j1 * n2);
-      const int sl = slot_of[slot25(j1 - i1, j2 - i2)];
+      int j1, j2, j3;
+      decomp3(indices[p], n2, n3, j1, j2, j3);
+      const int sl = slot_of[slot125(j1 - i1, j2 - i2, j3 - i3)];
       cplx* dst = coef + (long)sl * N + row;
       *dst = cadd(*dst, data[p]);
     }
   }
 }
-void launch_csr_scatter(cudaStream_t s, int n1, int n2, const int64_t* indptr, const int32_t* indices,
+void launch_csr_scatter(cudaStream_t s, int n1, int n2, int n3, const int64_t* indptr, const int32_t* indices,
                         const cplx* data, const int* slot_of, cplx* coef) {
   ++g_launch_count;
-  long N = (long)n1 * n2;
+  long N = (long)n1 * n2 * n3;
   int blocks = (int)((N + 255) / 256);
   if (blocks > 4096) blocks = 4096;
-  k_csr_scatter<<<blocks, 256, 0, s>>>(n1, n2, indptr, indices, data, slot_of, coef);
+  k_csr_scatter<<<blocks, 256, 0, s>>>(n1, n2, n3, indptr, indices, data, slot_of, coef);
 }
 
 // z = r / d elementwise (numpy complex division), helmadr/krylov.py:68-73
@@ -684,16 +740,17 @@ void launch_add_diag_real(cudaStream_t s, long n, cplx* center, cplx sc, const d
 
 // diag(left) @ A @ diag(right): scipy csr_matmat products, left first (helmadr/operators.py:264)
 __global__ void k_similarity(StencilDev A, cplx* out, const cplx* left, const cplx* right) {
-  const int n1 = A.n1, n2 = A.n2;
-  const long N = (long)n1 * n2;
+  const int n1 = A.n1, n2 = A.n2, n3 = A.n3;
+  const long N = (long)n1 * n2 * n3;
   for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (long)gridDim.x * blockDim.x) {
-    const int i1 = (int)(k / n2), i2 = (int)(k - (long)i1 * n2);
+    int i1, i2, i3;
+    decomp3(k, n2, n3, i1, i2, i3);
     for (int o = 0; o < A.nofs; ++o) {
-      const int j1 = i1 + A.d1[o], j2 = i2 + A.d2[o];
+      const int j1 = i1 + A.d1[o], j2 = i2 + A.d2[o], j3 = i3 + A.d3[o];
       cplx v = mk(0.0, 0.0);
-      if (j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2) {
+      if (j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2 && j3 >= 0 && j3 < n3) {
         const cplx c = A.coef[(long)o * N + k];
-        v = cmul_sp(cmul_sp(left[k], c), right[(long)j1 * n2 + j2]);
+        v = cmul_sp(cmul_sp(left[k], c), right[((long)j1 * n2 + j2) * n3 + j3]);
       }
       out[(long)o * N + k] = v;
     }
@@ -701,66 +758,76 @@ __global__ void k_similarity(StencilDev A, cplx* out, const cplx* left, const cp
 }
 void launch_similarity(cudaStream_t s, const StencilDev& A, cplx* out, const cplx* left, const cplx* right) {
   ++g_launch_count;
-  long N = (long)A.n1 * A.n2;
+  long N = (long)A.n1 * A.n2 * A.n3;
   int blocks = (int)((N + 255) / 256);
   if (blocks > 4096) blocks = 4096;
   k_similarity<<<blocks, 256, 0, s>>>(A, out, left, right);
 }
 
 // K8: Galerkin coarse operator A_c = P^T A P on the stencil representation.
-// Pass 1 (coef_c == null): OR the mask of non-zero coarse offsets (5x5 box).
+// Pass 1 (coef_c == null): OR the mask of non-zero coarse offsets (5x5x5 box).
 // Pass 2: write the compacted planes (slot_of maps box slot -> plane).
-__global__ void k_galerkin(StencilDev Af, int n1c, int n2c, unsigned* mask, const int* slot_of, cplx* coef_c) {
-  const int n1f = Af.n1, n2f = Af.n2;
-  const long Nf = (long)n1f * n2f, Nc = (long)n1c * n2c;
-  unsigned m = 0u;
+__global__ void k_galerkin(StencilDev Af, int n1c, int n2c, int n3c, unsigned long long* mask, const int* slot_of,
+                           cplx* coef_c) {
+  const int n1f = Af.n1, n2f = Af.n2, n3f = Af.n3;
+  const long Nf = (long)n1f * n2f * n3f, Nc = (long)n1c * n2c * n3c;
+  const int c3lo = n3f > 1 ? -1 : 0, c3hi = n3f > 1 ? 1 : 0;
+  unsigned long long m0 = 0ull, m1 = 0ull;
   for (long c = (long)blockIdx.x * blockDim.x + threadIdx.x; c < Nc; c += (long)gridDim.x * blockDim.x) {
-    const int I1 = (int)(c / n2c), I2 = (int)(c - (long)I1 * n2c);
-    cplx acc[25];
-#pragma unroll
-    for (int q = 0; q < 25; ++q) acc[q] = mk(0.0, 0.0);
+    int I1, I2, I3;
+    decomp3(c, n2c, n3c, I1, I2, I3);
+    cplx acc[125];
+    for (int q = 0; q < 125; ++q) acc[q] = mk(0.0, 0.0);
     for (int a = -1; a <= 1; ++a) {
       const int f1 = 2 * I1 + a;
       if (f1 < 0 || f1 >= n1f) continue;
       for (int b = -1; b <= 1; ++b) {
         const int f2 = 2 * I2 + b;
         if (f2 < 0 || f2 >= n2f) continue;
-        const double wf = (a == 0 ? 1.0 : 0.5) * (b == 0 ? 1.0 : 0.5);
-        const long f = (long)f1 * n2f + f2;
-        for (int o = 0; o < Af.nofs; ++o) {
-          const int g1 = f1 + Af.d1[o], g2 = f2 + Af.d2[o];
-          if (g1 < 0 || g1 >= n1f || g2 < 0 || g2 >= n2f) continue;
-          const cplx cf = Af.coef[(long)o * Nf + f];
-          if (cf.x == 0.0 && cf.y == 0.0) continue;
-          const cplx wc = mk(wf * cf.x, wf * cf.y);
-          int p1[2], p2[2], m1, m2;
-          double v1, v2;
-          if (g1 & 1) { p1[0] = g1 >> 1; p1[1] = (g1 >> 1) + 1; m1 = 2; v1 = 0.5; } else { p1[0] = g1 >> 1; m1 = 1; v1 = 1.0; }
-          if (g2 & 1) { p2[0] = g2 >> 1; p2[1] = (g2 >> 1) + 1; m2 = 2; v2 = 0.5; } else { p2[0] = g2 >> 1; m2 = 1; v2 = 1.0; }
-          for (int x = 0; x < m1; ++x)
-            for (int y = 0; y < m2; ++y) {
-              const int D1 = p1[x] - I1, D2 = p2[y] - I2;
-              const double pw = v1 * v2;
-              const int sl = slot25(D1, D2);
-              acc[sl] = cadd(acc[sl], mk(pw * wc.x, pw * wc.y));
-            }
+        for (int cc = c3lo; cc <= c3hi; ++cc) {
+          const int f3 = 2 * I3 + cc;
+          if (f3 < 0 || f3 >= n3f) continue;
+          const double wf = (a == 0 ? 1.0 : 0.5) * (b == 0 ? 1.0 : 0.5) * (cc == 0 ? 1.0 : 0.5);
+          const long f = ((long)f1 * n2f + f2) * n3f + f3;
+          for (int o = 0; o < Af.nofs; ++o) {
+            const int g1 = f1 + Af.d1[o], g2 = f2 + Af.d2[o], g3 = f3 + Af.d3[o];
+            if (g1 < 0 || g1 >= n1f || g2 < 0 || g2 >= n2f || g3 < 0 || g3 >= n3f) continue;
+            const cplx cf = Af.coef[(long)o * Nf + f];
+            if (cf.x == 0.0 && cf.y == 0.0) continue;
+            const cplx wc = mk(wf * cf.x, wf * cf.y);
+            int p1[2], p2[2], p3[2];
+            double v1, v2, v3;
+            const int m1n = parents(g1, p1, v1), m2n = parents(g2, p2, v2), m3n = parents(g3, p3, v3);
+            for (int x = 0; x < m1n; ++x)
+              for (int y = 0; y < m2n; ++y)
+                for (int z = 0; z < m3n; ++z) {
+                  const int sl = slot125(p1[x] - I1, p2[y] - I2, p3[z] - I3);
+                  const double pw = v1 * v2 * v3;
+                  acc[sl] = cadd(acc[sl], mk(pw * wc.x, pw * wc.y));
+                }
+          }
         }
       }
     }
-    for (int q = 0; q < 25; ++q) {
-      if (acc[q].x != 0.0 || acc[q].y != 0.0) m |= 1u << q;
+    for (int q = 0; q < 125; ++q) {
+      if (acc[q].x != 0.0 || acc[q].y != 0.0) {
+        if (q < 64) m0 |= 1ull << q; else m1 |= 1ull << (q - 64);
+      }
       if (coef_c && slot_of[q] >= 0) coef_c[(long)slot_of[q] * Nc + c] = acc[q];
     }
   }
-  if (mask && m) atomicOr(mask, m);
+  if (mask) {
+    if (m0) atomicOr(mask, m0);
+    if (m1) atomicOr(mask + 1, m1);
+  }
 }
-void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, unsigned* mask, const int* slot_of,
-                     cplx* coef_c) {
+void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, int n3c, unsigned long long* mask,
+                     const int* slot_of, cplx* coef_c) {
   ++g_launch_count;
-  long Nc = (long)n1c * n2c;
+  long Nc = (long)n1c * n2c * n3c;
   int blocks = (int)((Nc + 127) / 128);
   if (blocks > 4096) blocks = 4096;
-  k_galerkin<<<blocks, 128, 0, s>>>(Af, n1c, n2c, mask, slot_of, coef_c);
+  k_galerkin<<<blocks, 128, 0, s>>>(Af, n1c, n2c, n3c, mask, slot_of, coef_c);
 }
 
 }  // namespace hadr
@@ -768,16 +835,26 @@ void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, uns
 namespace hadr {
 
 // ---------------------------------------------------------------------------
-// On-device assembly of the ADR / Helmholtz operators (helmadr/operators.py:85-234)
-// into the 9 plus-radius-2 planes, ordered (d1, d2) ascending:
-//   0:(-2,0) 1:(-1,0) 2:(0,-2) 3:(0,-1) 4:(0,0) 5:(0,1) 6:(0,2) 7:(1,0) 8:(2,0)
+// On-device assembly of the ADR / Helmholtz operators (helmadr/operators.py:85-234),
+// per axis, into the plus-radius-2 planes of `dim` axes, ordered (d1, d2, d3):
+//   2D (9):  (-2,0) (-1,0) (0,-2) (0,-1) (0,0) (0,1) (0,2) (1,0) (2,0)
+//   3D (13): the same with a third axis.
 // Each term is formed with the reference's numpy expression semantics; the
 // duplicates of a row are summed in the order the reference appends them.
+// 3D restatement decisions: faces (left,right) / (front,back) / (top,bottom) for
+// axes 0 / 1 / last; mass weight -i/(2 dim) (2D: the reference's -0.25j).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int p9(int ax, int d) {  // plane of offset d along axis ax
-  if (d == 0) return 4;
-  if (ax == 0) return d == -2 ? 0 : d == -1 ? 1 : d == 1 ? 7 : 8;
-  return d == -2 ? 2 : d == -1 ? 3 : d == 1 ? 5 : 6;
+__device__ __forceinline__ int pl(int dim, int ax, int d) {  // plane of offset d along axis ax
+  if (dim == 2) {
+    if (d == 0) return 4;
+    if (ax == 0) return d == -2 ? 0 : d == -1 ? 1 : d == 1 ? 7 : 8;
+    return d == -2 ? 2 : d == -1 ? 3 : d == 1 ? 5 : 6;
+  }
+  // 3D order: (-2,0,0) (-1,0,0) (0,-2,0) (0,-1,0) (0,0,-2) (0,0,-1) (0,0,0) (0,0,1) (0,0,2) (0,1,0) (0,2,0) (1,0,0) (2,0,0)
+  if (d == 0) return 6;
+  if (ax == 0) return d == -2 ? 0 : d == -1 ? 1 : d == 1 ? 11 : 12;
+  if (ax == 1) return d == -2 ? 2 : d == -1 ? 3 : d == 1 ? 9 : 10;
+  return d == -2 ? 4 : d == -1 ? 5 : d == 1 ? 7 : 8;
 }
 
 // complex scalar (python complex) times real array element, numpy complex multiply
@@ -786,26 +863,32 @@ __device__ __forceinline__ cplx cs_times_real(cplx s, double v) { return cmul_np
 __device__ __forceinline__ cplx cdiv_real(cplx a, double d) { return cdiv_np(a, mk(d, 0.0)); }
 
 struct AsmArgs {
-  int n1, n2;
-  double h1, h2, omega;
+  int dim;
+  int n[3];
+  double h[3];
+  double omega;
   int scheme;       // 0 central, 1 upwind1, 2 upwind2, 3 helmholtz
-  int bc[4];        // top, bottom, left, right: 0 neumann, 1 sommerfeld
-  int src1, src2;   // source node (near-source set), -1 = none
-  const double *ksq, *gam, *g1, *g2, *lap;
-  cplx* coef;       // 9 planes
+  int face[3][2];   // per axis (low, high): 0 neumann, 1 sommerfeld
+  int src[3];       // source node (near-source set), src[0] = -1: none
+  const double *ksq, *gam, *g[3], *lap;
+  cplx* coef;       // 9 (2D) / 13 (3D) planes
   unsigned* mask;   // OR of non-zero planes
 };
 
 __global__ void k_assemble(AsmArgs a) {
-  const long N = (long)a.n1 * a.n2;
+  const int dim = a.dim;
+  const int n1 = a.n[0], n2 = a.n[1], n3 = dim == 3 ? a.n[2] : 1;
+  const long N = (long)n1 * n2 * n3;
+  const int NP = dim == 2 ? 9 : 13;
   unsigned m = 0u;
   const double om = a.omega;
   for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (long)gridDim.x * blockDim.x) {
-    const int i1 = (int)(k / a.n2), i2 = (int)(k - (long)i1 * a.n2);
-    cplx acc[9];
-    bool has[9];
+    int ii[3];
+    decomp3(k, n2, n3, ii[0], ii[1], ii[2]);
+    cplx acc[13];
+    bool has[13];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) {
+    for (int q = 0; q < 13; ++q) {
       acc[q] = mk(0.0, 0.0);
       has[q] = false;
     }
@@ -814,86 +897,89 @@ __global__ void k_assemble(AsmArgs a) {
       has[q] = true;
     };
     const bool helm = a.scheme == 3;
-    const double gr[2] = {helm ? 0.0 : a.g1[k], helm ? 0.0 : a.g2[k]};
+    double gr[3] = {0.0, 0.0, 0.0};
+    if (!helm)
+      for (int ax = 0; ax < dim; ++ax) gr[ax] = a.g[ax][k];
     const double kap = sqrt(a.ksq[k]);
+    const int cen = pl(dim, 0, 0);
     // ---- Laplacian + ghost-eliminated BC (helmadr/operators.py:85-120) ----
-    for (int ax = 0; ax < 2; ++ax) {
-      const double h = ax == 0 ? a.h1 : a.h2;
-      const int idx = ax == 0 ? i1 : i2, size = ax == 0 ? a.n1 : a.n2;
+    for (int ax = 0; ax < dim; ++ax) {
+      const double h = a.h[ax];
+      const int idx = ii[ax], size = a.n[ax];
       const double ih2 = 1.0 / (h * h);
-      if (idx >= 1) put(p9(ax, -1), mk(ih2, 0.0));
-      if (idx <= size - 2) put(p9(ax, 1), mk(ih2, 0.0));
-      put(4, mk(-2.0 * ih2, 0.0));
+      if (idx >= 1) put(pl(dim, ax, -1), mk(ih2, 0.0));
+      if (idx <= size - 2) put(pl(dim, ax, 1), mk(ih2, 0.0));
+      put(cen, mk(-2.0 * ih2, 0.0));
       for (int lo = 1; lo >= 0; --lo) {
         if (lo ? idx != 0 : idx != size - 1) continue;
         const double nd = lo ? -gr[ax] : gr[ax];
-        const int kind = ax == 0 ? a.bc[lo ? 2 : 3] : a.bc[lo ? 0 : 1];
+        const int kind = a.face[ax][lo ? 0 : 1];
         if (kind == 0) {
-          put(p9(ax, lo ? 1 : -1), mk(ih2, 0.0));
-          // 2j * omega * nd / h
-          const cplx c2 = mk(0.0 * om, 2.0 * om);
-          put(4, cdiv_real(cs_times_real(c2, nd), h));
+          put(pl(dim, ax, lo ? 1 : -1), mk(ih2, 0.0));
+          const cplx c2 = mk(0.0 * om, 2.0 * om);  // 2j * omega * nd / h
+          put(cen, cdiv_real(cs_times_real(c2, nd), h));
         } else {
-          // (1.0 + 1j * omega * h * (nd - kappa)) * ih2
-          const cplx c1 = mk(0.0 * om * h, 1.0 * om * h);
+          const cplx c1 = mk(0.0 * om * h, 1.0 * om * h);  // (1.0 + 1j*omega*h*(nd - kappa)) * ih2
           const cplx t = cs_times_real(c1, nd - kap);
           const cplx u = mk(1.0 + t.x, t.y);
-          put(4, cmul_np(u, mk(ih2, 0.0)));
+          put(cen, cmul_np(u, mk(ih2, 0.0)));
         }
       }
     }
     if (!helm) {
       // ---- advection (helmadr/operators.py:123-170) ----
-      const bool near = a.src1 >= 0 && abs(i1 - a.src1) <= 1 && abs(i2 - a.src2) <= 1;
-      for (int ax = 0; ax < 2; ++ax) {
-        const double h = ax == 0 ? a.h1 : a.h2;
-        const int idx = ax == 0 ? i1 : i2, size = ax == 0 ? a.n1 : a.n2;
+      bool near = a.src[0] >= 0;
+      for (int ax = 0; ax < dim; ++ax) near = near && abs(ii[ax] - a.src[ax]) <= 1;
+      for (int ax = 0; ax < dim; ++ax) {
+        const double h = a.h[ax];
+        const int idx = ii[ax], size = a.n[ax];
         const double c = gr[ax];
         const cplx F = cs_times_real(mk(-0.0 * om, -2.0 * om), c);  // -2j * omega * c
         const bool inner = idx >= 1 && idx <= size - 2;
-        const bool cen = a.scheme == 0 ? inner : (inner && near);
-        if (cen) {
-          put(p9(ax, 1), cdiv_real(F, 2.0 * h));
-          put(p9(ax, -1), cdiv_real(cneg(F), 2.0 * h));
+        const bool ctr = a.scheme == 0 ? inner : (inner && near);
+        if (ctr) {
+          put(pl(dim, ax, 1), cdiv_real(F, 2.0 * h));
+          put(pl(dim, ax, -1), cdiv_real(cneg(F), 2.0 * h));
         } else if (c != 0.0) {
           const int sg = c > 0 ? 1 : -1;
           const bool ok2 = sg == 1 ? idx >= 2 : idx <= size - 3;
           const bool ok1 = sg == 1 ? idx >= 1 : idx <= size - 2;
           if (a.scheme != 1 && ok2) {
-            put(4, cdiv_real(cs_times_real(F, sg * 3.0), 2.0 * h));
-            put(p9(ax, -sg), cdiv_real(cs_times_real(F, -sg * 4.0), 2.0 * h));
-            put(p9(ax, -2 * sg), cdiv_real(cs_times_real(F, (double)sg), 2.0 * h));
+            put(cen, cdiv_real(cs_times_real(F, sg * 3.0), 2.0 * h));
+            put(pl(dim, ax, -sg), cdiv_real(cs_times_real(F, -sg * 4.0), 2.0 * h));
+            put(pl(dim, ax, -2 * sg), cdiv_real(cs_times_real(F, (double)sg), 2.0 * h));
           } else if (ok1) {
-            put(4, cdiv_real(cs_times_real(F, (double)sg), h));
-            put(p9(ax, -sg), cdiv_real(cs_times_real(F, (double)-sg), h));
+            put(cen, cdiv_real(cs_times_real(F, (double)sg), h));
+            put(pl(dim, ax, -sg), cdiv_real(cs_times_real(F, (double)-sg), h));
           } else {
-            put(4, cdiv_real(cs_times_real(F, (double)-sg), h));
-            put(p9(ax, sg), cdiv_real(cs_times_real(F, (double)sg), h));
+            put(cen, cdiv_real(cs_times_real(F, (double)-sg), h));
+            put(pl(dim, ax, sg), cdiv_real(cs_times_real(F, (double)sg), h));
           }
         }
       }
       // ---- neighbour-averaged mass term (helmadr/operators.py:173-187) ----
-      const cplx G = cs_times_real(mk(-0.0 * om, -0.25 * om), a.lap[k]);  // -0.25j * omega * lap
-      for (int ax = 0; ax < 2; ++ax) {
-        const int idx = ax == 0 ? i1 : i2, size = ax == 0 ? a.n1 : a.n2;
+      const cplx mw = dim == 2 ? mk(-0.0, -0.25) : mk(-0.0, -1.0 / 6.0);
+      const cplx G = cs_times_real(mk(mw.x * om, mw.y * om), a.lap[k]);
+      for (int ax = 0; ax < dim; ++ax) {
+        const int idx = ii[ax], size = a.n[ax];
         for (int sg = 1; sg >= -1; sg -= 2) {
           const bool ins = sg == 1 ? idx <= size - 2 : idx >= 1;
-          put(ins ? p9(ax, sg) : 4, G);
+          put(ins ? pl(dim, ax, sg) : cen, G);
         }
       }
       // ---- reaction + attenuation (helmadr/operators.py:230-233) ----
-      const double gsq = gr[0] * gr[0] + gr[1] * gr[1];
+      double gsq = gr[0] * gr[0] + gr[1] * gr[1];
+      if (dim == 3) gsq = gsq + gr[2] * gr[2];
       const double react = -(om * om) * (gsq - a.ksq[k]);
       const cplx att = cs_times_real(cs_times_real(mk(-0.0 * om, -1.0 * om), a.gam[k]), a.ksq[k]);
-      put(4, mk(react + att.x, att.y));
+      put(cen, mk(react + att.x, att.y));
     } else {
       // omega**2 * kappa_sq - 1j * omega * gamma * kappa_sq (helmadr/operators.py:198)
       const double w2k = (om * om) * a.ksq[k];
       const cplx t = cs_times_real(cs_times_real(mk(0.0 * om, 1.0 * om), a.gam[k]), a.ksq[k]);
-      put(4, mk(w2k - t.x, 0.0 - t.y));
+      put(cen, mk(w2k - t.x, 0.0 - t.y));
     }
-#pragma unroll
-    for (int q = 0; q < 9; ++q) {
+    for (int q = 0; q < NP; ++q) {
       a.coef[(long)q * N + k] = acc[q];
       if (acc[q].x != 0.0 || acc[q].y != 0.0) m |= 1u << q;
     }
@@ -901,28 +987,45 @@ __global__ void k_assemble(AsmArgs a) {
   if (m) atomicOr(a.mask, m);
 }
 
-void launch_assemble(cudaStream_t s, int n1, int n2, double h1, double h2, double omega, int scheme, const int* bc,
-                     int src1, int src2, const double* ksq, const double* gam, const double* g1, const double* g2,
-                     const double* lap, cplx* coef9, unsigned* mask) {
+void launch_assemble(cudaStream_t s, int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega,
+                     int scheme, const int* bc, int src1, int src2, int src3, const double* ksq, const double* gam,
+                     const double* g1, const double* g2, const double* g3, const double* lap, cplx* coefp,
+                     unsigned* mask) {
   ++g_launch_count;
   AsmArgs a{};
-  a.n1 = n1;
-  a.n2 = n2;
-  a.h1 = h1;
-  a.h2 = h2;
+  a.dim = dim;
+  a.n[0] = n1;
+  a.n[1] = n2;
+  a.n[2] = n3;
+  a.h[0] = h1;
+  a.h[1] = h2;
+  a.h[2] = h3;
   a.omega = omega;
   a.scheme = scheme;
-  for (int i = 0; i < 4; ++i) a.bc[i] = bc[i];
-  a.src1 = src1;
-  a.src2 = src2;
+  // bc = (top, bottom, left, right, front, back)
+  a.face[0][0] = bc[2];
+  a.face[0][1] = bc[3];
+  if (dim == 2) {
+    a.face[1][0] = bc[0];
+    a.face[1][1] = bc[1];
+  } else {
+    a.face[1][0] = bc[4];
+    a.face[1][1] = bc[5];
+    a.face[2][0] = bc[0];
+    a.face[2][1] = bc[1];
+  }
+  a.src[0] = src1;
+  a.src[1] = src2;
+  a.src[2] = src3;
   a.ksq = ksq;
   a.gam = gam;
-  a.g1 = g1;
-  a.g2 = g2;
+  a.g[0] = g1;
+  a.g[1] = g2;
+  a.g[2] = g3;
   a.lap = lap;
-  a.coef = coef9;
+  a.coef = coefp;
   a.mask = mask;
-  long N = (long)n1 * n2;
+  long N = (long)n1 * n2 * (dim == 3 ? n3 : 1);
   int blocks = (int)((N + 127) / 128);
   if (blocks > 4096) blocks = 4096;
   k_assemble<<<blocks, 128, 0, s>>>(a);

@@ -6,17 +6,24 @@ namespace hadr {
 
 extern long long g_launch_count;
 
-// Structured 2D stencil in union-offset, plane-major layout:
-//   coef[o*N + k] multiplies x[k + d1[o]*n2 + d2[o]],  offsets sorted by (d1, d2)
-//   == ascending column index of the reference CSR row, so the accumulation
-//   order equals scipy csr_matvec's.
+// Structured 2D/3D stencil in union-offset, plane-major layout (2D: n3 = 1, d3 = 0):
+//   k = (i1*n2 + i2)*n3 + i3,  coef[o*N + k] multiplies x[k + (d1*n2 + d2)*n3 + d3],
+//   offsets sorted by (d1, d2, d3) == ascending column index of the reference
+//   CSR row for every in-grid entry, so the accumulation order equals scipy
+//   csr_matvec's.
 struct StencilDev {
-  int n1, n2;
+  int n1, n2, n3;
   int nofs;
-  int pad_;
   int8_t d1[HADR_MAX_OFS];
   int8_t d2[HADR_MAX_OFS];
+  int8_t d3[HADR_MAX_OFS];
   const cplx* coef;
+};
+
+// 125 offset slots of the 5x5x5 box, ascending == lexicographic (d1, d2, d3)
+__host__ __device__ __forceinline__ int slot125(int d1, int d2, int d3) { return ((d1 + 2) * 5 + (d2 + 2)) * 5 + (d3 + 2); }
+struct Mask125 {
+  unsigned long long w[2];
 };
 
 enum : int { IN_PLAIN = 0, IN_SCALE = 1, IN_JAC = 2, IN_WRITEV = 4 };
@@ -98,16 +105,19 @@ void launch_fg_finalize(const LaunchCfg& lc, long n, FgCtl* f, const cplx* Z0, c
                         int brk_stage);
 
 // Restriction rc = P^T r and prolongation x += P e (bilinear P, helmadr/multigrid.py:19-46).
-void launch_restrict(const LaunchCfg& lc, int n1f, int n2f, const cplx* r, cplx* rc, Gate g);
-void launch_prolong_add(const LaunchCfg& lc, int n1f, int n2f, const cplx* ec, cplx* x, Gate g);
+// (tri)linear P = kron(P1(n1), P1(n2), P1(n3)); an axis of size 1 is not coarsened.
+void launch_restrict(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx* r, cplx* rc, Gate g);
+void launch_prolong_add(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx* ec, cplx* x, Gate g);
 
 void launch_set_gate(cudaStream_t s, int* dst, Gate g);
 void launch_relax_init(cudaStream_t s, RelaxCtl* c, int steps, Gate g);
 void launch_fg_setup(cudaStream_t s, FgCtl* f, double tol, Gate g);
 
 // ---- operator construction (setup) ----
-void launch_csr_mask(cudaStream_t s, int n1, int n2, const int64_t* indptr, const int32_t* indices, unsigned* mask);
-void launch_csr_scatter(cudaStream_t s, int n1, int n2, const int64_t* indptr, const int32_t* indices,
+// mask: 2 x u64 offset bitset + 1 u64 "reach beyond the box" flag
+void launch_csr_mask(cudaStream_t s, int n1, int n2, int n3, const int64_t* indptr, const int32_t* indices,
+                     unsigned long long* mask);
+void launch_csr_scatter(cudaStream_t s, int n1, int n2, int n3, const int64_t* indptr, const int32_t* indices,
                         const cplx* data, const int* slot_of, cplx* coef);
 void launch_cdiv(cudaStream_t s, long n, const cplx* r, const cplx* d, cplx* z);
 void launch_inv_diag(cudaStream_t s, long n, const cplx* diag, cplx* dinv, int* zero_flag);
@@ -115,10 +125,13 @@ void launch_remap_planes(cudaStream_t s, long n, const cplx* src, int nsrc, cons
                          cplx alpha, int accumulate);
 void launch_add_diag_real(cudaStream_t s, long n, cplx* center, cplx sc, const double* field);
 void launch_similarity(cudaStream_t s, const StencilDev& A, cplx* out, const cplx* left, const cplx* right);
-void launch_assemble(cudaStream_t s, int n1, int n2, double h1, double h2, double omega, int scheme, const int* bc,
-                     int src1, int src2, const double* ksq, const double* gam, const double* g1, const double* g2,
-                     const double* lap, cplx* coef9, unsigned* mask);
-void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, unsigned* mask, const int* slot_of,
-                     cplx* coef_c);
+// ADR/Helmholtz assembly into the plus-radius-2 planes of `dim` axes (2D: 9, 3D: 13 planes);
+// bc[6] = (top, bottom, left, right, front, back) face kinds (0 neumann, 1 sommerfeld)
+void launch_assemble(cudaStream_t s, int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega,
+                     int scheme, const int* bc, int src1, int src2, int src3, const double* ksq, const double* gam,
+                     const double* g1, const double* g2, const double* g3, const double* lap, cplx* coefp,
+                     unsigned* mask);
+void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, int n3c, unsigned long long* mask,
+                     const int* slot_of, cplx* coef_c);
 
 }  // namespace hadr

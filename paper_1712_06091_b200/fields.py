@@ -50,6 +50,73 @@ class GridSpec:
     def coords(self):
         return np.meshgrid(np.linspace(0.0, self.L1, self.n1), np.linspace(0.0, self.L2, self.n2), indexing="ij")
 
+    @property
+    def hs(self):
+        return (self.h1, self.h2)
+
+    @property
+    def Ls(self):
+        return (self.L1, self.L2)
+
+    @property
+    def dim(self) -> int:
+        return 2
+
+
+@dataclass(frozen=True)
+class GridSpec3:
+    """3D nodal grid on [0,L1]x[0,L2]x[0,L3]; the last axis is depth (fastest),
+    k = (i1*n2 + i2)*n3 + i3 — the 2D convention of helmadr/grid.py:5-9 with a
+    second lateral axis (3D restatement decision)."""
+
+    n1: int
+    n2: int
+    n3: int
+    L1: float
+    L2: float
+    L3: float
+
+    def __post_init__(self):
+        if min(self.n1, self.n2, self.n3) < 5:
+            raise ValueError("grid needs at least 5 nodes per dimension")
+        if min(self.L1, self.L2, self.L3) <= 0:
+            raise ValueError("domain lengths must be positive")
+
+    @property
+    def hs(self):
+        return (self.L1 / (self.n1 - 1), self.L2 / (self.n2 - 1), self.L3 / (self.n3 - 1))
+
+    @property
+    def h1(self):
+        return self.hs[0]
+
+    @property
+    def h2(self):
+        return self.hs[1]
+
+    @property
+    def h3(self):
+        return self.hs[2]
+
+    @property
+    def Ls(self):
+        return (self.L1, self.L2, self.L3)
+
+    @property
+    def shape(self):
+        return (self.n1, self.n2, self.n3)
+
+    @property
+    def n_nodes(self) -> int:
+        return self.n1 * self.n2 * self.n3
+
+    @property
+    def dim(self) -> int:
+        return 3
+
+    def coords(self):
+        return np.meshgrid(*[np.linspace(0.0, L, n) for n, L in zip(self.shape, self.Ls)], indexing="ij")
+
 
 @dataclass
 class Medium:
@@ -95,6 +162,35 @@ class SourceSpec:
     def position(self, grid: GridSpec):
         return (self.i1 * grid.h1, self.i2 * grid.h2)
 
+    @property
+    def index(self):
+        return (self.i1, self.i2)
+
+
+@dataclass(frozen=True)
+class SourceSpec3:
+    """Point source at node (i1, i2, i3) of a 3D grid."""
+
+    i1: int
+    i2: int
+    i3: int
+    omega: float
+
+    def validate(self, grid) -> None:
+        if self.omega <= 0:
+            raise ValueError("omega must be positive")
+        on_top = self.i3 == 0 and 0 <= self.i1 < grid.n1 and 0 <= self.i2 < grid.n2
+        inside = all(1 <= i <= n - 2 for i, n in zip(self.index, grid.shape))
+        if not (on_top or inside):
+            raise ValueError(f"source node {self.index} must be inside the grid or on the top face")
+
+    @property
+    def index(self):
+        return (self.i1, self.i2, self.i3)
+
+    def position(self, grid):
+        return tuple(i * h for i, h in zip(self.index, grid.hs))
+
 
 class AnalyticBase:
     """tau0 = |x - x0| with analytic gradient and Laplacian, zeroed at x0
@@ -128,14 +224,26 @@ class TravelTime:
     base: AnalyticBase | None = None
     fm_time: float = 0.0
 
+    grad3: np.ndarray | None = None
+
+    @property
+    def grads(self):
+        return [self.grad1, self.grad2] + ([self.grad3] if self.grad3 is not None else [])
+
     @property
     def grad_sq(self) -> np.ndarray:
-        return self.grad1**2 + self.grad2**2
+        s = self.grad1**2 + self.grad2**2
+        if self.grad3 is not None:
+            s = s + self.grad3**2
+        return s
 
 
 def point_source(grid, source) -> np.ndarray:
-    """1/(h1 h2) at the source node (helmadr/grid.py:128-136)."""
+    """1/(h1 h2 [h3]) at the source node (helmadr/grid.py:128-136)."""
     source.validate(grid)
     q = np.zeros(grid.shape, dtype=np.complex128)
-    q[source.i1, source.i2] = 1.0 / (grid.h1 * grid.h2)
+    if len(grid.shape) == 2:
+        q[source.i1, source.i2] = 1.0 / (grid.h1 * grid.h2)
+    else:
+        q[tuple(source.index)] = 1.0 / float(np.prod(grid.hs))
     return q

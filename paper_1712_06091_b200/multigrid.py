@@ -37,16 +37,16 @@ def galerkin_coarsen(A, P: Prolongation) -> StencilOperator:
 
 
 def coarsenable_levels(shape, max_levels: int):
-    """helmadr/multigrid.py:98-110."""
+    """helmadr/multigrid.py:98-110 (per axis in 3D)."""
     shapes = [tuple(shape)]
     while len(shapes) < max_levels:
-        m1, m2 = shapes[-1]
-        if (m1 - 1) % 2 or (m2 - 1) % 2:
+        m = shapes[-1]
+        if any((mi - 1) % 2 for mi in m):
             break
-        c1, c2 = (m1 - 1) // 2 + 1, (m2 - 1) // 2 + 1
-        if c1 < 3 or c2 < 3:
+        c = tuple((mi - 1) // 2 + 1 for mi in m)
+        if any(ci < 3 for ci in c):
             break
-        shapes.append((c1, c2))
+        shapes.append(c)
     return shapes
 
 
@@ -59,9 +59,10 @@ class MGHierarchy:
         self.coarse_steps = coarse_steps
         self.coarse_tol = coarse_tol
         nl = C.c_int()
-        shp = (C.c_int * 64)()
+        shp = (C.c_int * 96)()
         check(_lib.lib().hadr_hier_info(self._h, C.byref(nl), shp))
-        self.shapes = [(shp[2 * i], shp[2 * i + 1]) for i in range(nl.value)]
+        self.shapes = [(shp[3 * i], shp[3 * i + 1]) if shp[3 * i + 2] == 1 else
+                       (shp[3 * i], shp[3 * i + 1], shp[3 * i + 2]) for i in range(nl.value)]
         self.ops = []
         for l in range(1, nl.value + 1):
             oh = C.c_void_p()
@@ -96,7 +97,7 @@ class MGHierarchy:
         lines = []
         for l, (A, shape) in enumerate(zip(self.ops, self.shapes), start=1):
             relax = f"{self.relax_steps(l)} pre/post" if l < self.n_levels else f"{self.coarse_steps} coarsest"
-            lines.append(f"level {l}: grid {shape[0]}x{shape[1]}, nnz {A.nnz}, relax {relax}")
+            lines.append(f"level {l}: grid {'x'.join(map(str, shape))}, nnz {A.nnz}, relax {relax}")
         return "\n".join(lines)
 
 
@@ -104,7 +105,7 @@ def build_hierarchy(A0, grid, max_levels: int = 5, coarse_steps: int = COARSE_GM
                     coarse_tol: float = COARSE_FGMRES_TOL) -> MGHierarchy:
     """Chain of Galerkin operators on the device (helmadr/multigrid.py:113-129)."""
     shape = tuple(grid.shape) if hasattr(grid, "shape") else tuple(grid)
-    if A0.shape[0] != shape[0] * shape[1]:
+    if A0.shape[0] != int(np.prod(shape)):
         raise ValueError("operator dimension does not match the grid")
     if len(coarsenable_levels(shape, max_levels)) < 2:
         raise ValueError(
@@ -135,7 +136,7 @@ def k_cycle(hier: MGHierarchy, level: int, b, x, stats: dict | None = None) -> n
     """One K-cycle at `level` (1 = finest) on the device (helmadr/multigrid.py:132-171)."""
     if not 1 <= level <= hier.n_levels:
         raise ValueError(f"level {level} outside 1..{hier.n_levels}")
-    n = hier.shapes[level - 1][0] * hier.shapes[level - 1][1]
+    n = int(np.prod(hier.shapes[level - 1]))
     b = as_c128(b, n)
     x = as_c128(x, n)
     x_is_zero = not np.any(x)
@@ -159,7 +160,7 @@ class KCyclePreconditioner:
         self.hier = hier
 
     def __call__(self, r) -> np.ndarray:
-        n = self.hier.shapes[0][0] * self.hier.shapes[0][1]
+        n = int(np.prod(self.hier.shapes[0]))
         r = as_c128(r, n)
         z = np.empty_like(r)
         check(_lib.lib().hadr_precond_apply(self.hier.handle, cbuf(r), cbuf(z), 0))

@@ -25,29 +25,33 @@ _SCHEME_ID = {"central": 0, "upwind1": 1, "upwind2": 2, "helmholtz": 3}
 
 @dataclass(frozen=True)
 class BCSpec:
-    """Boundary condition per side (helmadr/operators.py:30-51)."""
+    """Boundary condition per side (helmadr/operators.py:30-51); front/back are the
+    faces of the second lateral axis of 3D grids (restatement decision)."""
 
     top: str = "neumann"
     bottom: str = "sommerfeld"
     left: str = "sommerfeld"
     right: str = "sommerfeld"
+    front: str = "sommerfeld"
+    back: str = "sommerfeld"
 
     def __post_init__(self):
-        for side in ("top", "bottom", "left", "right"):
+        for side in ("top", "bottom", "left", "right", "front", "back"):
             kind = getattr(self, side)
             if kind not in BC_KINDS:
                 raise ValueError(f"{side} condition {kind!r} not in {BC_KINDS}")
 
     @classmethod
     def all_neumann(cls) -> "BCSpec":
-        return cls("neumann", "neumann", "neumann", "neumann")
+        return cls(*(["neumann"] * 6))
 
     @classmethod
     def all_sommerfeld(cls) -> "BCSpec":
-        return cls("sommerfeld", "sommerfeld", "sommerfeld", "sommerfeld")
+        return cls(*(["sommerfeld"] * 6))
 
     def codes(self):
-        return np.array([BC_KINDS.index(k) for k in (self.top, self.bottom, self.left, self.right)], dtype=np.int32)
+        sides = (self.top, self.bottom, self.left, self.right, self.front, self.back)
+        return np.array([BC_KINDS.index(k) for k in sides], dtype=np.int32)
 
 
 def _bc(bc) -> BCSpec:
@@ -57,7 +61,8 @@ def _bc(bc) -> BCSpec:
         return bc
     if isinstance(bc, (tuple, list)):
         return BCSpec(*bc)
-    return BCSpec(bc.top, bc.bottom, bc.left, bc.right)  # reference BCSpec (duck-typed)
+    return BCSpec(bc.top, bc.bottom, bc.left, bc.right, getattr(bc, "front", "sommerfeld"),
+                  getattr(bc, "back", "sommerfeld"))  # reference BCSpec (duck-typed)
 
 
 def _f64(a, shape):
@@ -67,27 +72,38 @@ def _f64(a, shape):
     return a
 
 
-def _assemble(grid, omega, scheme, bc, kappa_sq, gamma, g1, g2, lap, src):
-    n1, n2 = grid.shape
-    sh = (n1, n2)
+def _assemble(grid, omega, scheme, bc, kappa_sq, gamma, grads, lap, src):
+    sh = tuple(grid.shape)
+    dim = len(sh)
+    n1, n2, n3 = sh[0], sh[1], (sh[2] if dim == 3 else 1)
+    hs = tuple(getattr(grid, "hs", (grid.h1, grid.h2)))
+    h3 = hs[2] if dim == 3 else 1.0
     ksq = _f64(kappa_sq, sh)
     gam = _f64(gamma, sh)
     zero = np.zeros(sh)
-    g1 = _f64(g1 if g1 is not None else zero, sh)
-    g2 = _f64(g2 if g2 is not None else zero, sh)
+    g = [_f64(grads[a] if grads is not None else zero, sh) for a in range(dim)]
+    g3 = g[2] if dim == 3 else zero
     lp = _f64(lap if lap is not None else zero, sh)
     codes = _bc(bc).codes()
-    s1, s2 = (-1, -1) if src is None else (int(src[0]), int(src[1]))
+    s = (-1, -1, -1) if src is None else (tuple(int(v) for v in src) + (0,))[:3]
     h = C.c_void_p()
-    check(_lib.lib().hadr_assemble(n1, n2, float(grid.h1), float(grid.h2), float(omega), _SCHEME_ID[scheme],
-                                   cbuf(codes), s1, s2, cbuf(ksq), cbuf(gam), cbuf(g1), cbuf(g2), cbuf(lp), 0,
-                                   C.byref(h)))
+    check(_lib.lib().hadr_assemble(dim, n1, n2, n3, float(hs[0]), float(hs[1]), float(h3), float(omega),
+                                   _SCHEME_ID[scheme], cbuf(codes), s[0], s[1], s[2], cbuf(ksq), cbuf(gam),
+                                   cbuf(g[0]), cbuf(g[1]), cbuf(g3), cbuf(lp), 0, C.byref(h)))
     return StencilOperator(h)
+
+
+def _source_index(tt):
+    base = getattr(tt, "base", None)
+    if base is None:
+        return None
+    src = base.source
+    return tuple(src.index) if hasattr(src, "index") else (src.i1, src.i2)
 
 
 def assemble_helmholtz(medium, grid, omega: float, bc) -> StencilOperator:
     """Standard five-point Helmholtz operator (helmadr/operators.py:190-200)."""
-    return _assemble(grid, omega, "helmholtz", bc, medium.kappa_sq, medium.gamma, None, None, None, None)
+    return _assemble(grid, omega, "helmholtz", bc, medium.kappa_sq, medium.gamma, None, None, None)
 
 
 def assemble_adr(medium, grid, omega: float, tt, scheme: str, bc) -> StencilOperator:
@@ -96,8 +112,8 @@ def assemble_adr(medium, grid, omega: float, tt, scheme: str, bc) -> StencilOper
         raise ValueError(f"scheme {scheme!r} not in {ADR_SCHEMES}")
     if tuple(tt.grid.shape) != tuple(grid.shape):
         raise ValueError("travel time grid does not match")
-    src = None if getattr(tt, "base", None) is None else (tt.base.source.i1, tt.base.source.i2)
-    return _assemble(grid, omega, scheme, bc, medium.kappa_sq, medium.gamma, tt.grad1, tt.grad2, tt.lap, src)
+    grads = list(getattr(tt, "grads", None) or [tt.grad1, tt.grad2])
+    return _assemble(grid, omega, scheme, bc, medium.kappa_sq, medium.gamma, grads, tt.lap, _source_index(tt))
 
 
 def shift_operator(A, alpha: float, omega: float, medium) -> StencilOperator:

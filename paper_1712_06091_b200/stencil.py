@@ -27,20 +27,24 @@ class StencilOperator:
         self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
         self._owner = owner            # hierarchy that owns a borrowed handle
         self._keep = tuple(keepalive)  # operators a derived handle depends on
-        n1, n2, no = C.c_int(), C.c_int(), C.c_int()
-        offs = (C.c_int * 50)()
-        check(_lib.lib().hadr_op_info(self._h, C.byref(n1), C.byref(n2), C.byref(no), offs))
-        self.grid_shape = (n1.value, n2.value)
-        self.offsets = [(offs[2 * i], offs[2 * i + 1]) for i in range(no.value)]
+        n1, n2, n3, no = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        offs = (C.c_int * 375)()
+        check(_lib.lib().hadr_op_info(self._h, C.byref(n1), C.byref(n2), C.byref(n3), C.byref(no), offs))
+        if n3.value == 1:  # 2D operator
+            self.grid_shape = (n1.value, n2.value)
+            self.offsets = [(offs[3 * i], offs[3 * i + 1]) for i in range(no.value)]
+        else:
+            self.grid_shape = (n1.value, n2.value, n3.value)
+            self.offsets = [(offs[3 * i], offs[3 * i + 1], offs[3 * i + 2]) for i in range(no.value)]
 
     # ---- construction ----
     @classmethod
     def from_csr(cls, A, grid_shape) -> "StencilOperator":
-        """Convert a square CSR matrix on the (n1, n2) grid (bit-exact value copy)."""
-        n1, n2 = int(grid_shape[0]), int(grid_shape[1])
+        """Convert a square CSR matrix on the (n1, n2[, n3]) grid (bit-exact value copy)."""
+        n1, n2, n3 = _dims(grid_shape)
         A = sp.csr_matrix(A)
-        if A.shape != (n1 * n2, n1 * n2):
-            raise ValueError(f"operator {A.shape} does not match grid {n1}x{n2}")
+        if A.shape != (n1 * n2 * n3, n1 * n2 * n3):
+            raise ValueError(f"operator {A.shape} does not match grid {tuple(grid_shape)}")
         if not A.has_canonical_format:
             A = A.copy()
             A.sum_duplicates()
@@ -48,16 +52,18 @@ class StencilOperator:
         indices = np.ascontiguousarray(A.indices, dtype=np.int32)
         data = np.ascontiguousarray(A.data, dtype=np.complex128)
         h = C.c_void_p()
-        check(_lib.lib().hadr_op_from_csr(n1, n2, int(A.nnz), cbuf(indptr), cbuf(indices), cbuf(data), C.byref(h)))
+        check(_lib.lib().hadr_op_from_csr(n1, n2, n3, int(A.nnz), cbuf(indptr), cbuf(indices), cbuf(data),
+                                          C.byref(h)))
         return cls(h)
 
     @classmethod
     def from_planes(cls, grid_shape, offsets, coef) -> "StencilOperator":
-        n1, n2 = int(grid_shape[0]), int(grid_shape[1])
-        offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.int32).reshape(-1))
-        coef = np.ascontiguousarray(np.asarray(coef, dtype=np.complex128).reshape(len(offsets), n1 * n2))
+        n1, n2, n3 = _dims(grid_shape)
+        offs3 = [tuple(o) + (0,) * (3 - len(o)) for o in offsets]
+        offs = np.ascontiguousarray(np.asarray(offs3, dtype=np.int32).reshape(-1))
+        coef = np.ascontiguousarray(np.asarray(coef, dtype=np.complex128).reshape(len(offsets), n1 * n2 * n3))
         h = C.c_void_p()
-        check(_lib.lib().hadr_op_from_planes(n1, n2, len(offsets), cbuf(offs), cbuf(coef), C.byref(h)))
+        check(_lib.lib().hadr_op_from_planes(n1, n2, n3, len(offsets), cbuf(offs), cbuf(coef), C.byref(h)))
         return cls(h)
 
     def __del__(self):
@@ -75,7 +81,7 @@ class StencilOperator:
     # ---- duck-typed matrix surface ----
     @property
     def shape(self):
-        n = self.grid_shape[0] * self.grid_shape[1]
+        n = int(np.prod(self.grid_shape))
         return (n, n)
 
     @property
@@ -90,17 +96,19 @@ class StencilOperator:
 
     def tocsr(self) -> sp.csr_matrix:
         """Export to canonical scipy CSR (structural zeros dropped)."""
-        n1, n2 = self.grid_shape
-        n = n1 * n2
+        n1, n2, n3 = _dims(self.grid_shape)
+        n = n1 * n2 * n3
         P = self.planes()
         k = np.arange(n)
-        i1, i2 = k // n2, k % n2
+        i1, rem = k // (n2 * n3), k % (n2 * n3)
+        i2, i3 = rem // n3, rem % n3
         rows, cols, vals = [], [], []
-        for o, (d1, d2) in enumerate(self.offsets):
-            j1, j2 = i1 + d1, i2 + d2
-            ok = (j1 >= 0) & (j1 < n1) & (j2 >= 0) & (j2 < n2) & (P[o] != 0)
+        for o, d in enumerate(self.offsets):
+            d1, d2, d3 = tuple(d) + (0,) * (3 - len(d))
+            j1, j2, j3 = i1 + d1, i2 + d2, i3 + d3
+            ok = (j1 >= 0) & (j1 < n1) & (j2 >= 0) & (j2 < n2) & (j3 >= 0) & (j3 < n3) & (P[o] != 0)
             rows.append(k[ok])
-            cols.append((j1 * n2 + j2)[ok])
+            cols.append(((j1 * n2 + j2) * n3 + j3)[ok])
             vals.append(P[o][ok])
         A = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(n, n))
         A.sort_indices()
@@ -112,7 +120,7 @@ class StencilOperator:
 
     def diagonal(self) -> np.ndarray:
         try:
-            o = self.offsets.index((0, 0))
+            o = self.offsets.index((0,) * len(self.grid_shape))
         except ValueError:
             return np.zeros(self.shape[0], dtype=np.complex128)
         return self.planes()[o].copy()
@@ -133,7 +141,16 @@ class StencilOperator:
         return self.matvec(x)
 
     def __repr__(self):
-        return f"<StencilOperator {self.grid_shape[0]}x{self.grid_shape[1]}, {len(self.offsets)} offsets, device>"
+        return f"<StencilOperator {'x'.join(map(str, self.grid_shape))}, {len(self.offsets)} offsets, device>"
+
+
+def _dims(shape):
+    shape = tuple(int(v) for v in shape)
+    if len(shape) == 2:
+        return shape[0], shape[1], 1
+    if len(shape) == 3:
+        return shape
+    raise ValueError(f"grid shape must have 2 or 3 axes, got {shape}")
 
 
 def as_operator(A, grid_shape=None) -> StencilOperator:
@@ -161,24 +178,25 @@ class _TransposedProlongation:
     def __matmul__(self, r):
         r = as_c128(r, self.shape[1])
         out = np.empty(self.shape[0], dtype=np.complex128)
-        check(_lib.lib().hadr_transfer(self.P.fine_shape[0], self.P.fine_shape[1], 0, cbuf(r), cbuf(out), 0))
+        check(_lib.lib().hadr_transfer(*_dims(self.P.fine_shape), 0, cbuf(r), cbuf(out), 0))
         return out
 
 
 class Prolongation:
-    """Bilinear P = kron(P1(n1), P1(n2)) applied matrix-free on the device
-    (helmadr/multigrid.py:19-46).  ``P @ e`` prolongs, ``P.T @ r`` restricts."""
+    """Bilinear (2D) / trilinear (3D) P = kron of 1D interpolations, applied
+    matrix-free on the device (helmadr/multigrid.py:19-46).  ``P @ e`` prolongs,
+    ``P.T @ r`` restricts."""
 
     def __init__(self, fine_shape):
-        n1, n2 = int(fine_shape[0]), int(fine_shape[1])
-        if (n1 - 1) % 2 or (n2 - 1) % 2:
+        fine_shape = tuple(int(v) for v in fine_shape)
+        if any((n - 1) % 2 for n in fine_shape):
             raise ValueError(f"cannot coarsen {fine_shape}: interval count is odd")
-        self.fine_shape = (n1, n2)
-        self.coarse_shape = ((n1 - 1) // 2 + 1, (n2 - 1) // 2 + 1)
+        self.fine_shape = fine_shape
+        self.coarse_shape = tuple((n - 1) // 2 + 1 for n in fine_shape)
 
     @property
     def shape(self):
-        return (self.fine_shape[0] * self.fine_shape[1], self.coarse_shape[0] * self.coarse_shape[1])
+        return (int(np.prod(self.fine_shape)), int(np.prod(self.coarse_shape)))
 
     @property
     def T(self):
@@ -187,7 +205,7 @@ class Prolongation:
     def __matmul__(self, e):
         e = as_c128(e, self.shape[1])
         out = np.empty(self.shape[0], dtype=np.complex128)
-        check(_lib.lib().hadr_transfer(self.fine_shape[0], self.fine_shape[1], 1, cbuf(e), cbuf(out), 0))
+        check(_lib.lib().hadr_transfer(*_dims(self.fine_shape), 1, cbuf(e), cbuf(out), 0))
         return out
 
     def tocsr(self) -> sp.csr_matrix:
@@ -203,6 +221,9 @@ class Prolongation:
                     v += [0.5, 0.5]
             return sp.csr_matrix((v, (r, c)), shape=(nf, nc))
 
-        P = sp.kron(p1(self.fine_shape[0]), p1(self.fine_shape[1])).tocsr()
+        P = p1(self.fine_shape[0])
+        for n in self.fine_shape[1:]:
+            P = sp.kron(P, p1(n))
+        P = P.tocsr()
         P.sort_indices()
         return P

@@ -148,8 +148,75 @@ def cfg2(n: int = 1025, ppw: float = 12.0, layer: int | None = None) -> Workload
     return Workload(f"cfg2_{n}", grid, med, src, tt, ALL_SOMMERFELD)
 
 
+class _Base3:
+    def __init__(self, source):
+        self.source = source
+
+
+def travel_time_nd(grid, source, tau1) -> TravelTime:
+    """3D chain rule on tau = tau0*tau1: the per-axis generalisation of
+    helmadr/eikonal.py:204-226 (lap(tau0) = 2/r in 3D; grad = 0 and lap = 2 tau1
+    at the source node)."""
+    X = grid.coords()
+    pos = source.position(grid)
+    e = [X[a] - pos[a] for a in range(3)]
+    r = np.sqrt(e[0] ** 2 + e[1] ** 2 + e[2] ** 2)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        g = [np.where(r > 0, ea / r, 0.0) for ea in e]
+        l0 = np.where(r > 0, 2.0 / r, 0.0)
+    hs = grid.hs
+    a = [_d1(tau1, hs[ax], ax) for ax in range(3)]
+    lap1 = _d2(tau1, hs[0], 0) + _d2(tau1, hs[1], 1)
+    lap1 = lap1 + _d2(tau1, hs[2], 2)
+    grads = [r * a[ax] + tau1 * g[ax] for ax in range(3)]
+    s = g[0] * a[0] + g[1] * a[1]
+    s = s + g[2] * a[2]
+    lap = tau1 * l0 + 2.0 * s + r * lap1
+    idx = source.index
+    for gr in grads:
+        gr[idx] = 0.0
+    lap[idx] = 2.0 * tau1[idx]
+    return TravelTime(grid, tau1, r * tau1, grads[0], grads[1], lap, _Base3(source), 0.0, grads[2])
+
+
+def cfg4(n: int = 513, ppw: float = 10.0, layer: int | None = None) -> Workload:
+    """BASELINE config 4 (n=513): 513 x 513 x 257 on [0,1]^2 x [0,0.5], h = 1/512,
+    v = 1.5 + 2.5 z (z = depth, the last axis), source (0.5, 0.5, 0.05), 10 ppw at
+    v = 1.5, 16-cell layer on all six faces, all-Sommerfeld, analytic tau."""
+    from .fields import GridSpec3, SourceSpec3
+
+    n3 = (n - 1) // 2 + 1
+    grid = GridSpec3(n, n, n3, 1.0, 1.0, 0.5)
+    h = grid.h1
+    vmin, g = 1.5, 2.5
+    omega = 2.0 * np.pi * vmin / (ppw * h)
+    layer = layer if layer is not None else max(2, round(16 * (n - 1) / 512))
+    i3 = max(layer + 2, round(0.05 / grid.h3))
+    src = SourceSpec3((n - 1) // 2, (n - 1) // 2, i3, omega)
+    X = grid.coords()
+    v = vmin + g * X[2]
+    ksq = 1.0 / v**2
+    gam = np.zeros(grid.shape)
+    for ax in range(3):
+        w = layer * grid.hs[ax]
+        for depth in (w - X[ax], X[ax] - (grid.Ls[ax] - w)):
+            d = np.clip(depth, 0.0, w)
+            gam = np.maximum(gam, omega * (d / w) ** 2)
+    med = Medium(grid, ksq, gam)
+    pos = src.position(grid)
+    vs = vmin + g * pos[2]
+    r = np.sqrt((X[0] - pos[0]) ** 2 + (X[1] - pos[1]) ** 2 + (X[2] - pos[2]) ** 2)
+    tau = np.arccosh(1.0 + (g * r) ** 2 / (2.0 * v * vs)) / g
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t1 = np.where(r > 0, tau / r, 1.0 / vs)
+    t1[src.index] = 1.0 / vs
+    tt = travel_time_nd(grid, src, t1)
+    bc = ("sommerfeld",) * 6  # (top, bottom, left, right, front, back)
+    return Workload(f"cfg4_{n}", grid, med, src, tt, bc)
+
+
 def by_name(name: str, n: int | None = None) -> Workload:
-    builders = {"cfg1": cfg1, "cfg2": cfg2}
+    builders = {"cfg1": cfg1, "cfg2": cfg2, "cfg4": cfg4}
     if name not in builders:
         raise ValueError(f"unknown workload {name!r}; known: {sorted(builders)}")
     return builders[name]() if n is None else builders[name](n)

@@ -1,0 +1,110 @@
+"""3D GPU parity (BASELINE configs 4/5 have no reference: the oracle is the
+dimension-generic restatement oracle/hadr_oracle_nd.py, whose 2D instantiation
+is pinned bit-exact to the reference).  Tolerances as in test_gpu_parity.py."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def hadr():
+    import paper_1712_06091_b200 as H
+
+    H._lib.lib()
+    return H
+
+
+@pytest.fixture(scope="module", params=[17, 33])
+def case3d(request):
+    from oracle import hadr_oracle_nd as ND
+    from paper_1712_06091_b200 import workloads
+
+    wl = workloads.cfg4(request.param)
+    g = wl.grid
+    shape, hs, src = g.shape, g.hs, wl.source.index
+    bc = ND.bc_dict(3, wl.bc)
+    grads, lap, tau = ND.tau_fields(wl.tt.tau1, g.Ls, src)
+    args = (shape, hs, wl.omega, wl.medium.kappa_sq, wl.medium.gamma, grads, lap, src)
+    H2 = ND.adr_csr(*args, "upwind2", bc)
+    H1 = ND.adr_csr(*args, "upwind1", bc)
+    B = (0.75 * H2 + 0.25 * H1).tocsr()
+    return dict(wl=wl, shape=shape, hs=hs, src=src, bc=bc, grads=grads, lap=lap, tau=tau, H2=H2, H1=H1, B=B,
+                Hi=ND.hierarchy(B, shape, 5))
+
+
+def test_spmv_and_transfer_bitexact_3d(hadr, case3d):
+    from oracle import hadr_oracle_nd as ND
+
+    shape, H2 = case3d["shape"], case3d["H2"]
+    op = hadr.StencilOperator.from_csr(H2, shape)
+    assert len(op.offsets) <= 13
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(H2.shape[0]) + 1j * rng.standard_normal(H2.shape[0])
+    assert np.array_equal(op @ x, H2 @ x)
+    P = ND.prolongation(shape)
+    Pd = hadr.build_prolongation(shape)
+    assert np.array_equal(Pd.T @ x, P.T @ x)
+    e = x[: P.shape[1]]
+    assert np.array_equal(Pd @ e, P @ e)
+    # coarse 81-offset operator: chunked stencil path
+    A1 = case3d["Hi"].ops[1]
+    op1 = hadr.StencilOperator.from_csr(A1, case3d["Hi"].shapes[1])
+    x1 = x[: A1.shape[0]]
+    assert np.array_equal(op1 @ x1, A1 @ x1)
+
+
+def test_device_assembly_3d(hadr, case3d):
+    from paper_1712_06091_b200 import operators
+
+    wl = case3d["wl"]
+    for scheme, ref in (("upwind2", case3d["H2"]), ("upwind1", case3d["H1"])):
+        got = operators.assemble_adr(wl.medium, wl.grid, wl.omega, wl.tt, scheme, wl.bc).tocsr()
+        assert np.array_equal(got.indptr, ref.indptr) and np.array_equal(got.indices, ref.indices)
+        assert np.abs(got.data - ref.data).max() <= 4e-16 * np.abs(ref.data).max()
+
+
+def test_galerkin_3d(hadr, case3d):
+    Hi = case3d["Hi"]
+    H = hadr.build_hierarchy(case3d["B"], case3d["shape"], 5)
+    assert [tuple(s) for s in H.shapes] == [tuple(s) for s in Hi.shapes]
+    for l in range(1, H.n_levels):
+        ref = Hi.ops[l]
+        err = abs(H.ops[l].tocsr() - ref).max()
+        assert err <= 1e-12 * abs(ref).max(), (l, err)
+
+
+@pytest.mark.parametrize("engine", ["cluster", "graph"])
+def test_kcycle_3d(hadr, case3d, engine):
+    from oracle import hadr_oracle as O
+
+    hadr._lib.set_option("ce_max_n", 32768 if engine == "cluster" else 0)
+    try:
+        Hi = case3d["Hi"]
+        H = hadr.hierarchy_from_ops(Hi.ops, shapes=Hi.shapes)
+        n = Hi.ops[0].shape[0]
+        rng = np.random.default_rng(9)
+        b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        ref = O.kcycle(Hi, 1, b, np.zeros_like(b))
+        assert rel(hadr.k_cycle(H, 1, b, np.zeros_like(b)), ref) <= 1e-12
+        assert rel(hadr.make_kcycle_preconditioner(H)(b), ref) <= 1e-12
+    finally:
+        hadr._lib.set_option("ce_max_n", 32768)
+
+
+def test_solve_upwind_3d(hadr, case3d):
+    from oracle import hadr_oracle_nd as ND
+    from paper_1712_06091_b200 import drivers
+
+    wl = case3d["wl"]
+    a_ref, rep_ref = ND.solve_upwind(case3d["shape"], case3d["hs"], wl.omega, case3d["src"], wl.medium.kappa_sq,
+                                     wl.medium.gamma, case3d["grads"], case3d["lap"], case3d["tau"], case3d["bc"])
+    cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=1e-6, max_iter=1000)
+    u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
+    assert rep.converged and abs(rep.iterations - rep_ref.iterations) <= 1
+    assert rel(a, a_ref) <= 1e-6

@@ -106,3 +106,58 @@ def test_cfg1_iteration_counts_match_survey(gcfg1):
     assert int(gcfg1["upwind_iterations"]) == 18
     assert int(gcfg1["central_iterations"]) == 19
     assert int(gcfg1["standard_iterations"]) == 20
+
+
+@pytest.mark.parametrize("case", ["g33", "g65"])
+def test_nd_oracle_2d_is_bitexact(case, request):
+    """The dimension-generic oracle (used for 3D) reproduces the reference in 2D bit for bit."""
+    from oracle import hadr_oracle_nd as ND
+
+    g = request.getfixturevalue(case)
+    wl = CASES[case]()
+    shape, Ls = wl.grid.shape, (wl.grid.L1, wl.grid.L2)
+    src = (wl.source.i1, wl.source.i2)
+    grads, lap, tau = ND.tau_fields(wl.tt.tau1, Ls, src)
+    assert np.array_equal(grads[0], g["grad1"]) and np.array_equal(grads[1], g["grad2"])
+    assert np.array_equal(lap, g["lap"]) and np.array_equal(tau, g["tau"])
+    hs = (wl.grid.h1, wl.grid.h2)
+    bc = ND.bc_dict(2, wl.bc)
+    H2 = ND.adr_csr(shape, hs, wl.omega, wl.medium.kappa_sq, wl.medium.gamma, grads, lap, src, "upwind2", bc)
+    _same_csr(H2, g, "H2up")
+    B = csr_from(g, "blend")
+    Hi = ND.hierarchy(B, shape, 5)
+    for l, A in enumerate(Hi.ops):
+        _same_csr(A, g, f"lev{l}")
+    if case == "g33":
+        _same_csr(ND.helmholtz_csr(shape, hs, wl.omega, wl.medium.kappa_sq, wl.medium.gamma, bc), g, "H")
+        for scheme, key in (("upwind1", "H1up"), ("central", "Hcen")):
+            A = ND.adr_csr(shape, hs, wl.omega, wl.medium.kappa_sq, wl.medium.gamma, grads, lap, src, scheme, bc)
+            _same_csr(A, g, key)
+
+
+def test_nd_oracle_3d_structure():
+    """3D instantiation: stencil reach, Galerkin identity, P partition of unity, a converging solve."""
+    from oracle import hadr_oracle as O
+    from oracle import hadr_oracle_nd as ND
+    from paper_1712_06091_b200 import workloads
+
+    wl = workloads.cfg4(17)
+    shape = wl.grid.shape
+    hs = wl.grid.hs
+    src = wl.source.index
+    bc = ND.bc_dict(3, wl.bc)
+    grads, lap, tau = ND.tau_fields(wl.tt.tau1, wl.grid.Ls, src)
+    for a, b_ in zip(grads, wl.tt.grads):
+        assert np.array_equal(a, b_)
+    H2 = ND.adr_csr(shape, hs, wl.omega, wl.medium.kappa_sq, wl.medium.gamma, grads, lap, src, "upwind2", bc)
+    assert np.diff(H2.indptr).max() <= 13
+    P = ND.prolongation(shape)
+    assert np.allclose(P @ np.ones(P.shape[1]), 1.0)
+    B = (0.75 * H2 + 0.25 * ND.adr_csr(shape, hs, wl.omega, wl.medium.kappa_sq, wl.medium.gamma, grads, lap,
+                                         src, "upwind1", bc)).tocsr()
+    Hi = ND.hierarchy(B, shape, 5)
+    Ac = (P.T @ B @ P).toarray()
+    assert np.abs(Hi.ops[1].toarray() - Ac).max() <= 1e-12 * np.abs(Ac).max()
+    assert max(np.diff(A.indptr).max() for A in Hi.ops[1:]) <= 81
+    a, rep = ND.solve_upwind(shape, hs, wl.omega, src, wl.medium.kappa_sq, wl.medium.gamma, grads, lap, tau, bc)
+    assert rep.converged and rep.iterations < 60

@@ -26,23 +26,27 @@ def main():
     from paper_1712_06091_b200.operators import rhs_transform
 
     L = _lib.lib()
-    wl = workloads.cfg2(args.n)
+    wl = workloads.by_name(os.environ.get("HADR_WORKLOAD", "cfg2"), args.n)
     g = wl.grid
-    n1, n2 = g.shape
+    dim = len(g.shape)
+    n1, n2, n3 = g.shape[0], g.shape[1], (g.shape[2] if dim == 3 else 1)
+    hs = tuple(g.hs) + (1.0,)
+    src = tuple(wl.source.index) + (0,)
     qhat = rhs_transform(point_source(g, wl.source), wl.tt, wl.omega, "to_adr").reshape(-1)
-    codes = np.array([1, 1, 1, 1], dtype=np.int32)
-    f = [np.ascontiguousarray(x, dtype=np.float64) for x in
-         (wl.medium.kappa_sq, wl.medium.gamma, wl.tt.grad1, wl.tt.grad2, wl.tt.lap)]
-    a = np.empty(n1 * n2, complex)
+    codes = np.array([1] * 6, dtype=np.int32)
+    grads = list(wl.tt.grads) + [np.zeros(g.shape)] * (3 - dim)
+    f = [np.ascontiguousarray(x, dtype=np.float64) for x in [wl.medium.kappa_sq, wl.medium.gamma] + grads +
+         [wl.tt.lap]]
+    a = np.empty(n1 * n2 * n3, complex)
     rep = _lib.HadrReport()
     hist = np.zeros(2000)
     ts = C.c_double()
 
     def solve(its):
-        _lib.check(L.hadr_solve_adr_upwind(n1, n2, g.h1, g.h2, wl.omega, _lib.cbuf(codes), wl.source.i1,
-                                           wl.source.i2, *[_lib.cbuf(x) for x in f], _lib.cbuf(qhat), 0.25, 5, 5,
-                                           its, 1e-6, _lib.cbuf(a), C.byref(rep), _lib.cbuf(hist), 2000,
-                                           C.byref(ts), 0))
+        _lib.check(L.hadr_solve_adr_upwind(dim, n1, n2, n3, hs[0], hs[1], hs[2], wl.omega, _lib.cbuf(codes),
+                                           src[0], src[1], src[2], *[_lib.cbuf(x) for x in f], _lib.cbuf(qhat),
+                                           0.25, 5, 5, its, 1e-6, _lib.cbuf(a), C.byref(rep), _lib.cbuf(hist),
+                                           2000, C.byref(ts), 0))
         return rep.device_time
 
     for _ in range(args.warm):
