@@ -266,6 +266,85 @@ def run_ours(args, ws, rank, local, dist):
     }
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, args, sample_its=args.cpu_its, threads_one=True)
+    if args.extra_3d:
+        out["config_4_3d"] = run_3d(args, L, local, dist)
+    return out
+
+
+B_OP_3D_UPWIND_C128 = 6788.0  # 3D adr_upwind c128 (10 / 10 / 54 non-zeros)
+
+
+def run_3d(args, L, local, dist):
+    """BASELINE configs[3] (3D 513^2 x 257, c128) on one GPU: device-resident inputs,
+    CUDA events; the CPU sample is the dimension-generic oracle on a down-scaled grid."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1712_06091_b200 import _lib, drivers, workloads
+    from paper_1712_06091_b200.fields import point_source
+    from paper_1712_06091_b200.operators import _bc, rhs_transform
+
+    wl = workloads.cfg4(args.extra_3d)
+    g = wl.grid
+    n1, n2, n3 = g.shape
+    N = n1 * n2 * n3
+    cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=args.tol, max_iter=args.maxiter)
+    qhat = rhs_transform(point_source(g, wl.source), wl.tt, wl.omega, "to_adr").reshape(-1)
+    dev = torch.device("cuda", local)
+    fields = [torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
+              for x in [wl.medium.kappa_sq, wl.medium.gamma] + list(wl.tt.grads) + [wl.tt.lap]]
+    q_d = torch.from_numpy(qhat).to(dev)
+    a_d = torch.empty(N, dtype=torch.complex128, device=dev)
+    del qhat
+    torch.cuda.synchronize()
+    codes = _bc(wl.bc).codes()
+    rep = _lib.HadrReport()
+    hist = np.zeros(cfg.max_iter + 2)
+    tset = C.c_double()
+    hs, src = g.hs, wl.source.index
+
+    def step():
+        _lib.check(L.hadr_solve_adr_upwind(
+            3, n1, n2, n3, hs[0], hs[1], hs[2], float(wl.omega), _lib.cbuf(codes), src[0], src[1], src[2],
+            *[C.c_void_p(f.data_ptr()) for f in fields], C.c_void_p(q_d.data_ptr()), float(cfg.beta),
+            int(cfg.levels), int(cfg.restart), int(cfg.max_iter), float(cfg.tol), C.c_void_p(a_d.data_ptr()),
+            C.byref(rep), _lib.cbuf(hist), len(hist), C.byref(tset), 1))
+        return rep.iterations, tset.value, rep.device_time
+
+    step()
+    its, tk = [], []
+    L.hadr_stream_timer(1)
+    for _ in range(args.steps_3d):
+        i, _, t = step()
+        its.append(i)
+        tk.append(t)
+    t_dev = max_over_ranks(L.hadr_stream_timer(0) * 1e-3, dist)
+    hbm, srcp = peaks()
+    bw = B_OP_3D_UPWIND_C128 * N * (sum(its) / len(its)) / (sum(tk) / len(tk)) / 1e9
+    out = {"workload": f"{wl.name} (BASELINE configs[3], 3D {n1}x{n2}x{n3}, c128, 1 GPU)",
+           "value": N * sum(its) / t_dev / 1e6, "unit": "Mdof*iter/s", "outer_iterations": its,
+           "ms_per_step": t_dev / len(its) * 1e3, "t_krylov_ms": [t * 1e3 for t in tk],
+           "solve_roofline": {"bound": "hbm", "model_bytes_per_dof_iter": B_OP_3D_UPWIND_C128, "achieved": bw,
+                              "peak": hbm, "unit": "GB/s", "frac": bw / hbm, "peak_source": srcp}}
+    del fields, q_d, a_d
+    torch.cuda.empty_cache()
+    if not args.no_cpu_baseline:
+        from threadpoolctl import threadpool_limits
+
+        from oracle import hadr_oracle_nd as ND
+
+        ws = workloads.cfg4(65)
+        gg = ws.grid
+        bc = ND.bc_dict(3, ws.bc)
+        with threadpool_limits(1):
+            t0 = time.perf_counter()
+            _, r = ND.solve_upwind(gg.shape, gg.hs, ws.omega, ws.source.index, ws.medium.kappa_sq, ws.medium.gamma,
+                                   list(ws.tt.grads), ws.tt.lap, ws.tt.tau, bc, maxiter=3)
+            tc = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": gg.n_nodes * r.iterations / tc / 1e6, "unit": "Mdof*iter/s", "cores": 1,
+                               "kind": "port", "sample": f"nd oracle on cfg4_65 (65x65x33): assembly + hierarchy + "
+                                                         f"{r.iterations} outer iterations ({tc:.1f} s)"}
     return out
 
 
@@ -372,6 +451,8 @@ def main():
     ap.add_argument("--cpu-its", type=int, default=6, help="outer iterations in the cpu_baseline sample")
     ap.add_argument("--ref-its", type=int, default=4, help="outer iterations per reference-arm step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--extra-3d", type=int, default=513, help="also run BASELINE config 4 at this n (0: skip)")
+    ap.add_argument("--steps-3d", type=int, default=2)
     args = ap.parse_args()
     ws, rank, local, dist = dist_init()
     if args.impl == "reference":
