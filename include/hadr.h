@@ -124,7 +124,9 @@ int hadr_kcycle(hadr_hier h, int level, const double* b, const double* x, double
 int hadr_precond_apply(hadr_hier h, const double* r, double* z, int on_device);
 void hadr_hier_destroy(hadr_hier h);
 /* runtime options: "ce_max_n" = levels with at most this many points run their coarse part inside
- * the single-cluster engine (default 32768; 0 = every operation is its own kernel) */
+ * the single-cluster engine (default 32768; 0 = every operation is its own kernel);
+ * "kcycle_c64" = 1: hierarchies built afterwards apply their operators from complex64 storage
+ * (mixed precision: K-cycle operators c64, vectors / reductions / outer FGMRES c128) */
 int hadr_set_option(const char* name, double value);
 /* cluster-engine phase counters (enable with hadr_set_option("ce_profile", 1)): cycles seen by CTA 0
  * [total, allreduce, n_allreduce, scalar epilogue, n_epilogue, stencil, n_stencil, launches] */

@@ -414,6 +414,8 @@ int hadr_set_option(const char* name, double value) {
     std::string n(name ? name : "");
     if (n == "ce_profile") {
       g_ce_prof_on = value != 0.0;
+    } else if (n == "kcycle_c64") {
+      g_kcycle_c64 = value != 0.0;
     } else if (n == "ce_max_n") {
       g_ce_max_n = (long)value;
       // recycled hierarchies hold graphs captured under the old setting

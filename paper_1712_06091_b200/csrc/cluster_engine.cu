@@ -126,7 +126,7 @@ __device__ void ce_allreduce(CEC& c, double (&v)[NV]) {
 // are applied once per point (same values as applying them per neighbour).
 extern __shared__ cplx ce_tile[];
 
-template <int NO, int INM, int OUTM, int RED>
+template <int NO, int INM, int OUTM, int RED, bool C32>
 __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double s, const cplx* dinv, cplx* vout,
                               const cplx* b, cplx* y, const cplx* u, double (&red)[3]) {
   const int n1 = A.n1, n2 = A.n2, n3 = A.n3, nofs = A.nofs;
@@ -157,7 +157,11 @@ __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double
 #pragma unroll
       for (int q = 0; q < CH; ++q) {
         const int o = o0 + q;
-        cv[q] = ldk(A.coef, o < nofs ? (long)o * N + k : k);
+        const long ci = o < nofs ? (long)o * N + k : k;
+        if constexpr (C32)
+          cv[q] = ld_c64(A, ci);
+        else
+          cv[q] = ldk(A.coef, ci);
       }
 #pragma unroll
       for (int q = 0; q < CH; ++q) {
@@ -194,11 +198,19 @@ __device__ __noinline__ void ce_stencil(CEC& c, const StencilDev& A, const cplx*
                                         cplx* vout, const cplx* b, cplx* y, const cplx* u, double (&red)[3]) {
   CEProfScope prof_(c, 5);
   red[0] = red[1] = red[2] = 0.0;
+  if (A.coef32) {  // mixed precision: complex64-stored operator
+    switch (A.nofs) {
+      case 9: ce_stencil_no<9, INM, OUTM, RED, true>(c, A, x, s, dinv, vout, b, y, u, red); break;
+      case 21: ce_stencil_no<21, INM, OUTM, RED, true>(c, A, x, s, dinv, vout, b, y, u, red); break;
+      default: ce_stencil_no<0, INM, OUTM, RED, true>(c, A, x, s, dinv, vout, b, y, u, red); break;
+    }
+    return;
+  }
   switch (A.nofs) {
-    case 5: ce_stencil_no<5, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
-    case 9: ce_stencil_no<9, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
-    case 21: ce_stencil_no<21, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
-    default: ce_stencil_no<0, INM, OUTM, RED>(c, A, x, s, dinv, vout, b, y, u, red); break;
+    case 5: ce_stencil_no<5, INM, OUTM, RED, false>(c, A, x, s, dinv, vout, b, y, u, red); break;
+    case 9: ce_stencil_no<9, INM, OUTM, RED, false>(c, A, x, s, dinv, vout, b, y, u, red); break;
+    case 21: ce_stencil_no<21, INM, OUTM, RED, false>(c, A, x, s, dinv, vout, b, y, u, red); break;
+    default: ce_stencil_no<0, INM, OUTM, RED, false>(c, A, x, s, dinv, vout, b, y, u, red); break;
   }
 }
 

@@ -12,6 +12,7 @@
 namespace hadr {
 
 long g_ce_max_n = 32768;
+int g_kcycle_c64 = 0;
 
 // ---------------------------------------------------------------------------
 // caching allocator
@@ -90,7 +91,13 @@ Ctx& Ctx::get() {
 // ---------------------------------------------------------------------------
 Op::~Op() {
   dfree(coef);
+  dfree(coef32);
   dfree(dinv);
+}
+
+void Op::make_c64() {
+  if (!coef32) coef32 = dalloc<float2>((size_t)nofs * N);
+  launch_to_c64(Ctx::get().stream, (long)nofs * N, coef, coef32);
 }
 
 StencilDev Op::dev() const {
@@ -105,6 +112,7 @@ StencilDev Op::dev() const {
     s.d3[o] = d3[o];
   }
   s.coef = coef;
+  s.coef32 = coef32;
   return s;
 }
 
@@ -558,6 +566,8 @@ void Hier::alloc_workspace() {
   visits = dalloc<int>(nl + 1);
   HADR_CUDA(cudaMemset(kact, 0, (nl + 1) * sizeof(int)));
   HADR_CUDA(cudaMemset(visits, 0, (nl + 1) * sizeof(int)));
+  if (c64)  // mixed precision: the K-cycle applies complex64-stored operators
+    for (auto& L : lv) L.A->make_c64();
   if (nl <= CE_MAXLEV) {
     CEDesc h{};
     h.nlev = nl;
@@ -619,7 +629,10 @@ static bool hier_refresh(Hier* h, const Op& fine) {
     if (!mask_eq(galerkin_mask(F), layout_mask(C))) return false;
     galerkin_write(F, C);
   }
-  for (auto& L : h->lv) L.A->refresh_inv_diag();
+  for (auto& L : h->lv) {
+    L.A->refresh_inv_diag();
+    if (h->c64) L.A->make_c64();
+  }
   return true;
 }
 
@@ -630,7 +643,9 @@ Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol) 
   auto& pool = hier_pool();
   for (size_t i = 0; i < pool.size(); ++i) {
     Hier* h = pool[i];
-    if (h->lv.size() != shapes.size() || h->coarse_steps != coarse_steps || h->coarse_tol != coarse_tol) continue;
+    if (h->lv.size() != shapes.size() || h->coarse_steps != coarse_steps || h->coarse_tol != coarse_tol ||
+        h->c64 != (g_kcycle_c64 != 0))
+      continue;
     bool same = true;
     for (size_t l = 0; l < shapes.size(); ++l)
       same = same && h->lv[l].n1 == shapes[l].n1 && h->lv[l].n2 == shapes[l].n2 && h->lv[l].n3 == shapes[l].n3;
@@ -644,6 +659,7 @@ Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol) 
   h->coarse_steps = coarse_steps;
   h->coarse_tol = coarse_tol;
   h->poolable = true;
+  h->c64 = g_kcycle_c64 != 0;
   try {
     Level L0;
     L0.A = op_copy(*fine);  // own a copy: the graphs then never depend on the caller's buffers

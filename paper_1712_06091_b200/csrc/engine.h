@@ -56,8 +56,10 @@ struct Op {
   int nofs = 0;
   int8_t d1[HADR_MAX_OFS] = {0}, d2[HADR_MAX_OFS] = {0}, d3[HADR_MAX_OFS] = {0};
   cplx* coef = nullptr;
-  cplx* dinv = nullptr;  // lazily computed inverse diagonal
+  float2* coef32 = nullptr;  // complex64 copy used by the K-cycle in mixed precision (null: c128)
+  cplx* dinv = nullptr;      // lazily computed inverse diagonal
   ~Op();
+  void make_c64();           // (re)build coef32 from coef
   StencilDev dev() const;
   int center() const;
   const cplx* inv_diag();  // computes on first use; throws ValueError on a zero diagonal
@@ -103,6 +105,7 @@ struct Level {
 struct Hier {
   std::vector<Level> lv;
   bool poolable = false;     // owns copies of every level operator: may be recycled
+  bool c64 = false;          // K-cycle operators applied from complex64 storage (mixed precision)
   int coarse_steps = 10;
   double coarse_tol = 0.1;
   int* kact = nullptr;      // device: K-cycle-active flag per level
@@ -125,6 +128,7 @@ struct Hier {
 
 // runtime options (hadr_set_option)
 extern long g_ce_max_n;  // levels with N <= this run inside the cluster engine (0 disables)
+extern int g_kcycle_c64; // build hierarchies with complex64 operator storage (mixed-precision K-cycle)
 
 Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol);
 void hier_release(Hier* h);  // recycle (workspace + captured graphs) or delete

@@ -206,7 +206,7 @@ static void launch_finalize(const LaunchCfg& lc, const Geo& geo, Gate g, RedScra
 // NO > 0: all NO offsets unrolled with batched loads; NO == 0: runtime chunks of
 // 9 offsets (3D coarse unions of 27..81 offsets).
 // ---------------------------------------------------------------------------
-template <int CH, int INM>
+template <int CH, int INM, bool C32>
 __device__ __forceinline__ void stencil_chunk(const StencilArgs& a, int o0, int nofs, long k, int i1, int i2, int i3,
                                               int n1, int n2, int n3, long N, double s, cplx& acc) {
   // All loads are unconditional (out-of-grid neighbours read the centre, dead
@@ -222,7 +222,7 @@ __device__ __forceinline__ void stencil_chunk(const StencilArgs& a, int o0, int 
     const int j1 = i1 + a.A.d1[oo], j2 = i2 + a.A.d2[oo], j3 = i3 + a.A.d3[oo];
     ok[q] = live && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2 && j3 >= 0 && j3 < n3;
     const long jj = ok[q] ? ((long)j1 * n2 + j2) * n3 + j3 : k;
-    cv[q] = ldc(a.A.coef, live ? (long)o * N + k : k);
+    cv[q] = C32 ? ld_c64(a.A, live ? (long)o * N + k : k) : ldc(a.A.coef, live ? (long)o * N + k : k);
     xv[q] = ldc(a.x, jj);
     if (INM & IN_JAC) dv[q] = ldc(a.dinv, jj);
   }
@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(StencilArgs a) {
   const int n23 = n2 * n3;
   const long N = (long)n1 * n23;
   const double s = (INM & IN_SCALE) ? *a.scale : 1.0;
+  const bool c32 = a.A.coef32 != nullptr;
   constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & (RED_DOT | RED_DOT_CENTER)) ? 2 : 0);
   double red[NV > 0 ? NV : 1];
 #pragma unroll
@@ -255,9 +256,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(StencilArgs a) {
     const int i3 = rem - i2 * n3;
     cplx acc = mk(0.0, 0.0);
     if constexpr (NO > 0) {
-      stencil_chunk<NO, INM>(a, 0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
+      if (c32)
+        stencil_chunk<NO, INM, true>(a, 0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
+      else
+        stencil_chunk<NO, INM, false>(a, 0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
     } else {
-      for (int o0 = 0; o0 < nofs; o0 += 9) stencil_chunk<9, INM>(a, o0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
+      for (int o0 = 0; o0 < nofs; o0 += 9) {
+        if (c32)
+          stencil_chunk<9, INM, true>(a, o0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
+        else
+          stencil_chunk<9, INM, false>(a, o0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
+      }
     }
     cplx vc = mk(0.0, 0.0);
     if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) {
@@ -1029,6 +1038,24 @@ void launch_assemble(cudaStream_t s, int dim, int n1, int n2, int n3, double h1,
   int blocks = (int)((N + 127) / 128);
   if (blocks > 4096) blocks = 4096;
   k_assemble<<<blocks, 128, 0, s>>>(a);
+}
+
+}  // namespace hadr
+
+namespace hadr {
+
+// complex128 -> complex64 (round to nearest) for the mixed-precision K-cycle operators
+__global__ void k_to_c64(long n, const cplx* __restrict__ in, float2* __restrict__ out) {
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    const cplx v = in[k];
+    out[k] = make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
+  }
+}
+void launch_to_c64(cudaStream_t s, long n, const cplx* in, float2* out) {
+  ++g_launch_count;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 8192) blocks = 8192;
+  k_to_c64<<<blocks, 256, 0, s>>>(n, in, out);
 }
 
 }  // namespace hadr

@@ -18,7 +18,14 @@ struct StencilDev {
   int8_t d2[HADR_MAX_OFS];
   int8_t d3[HADR_MAX_OFS];
   const cplx* coef;
+  const float2* coef32;  // non-null: apply with complex64-stored coefficients (mixed-precision K-cycle)
 };
+
+// coefficient from complex64 storage, widened to complex128 for the arithmetic
+__device__ __forceinline__ cplx ld_c64(const StencilDev& A, long idx) {
+  const float2 c = __ldg(A.coef32 + idx);
+  return make_double2((double)c.x, (double)c.y);
+}
 
 // 125 offset slots of the 5x5x5 box, ascending == lexicographic (d1, d2, d3)
 __host__ __device__ __forceinline__ int slot125(int d1, int d2, int d3) { return ((d1 + 2) * 5 + (d2 + 2)) * 5 + (d3 + 2); }
@@ -131,6 +138,7 @@ void launch_assemble(cudaStream_t s, int dim, int n1, int n2, int n3, double h1,
                      int scheme, const int* bc, int src1, int src2, int src3, const double* ksq, const double* gam,
                      const double* g1, const double* g2, const double* g3, const double* lap, cplx* coefp,
                      unsigned* mask);
+void launch_to_c64(cudaStream_t s, long n, const cplx* in, float2* out);
 void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, int n3c, unsigned long long* mask,
                      const int* slot_of, cplx* coef_c);
 

@@ -266,3 +266,22 @@ def test_drivers_end_to_end(hadr, case, request):
     u, a, rep = drivers.solve_adr_central(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
     assert rep.converged and abs(rep.iterations - int(g["central_iterations"])) <= 1
     assert rel(u, g["central_u"]) <= 1e-6
+
+
+@pytest.mark.parametrize("case", ["g65", "gcfg1"])
+def test_solve_upwind_c64_mixed(hadr, case, request):
+    """'complex64' variant = mixed precision: K-cycle operators
+    stored in complex64, outer FGMRES in complex128.  Parity bar (north_star): <= 1e-4
+    relative L2 to the complex128 reference, iterations within +-1."""
+    from paper_1712_06091_b200 import drivers, workloads
+
+    g = request.getfixturevalue(case)
+    wl = {"g65": lambda: workloads.cfg2(65), "gcfg1": lambda: workloads.cfg1(129)}[case]()
+    cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=1e-6, max_iter=1000)
+    hadr._lib.set_option("kcycle_c64", 1)
+    try:
+        u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
+    finally:
+        hadr._lib.set_option("kcycle_c64", 0)
+    assert rep.converged and abs(rep.iterations - int(g["upwind_iterations"])) <= 1
+    assert rel(a, g["upwind_a"]) <= 1e-4
