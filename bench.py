@@ -282,16 +282,18 @@ def run_ours(args, ws, rank, local, dist):
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, args, sample_its=args.cpu_its, threads_one=True)
     if args.extra_3d:
-        out["config_4_3d"] = run_3d(args, L, local, dist)
+        out["config_4_3d"] = run_3d(args, L, local, dist, ws, rank)
     return out
 
 
 B_OP_3D_UPWIND_C128 = 6788.0  # 3D adr_upwind c128 (10 / 10 / 54 non-zeros)
 
 
-def run_3d(args, L, local, dist):
-    """BASELINE configs[3] (3D 513^2 x 257, c128) on one GPU: device-resident inputs,
-    CUDA events; the CPU sample is the dimension-generic oracle on a down-scaled grid."""
+def run_3d(args, L, local, dist, ws=1, rank=0):
+    """BASELINE configs[3] (3D 513^2 x 257, c128): device-resident inputs, CUDA events.
+    N > 1 (torchrun): ONE solve split in axis-0 slabs over the N GPUs (NCCL halo exchange /
+    all-gather / broadcast, coarse levels agglomerated) — strong scaling, max over ranks.
+    The CPU sample is the dimension-generic oracle on a down-scaled grid (rank 0)."""
     import ctypes as C
 
     import torch
@@ -318,6 +320,13 @@ def run_3d(args, L, local, dist):
     hist = np.zeros(cfg.max_iter + 2)
     tset = C.c_double()
     hs, src = g.hs, wl.source.index
+    slab = None
+    if ws > 1:
+        from paper_1712_06091_b200 import distributed as D
+
+        D.init("nccl")
+        bounds, nd, nl = D.plan(g.shape, cfg.levels)
+        slab = {"bounds": bounds, "slab_levels": nd, "levels": nl}
 
     def step():
         _lib.check(L.hadr_solve_adr_upwind(
@@ -335,16 +344,22 @@ def run_3d(args, L, local, dist):
         its.append(i)
         tk.append(t)
     t_dev = max_over_ranks(L.hadr_stream_timer(0) * 1e-3, dist)
+    if slab is not None:
+        D.finalize()
     hbm, srcp = peaks()
-    bw = B_OP_3D_UPWIND_C128 * N * (sum(its) / len(its)) / (sum(tk) / len(tk)) / 1e9
-    out = {"workload": f"{wl.name} (BASELINE configs[3], 3D {n1}x{n2}x{n3}, c128, 1 GPU)",
+    t_k = max_over_ranks(sum(tk) / len(tk), dist)
+    bw = B_OP_3D_UPWIND_C128 * N * (sum(its) / len(its)) / t_k / 1e9 / ws  # per-GPU bytes
+    out = {"workload": f"{wl.name} (BASELINE configs[3], 3D {n1}x{n2}x{n3}, c128, {ws} GPU)",
            "value": N * sum(its) / t_dev / 1e6, "unit": "Mdof*iter/s", "outer_iterations": its,
+           "n_gpus": ws, "scaling": "strong" if ws > 1 else None,
+           "parallelism": f"axis-0 slabs x{ws} (NCCL)" if ws > 1 else "single GPU", "slab_plan": slab,
            "ms_per_step": t_dev / len(its) * 1e3, "t_krylov_ms": [t * 1e3 for t in tk],
            "solve_roofline": {"bound": "hbm", "model_bytes_per_dof_iter": B_OP_3D_UPWIND_C128, "achieved": bw,
-                              "peak": hbm, "unit": "GB/s", "frac": bw / hbm, "peak_source": srcp}}
+                              "peak": hbm, "unit": "GB/s", "frac": bw / hbm, "peak_source": srcp,
+                              "note": "per GPU" if ws > 1 else ""}}
     del fields, q_d, a_d
     torch.cuda.empty_cache()
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and rank == 0:
         from threadpoolctl import threadpool_limits
 
         from oracle import hadr_oracle_nd as ND

@@ -123,7 +123,8 @@ int hadr_kcycle(hadr_hier h, int level, const double* b, const double* x, double
 /* make_kcycle_preconditioner(hier)(r) (helmadr/multigrid.py:174-184): graph-captured K-cycle */
 int hadr_precond_apply(hadr_hier h, const double* r, double* z, int on_device);
 void hadr_hier_destroy(hadr_hier h);
-/* runtime options: "ce_max_n" = levels with at most this many points run their coarse part inside
+/* runtime options: "dist_min_planes" / "dist_levels" = slab levels policy (multi-GPU);
+ * "ce_max_n" = levels with at most this many points run their coarse part inside
  * the single-cluster engine (default 32768; 0 = every operation is its own kernel);
  * "kcycle_c64" = 1: hierarchies built afterwards apply their operators from complex64 storage
  * (mixed precision: K-cycle operators c64, vectors / reductions / outer FGMRES c128) */
@@ -140,6 +141,28 @@ long long hadr_launch_count(void);
 /* CUDA-event timer on the library stream: start=1 records the start event (returns 0);
  * start=0 records the stop event, waits for it and returns the elapsed milliseconds (-1 on error) */
 double hadr_stream_timer(int start);
+
+/* ---- multi-GPU slab decomposition (the reference is single-process) ----
+ * One process per GPU.  After hadr_dist_init_*, hadr_solve_adr_upwind runs collectively: every rank
+ * passes the same global inputs, assembles and solves the axis-0 slab it owns (coarse levels below
+ * "dist_min_planes" planes per rank are agglomerated = replicated), and receives the global amplitude. */
+/* NCCL (one GPU per rank): rank 0 creates the id, the caller broadcasts its 128 bytes */
+int hadr_dist_nccl_id(char* unique_id /* 128 bytes */);
+int hadr_dist_init_nccl(int rank, int size, const char* unique_id);
+/* Host communicator: blocking callbacks on host buffers (e.g. torch.distributed gloo); ranks may
+ * share a GPU.  allgather: recv = size x nbytes in rank order; sendrecv: dst/src = -1 for none. */
+typedef int (*hadr_host_allgather)(const void* send, void* recv, long long nbytes);
+typedef int (*hadr_host_sendrecv)(const void* send, long long sbytes, int dst, void* recv, long long rbytes, int src);
+typedef int (*hadr_host_bcast)(void* buf, long long nbytes, int root);
+int hadr_dist_init_host(int rank, int size, hadr_host_allgather ag, hadr_host_sendrecv sr, hadr_host_bcast bc);
+int hadr_dist_finalize(void);
+/* kind: 0 none, 1 NCCL, 2 host callbacks */
+int hadr_dist_info(int* rank, int* size, int* kind);
+/* slab plan of a global grid under the active communicator: bounds[size + 1] fine-axis slab starts,
+ * *n_dist_levels leading slab levels out of *n_levels */
+int hadr_dist_plan(int n1, int n2, int n3, int max_levels, int* bounds, int* n_dist_levels, int* n_levels);
+/* pure host helper: split n1 planes into `size` slabs with interior bounds multiples of `align` */
+int hadr_slab_bounds(int n1, int size, int align, int* bounds /* size + 1 */);
 
 /* ---- Krylov (helmadr/krylov.py) ---- */
 /* _gmres_relax_pre / gmres_relax (helmadr/krylov.py:82-119) */

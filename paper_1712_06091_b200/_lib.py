@@ -26,7 +26,14 @@ EXPORTS = (
     "hadr_hier_level_op", "hadr_kcycle", "hadr_precond_apply", "hadr_hier_destroy", "hadr_gmres_relax",
     "hadr_fgmres", "hadr_launch_count", "hadr_assemble", "hadr_solve_adr_upwind", "hadr_pool_trim",
     "hadr_stream_timer", "hadr_set_option", "hadr_ce_profile", "hadr_op_bench",
+    "hadr_dist_nccl_id", "hadr_dist_init_nccl", "hadr_dist_init_host", "hadr_dist_finalize", "hadr_dist_info",
+    "hadr_dist_plan", "hadr_slab_bounds",
 )
+
+# host-communicator callbacks (include/hadr.h hadr_host_*)
+HOST_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_longlong)
+HOST_SENDRECV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_longlong, C.c_int, C.c_void_p, C.c_longlong, C.c_int)
+HOST_BCAST = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_longlong, C.c_int)
 
 
 class HadrReport(C.Structure):
@@ -81,6 +88,13 @@ _SIGS = {
     "hadr_launch_count": (C.c_longlong, []),
     "hadr_gmres_relax": (_i, [_vp, _vp, _vp, _i, _vp, _i]),
     "hadr_fgmres": (_i, [_vp, _vp, _vp, _vp, _i, _i, _d, _vp, C.POINTER(HadrReport), _vp, _i, _i]),
+    "hadr_dist_nccl_id": (_i, [_vp]),
+    "hadr_dist_init_nccl": (_i, [_i, _i, _vp]),
+    "hadr_dist_init_host": (_i, [_i, _i, HOST_ALLGATHER, HOST_SENDRECV, HOST_BCAST]),
+    "hadr_dist_finalize": (_i, []),
+    "hadr_dist_info": (_i, [C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
+    "hadr_dist_plan": (_i, [_i, _i, _i, _i, _vp, C.POINTER(_i), C.POINTER(_i)]),
+    "hadr_slab_bounds": (_i, [_i, _i, _i, _vp]),
 }
 
 _lib = None

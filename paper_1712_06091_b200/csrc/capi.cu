@@ -3,6 +3,7 @@
 #include <string>
 
 #include "../../include/hadr.h"
+#include "dist.h"
 #include "engine.h"
 
 using namespace hadr;
@@ -66,6 +67,79 @@ struct DevVec {
 };
 
 static hadr_op wrap(Op* op, bool own = true) { return new hadr_op_s{op, own}; }
+
+// Multi-GPU solve_adr_upwind: slab assembly, slab hierarchy with agglomerated coarse
+// levels, distributed FGMRES; every rank passes the global inputs and receives the
+// global amplitude (rows gathered from their owners).
+static void solve_adr_upwind_dist(int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega,
+                                  const int* bc, int src1, int src2, int src3, const double* ksq, const double* gam,
+                                  const double* g1, const double* g2, const double* g3, const double* lap,
+                                  const double* qhat, double beta, int levels, int restart, int maxiter, double tol,
+                                  double* a_out, Report& r, double* t_setup, int on_device) {
+  Ctx& c = Ctx::get();
+  Comm* cm = dist_comm();
+  const int rk = cm->rank, R = cm->size;
+  const SlabPlan plan = slab_plan(n1, n2, n3, levels);
+  const int p0 = plan.bounds[rk], nown = plan.bounds[rk + 1] - p0;
+  const long n23 = (long)n2 * n3, N = (long)n1 * n23, nloc = (long)nown * n23, hh = (long)kHalo * n23;
+  cudaEvent_t e0, e1;
+  HADR_CUDA(cudaEventCreate(&e0));
+  HADR_CUDA(cudaEventCreate(&e1));
+  HADR_CUDA(cudaEventRecord(e0, c.stream));
+  Op *H2 = nullptr, *H1 = nullptr, *B = nullptr;
+  Hier* hier = nullptr;
+  cplx *b = nullptr, *x = nullptr, *full = nullptr;
+  auto cleanup = [&]() {
+    delete H1;
+    delete B;
+    delete hier;
+    delete H2;
+    dfree(b);
+    dfree(x);
+    dfree(full);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  };
+  try {
+    H2 = op_assemble_slab(dim, n1, n2, n3, h1, h2, h3, omega, 2, bc, src1, src2, src3, ksq, gam, g1, g2, g3, lap,
+                          on_device, p0, nown);
+    H1 = op_assemble_slab(dim, n1, n2, n3, h1, h2, h3, omega, 1, bc, src1, src2, src3, ksq, gam, g1, g2, g3, lap,
+                          on_device, p0, nown);
+    B = op_axpby(mk(1.0 - beta, 0.0), *H2, mk(beta, 0.0), *H1);
+    delete H1;
+    H1 = nullptr;
+    hier = hier_build_dist(B, plan, 10, 0.1);
+    delete B;
+    B = nullptr;
+    HADR_CUDA(cudaEventRecord(e1, c.stream));
+    HADR_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    HADR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (t_setup) *t_setup = ms * 1e-3;
+    b = dalloc<cplx>(nloc + 2 * hh) + hh;
+    x = dalloc<cplx>(nloc + 2 * hh) + hh;
+    HADR_CUDA(cudaMemsetAsync(x - hh, 0, (nloc + 2 * hh) * sizeof(cplx), c.stream));
+    HADR_CUDA(cudaMemcpyAsync(b, (const cplx*)qhat + (long)p0 * n23, nloc * sizeof(cplx),
+                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+    fgmres(*H2, hier, b, nullptr, x, restart, maxiter, tol, r);
+    // gather the owned rows of every rank
+    full = on_device ? (cplx*)a_out : dalloc<cplx>(N);
+    HADR_CUDA(cudaMemcpyAsync(full + (long)p0 * n23, x, nloc * sizeof(cplx), cudaMemcpyDeviceToDevice, c.stream));
+    cm->group_start();
+    for (int q = 0; q < R; ++q)
+      cm->bcast(full + (long)plan.bounds[q] * n23, (size_t)(plan.bounds[q + 1] - plan.bounds[q]) * n23 * sizeof(cplx),
+                q, c.stream);
+    cm->group_end();
+    if (!on_device) HADR_CUDA(cudaMemcpyAsync(a_out, full, N * sizeof(cplx), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (on_device) full = nullptr;
+  } catch (...) {
+    if (on_device) full = nullptr;
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
 
 extern "C" {
 
@@ -196,6 +270,23 @@ int hadr_solve_adr_upwind(int dim, int n1, int n2, int n3, double h1, double h2,
     Ctx& c = Ctx::get();
     if (dim == 2) n3 = 1;
     const long N = (long)n1 * n2 * n3;
+    if (dist_comm()) {
+      Report r;
+      solve_adr_upwind_dist(dim, n1, n2, n3, h1, h2, h3, omega, bc, src1, src2, src3, kappa_sq, gamma, grad1, grad2,
+                            grad3, lap_tau, qhat, beta, levels, restart, maxiter, tol, a_out, r, t_setup, on_device);
+      rep->iterations = r.iterations;
+      rep->converged = r.converged;
+      rep->note = r.note;
+      rep->bnorm = r.bnorm;
+      rep->final_relres = r.final_relres;
+      rep->wall_time = r.wall_time;
+      rep->device_time = r.device_time;
+      const int nh = (int)r.history.size();
+      rep->history_len = nh;
+      if (history)
+        for (int i = 0; i < nh && i < history_cap; ++i) history[i] = r.history[i];
+      return;
+    }
     cudaEvent_t e0, e1;
     HADR_CUDA(cudaEventCreate(&e0));
     HADR_CUDA(cudaEventCreate(&e1));
@@ -416,6 +507,10 @@ int hadr_set_option(const char* name, double value) {
       g_ce_prof_on = value != 0.0;
     } else if (n == "kcycle_c64") {
       g_kcycle_c64 = value != 0.0;
+    } else if (n == "dist_min_planes") {
+      g_dist_min_planes = (int)value;
+    } else if (n == "dist_levels") {
+      g_dist_levels = (int)value;
     } else if (n == "ce_max_n") {
       g_ce_max_n = (long)value;
       // recycled hierarchies hold graphs captured under the old setting
@@ -427,6 +522,47 @@ int hadr_set_option(const char* name, double value) {
     } else {
       throw ValueError("unknown option " + n);
     }
+  });
+}
+
+int hadr_dist_nccl_id(char* out) {
+  return guarded([&] { dist_nccl_unique_id(out); });
+}
+
+int hadr_dist_init_nccl(int rank, int size, const char* unique_id) {
+  return guarded([&] { dist_init_nccl(rank, size, unique_id); });
+}
+
+int hadr_dist_init_host(int rank, int size, hadr_host_allgather ag, hadr_host_sendrecv sr, hadr_host_bcast bc) {
+  return guarded([&] { dist_init_host(rank, size, ag, sr, bc); });
+}
+
+int hadr_dist_finalize(void) {
+  return guarded([&] { dist_finalize(); });
+}
+
+int hadr_dist_info(int* rank, int* size, int* kind) {
+  Comm* cm = dist_comm();
+  if (rank) *rank = cm ? cm->rank : 0;
+  if (size) *size = cm ? cm->size : 1;
+  if (kind) *kind = cm ? cm->kind : 0;
+  return 0;
+}
+
+int hadr_dist_plan(int n1, int n2, int n3, int max_levels, int* bounds, int* n_dist_levels, int* n_levels) {
+  return guarded([&] {
+    const SlabPlan p = slab_plan(n1, n2, n3, max_levels);
+    for (size_t i = 0; i < p.bounds.size(); ++i) bounds[i] = p.bounds[i];
+    *n_dist_levels = p.ndist;
+    *n_levels = p.nlev;
+  });
+}
+
+int hadr_slab_bounds(int n1, int size, int align, int* bounds) {
+  return guarded([&] {
+    const std::vector<int> b = slab_bounds(n1, size, align);
+    if (b.empty()) throw ValueError("cannot split the axis into slabs");
+    for (size_t i = 0; i < b.size(); ++i) bounds[i] = b[i];
   });
 }
 

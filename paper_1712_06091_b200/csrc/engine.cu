@@ -3,6 +3,7 @@
 // every data-dependent branch of the preconditioner, the host only drives the
 // outer FGMRES (one small read-back per outer iteration).
 #include "engine.h"
+#include "dist.h"
 
 #include <algorithm>
 #include <chrono>
@@ -49,8 +50,13 @@ void* pool_alloc(size_t bytes) {
 void pool_free(void* p) {
   auto& lb = live_blocks();
   auto it = lb.find(p);
-  if (it == lb.end()) return;
-  free_blocks().emplace(it->second, p);
+  if (it == lb.end()) {  // interior pointer (slab vectors point past their lower halo)
+    it = lb.upper_bound(p);
+    if (it == lb.begin()) return;
+    --it;
+    if ((char*)p >= (char*)it->first + it->second) return;
+  }
+  free_blocks().emplace(it->second, it->first);
   lb.erase(it);
 }
 
@@ -96,8 +102,8 @@ Op::~Op() {
 }
 
 void Op::make_c64() {
-  if (!coef32) coef32 = dalloc<float2>((size_t)nofs * N);
-  launch_to_c64(Ctx::get().stream, (long)nofs * N, coef, coef32);
+  if (!coef32) coef32 = dalloc<float2>((size_t)alloc_len()) + base_off();
+  launch_to_c64(Ctx::get().stream, alloc_len(), coef - base_off(), coef32 - base_off());
 }
 
 StencilDev Op::dev() const {
@@ -106,6 +112,9 @@ StencilDev Op::dev() const {
   s.n2 = n2;
   s.n3 = n3;
   s.nofs = nofs;
+  s.p0 = p0;
+  s.n1own = own();
+  s.pstride = stride();
   for (int o = 0; o < nofs; ++o) {
     s.d1[o] = d1[o];
     s.d2[o] = d2[o];
@@ -122,23 +131,35 @@ int Op::center() const {
   return -1;
 }
 
-const cplx* Op::inv_diag() {
-  if (dinv) return dinv;
+// dinv over the owned points; slab operators keep kHalo halo planes (filled by exchange)
+static void compute_inv_diag(const Op& A, cplx* dinv) {
   Ctx& c = Ctx::get();
-  const int ce = center();
-  dinv = dalloc<cplx>(N);
-  int* flag = dalloc<int>(1);
+  const int ce = A.center();
+  int* flag = (int*)c.dscal + 32;
   HADR_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), c.stream));
-  launch_inv_diag(c.stream, N, ce >= 0 ? coef + (long)ce * N : nullptr, dinv, flag);
-  int hflag = 0;
+  launch_inv_diag(c.stream, A.nloc(), ce >= 0 ? A.coef + (long)ce * A.stride() : nullptr, dinv, flag);
+  unsigned long long hflag = 0;
   HADR_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   c.sync();
-  dfree(flag);
-  if (hflag || ce < 0) {
-    dfree(dinv);
-    dinv = nullptr;
-    throw ValueError("hierarchy operator has zero diagonal entries");
+  if (A.slab()) {
+    Comm* cm = dist_comm();
+    cm->halo(dinv, A.n23() * sizeof(cplx), A.own(), kHalo, c.stream);
+    cm->allreduce_or_u64(&hflag, 1, c.stream);
   }
+  if (hflag || ce < 0) throw ValueError("hierarchy operator has zero diagonal entries");
+}
+
+const cplx* Op::inv_diag() {
+  if (dinv) return dinv;
+  const long h = slab() ? (long)kHalo * n23() : 0;
+  cplx* d = dalloc<cplx>(nloc() + 2 * h) + h;
+  try {
+    compute_inv_diag(*this, d);
+  } catch (...) {
+    dfree(d);
+    throw;
+  }
+  dinv = d;
   return dinv;
 }
 
@@ -147,15 +168,7 @@ void Op::refresh_inv_diag() {
     inv_diag();
     return;
   }
-  Ctx& c = Ctx::get();
-  const int ce = center();
-  int* flag = (int*)c.dscal + 32;
-  HADR_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), c.stream));
-  launch_inv_diag(c.stream, N, ce >= 0 ? coef + (long)ce * N : nullptr, dinv, flag);
-  int hflag = 0;
-  HADR_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  c.sync();
-  if (hflag || ce < 0) throw ValueError("hierarchy operator has zero diagonal entries");
+  compute_inv_diag(*this, dinv);
 }
 
 static void copy_geometry(Op* op, const Op& A) {
@@ -163,6 +176,13 @@ static void copy_geometry(Op* op, const Op& A) {
   op->n2 = A.n2;
   op->n3 = A.n3;
   op->N = A.N;
+  op->p0 = A.p0;
+  op->nown = A.nown;
+  op->hal = A.hal;
+  op->pstride = A.pstride;
+}
+static void alloc_coef(Op* op) {  // after geometry + nofs
+  op->coef = dalloc<cplx>((size_t)op->alloc_len()) + op->base_off();
 }
 
 Op* op_copy(const Op& A) {
@@ -175,9 +195,9 @@ Op* op_copy(const Op& A) {
     op->d2[o] = A.d2[o];
     op->d3[o] = A.d3[o];
   }
-  op->coef = dalloc<cplx>((size_t)A.nofs * A.N);
-  HADR_CUDA(cudaMemcpyAsync(op->coef, A.coef, (size_t)A.nofs * A.N * sizeof(cplx), cudaMemcpyDeviceToDevice,
-                            c.stream));
+  alloc_coef(op);
+  HADR_CUDA(cudaMemcpyAsync(op->coef - op->base_off(), A.coef - A.base_off(), (size_t)A.alloc_len() * sizeof(cplx),
+                            cudaMemcpyDeviceToDevice, c.stream));
   return op;
 }
 
@@ -281,6 +301,8 @@ Op* op_from_planes(int n1, int n2, int n3, int nofs, const int* offsets, const c
 // alpha*A + beta*B on the union pattern: (alpha*A).data, (beta*B).data, CSR + CSR (helmadr/drivers.py:156)
 Op* op_axpby(cplx alpha, const Op& A, cplx beta, const Op& B) {
   if (A.n1 != B.n1 || A.n2 != B.n2 || A.n3 != B.n3) throw ValueError("dimension mismatch");
+  if (A.p0 != B.p0 || A.nown != B.nown || A.hal != B.hal || A.stride() != B.stride())
+    throw ValueError("slab layout mismatch");
   Ctx& c = Ctx::get();
   Mask125 m = layout_mask(A);
   const Mask125 mb = layout_mask(B);
@@ -296,10 +318,11 @@ Op* op_axpby(cplx alpha, const Op& A, cplx beta, const Op& B) {
   int* dm = dalloc<int>(2 * HADR_MAX_OFS);
   HADR_CUDA(cudaMemcpyAsync(dm, ma, sizeof(ma), cudaMemcpyHostToDevice, c.stream));
   HADR_CUDA(cudaMemcpyAsync(dm + HADR_MAX_OFS, mbs, sizeof(mbs), cudaMemcpyHostToDevice, c.stream));
-  op->coef = dalloc<cplx>((size_t)op->nofs * op->N);
-  HADR_CUDA(cudaMemsetAsync(op->coef, 0, (size_t)op->nofs * op->N * sizeof(cplx), c.stream));
-  launch_remap_planes(c.stream, A.N, A.coef, A.nofs, dm, op->coef, alpha, 1);
-  launch_remap_planes(c.stream, B.N, B.coef, B.nofs, dm + HADR_MAX_OFS, op->coef, beta, 1);
+  alloc_coef(op);
+  cplx* ob = op->coef - op->base_off();
+  HADR_CUDA(cudaMemsetAsync(ob, 0, (size_t)op->alloc_len() * sizeof(cplx), c.stream));
+  launch_remap_planes(c.stream, A.stride(), A.coef - A.base_off(), A.nofs, dm, ob, alpha, 1);
+  launch_remap_planes(c.stream, B.stride(), B.coef - B.base_off(), B.nofs, dm + HADR_MAX_OFS, ob, beta, 1);
   HADR_CUDA(cudaGetLastError());
   c.sync();
   dfree(dm);
@@ -307,6 +330,7 @@ Op* op_axpby(cplx alpha, const Op& A, cplx beta, const Op& B) {
 }
 
 static Op* op_clone_with_center(const Op& A) {
+  if (A.slab()) throw ValueError("operation not available on slab operators");
   Ctx& c = Ctx::get();
   Mask125 m = layout_mask(A);
   mask_set(m, slot125(0, 0, 0));
@@ -339,6 +363,7 @@ Op* op_add_diag_real(const Op& A, cplx sc, const double* field_host) {
 }
 
 Op* op_similarity(const Op& A, const cplx* left_host, const cplx* right_host) {
+  if (A.slab()) throw ValueError("operation not available on slab operators");
   Ctx& c = Ctx::get();
   Op* op = new Op();
   copy_geometry(op, A);
@@ -404,38 +429,56 @@ Op* op_galerkin(const Op& A) {
   return op;
 }
 
-Op* op_assemble(int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega, int scheme,
-                const int* bc, int src1, int src2, int src3, const double* ksq, const double* gam, const double* g1,
-                const double* g2, const double* g3, const double* lap, bool fields_on_device) {
+// Assembly of the rows of global axis-0 planes [r0, r0 + nr) into an operator whose
+// geometry (slab or whole grid) is given; fields are global arrays (host or device).
+static Op* assemble_rows(int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega, int scheme,
+                         const int* bc, int src1, int src2, int src3, const double* ksq, const double* gam,
+                         const double* g1, const double* g2, const double* g3, const double* lap,
+                         bool fields_on_device, int p0, int nown, int hal) {
   if (dim != 2 && dim != 3) throw ValueError("dim must be 2 or 3");
   if (n1 < 5 || n2 < 5 || (dim == 3 && n3 < 5)) throw ValueError("grid needs at least 5 nodes per dimension");
   if (scheme < 0 || scheme > 3) throw ValueError("scheme must be central/upwind1/upwind2/helmholtz");
   if (dim == 2) n3 = 1;
   Ctx& c = Ctx::get();
   const long N = (long)n1 * n2 * n3;
+  const long n23 = (long)n2 * n3;
+  const bool slab = nown > 0;
+  const int own = slab ? nown : n1;
+  const int r0 = std::max(p0 - hal, 0), r1 = std::min(p0 + own + hal, n1);
+  const int nr = r1 - r0;
+  const long NR = (long)nr * n23;
   const double* src[6] = {ksq, gam, g1, g2, g3, lap};
   const bool need[6] = {true, true, scheme != 3, scheme != 3, scheme != 3 && dim == 3, scheme != 3};
   const double* fld[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   double* df = nullptr;
   if (fields_on_device) {
-    for (int i = 0; i < 6; ++i) fld[i] = need[i] ? src[i] : nullptr;
+    for (int i = 0; i < 6; ++i) fld[i] = need[i] ? src[i] + (long)r0 * n23 : nullptr;
   } else {
-    df = dalloc<double>(6 * N);
+    df = dalloc<double>(6 * NR);
     for (int i = 0; i < 6; ++i)
       if (need[i]) {
-        HADR_CUDA(cudaMemcpyAsync(df + i * N, src[i], N * sizeof(double), cudaMemcpyHostToDevice, c.stream));
-        fld[i] = df + i * N;
+        HADR_CUDA(cudaMemcpyAsync(df + i * NR, src[i] + (long)r0 * n23, NR * sizeof(double), cudaMemcpyHostToDevice,
+                                  c.stream));
+        fld[i] = df + i * NR;
       }
   }
   const int NP = dim == 2 ? 9 : 13;
-  cplx* cp = dalloc<cplx>(NP * N);
+  const long pst = slab ? (long)(own + 2 * hal) * n23 : N;  // plane stride
+  const long boff = slab ? (long)hal * n23 : 0;
+  cplx* cp = dalloc<cplx>(NP * pst);
+  HADR_CUDA(cudaMemsetAsync(cp, 0, NP * pst * sizeof(cplx), c.stream));
   unsigned* dmask = dalloc<unsigned>(1);
   HADR_CUDA(cudaMemsetAsync(dmask, 0, sizeof(unsigned), c.stream));
   launch_assemble(c.stream, dim, n1, n2, n3, h1, h2, h3, omega, scheme, bc, src1, src2, src3, fld[0], fld[1], fld[2],
-                  fld[3], fld[4], fld[5], cp, dmask);
+                  fld[3], fld[4], fld[5], cp + boff + (long)(r0 - p0) * n23, dmask, r0, nr, pst);
   unsigned hm = 0;
   HADR_CUDA(cudaMemcpyAsync(&hm, dmask, sizeof(unsigned), cudaMemcpyDeviceToHost, c.stream));
   c.sync();
+  if (slab) {  // every rank must agree on the offset planes
+    unsigned long long w = hm;
+    dist_comm()->allreduce_or_u64(&w, 1, c.stream);
+    hm = (unsigned)w;
+  }
   static const int d9[9][3] = {{-2, 0, 0}, {-1, 0, 0}, {0, -2, 0}, {0, -1, 0}, {0, 0, 0},
                                {0, 1, 0},  {0, 2, 0},  {1, 0, 0},  {2, 0, 0}};
   static const int d13[13][3] = {{-2, 0, 0}, {-1, 0, 0}, {0, -2, 0}, {0, -1, 0}, {0, 0, -2}, {0, 0, -1}, {0, 0, 0},
@@ -446,6 +489,12 @@ Op* op_assemble(int dim, int n1, int n2, int n3, double h1, double h2, double h3
   op->n2 = n2;
   op->n3 = n3;
   op->N = N;
+  if (slab) {
+    op->p0 = p0;
+    op->nown = nown;
+    op->hal = hal;
+    op->pstride = pst;
+  }
   int used[13], nu = 0;
   for (int q = 0; q < NP; ++q)
     if (hm & (1u << q)) {
@@ -456,15 +505,98 @@ Op* op_assemble(int dim, int n1, int n2, int n3, double h1, double h2, double h3
       used[nu++] = q;
     }
   op->nofs = nu;
-  op->coef = dalloc<cplx>((size_t)nu * N);
+  alloc_coef(op);
   for (int o = 0; o < nu; ++o)
-    HADR_CUDA(cudaMemcpyAsync(op->coef + (long)o * N, cp + (long)used[o] * N, N * sizeof(cplx),
+    HADR_CUDA(cudaMemcpyAsync(op->coef - boff + (long)o * pst, cp + (long)used[o] * pst, pst * sizeof(cplx),
                               cudaMemcpyDeviceToDevice, c.stream));
   HADR_CUDA(cudaGetLastError());
   c.sync();
   dfree(df);
   dfree(cp);
   dfree(dmask);
+  return op;
+}
+
+Op* op_assemble(int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega, int scheme,
+                const int* bc, int src1, int src2, int src3, const double* ksq, const double* gam, const double* g1,
+                const double* g2, const double* g3, const double* lap, bool fields_on_device) {
+  return assemble_rows(dim, n1, n2, n3, h1, h2, h3, omega, scheme, bc, src1, src2, src3, ksq, gam, g1, g2, g3, lap,
+                       fields_on_device, 0, 0, 0);
+}
+
+Op* op_assemble_slab(int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega, int scheme,
+                     const int* bc, int src1, int src2, int src3, const double* ksq, const double* gam,
+                     const double* g1, const double* g2, const double* g3, const double* lap, bool fields_on_device,
+                     int p0, int nown) {
+  if (!dist_comm()) throw ValueError("no distributed context");
+  return assemble_rows(dim, n1, n2, n3, h1, h2, h3, omega, scheme, bc, src1, src2, src3, ksq, gam, g1, g2, g3, lap,
+                       fields_on_device, p0, nown, 1);
+}
+
+// Slab Galerkin (multi-GPU): this rank forms coarse rows [cb[r], cb[r+1]) from its fine slab,
+// whose lower halo row is exchanged first.  gather = 1: the rows of every rank are
+// broadcast so each rank holds the full (replicated) coarse operator; gather = 0: a slab
+// operator with one halo row each side.
+static Op* op_galerkin_slab(Op& A, const std::vector<int>& cb, bool gather) {
+  Comm* cm = dist_comm();
+  Ctx& c = Ctx::get();
+  if (!A.slab() || A.hal < 1) throw ValueError("galerkin_slab: fine operator is not a slab operator");
+  const int r = cm->rank, R = cm->size;
+  const int q0 = cb[r], nq = cb[r + 1] - cb[r];
+  for (int o = 0; o < A.nofs; ++o)
+    cm->halo(A.coef + (long)o * A.stride(), A.n23() * sizeof(cplx), A.own(), 1, c.stream);
+  const int n1c = coarse_dim(A.n1), n2c = coarse_dim(A.n2), n3c = coarse_dim(A.n3);
+  const long n23c = (long)n2c * n3c, Nc = (long)n1c * n23c;
+  unsigned long long* dmask = (unsigned long long*)(c.dscal + 40);
+  HADR_CUDA(cudaMemsetAsync(dmask, 0, 2 * sizeof(unsigned long long), c.stream));
+  launch_galerkin(c.stream, A.dev(), n1c, n2c, n3c, dmask, nullptr, nullptr, q0, nq, 0);
+  Mask125 m{{0ull, 0ull}};
+  HADR_CUDA(cudaMemcpyAsync(m.w, dmask, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  cm->allreduce_or_u64(m.w, 2, c.stream);
+  mask_set(m, slot125(0, 0, 0));
+  Op* op = new Op();
+  op->n1 = n1c;
+  op->n2 = n2c;
+  op->n3 = n3c;
+  op->N = Nc;
+  int slot[125];
+  set_offsets_from_mask(op, m, slot);
+  if (!gather) {
+    op->p0 = q0;
+    op->nown = nq;
+    op->hal = 1;
+    op->pstride = (long)(nq + 2) * n23c;
+  }
+  alloc_coef(op);
+  HADR_CUDA(cudaMemsetAsync(op->coef - op->base_off(), 0, op->alloc_len() * sizeof(cplx), c.stream));
+  int* dslot = dalloc<int>(125);
+  HADR_CUDA(cudaMemcpyAsync(dslot, slot, sizeof(slot), cudaMemcpyHostToDevice, c.stream));
+  if (!gather) {
+    launch_galerkin(c.stream, A.dev(), n1c, n2c, n3c, nullptr, dslot, op->coef, q0, nq, op->stride());
+  } else {
+    // rank-major staging (each rank's rows of all planes contiguous) -> R broadcasts -> plane layout
+    cplx* tmp = dalloc<cplx>((size_t)op->nofs * Nc);
+    launch_galerkin(c.stream, A.dev(), n1c, n2c, n3c, nullptr, dslot, tmp + (long)op->nofs * q0 * n23c, q0, nq,
+                    (long)nq * n23c);
+    cm->group_start();
+    for (int rr = 0; rr < R; ++rr)
+      cm->bcast(tmp + (long)op->nofs * cb[rr] * n23c, (size_t)op->nofs * (cb[rr + 1] - cb[rr]) * n23c * sizeof(cplx),
+                rr, c.stream);
+    cm->group_end();
+    for (int rr = 0; rr < R; ++rr) {
+      const size_t w = (size_t)(cb[rr + 1] - cb[rr]) * n23c * sizeof(cplx);
+      if (!w) continue;
+      HADR_CUDA(cudaMemcpy2DAsync(op->coef + (long)cb[rr] * n23c, Nc * sizeof(cplx),
+                                  tmp + (long)op->nofs * cb[rr] * n23c, w, w, op->nofs, cudaMemcpyDeviceToDevice,
+                                  c.stream));
+    }
+    c.sync();
+    dfree(tmp);
+  }
+  HADR_CUDA(cudaGetLastError());
+  c.sync();
+  dfree(dslot);
   return op;
 }
 
@@ -527,8 +659,22 @@ size_t Hier::ce_tile(int li) const {
 }
 
 bool Hier::use_ce(int li) const {
-  return ce_desc != nullptr && g_ce_max_n > 0 && li < (int)lv.size() && lv[li].N <= g_ce_max_n &&
+  return ce_desc != nullptr && g_ce_max_n > 0 && li < (int)lv.size() && !lv[li].dist && lv[li].N <= g_ce_max_n &&
          (int)lv.size() <= CE_MAXLEV && ce_tile(li) <= 200 * 1024;
+}
+
+const LaunchCfg& Hier::lcf(const Level& L) const { return L.dist ? dlc : Ctx::get().lc; }
+
+void Hier::xchg(const Level& L, const cplx* v) const {
+  if (L.dist) dist_comm()->halo((void*)v, (size_t)L.n2 * L.n3 * sizeof(cplx), L.nown, kHalo, Ctx::get().stream);
+}
+
+cplx* Hier::valloc(const Level& L) const {
+  if (!L.dist) return dalloc<cplx>(L.N);
+  const long h = (long)kHalo * L.n2 * L.n3;
+  cplx* p = dalloc<cplx>(L.N + 2 * h);
+  HADR_CUDA(cudaMemset(p, 0, (L.N + 2 * h) * sizeof(cplx)));
+  return p + h;
 }
 
 void Hier::alloc_workspace() {
@@ -538,26 +684,29 @@ void Hier::alloc_workspace() {
     L.n1 = L.A->n1;
     L.n2 = L.A->n2;
     L.n3 = L.A->n3;
-    L.N = L.A->N;
+    L.N = L.A->nloc();
+    L.dist = L.A->slab();
+    L.p0 = L.A->p0;
+    L.nown = L.A->own();
     L.dinv = L.A->inv_diag();
     L.s = (i == nl - 1) ? coarse_steps : (i + 2);  // relax_steps(l) = l + 1 (helmadr/multigrid.py:87-88)
     if (L.s > RMAX) throw ValueError("relaxation length exceeds the device limit (16)");
-    L.s = (int)std::min<long>(L.s, L.N);
-    for (int j = 0; j <= L.s; ++j) L.V[j] = dalloc<cplx>(L.N);
-    L.w[0] = dalloc<cplx>(L.N);
-    L.w[1] = dalloc<cplx>(L.N);
-    L.r = dalloc<cplx>(L.N);
+    L.s = (int)std::min<long>(L.s, L.A->N);
+    for (int j = 0; j <= L.s; ++j) L.V[j] = valloc(L);
+    L.w[0] = valloc(L);
+    L.w[1] = valloc(L);
+    L.r = valloc(L);
     L.rctl = dalloc<RelaxCtl>(1);
     HADR_CUDA(cudaMemset(L.rctl, 0, sizeof(RelaxCtl)));
     if (i >= 1) {
-      L.fb = dalloc<cplx>(L.N);
-      L.fx = dalloc<cplx>(L.N);
-      L.fV0 = dalloc<cplx>(L.N);
-      L.fu = dalloc<cplx>(L.N);
-      L.fZ0 = dalloc<cplx>(L.N);
-      L.fZ1 = dalloc<cplx>(L.N);
-      L.fw = dalloc<cplx>(L.N);
-      L.fr = dalloc<cplx>(L.N);
+      L.fb = valloc(L);
+      L.fx = valloc(L);
+      L.fV0 = valloc(L);
+      L.fu = valloc(L);
+      L.fZ0 = valloc(L);
+      L.fZ1 = valloc(L);
+      L.fw = valloc(L);
+      L.fr = valloc(L);
       L.fctl = dalloc<FgCtl>(1);
       HADR_CUDA(cudaMemset(L.fctl, 0, sizeof(FgCtl)));
     }
@@ -701,6 +850,81 @@ Hier* hier_from_ops(int nlev, Op** ops, int coarse_steps, double coarse_tol) {
   return h;
 }
 
+// ---------------------------------------------------------------------------
+// multi-GPU slab hierarchy: levels 0 .. ndist-1 are split in
+// axis-0 slabs, the coarse rest is agglomerated (replicated on every rank)
+// ---------------------------------------------------------------------------
+static std::vector<int> level_bounds(const std::vector<int>& fine, int l, int n1l) {
+  std::vector<int> b(fine.size());
+  for (size_t r = 0; r + 1 < fine.size(); ++r) b[r] = fine[r] >> l;
+  b.back() = n1l;
+  return b;
+}
+
+SlabPlan slab_plan(int n1, int n2, int n3, int max_levels) {
+  Comm* cm = dist_comm();
+  if (!cm) throw ValueError("no distributed context (hadr_dist_init_*)");
+  auto shapes = coarsenable_levels(n1, n2, n3, max_levels);
+  const int nl = (int)shapes.size();
+  if (nl < 2)
+    throw ValueError("grid cannot support two multigrid levels ((n_d - 1) must be even with at least 3 coarse nodes)");
+  const int R = cm->size;
+  for (int nd = nl - 1; nd >= 1; --nd) {
+    if (g_dist_levels > 0 && nd != std::min(g_dist_levels, nl - 1)) continue;
+    std::vector<int> b = slab_bounds(n1, R, 1 << nd);
+    if (b.empty()) continue;
+    bool ok = true;
+    for (int l = 0; l < nd && ok; ++l) {
+      const std::vector<int> bl = level_bounds(b, l, shapes[l].n1);
+      const int need = l == 0 ? kHalo : std::max(kHalo, g_dist_levels > 0 ? kHalo : g_dist_min_planes);
+      for (int r = 0; r < R; ++r) ok = ok && bl[r + 1] - bl[r] >= need;
+    }
+    if (ok) return SlabPlan{b, nd, nl};
+  }
+  throw ValueError("grid too small for the requested number of slab ranks");
+}
+
+Hier* hier_build_dist(Op* fine, const SlabPlan& plan, int coarse_steps, double coarse_tol) {
+  Comm* cm = dist_comm();
+  if (!cm) throw ValueError("no distributed context (hadr_dist_init_*)");
+  const int rk = cm->rank;
+  if (!fine->slab() || fine->p0 != plan.bounds[rk] || fine->own() != plan.bounds[rk + 1] - plan.bounds[rk])
+    throw ValueError("fine operator does not match the slab plan");
+  auto shapes = coarsenable_levels(fine->n1, fine->n2, fine->n3, plan.nlev);
+  Hier* h = new Hier();
+  h->coarse_steps = coarse_steps;
+  h->coarse_tol = coarse_tol;
+  h->c64 = g_kcycle_c64 != 0;
+  h->ndist = plan.ndist;
+  h->dlc = Ctx::get().lc;
+  h->dlc.dist = &cm->red;
+  try {
+    Level L0;
+    L0.A = op_copy(*fine);
+    L0.own = true;
+    L0.bounds = level_bounds(plan.bounds, 0, shapes[0].n1);
+    h->lv.push_back(L0);
+    for (int l = 1; l < plan.nlev; ++l) {
+      Op& F = *h->lv.back().A;
+      Level L;
+      if (l <= plan.ndist) {
+        const std::vector<int> cb = level_bounds(plan.bounds, l, shapes[l].n1);
+        L.A = op_galerkin_slab(F, cb, l == plan.ndist);
+        if (l < plan.ndist) L.bounds = cb;
+      } else {
+        L.A = op_galerkin(F);
+      }
+      L.own = true;
+      h->lv.push_back(L);
+    }
+    h->alloc_workspace();
+  } catch (...) {
+    delete h;
+    throw;
+  }
+  return h;
+}
+
 __global__ void k_count(int* visits, int idx, Gate g) {
   if (gate_open(g)) visits[idx] += 1;
 }
@@ -708,10 +932,12 @@ __global__ void k_count(int* visits, int idx, Gate g) {
 void Hier::emit_relax(Level& L, const cplx* b, const cplx* x, cplx* xo, int s, Gate g) {
   // helmadr/krylov.py:91-119 ; r = b - A x (skipped for x == 0: r = b exactly)
   Ctx& c = Ctx::get();
+  const LaunchCfg& lc0 = lcf(L);
   const StencilDev A = L.A->dev();
   launch_relax_init(c.stream, L.rctl, s, g);
   const cplx* r = b;
   if (x) {
+    xchg(L, x);
     StencilArgs a{};
     a.A = A;
     a.x = x;
@@ -720,10 +946,10 @@ void Hier::emit_relax(Level& L, const cplx* b, const cplx* x, cplx* xo, int s, G
     a.gate = g;
     a.rs = c.rs;
     a.epi = epi(EPI_RELAX_BETA, L.rctl);
-    launch_stencil(c.lc, IN_PLAIN, OUT_RESID, RED_NORM, a);
+    launch_stencil(lc0, IN_PLAIN, OUT_RESID, RED_NORM, a);
     r = L.w[1];
   } else {
-    launch_scale(c.lc, L.N, b, nullptr, nullptr, RED_NORM, g, c.rs, epi(EPI_RELAX_BETA, L.rctl));
+    launch_scale(lc0, L.N, b, nullptr, nullptr, RED_NORM, g, c.rs, epi(EPI_RELAX_BETA, L.rctl));
   }
   RelaxCtl* rc = L.rctl;
   for (int j = 0; j < s; ++j) {
@@ -740,11 +966,12 @@ void Hier::emit_relax(Level& L, const cplx* b, const cplx* x, cplx* xo, int s, G
     a.gate = gj;
     a.rs = c.rs;
     a.epi = epi(EPI_RELAX_H, rc, 0, j);
-    launch_stencil(c.lc, IN_SCALE | IN_JAC | IN_WRITEV, OUT_APPLY, j == 0 ? RED_DOT_CENTER : RED_DOT, a);
+    xchg(L, a.x);
+    launch_stencil(lc0, IN_SCALE | IN_JAC | IN_WRITEV, OUT_APPLY, j == 0 ? RED_DOT_CENTER : RED_DOT, a);
     for (int i = 0; i < j; ++i)
-      launch_axpy_red(c.lc, L.N, w, &rc->H[i * RMAX + j], L.V[i], RED_DOT, L.V[i + 1], gj, c.rs,
+      launch_axpy_red(lc0, L.N, w, &rc->H[i * RMAX + j], L.V[i], RED_DOT, L.V[i + 1], gj, c.rs,
                       epi(EPI_RELAX_H, rc, i + 1, j));
-    launch_axpy_red(c.lc, L.N, w, &rc->H[j * RMAX + j], L.V[j], RED_NORM, nullptr, gj, c.rs,
+    launch_axpy_red(lc0, L.N, w, &rc->H[j * RMAX + j], L.V[j], RED_NORM, nullptr, gj, c.rs,
                     epi(EPI_RELAX_STEP, rc, 0, j));
   }
   LinComb lc{};
@@ -754,7 +981,7 @@ void Hier::emit_relax(Level& L, const cplx* b, const cplx* x, cplx* xo, int s, G
   lc.base = x;
   lc.dinv = L.dinv;
   lc.out = xo;
-  launch_lincomb(c.lc, L.N, lc, g);
+  launch_lincomb(lc0, L.N, lc, g);
 }
 
 void Hier::emit_kcycle(int li, const cplx* b, const cplx* x0, cplx* xo, Gate g, bool count) {
@@ -768,6 +995,7 @@ void Hier::emit_kcycle(int li, const cplx* b, const cplx* x0, cplx* xo, Gate g, 
   }
   Level& L = lv[li];
   Level& C = lv[li + 1];
+  const LaunchCfg& lc0 = lcf(L);
   if (count) k_count<<<1, 1, 0, c.stream>>>(visits, li, g);
   emit_relax(L, b, x0, xo, L.s, g);
   StencilArgs a{};
@@ -778,8 +1006,28 @@ void Hier::emit_kcycle(int li, const cplx* b, const cplx* x0, cplx* xo, Gate g, 
   a.gate = g;
   a.rs = c.rs;
   a.epi = epi_none();
-  launch_stencil(c.lc, IN_PLAIN, OUT_RESID, RED_NONE, a);
-  launch_restrict(c.lc, L.n1, L.n2, L.n3, L.r, C.fb, g);
+  xchg(L, xo);
+  launch_stencil(lc0, IN_PLAIN, OUT_RESID, RED_NONE, a);
+  if (!L.dist) {
+    launch_restrict(lc0, L.n1, L.n2, L.n3, L.r, C.fb, g);
+  } else {
+    // slab restriction: coarse rows [cb[r], cb[r+1]) need the fine row below the slab
+    Comm* cm = dist_comm();
+    const int rk = cm->rank;
+    const long n23c = (long)C.n2 * C.n3;
+    std::vector<int> cb(cm->size + 1);
+    for (int q = 0; q < cm->size; ++q) cb[q] = L.bounds[q] / 2;
+    cb[cm->size] = C.n1;
+    xchg(L, L.r);
+    launch_restrict(lc0, L.n1, L.n2, L.n3, L.r, C.dist ? C.fb : C.fb + (long)cb[rk] * n23c, g, L.p0, cb[rk],
+                    cb[rk + 1] - cb[rk]);
+    if (!C.dist) {  // agglomerate: every rank gets the whole coarse right-hand side
+      cm->group_start();
+      for (int q = 0; q < cm->size; ++q)
+        cm->bcast(C.fb + (long)cb[q] * n23c, (size_t)(cb[q + 1] - cb[q]) * n23c * sizeof(cplx), q, c.stream);
+      cm->group_end();
+    }
+  }
   if (li + 1 == nl - 1) {
     if (count) k_count<<<1, 1, 0, c.stream>>>(visits, li + 1, g);
     if (!count && use_ce(li + 1))
@@ -791,7 +1039,12 @@ void Hier::emit_kcycle(int li, const cplx* b, const cplx* x0, cplx* xo, Gate g, 
   } else {
     emit_inner(li + 1, g, count);
   }
-  launch_prolong_add(c.lc, L.n1, L.n2, L.n3, C.fx, xo, g);
+  if (!L.dist) {
+    launch_prolong_add(lc0, L.n1, L.n2, L.n3, C.fx, xo, g);
+  } else {
+    xchg(C, C.fx);  // slab coarse level: the row above the coarse slab
+    launch_prolong_add(lc0, L.n1, L.n2, L.n3, C.fx, xo, g, L.p0, L.nown, C.dist ? C.p0 : 0);
+  }
   emit_relax(L, b, xo, xo, L.s, g);
 }
 
@@ -803,12 +1056,13 @@ void Hier::emit_inner(int ci, Gate g, bool count) {
   FgCtl* f = C.fctl;
   const StencilDev A = C.A->dev();
   const long n = C.N;
+  const LaunchCfg& lcc = lcf(C);
   int* act = kact + ci;
   const unsigned bA = 1u << FG_A, bC = 1u << FG_CONT, bB = 1u << FG_BRK, bR = 1u << FG_RST;
   launch_fg_setup(c.stream, f, coarse_tol, g);
-  launch_scale(c.lc, n, C.fb, nullptr, nullptr, RED_NORM, g, c.rs, epi(EPI_FG_INIT, f));
+  launch_scale(lcc, n, C.fb, nullptr, nullptr, RED_NORM, g, c.rs, epi(EPI_FG_INIT, f));
   const Gate gA = gate_var(g.active, &f->path, bA);
-  launch_scale(c.lc, n, C.fb, &f->inv_r, C.fV0, 0, gA, c.rs, epi_none());
+  launch_scale(lcc, n, C.fb, &f->inv_r, C.fV0, 0, gA, c.rs, epi_none());
   // ---- iteration 1 ----
   launch_set_gate(c.stream, act, gA);
   emit_kcycle(ci, C.fV0, nullptr, C.fZ0, gate_on(act), count);
@@ -821,16 +1075,17 @@ void Hier::emit_inner(int ci, Gate g, bool count) {
     a.gate = gA;
     a.rs = c.rs;
     a.epi = epi(EPI_FG_S, f, 0, 0);
-    launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT, a);
-    launch_axpy_red(c.lc, n, C.fw, &f->H[0], C.fV0, RED_NORM, nullptr, gA, c.rs, epi(EPI_FG_N, f, 0, 0, 1));
+    xchg(C, a.x);
+    launch_stencil(lcc, IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT, a);
+    launch_axpy_red(lcc, n, C.fw, &f->H[0], C.fV0, RED_NORM, nullptr, gA, c.rs, epi(EPI_FG_N, f, 0, 0, 1));
     const Gate gAr = gate_var2(g.active, &f->path, bA, &f->reo, 2u);
-    launch_dot(c.lc, n, C.fV0, C.fw, gAr, c.rs, epi(EPI_FG_CORR, f, 0, 0));
-    launch_axpy_red(c.lc, n, C.fw, &f->corr[0], C.fV0, RED_NORM, nullptr, gAr, c.rs, epi(EPI_FG_N2, f, 0, 0, 1));
+    launch_dot(lcc, n, C.fV0, C.fw, gAr, c.rs, epi(EPI_FG_CORR, f, 0, 0));
+    launch_axpy_red(lcc, n, C.fw, &f->corr[0], C.fV0, RED_NORM, nullptr, gAr, c.rs, epi(EPI_FG_N2, f, 0, 0, 1));
   }
   // ---- early exit after iteration 1: x = Z0 y0, r = b - A x, restart decision ----
   {
     const Gate gB = gate_var(g.active, &f->path, bB);
-    launch_fg_finalize(c.lc, n, f, C.fZ0, C.fZ1, C.fx, gB, 1);
+    launch_fg_finalize(lcc, n, f, C.fZ0, C.fZ1, C.fx, gB, 1);
     StencilArgs a{};
     a.A = A;
     a.x = C.fx;
@@ -839,11 +1094,12 @@ void Hier::emit_inner(int ci, Gate g, bool count) {
     a.gate = gB;
     a.rs = c.rs;
     a.epi = epi(EPI_FG_RES, f);
-    launch_stencil(c.lc, IN_PLAIN, OUT_RESID, RED_NORM, a);
+    xchg(C, a.x);
+    launch_stencil(lcc, IN_PLAIN, OUT_RESID, RED_NORM, a);
   }
   // ---- iteration 2: u = V1 (continue) or u = r/||r|| (restart cycle) ----
-  launch_scale(c.lc, n, C.fw, &f->inv_w, C.fu, 0, gate_var(g.active, &f->path, bC), c.rs, epi_none());
-  launch_scale(c.lc, n, C.fr, &f->inv_r, C.fu, 0, gate_var(g.active, &f->path, bR), c.rs, epi_none());
+  launch_scale(lcc, n, C.fw, &f->inv_w, C.fu, 0, gate_var(g.active, &f->path, bC), c.rs, epi_none());
+  launch_scale(lcc, n, C.fr, &f->inv_r, C.fu, 0, gate_var(g.active, &f->path, bR), c.rs, epi_none());
   const Gate gCR = gate_var(g.active, &f->path, bC | bR);
   launch_set_gate(c.stream, act, gCR);
   emit_kcycle(ci, C.fu, nullptr, C.fZ1, gate_on(act), count);
@@ -857,14 +1113,15 @@ void Hier::emit_inner(int ci, Gate g, bool count) {
     a.gate = gC;
     a.rs = c.rs;
     a.epi = epi(EPI_FG_S, f, 0, 1);
-    launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT, a);
-    launch_axpy_red(c.lc, n, C.fw, &f->H[0 * MMAX + 1], C.fV0, RED_DOT, C.fu, gC, c.rs, epi(EPI_FG_H, f, 1, 1));
-    launch_axpy_red(c.lc, n, C.fw, &f->H[1 * MMAX + 1], C.fu, RED_NORM, nullptr, gC, c.rs,
+    xchg(C, a.x);
+    launch_stencil(lcc, IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT, a);
+    launch_axpy_red(lcc, n, C.fw, &f->H[0 * MMAX + 1], C.fV0, RED_DOT, C.fu, gC, c.rs, epi(EPI_FG_H, f, 1, 1));
+    launch_axpy_red(lcc, n, C.fw, &f->H[1 * MMAX + 1], C.fu, RED_NORM, nullptr, gC, c.rs,
                     epi(EPI_FG_N, f, 0, 1, 1));
     const Gate gCr = gate_var2(g.active, &f->path, bC, &f->reo, 2u);
-    launch_dot(c.lc, n, C.fV0, C.fw, gCr, c.rs, epi(EPI_FG_CORR, f, 0, 1));
-    launch_axpy_red(c.lc, n, C.fw, &f->corr[0], C.fV0, RED_DOT, C.fu, gCr, c.rs, epi(EPI_FG_CORR, f, 1, 1));
-    launch_axpy_red(c.lc, n, C.fw, &f->corr[1], C.fu, RED_NORM, nullptr, gCr, c.rs, epi(EPI_FG_N2, f, 0, 1, 1));
+    launch_dot(lcc, n, C.fV0, C.fw, gCr, c.rs, epi(EPI_FG_CORR, f, 0, 1));
+    launch_axpy_red(lcc, n, C.fw, &f->corr[0], C.fV0, RED_DOT, C.fu, gCr, c.rs, epi(EPI_FG_CORR, f, 1, 1));
+    launch_axpy_red(lcc, n, C.fw, &f->corr[1], C.fu, RED_NORM, nullptr, gCr, c.rs, epi(EPI_FG_N2, f, 0, 1, 1));
   }
   {  // restart cycle: j = 0 against basis (u)
     const Gate gR = gate_var(g.active, &f->path, bR);
@@ -876,18 +1133,25 @@ void Hier::emit_inner(int ci, Gate g, bool count) {
     a.gate = gR;
     a.rs = c.rs;
     a.epi = epi(EPI_FG_S, f, 0, 0);
-    launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT, a);
-    launch_axpy_red(c.lc, n, C.fw, &f->H[0], C.fu, RED_NORM, nullptr, gR, c.rs, epi(EPI_FG_N, f, 0, 0, 1));
+    xchg(C, a.x);
+    launch_stencil(lcc, IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT, a);
+    launch_axpy_red(lcc, n, C.fw, &f->H[0], C.fu, RED_NORM, nullptr, gR, c.rs, epi(EPI_FG_N, f, 0, 0, 1));
     const Gate gRr = gate_var2(g.active, &f->path, bR, &f->reo, 2u);
-    launch_dot(c.lc, n, C.fu, C.fw, gRr, c.rs, epi(EPI_FG_CORR, f, 0, 0));
-    launch_axpy_red(c.lc, n, C.fw, &f->corr[0], C.fu, RED_NORM, nullptr, gRr, c.rs, epi(EPI_FG_N2, f, 0, 0, 1));
+    launch_dot(lcc, n, C.fu, C.fw, gRr, c.rs, epi(EPI_FG_CORR, f, 0, 0));
+    launch_axpy_red(lcc, n, C.fw, &f->corr[0], C.fu, RED_NORM, nullptr, gRr, c.rs, epi(EPI_FG_N2, f, 0, 0, 1));
   }
-  launch_fg_finalize(c.lc, n, f, C.fZ0, C.fZ1, C.fx, gate_var(g.active, &f->path, (1u << FG_FIN) | (1u << FG_ZERO)),
+  launch_fg_finalize(lcc, n, f, C.fZ0, C.fZ1, C.fx, gate_var(g.active, &f->path, (1u << FG_FIN) | (1u << FG_ZERO)),
                      0);
 }
 
 void Hier::apply(const cplx* v, cplx* z) {
   Ctx& c = Ctx::get();
+  if (ndist > 0 && !dist_comm()->graphable()) {  // host-callback exchanges: emit directly
+    launch_set_gate(c.stream, kact, gate_always());
+    emit_kcycle(0, v, nullptr, z, gate_on(kact), false);
+    HADR_CUDA(cudaGetLastError());
+    return;
+  }
   auto key = std::make_pair((const void*)v, (void*)z);
   auto it = graphs.find(key);
   if (it == graphs.end()) {
@@ -966,6 +1230,7 @@ static inline double habs(cplx a) { return std::hypot(a.x, a.y); }
 struct OuterWS {
   long N = 0;
   int m = 0;
+  long h = 0;
   std::vector<cplx*> V, Z;
   cplx *w = nullptr, *r = nullptr;
   FgCtl* f = nullptr;
@@ -979,17 +1244,25 @@ struct OuterWS {
   }
 };
 
-static OuterWS* outer_ws(long N, int m) {
+static cplx* halo_vec(long N, long h) {  // h halo entries each side (slab vectors)
+  if (!h) return dalloc<cplx>(N);
+  cplx* p = dalloc<cplx>(N + 2 * h);
+  HADR_CUDA(cudaMemset(p, 0, (N + 2 * h) * sizeof(cplx)));
+  return p + h;
+}
+
+static OuterWS* outer_ws(long N, int m, long h) {
   static OuterWS* ws = nullptr;
-  if (ws && ws->N == N && ws->m >= m) return ws;
+  if (ws && ws->N == N && ws->m >= m && ws->h == h) return ws;
   delete ws;
   ws = new OuterWS();
   ws->N = N;
   ws->m = m;
-  for (int j = 0; j <= m; ++j) ws->V.push_back(dalloc<cplx>(N));
-  for (int j = 0; j < m; ++j) ws->Z.push_back(dalloc<cplx>(N));
-  ws->w = dalloc<cplx>(N);
-  ws->r = dalloc<cplx>(N);
+  ws->h = h;
+  for (int j = 0; j <= m; ++j) ws->V.push_back(halo_vec(N, h));
+  for (int j = 0; j < m; ++j) ws->Z.push_back(halo_vec(N, h));
+  ws->w = halo_vec(N, h);
+  ws->r = halo_vec(N, h);
   ws->f = dalloc<FgCtl>(1);
   HADR_CUDA(cudaMemset(ws->f, 0, sizeof(FgCtl)));
   HADR_CUDA(cudaMallocHost(&ws->hf, sizeof(FgCtl)));
@@ -1002,14 +1275,21 @@ void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart,
   if (restart < 1) throw ValueError("restart must be >= 1");
   if (tol <= 0) throw ValueError("tol must be positive");
   if (restart > MMAX) throw ValueError("restart exceeds the device limit (16)");
-  if (M && (M->lv[0].N != A.N)) throw ValueError("preconditioner dimension mismatch");
+  if (M && (M->lv[0].N != A.nloc() || M->lv[0].dist != A.slab())) throw ValueError("preconditioner dimension mismatch");
   Ctx& c = Ctx::get();
   auto t0 = std::chrono::steady_clock::now();
-  const long N = A.N;
-  OuterWS* ws = outer_ws(N, restart);
+  // slab operator (multi-GPU): vectors are this rank's owned points, with kHalo halo planes
+  // around every stencil input (x included: the caller allocates it with halos)
+  const long N = A.nloc();
+  LaunchCfg lcd = c.lc;
+  if (A.slab()) lcd.dist = &dist_comm()->red;
+  auto xchg = [&](const cplx* v) {
+    if (A.slab()) dist_comm()->halo((void*)v, A.n23() * sizeof(cplx), A.own(), kHalo, c.stream);
+  };
+  OuterWS* ws = outer_ws(N, restart, A.slab() ? (long)kHalo * A.n23() : 0);
   const StencilDev Ad = A.dev();
   auto norm2 = [&](const cplx* v) -> double {
-    launch_scale(c.lc, N, v, nullptr, nullptr, RED_NORM, gate_always(), c.rs, epi_store(c.dscal));
+    launch_scale(lcd, N, v, nullptr, nullptr, RED_NORM, gate_always(), c.rs, epi_store(c.dscal));
     HADR_CUDA(cudaMemcpyAsync(c.hscal, c.dscal, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     return std::sqrt(c.hscal[0]);
@@ -1023,7 +1303,8 @@ void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart,
     a.gate = gate_always();
     a.rs = c.rs;
     a.epi = epi_store(c.dscal);
-    launch_stencil(c.lc, IN_PLAIN, OUT_RESID, RED_NORM, a);
+    xchg(xx);
+    launch_stencil(lcd, IN_PLAIN, OUT_RESID, RED_NORM, a);
     HADR_CUDA(cudaMemcpyAsync(c.hscal, c.dscal, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     return std::sqrt(c.hscal[0]);
@@ -1080,7 +1361,7 @@ void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart,
     // V[0] = r / rnorm
     c.hscal[1] = 1.0 / rnorm;  // r / rnorm == r * (1/rnorm) in numpy (Smith division by a real)
     HADR_CUDA(cudaMemcpyAsync(ws->inv, &c.hscal[1], sizeof(double), cudaMemcpyHostToDevice, c.stream));
-    launch_scale(c.lc, N, ws->r, ws->inv, ws->V[0], 0, gate_always(), c.rs, epi_none());
+    launch_scale(lcd, N, ws->r, ws->inv, ws->V[0], 0, gate_always(), c.rs, epi_none());
     int k = 0;
     bool broke = false;
     for (int j = 0; j < m; ++j) {
@@ -1098,18 +1379,19 @@ void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart,
       a.gate = gate_always();
       a.rs = c.rs;
       a.epi = epi(EPI_FG_S, f, 0, j);
-      launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT, a);
+      xchg(z);
+      launch_stencil(lcd, IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT, a);
       for (int i = 0; i < j; ++i)
-        launch_axpy_red(c.lc, N, ws->w, &f->H[i * MMAX + j], ws->V[i], RED_DOT, ws->V[i + 1], gate_always(), c.rs,
+        launch_axpy_red(lcd, N, ws->w, &f->H[i * MMAX + j], ws->V[i], RED_DOT, ws->V[i + 1], gate_always(), c.rs,
                         epi(EPI_FG_H, f, i + 1, j));
-      launch_axpy_red(c.lc, N, ws->w, &f->H[j * MMAX + j], ws->V[j], RED_NORM, nullptr, gate_always(), c.rs,
+      launch_axpy_red(lcd, N, ws->w, &f->H[j * MMAX + j], ws->V[j], RED_NORM, nullptr, gate_always(), c.rs,
                       epi(EPI_FG_N, f, 0, j, 0));
       const Gate gr = gate_var(nullptr, &f->reo, 2u);
-      launch_dot(c.lc, N, ws->V[0], ws->w, gr, c.rs, epi(EPI_FG_CORR, f, 0, j));
+      launch_dot(lcd, N, ws->V[0], ws->w, gr, c.rs, epi(EPI_FG_CORR, f, 0, j));
       for (int i = 0; i < j; ++i)
-        launch_axpy_red(c.lc, N, ws->w, &f->corr[i], ws->V[i], RED_DOT, ws->V[i + 1], gr, c.rs,
+        launch_axpy_red(lcd, N, ws->w, &f->corr[i], ws->V[i], RED_DOT, ws->V[i + 1], gr, c.rs,
                         epi(EPI_FG_CORR, f, i + 1, j));
-      launch_axpy_red(c.lc, N, ws->w, &f->corr[j], ws->V[j], RED_NORM, nullptr, gr, c.rs, epi(EPI_FG_N2, f, 0, j, 0));
+      launch_axpy_red(lcd, N, ws->w, &f->corr[j], ws->V[j], RED_NORM, nullptr, gr, c.rs, epi(EPI_FG_N2, f, 0, j, 0));
       HADR_CUDA(cudaGetLastError());
       HADR_CUDA(cudaMemcpyAsync(hf, f, sizeof(FgCtl), cudaMemcpyDeviceToHost, c.stream));
       c.sync();
@@ -1126,7 +1408,7 @@ void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart,
       if (!lucky) {
         c.hscal[2] = 1.0 / wnorm;
         HADR_CUDA(cudaMemcpyAsync(ws->inv + 1, &c.hscal[2], sizeof(double), cudaMemcpyHostToDevice, c.stream));
-        launch_scale(c.lc, N, ws->w, ws->inv + 1, ws->V[j + 1], 0, gate_always(), c.rs, epi_none());
+        launch_scale(lcd, N, ws->w, ws->inv + 1, ws->V[j + 1], 0, gate_always(), c.rs, epi_none());
       }
       for (int i = 0; i < j; ++i) {
         cplx t = hadd(hmul(cs[i], Hm(i, j)), hmul(sn[i], Hm(i + 1, j)));
@@ -1169,7 +1451,7 @@ void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart,
       lcb.kfix = k;
       lcb.base = x;
       lcb.out = x;
-      launch_lincomb(c.lc, N, lcb, gate_always());
+      launch_lincomb(lcd, N, lcb, gate_always());
     }
     rnorm = resid_norm(x, ws->r);
     if (broke) break;

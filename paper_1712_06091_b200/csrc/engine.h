@@ -49,10 +49,15 @@ inline void dfree(void* p) {
   if (p) pool_free(p);
 }
 
-// Structured 2D operator (owns its coefficient planes).
+// Structured 2D/3D operator (owns its coefficient planes).
+// Slab operators (multi-GPU, dist.h) hold the rows of global axis-0 planes
+// [p0, p0 + nown) plus `hal` halo planes on each side; `coef` points at the
+// first owned row and coefficient planes are `pstride` apart.
 struct Op {
-  int n1 = 0, n2 = 0, n3 = 1;  // 2D: n3 = 1
-  long N = 0;
+  int n1 = 0, n2 = 0, n3 = 1;  // 2D: n3 = 1 (global shape)
+  long N = 0;                  // global points
+  int p0 = 0, nown = 0, hal = 0;
+  long pstride = 0;
   int nofs = 0;
   int8_t d1[HADR_MAX_OFS] = {0}, d2[HADR_MAX_OFS] = {0}, d3[HADR_MAX_OFS] = {0};
   cplx* coef = nullptr;
@@ -64,6 +69,13 @@ struct Op {
   int center() const;
   const cplx* inv_diag();  // computes on first use; throws ValueError on a zero diagonal
   void refresh_inv_diag();  // recompute into the existing buffer (coefficients changed)
+  bool slab() const { return nown > 0; }
+  int own() const { return nown > 0 ? nown : n1; }
+  long n23() const { return (long)n2 * n3; }
+  long nloc() const { return (long)own() * n2 * n3; }      // owned points
+  long stride() const { return pstride > 0 ? pstride : N; }
+  long alloc_len() const { return (long)nofs * stride(); }  // coefficient entries incl. halos
+  long base_off() const { return (long)hal * n23(); }       // coef - base
 };
 Op* op_copy(const Op& A);
 
@@ -88,7 +100,10 @@ struct Level {
   Op* A = nullptr;
   bool own = false;
   int n1 = 0, n2 = 0, n3 = 1;
-  long N = 0;
+  long N = 0;                // points this rank computes (slab levels: owned points)
+  bool dist = false;         // slab level (vectors carry kHalo halo planes each side)
+  int p0 = 0, nown = 0;      // owned global planes [p0, p0 + nown)
+  std::vector<int> bounds;   // slab level: every rank's first plane (size + 1 entries)
   const cplx* dinv = nullptr;
   int s = 0;                 // relaxation length at this level
   // K-cycle workspace
@@ -115,6 +130,11 @@ struct Hier {
   int* visits = nullptr;    // device: visit counters (stats mode)
   std::map<std::pair<const void*, void*>, cudaGraphExec_t> graphs;
   std::map<std::pair<const void*, void*>, long long> graph_kernels;  // kernel nodes per graph
+  int ndist = 0;             // leading slab-distributed levels (multi-GPU)
+  LaunchCfg dlc{};           // launch config of slab levels (reductions across ranks)
+  const LaunchCfg& lcf(const Level& L) const;
+  void xchg(const Level& L, const cplx* v) const;  // halo exchange of a slab-level vector
+  cplx* valloc(const Level& L) const;              // level vector (with halos on slab levels)
   ~Hier();
   void alloc_workspace();
   // emit the kernels of k_cycle(level li, b, x0 -> xo) onto the context stream
@@ -134,6 +154,20 @@ Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol);
 void hier_release(Hier* h);  // recycle (workspace + captured graphs) or delete
 Hier* hier_pool_pop();       // take one recycled hierarchy (or null)
 Hier* hier_from_ops(int nlev, Op** ops, int coarse_steps, double coarse_tol);
+// Multi-GPU: slab plan of a global grid (fine slab bounds + number of distributed levels)
+struct SlabPlan {
+  std::vector<int> bounds;  // fine axis-0 slab starts, size + 1 entries
+  int ndist = 0;            // levels 0 .. ndist-1 are slab-distributed, the rest replicated
+  int nlev = 0;
+};
+SlabPlan slab_plan(int n1, int n2, int n3, int max_levels);
+// hierarchy over a slab fine operator (every rank calls it collectively)
+Hier* hier_build_dist(Op* fine_slab, const SlabPlan& plan, int coarse_steps, double coarse_tol);
+// slab assembly: rows of this rank's slab (+1 halo row each side) from global host/device fields
+Op* op_assemble_slab(int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega, int scheme,
+                     const int* bc, int src1, int src2, int src3, const double* ksq, const double* gam,
+                     const double* g1, const double* g2, const double* g3, const double* lap, bool fields_on_device,
+                     int p0, int nown);
 std::vector<Shape3> coarsenable_levels(int n1, int n2, int n3, int max_levels);
 
 struct Report {

@@ -147,7 +147,7 @@ struct Geo {
 
 static Geo geo_for(const LaunchCfg& lc, long n) {
   long b = (n + kThreads - 1) / kThreads;
-  if (n <= kClusterMaxN) {
+  if (n <= kClusterMaxN && !lc.dist) {  // distributed sums finish through the communicator
     if (b > kClusterMaxCTAs) b = kClusterMaxCTAs;
     if (b < 1) b = 1;
     return Geo{(int)b, (int)b};
@@ -191,11 +191,34 @@ static void launch_geo(void (*kern)(KArgs...), const Geo& geo, cudaStream_t s, A
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Distributed reduction: every rank's local totals are all-gathered and summed in
+// rank order (so every rank holds bit-identical control state), then the epilogue.
+template <int NV>
+__global__ void k_epi_gathered(const double* all, int size, Gate g, Epi e) {
+  if (!gate_open(g)) return;
+  double t[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) t[q] = 0.0;
+  for (int r = 0; r < size; ++r) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) t[q] += all[r * 4 + q];
+  }
+  run_epi(e, t, NV);
+}
+
 template <int NV>
 static void launch_finalize(const LaunchCfg& lc, const Geo& geo, Gate g, RedScratch rs, Epi e) {
   if (geo.cluster) return;
   ++g_launch_count;
-  k_finalize<NV><<<1, kThreads, 0, lc.stream>>>(rs, geo.blocks, g, e);
+  if (!lc.dist) {
+    k_finalize<NV><<<1, kThreads, 0, lc.stream>>>(rs, geo.blocks, g, e);
+    return;
+  }
+  const DistRed& d = *lc.dist;
+  k_finalize<NV><<<1, kThreads, 0, lc.stream>>>(rs, geo.blocks, g, epi_store(d.buf));
+  d.gather(d.ctx, lc.stream);
+  ++g_launch_count;
+  k_epi_gathered<NV><<<1, 1, 0, lc.stream>>>(d.all, d.size, g, e);
 }
 
 // ---------------------------------------------------------------------------
@@ -219,9 +242,10 @@ __device__ __forceinline__ void stencil_chunk(const StencilArgs& a, int o0, int 
     const int o = o0 + q;
     const bool live = o < nofs;
     const int oo = live ? o : 0;
-    const int j1 = i1 + a.A.d1[oo], j2 = i2 + a.A.d2[oo], j3 = i3 + a.A.d3[oo];
+    const int d1 = a.A.d1[oo], d2 = a.A.d2[oo], d3 = a.A.d3[oo];
+    const int j1 = i1 + d1, j2 = i2 + d2, j3 = i3 + d3;  // j1: global plane (i1 global)
     ok[q] = live && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2 && j3 >= 0 && j3 < n3;
-    const long jj = ok[q] ? ((long)j1 * n2 + j2) * n3 + j3 : k;
+    const long jj = ok[q] ? k + ((long)d1 * n2 + d2) * n3 + d3 : k;  // owned-relative (halos at < 0)
     cv[q] = C32 ? ld_c64(a.A, live ? (long)o * N + k : k) : ldc(a.A.coef, live ? (long)o * N + k : k);
     xv[q] = ldc(a.x, jj);
     if (INM & IN_JAC) dv[q] = ldc(a.dinv, jj);
@@ -241,7 +265,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(StencilArgs a) {
   if (!gate_open(a.gate)) return;
   const int n1 = a.A.n1, n2 = a.A.n2, n3 = a.A.n3, nofs = a.A.nofs;
   const int n23 = n2 * n3;
-  const long N = (long)n1 * n23;
+  const long N = a.A.pstride;                    // coefficient plane stride
+  const long Nown = (long)a.A.n1own * n23;       // points computed (owned slab)
+  const int p0 = a.A.p0;
   const double s = (INM & IN_SCALE) ? *a.scale : 1.0;
   const bool c32 = a.A.coef32 != nullptr;
   constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & (RED_DOT | RED_DOT_CENTER)) ? 2 : 0);
@@ -249,9 +275,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(StencilArgs a) {
 #pragma unroll
   for (int q = 0; q < (NV > 0 ? NV : 1); ++q) red[q] = 0.0;
   const long stride = (long)gridDim.x * blockDim.x;
-  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += stride) {
-    const int i1 = (int)(k / n23);
-    const int rem = (int)(k - (long)i1 * n23);
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < Nown; k += stride) {
+    const int il = (int)(k / n23);
+    const int i1 = il + p0;  // global plane
+    const int rem = (int)(k - (long)il * n23);
     const int i2 = rem / n3;
     const int i3 = rem - i2 * n3;
     cplx acc = mk(0.0, 0.0);
@@ -323,7 +350,7 @@ static void dispatch_no(const LaunchCfg& lc, const StencilArgs& a, const Geo& ge
 
 void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const StencilArgs& a) {
   ++g_launch_count;
-  const long N = (long)a.A.n1 * a.A.n2 * a.A.n3;
+  const long N = (long)a.A.n1own * a.A.n2 * a.A.n3;  // points computed (owned slab)
   const Geo geo = red ? geo_for(lc, N) : Geo{blocks_for(lc, N), 0};
   constexpr int J = IN_SCALE | IN_JAC | IN_WRITEV;
 #define HADR_CASE(I, O, R)                       \
@@ -517,16 +544,18 @@ void launch_fg_finalize(const LaunchCfg& lc, long n, FgCtl* f, const cplx* Z0, c
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int coarse_n(int n) { return (n - 1) / 2 + 1; }
 
-__global__ void __launch_bounds__(kThreads) k_restrict(int n1f, int n2f, int n3f, const cplx* __restrict__ r,
-                                                         cplx* __restrict__ rc, Gate g) {
+__global__ void __launch_bounds__(kThreads) k_restrict(int n1f, int n2f, int n3f, int p0f, int q0, int nq,
+                                                         const cplx* __restrict__ r, cplx* __restrict__ rc, Gate g) {
+  // coarse planes [q0, q0 + nq) (rc points at plane q0); r points at fine plane p0f (halo at < 0)
   if (!gate_open(g)) return;
-  const int n1c = coarse_n(n1f), n2c = coarse_n(n2f), n3c = coarse_n(n3f);
-  const long Nc = (long)n1c * n2c * n3c;
+  const int n2c = coarse_n(n2f), n3c = coarse_n(n3f);
+  const long Nc = (long)nq * n2c * n3c;
   const int c3lo = n3f > 1 ? -1 : 0, c3hi = n3f > 1 ? 1 : 0;
   const long stride = (long)gridDim.x * blockDim.x;
   for (long c = (long)blockIdx.x * blockDim.x + threadIdx.x; c < Nc; c += stride) {
-    const int I1 = (int)(c / ((long)n2c * n3c));
-    const int rem = (int)(c - (long)I1 * n2c * n3c);
+    const int Il = (int)(c / ((long)n2c * n3c));
+    const int I1 = Il + q0;
+    const int rem = (int)(c - (long)Il * n2c * n3c);
     const int I2 = rem / n3c, I3 = rem - (rem / n3c) * n3c;
     cplx acc = mk(0.0, 0.0);
 #pragma unroll
@@ -543,17 +572,19 @@ __global__ void __launch_bounds__(kThreads) k_restrict(int n1f, int n2f, int n3f
           const int f3 = 2 * I3 + cc;
           if (f3 < 0 || f3 >= n3f) continue;
           const double w = w12 * (cc == 0 ? 1.0 : 0.5);
-          acc = cadd(acc, cmul_sp(mk(w, 0.0), ldc(r, ((long)f1 * n2f + f2) * n3f + f3)));
+          acc = cadd(acc, cmul_sp(mk(w, 0.0), ldc(r, ((long)(f1 - p0f) * n2f + f2) * n3f + f3)));
         }
       }
     }
     rc[c] = acc;
   }
 }
-void launch_restrict(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx* r, cplx* rc, Gate g) {
+void launch_restrict(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx* r, cplx* rc, Gate g, int p0f,
+                     int q0, int nq) {
   ++g_launch_count;
-  const long Nc = (long)((n1f - 1) / 2 + 1) * ((n2f - 1) / 2 + 1) * ((n3f - 1) / 2 + 1);
-  k_restrict<<<blocks_for(lc, Nc), kThreads, 0, lc.stream>>>(n1f, n2f, n3f, r, rc, g);
+  if (nq < 0) nq = (n1f - 1) / 2 + 1;
+  const long Nc = (long)nq * ((n2f - 1) / 2 + 1) * ((n3f - 1) / 2 + 1);
+  k_restrict<<<blocks_for(lc, Nc), kThreads, 0, lc.stream>>>(n1f, n2f, n3f, p0f, q0, nq, r, rc, g);
 }
 
 __device__ __forceinline__ int parents(int f, int* p, double& w) {
@@ -569,16 +600,18 @@ __device__ __forceinline__ int parents(int f, int* p, double& w) {
   return 1;
 }
 
-__global__ void __launch_bounds__(kThreads) k_prolong_add(int n1f, int n2f, int n3f, const cplx* __restrict__ ec,
-                                                            cplx* __restrict__ x, Gate g) {
+__global__ void __launch_bounds__(kThreads) k_prolong_add(int n1f, int n2f, int n3f, int p0f, int nf, int q0c,
+                                                            const cplx* __restrict__ ec, cplx* __restrict__ x, Gate g) {
+  // fine planes [p0f, p0f + nf) (x points at plane p0f); ec points at coarse plane q0c
   if (!gate_open(g)) return;
   const int n2c = coarse_n(n2f), n3c = coarse_n(n3f);
   const int n23 = n2f * n3f;
-  const long Nf = (long)n1f * n23;
+  const long Nf = (long)nf * n23;
   const long stride = (long)gridDim.x * blockDim.x;
   for (long f = (long)blockIdx.x * blockDim.x + threadIdx.x; f < Nf; f += stride) {
-    const int f1 = (int)(f / n23);
-    const int rem = (int)(f - (long)f1 * n23);
+    const int fl = (int)(f / n23);
+    const int f1 = fl + p0f;
+    const int rem = (int)(f - (long)fl * n23);
     const int f2 = rem / n3f, f3 = rem - (rem / n3f) * n3f;
     int c1[2], c2[2], c3[2];
     double w1, w2, w3;
@@ -587,13 +620,16 @@ __global__ void __launch_bounds__(kThreads) k_prolong_add(int n1f, int n2f, int 
     for (int a = 0; a < m1; ++a)
       for (int b = 0; b < m2; ++b)
         for (int cc = 0; cc < m3; ++cc)
-          p = cadd(p, cmul_sp(mk(w1 * w2 * w3, 0.0), ldc(ec, ((long)c1[a] * n2c + c2[b]) * n3c + c3[cc])));
+          p = cadd(p, cmul_sp(mk(w1 * w2 * w3, 0.0), ldc(ec, ((long)(c1[a] - q0c) * n2c + c2[b]) * n3c + c3[cc])));
     x[f] = cadd(x[f], p);
   }
 }
-void launch_prolong_add(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx* ec, cplx* x, Gate g) {
+void launch_prolong_add(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx* ec, cplx* x, Gate g, int p0f,
+                        int nf, int q0c) {
   ++g_launch_count;
-  k_prolong_add<<<blocks_for(lc, (long)n1f * n2f * n3f), kThreads, 0, lc.stream>>>(n1f, n2f, n3f, ec, x, g);
+  if (nf < 0) nf = n1f;
+  k_prolong_add<<<blocks_for(lc, (long)nf * n2f * n3f), kThreads, 0, lc.stream>>>(n1f, n2f, n3f, p0f, nf, q0c, ec,
+                                                                                   x, g);
 }
 
 // ---------------------------------------------------------------------------
@@ -776,15 +812,19 @@ void launch_similarity(cudaStream_t s, const StencilDev& A, cplx* out, const cpl
 // K8: Galerkin coarse operator A_c = P^T A P on the stencil representation.
 // Pass 1 (coef_c == null): OR the mask of non-zero coarse offsets (5x5x5 box).
 // Pass 2: write the compacted planes (slot_of maps box slot -> plane).
-__global__ void k_galerkin(StencilDev Af, int n1c, int n2c, int n3c, unsigned long long* mask, const int* slot_of,
-                           cplx* coef_c) {
+// Slabs: coarse planes [q0, q0 + nq) are produced (coef_c points at plane q0, planes cstride apart); the fine
+// coefficients are read relative to Af.p0 with plane stride Af.pstride (one halo plane below is read).
+__global__ void k_galerkin(StencilDev Af, int n1c, int n2c, int n3c, int q0, int nq, long cstride,
+                           unsigned long long* mask, const int* slot_of, cplx* coef_c) {
   const int n1f = Af.n1, n2f = Af.n2, n3f = Af.n3;
-  const long Nf = (long)n1f * n2f * n3f, Nc = (long)n1c * n2c * n3c;
+  const long Nf = Af.pstride, Nc = (long)nq * n2c * n3c;
+  const long fbase = (long)Af.p0 * n2f * n3f;
   const int c3lo = n3f > 1 ? -1 : 0, c3hi = n3f > 1 ? 1 : 0;
   unsigned long long m0 = 0ull, m1 = 0ull;
   for (long c = (long)blockIdx.x * blockDim.x + threadIdx.x; c < Nc; c += (long)gridDim.x * blockDim.x) {
     int I1, I2, I3;
     decomp3(c, n2c, n3c, I1, I2, I3);
+    I1 += q0;
     cplx acc[125];
     for (int q = 0; q < 125; ++q) acc[q] = mk(0.0, 0.0);
     for (int a = -1; a <= 1; ++a) {
@@ -797,7 +837,7 @@ __global__ void k_galerkin(StencilDev Af, int n1c, int n2c, int n3c, unsigned lo
           const int f3 = 2 * I3 + cc;
           if (f3 < 0 || f3 >= n3f) continue;
           const double wf = (a == 0 ? 1.0 : 0.5) * (b == 0 ? 1.0 : 0.5) * (cc == 0 ? 1.0 : 0.5);
-          const long f = ((long)f1 * n2f + f2) * n3f + f3;
+          const long f = ((long)f1 * n2f + f2) * n3f + f3 - fbase;
           for (int o = 0; o < Af.nofs; ++o) {
             const int g1 = f1 + Af.d1[o], g2 = f2 + Af.d2[o], g3 = f3 + Af.d3[o];
             if (g1 < 0 || g1 >= n1f || g2 < 0 || g2 >= n2f || g3 < 0 || g3 >= n3f) continue;
@@ -822,7 +862,7 @@ __global__ void k_galerkin(StencilDev Af, int n1c, int n2c, int n3c, unsigned lo
       if (acc[q].x != 0.0 || acc[q].y != 0.0) {
         if (q < 64) m0 |= 1ull << q; else m1 |= 1ull << (q - 64);
       }
-      if (coef_c && slot_of[q] >= 0) coef_c[(long)slot_of[q] * Nc + c] = acc[q];
+      if (coef_c && slot_of[q] >= 0) coef_c[(long)slot_of[q] * cstride + c] = acc[q];
     }
   }
   if (mask) {
@@ -831,12 +871,15 @@ __global__ void k_galerkin(StencilDev Af, int n1c, int n2c, int n3c, unsigned lo
   }
 }
 void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, int n3c, unsigned long long* mask,
-                     const int* slot_of, cplx* coef_c) {
+                     const int* slot_of, cplx* coef_c, int q0, int nq, long cstride) {
   ++g_launch_count;
-  long Nc = (long)n1c * n2c * n3c;
+  if (nq < 0) nq = n1c;
+  if (cstride < 0) cstride = (long)n1c * n2c * n3c;
+  long Nc = (long)nq * n2c * n3c;
   int blocks = (int)((Nc + 127) / 128);
   if (blocks > 4096) blocks = 4096;
-  k_galerkin<<<blocks, 128, 0, s>>>(Af, n1c, n2c, n3c, mask, slot_of, coef_c);
+  if (blocks < 1) return;
+  k_galerkin<<<blocks, 128, 0, s>>>(Af, n1c, n2c, n3c, q0, nq, cstride, mask, slot_of, coef_c);
 }
 
 }  // namespace hadr
@@ -880,20 +923,23 @@ struct AsmArgs {
   int face[3][2];   // per axis (low, high): 0 neumann, 1 sommerfeld
   int src[3];       // source node (near-source set), src[0] = -1: none
   const double *ksq, *gam, *g[3], *lap;
-  cplx* coef;       // 9 (2D) / 13 (3D) planes
+  cplx* coef;       // 9 (2D) / 13 (3D) planes, `pstride` apart
   unsigned* mask;   // OR of non-zero planes
+  int r0, nr;       // rows (axis-0 planes) [r0, r0 + nr); fields and coef point at plane r0
+  long pstride;
 };
 
 __global__ void k_assemble(AsmArgs a) {
   const int dim = a.dim;
   const int n1 = a.n[0], n2 = a.n[1], n3 = dim == 3 ? a.n[2] : 1;
-  const long N = (long)n1 * n2 * n3;
+  const long N = (long)a.nr * n2 * n3;
   const int NP = dim == 2 ? 9 : 13;
   unsigned m = 0u;
   const double om = a.omega;
   for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (long)gridDim.x * blockDim.x) {
     int ii[3];
     decomp3(k, n2, n3, ii[0], ii[1], ii[2]);
+    ii[0] += a.r0;
     cplx acc[13];
     bool has[13];
 #pragma unroll
@@ -989,7 +1035,7 @@ __global__ void k_assemble(AsmArgs a) {
       put(cen, mk(w2k - t.x, 0.0 - t.y));
     }
     for (int q = 0; q < NP; ++q) {
-      a.coef[(long)q * N + k] = acc[q];
+      a.coef[(long)q * a.pstride + k] = acc[q];
       if (acc[q].x != 0.0 || acc[q].y != 0.0) m |= 1u << q;
     }
   }
@@ -999,9 +1045,14 @@ __global__ void k_assemble(AsmArgs a) {
 void launch_assemble(cudaStream_t s, int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega,
                      int scheme, const int* bc, int src1, int src2, int src3, const double* ksq, const double* gam,
                      const double* g1, const double* g2, const double* g3, const double* lap, cplx* coefp,
-                     unsigned* mask) {
+                     unsigned* mask, int r0, int nr, long pstride) {
   ++g_launch_count;
   AsmArgs a{};
+  if (nr < 0) nr = n1;
+  if (pstride < 0) pstride = (long)n1 * n2 * (dim == 3 ? n3 : 1);
+  a.r0 = r0;
+  a.nr = nr;
+  a.pstride = pstride;
   a.dim = dim;
   a.n[0] = n1;
   a.n[1] = n2;
@@ -1034,9 +1085,10 @@ void launch_assemble(cudaStream_t s, int dim, int n1, int n2, int n3, double h1,
   a.lap = lap;
   a.coef = coefp;
   a.mask = mask;
-  long N = (long)n1 * n2 * (dim == 3 ? n3 : 1);
+  long N = (long)nr * n2 * (dim == 3 ? n3 : 1);
   int blocks = (int)((N + 127) / 128);
   if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) return;
   k_assemble<<<blocks, 128, 0, s>>>(a);
 }
 

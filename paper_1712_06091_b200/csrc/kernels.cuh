@@ -11,9 +11,15 @@ extern long long g_launch_count;
 //   offsets sorted by (d1, d2, d3) == ascending column index of the reference
 //   CSR row for every in-grid entry, so the accumulation order equals scipy
 //   csr_matvec's.
+// Multi-GPU slabs along axis 0: a rank owns global planes [p0, p0 + n1own) of the
+// n1 global planes; every pointer handed to a kernel points at the first OWNED
+// point, halo planes sit at negative / past-the-end offsets, and coefficient
+// planes are `pstride` apart.  Single GPU: p0 = 0, n1own = n1, pstride = N.
 struct StencilDev {
   int n1, n2, n3;
   int nofs;
+  int p0, n1own;
+  long pstride;
   int8_t d1[HADR_MAX_OFS];
   int8_t d2[HADR_MAX_OFS];
   int8_t d3[HADR_MAX_OFS];
@@ -77,9 +83,21 @@ struct StencilArgs {
   Epi epi;
 };
 
+// Multi-GPU reductions: local totals -> `buf` (4 doubles), `gather` all-gathers every rank's
+// buf into `all` (size x 4) on the stream, a 1-thread kernel sums them in rank order and
+// runs the scalar epilogue (identical control state on every rank).
+struct DistRed {
+  int size;
+  double* buf;
+  double* all;
+  void (*gather)(void* ctx, cudaStream_t s);
+  void* ctx;
+};
+
 struct LaunchCfg {
   cudaStream_t stream;
-  int max_blocks;  // grid cap (multiple of the SM count)
+  int max_blocks;                  // grid cap (multiple of the SM count)
+  const DistRed* dist = nullptr;   // non-null: reductions are completed across the slab ranks
 };
 
 void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const StencilArgs& a);
@@ -113,8 +131,13 @@ void launch_fg_finalize(const LaunchCfg& lc, long n, FgCtl* f, const cplx* Z0, c
 
 // Restriction rc = P^T r and prolongation x += P e (bilinear P, helmadr/multigrid.py:19-46).
 // (tri)linear P = kron(P1(n1), P1(n2), P1(n3)); an axis of size 1 is not coarsened.
-void launch_restrict(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx* r, cplx* rc, Gate g);
-void launch_prolong_add(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx* ec, cplx* x, Gate g);
+// Slabs: restriction writes coarse planes [q0, q0 + nq) (nq < 0: all) from the fine slab starting at global
+// plane p0f (one halo plane below it is read); prolongation updates fine planes [p0f, p0f + nf) (nf < 0: all)
+// from a coarse vector whose index 0 is global coarse plane q0c.
+void launch_restrict(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx* r, cplx* rc, Gate g, int p0f = 0,
+                     int q0 = 0, int nq = -1);
+void launch_prolong_add(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx* ec, cplx* x, Gate g,
+                        int p0f = 0, int nf = -1, int q0c = 0);
 
 void launch_set_gate(cudaStream_t s, int* dst, Gate g);
 void launch_relax_init(cudaStream_t s, RelaxCtl* c, int steps, Gate g);
@@ -137,9 +160,9 @@ void launch_similarity(cudaStream_t s, const StencilDev& A, cplx* out, const cpl
 void launch_assemble(cudaStream_t s, int dim, int n1, int n2, int n3, double h1, double h2, double h3, double omega,
                      int scheme, const int* bc, int src1, int src2, int src3, const double* ksq, const double* gam,
                      const double* g1, const double* g2, const double* g3, const double* lap, cplx* coefp,
-                     unsigned* mask);
+                     unsigned* mask, int r0 = 0, int nr = -1, long pstride = -1);
 void launch_to_c64(cudaStream_t s, long n, const cplx* in, float2* out);
 void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, int n3c, unsigned long long* mask,
-                     const int* slot_of, cplx* coef_c);
+                     const int* slot_of, cplx* coef_c, int q0 = 0, int nq = -1, long cstride = -1);
 
 }  // namespace hadr

@@ -64,3 +64,83 @@ def test_reference_arm_under_torchrun():
     rec = json.loads(lines[0])
     assert rec["impl"] == "reference" and rec["n_gpus"] == 2 and rec["value"] > 0
     assert rec["e2e"]["h2d_bytes_per_step"] == 0
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU slab decomposition: host logic (no device)
+# ---------------------------------------------------------------------------
+def test_slab_bounds():
+    sys.path.insert(0, REPO)
+    from paper_1712_06091_b200 import distributed as D
+
+    for n1, size, align in [(513, 8, 8), (513, 2, 16), (33, 2, 8), (1025, 4, 8), (65, 3, 4), (257, 8, 1)]:
+        b = D.slab_bounds(n1, size, align)
+        assert len(b) == size + 1 and b[0] == 0 and b[-1] == n1
+        assert all(b[r] % align == 0 for r in range(size))
+        assert all(b[r + 1] > b[r] for r in range(size))
+        # nested coarse slabs: level l owns [b >> l) with the same rank order
+        for l in range(1, max(1, align.bit_length() - 1) + 1):
+            bl = [x >> l for x in b[:-1]] + [(n1 - 1) // (1 << l) + 1]
+            assert all(bl[r + 1] >= bl[r] for r in range(size))
+    assert D.slab_bounds(33, 2, 8) == [0, 16, 33]
+    with pytest.raises(ValueError):
+        D.slab_bounds(9, 8, 8)
+
+
+def _comm_worker(rank, world, port, q):
+    import ctypes as C
+
+    import numpy as np
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    sys.path.insert(0, REPO)
+    from paper_1712_06091_b200 import distributed as D
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ag, sr, bc = D._host_callbacks()
+    out = {}
+    # allgather: recv = every rank's bytes in rank order
+    send = (C.c_double * 4)(*[rank * 10.0 + q for q in range(4)])
+    recv = (C.c_double * (4 * world))()
+    assert ag(C.addressof(send), C.addressof(recv), 32) == 0
+    out["allgather"] = list(recv)
+    # the halo exchange's two sendrecv phases (Comm::halo): first planes down / last planes up
+    lo, hi = (rank - 1 if rank > 0 else -1), (rank + 1 if rank < world - 1 else -1)
+    first = (C.c_double * 2)(rank + 0.25, rank + 0.5)
+    last = (C.c_double * 2)(rank + 0.75, rank + 0.875)
+    above = (C.c_double * 2)(-1.0, -1.0)
+    below = (C.c_double * 2)(-1.0, -1.0)
+    assert sr(C.addressof(first), 16 if lo >= 0 else 0, lo, C.addressof(above), 16 if hi >= 0 else 0, hi) == 0
+    assert sr(C.addressof(last), 16 if hi >= 0 else 0, hi, C.addressof(below), 16 if lo >= 0 else 0, lo) == 0
+    out["above"], out["below"] = list(above), list(below)
+    # bcast from the last rank
+    buf = (C.c_double * 3)(*([7.0, 8.0, 9.0] if rank == world - 1 else [0.0, 0.0, 0.0]))
+    assert bc(C.addressof(buf), 24, world - 1) == 0
+    out["bcast"] = list(buf)
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_communicator_callbacks_gloo(world):
+    """The gloo host callbacks libhadr's host communicator calls (dist.h kind 2)."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_comm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect_ag = [r * 10.0 + k for r in range(world) for k in range(4)]
+    for r in range(world):
+        o = res[r]
+        assert o["allgather"] == expect_ag
+        assert o["above"] == ([r + 1 + 0.25, r + 1 + 0.5] if r < world - 1 else [-1.0, -1.0])
+        assert o["below"] == ([r - 1 + 0.75, r - 1 + 0.875] if r > 0 else [-1.0, -1.0])
+        assert o["bcast"] == [7.0, 8.0, 9.0]
