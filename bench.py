@@ -283,17 +283,21 @@ def run_ours(args, ws, rank, local, dist):
         out["cpu_baseline"] = cpu_baseline(wl, args, sample_its=args.cpu_its, threads_one=True)
     if args.extra_3d:
         out["config_4_3d"] = run_3d(args, L, local, dist, ws, rank)
+    if args.extra_cfg3:
+        out["config_3"] = run_3d(args, L, local, dist, 1, rank, which="cfg3")
     return out
 
 
 B_OP_3D_UPWIND_C128 = 6788.0  # 3D adr_upwind c128 (10 / 10 / 54 non-zeros)
 
 
-def run_3d(args, L, local, dist, ws=1, rank=0):
+def run_3d(args, L, local, dist, ws=1, rank=0, which="cfg4"):
     """BASELINE configs[3] (3D 513^2 x 257, c128): device-resident inputs, CUDA events.
     N > 1 (torchrun): ONE solve split in axis-0 slabs over the N GPUs (NCCL halo exchange /
     all-gather / broadcast, coarse levels agglomerated) — strong scaling, max over ranks.
-    The CPU sample is the dimension-generic oracle on a down-scaled grid (rank 0)."""
+    The CPU sample is the dimension-generic oracle on a down-scaled grid (rank 0).
+    which="cfg3": BASELINE configs[2] (2D 4097 x 2049, layered medium, fast-marching tau,
+    1 GPU; every rank solves its own replica when N > 1)."""
     import ctypes as C
 
     import torch
@@ -302,10 +306,18 @@ def run_3d(args, L, local, dist, ws=1, rank=0):
     from paper_1712_06091_b200.fields import point_source
     from paper_1712_06091_b200.operators import _bc, rhs_transform
 
-    wl = workloads.cfg4(args.extra_3d)
+    t_fm = None
+    if which == "cfg3":
+        wl = workloads.cfg3(args.extra_cfg3)
+        t_fm = wl.tt.fm_time
+    else:
+        wl = workloads.cfg4(args.extra_3d)
     g = wl.grid
-    n1, n2, n3 = g.shape
+    dim = len(g.shape)
+    n1, n2 = g.shape[0], g.shape[1]
+    n3 = g.shape[2] if dim == 3 else 1
     N = n1 * n2 * n3
+    b_op = B_OP_3D_UPWIND_C128 if dim == 3 else B_OP_2D_UPWIND_C128
     cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=args.tol, max_iter=args.maxiter)
     qhat = rhs_transform(point_source(g, wl.source), wl.tt, wl.omega, "to_adr").reshape(-1)
     dev = torch.device("cuda", local)
@@ -330,8 +342,10 @@ def run_3d(args, L, local, dist, ws=1, rank=0):
 
     def step():
         _lib.check(L.hadr_solve_adr_upwind(
-            3, n1, n2, n3, hs[0], hs[1], hs[2], float(wl.omega), _lib.cbuf(codes), src[0], src[1], src[2],
-            *[C.c_void_p(f.data_ptr()) for f in fields], C.c_void_p(q_d.data_ptr()), float(cfg.beta),
+            dim, n1, n2, n3, hs[0], hs[1], hs[2] if dim == 3 else 1.0, float(wl.omega), _lib.cbuf(codes), src[0],
+            src[1], src[2] if dim == 3 else 0, *[C.c_void_p(f.data_ptr()) for f in fields[:2 + dim]],
+            *([C.c_void_p(0)] if dim == 2 else []), C.c_void_p(fields[-1].data_ptr()), C.c_void_p(q_d.data_ptr()),
+            float(cfg.beta),
             int(cfg.levels), int(cfg.restart), int(cfg.max_iter), float(cfg.tol), C.c_void_p(a_d.data_ptr()),
             C.byref(rep), _lib.cbuf(hist), len(hist), C.byref(tset), 1))
         return rep.iterations, tset.value, rep.device_time
@@ -348,18 +362,39 @@ def run_3d(args, L, local, dist, ws=1, rank=0):
         D.finalize()
     hbm, srcp = peaks()
     t_k = max_over_ranks(sum(tk) / len(tk), dist)
-    bw = B_OP_3D_UPWIND_C128 * N * (sum(its) / len(its)) / t_k / 1e9 / ws  # per-GPU bytes
-    out = {"workload": f"{wl.name} (BASELINE configs[3], 3D {n1}x{n2}x{n3}, c128, {ws} GPU)",
+    bw = b_op * N * (sum(its) / len(its)) / t_k / 1e9 / ws  # per-GPU bytes
+    label = (f"BASELINE configs[2], 2D {n1}x{n2}, layered medium, fast-marching tau" if which == "cfg3"
+             else f"BASELINE configs[3], 3D {n1}x{n2}x{n3}")
+    out = {"workload": f"{wl.name} ({label}, c128, {ws} GPU)",
            "value": N * sum(its) / t_dev / 1e6, "unit": "Mdof*iter/s", "outer_iterations": its,
            "n_gpus": ws, "scaling": "strong" if ws > 1 else None,
            "parallelism": f"axis-0 slabs x{ws} (NCCL)" if ws > 1 else "single GPU", "slab_plan": slab,
            "ms_per_step": t_dev / len(its) * 1e3, "t_krylov_ms": [t * 1e3 for t in tk],
-           "solve_roofline": {"bound": "hbm", "model_bytes_per_dof_iter": B_OP_3D_UPWIND_C128, "achieved": bw,
+           "solve_roofline": {"bound": "hbm", "model_bytes_per_dof_iter": b_op, "achieved": bw,
                               "peak": hbm, "unit": "GB/s", "frac": bw / hbm, "peak_source": srcp,
                               "note": "per GPU" if ws > 1 else ""}}
+    if t_fm is not None:
+        out["t_fast_march_s"] = t_fm
+        out["note"] = "travel time from the fast-marching restatement at setup (host, untimed, t_fast_march_s)"
     del fields, q_d, a_d
     torch.cuda.empty_cache()
-    if not args.no_cpu_baseline and rank == 0:
+    if not args.no_cpu_baseline and rank == 0 and which == "cfg3":
+        from threadpoolctl import threadpool_limits
+
+        from oracle import hadr_oracle as O
+
+        ws_ = workloads.cfg3(513)  # 1025 x 513: same recipe, bounded CPU sample
+        gg = ws_.grid
+        p = O.Problem(gg.n1, gg.n2, gg.h1, gg.h2, ws_.omega, (ws_.source.i1, ws_.source.i2), ws_.medium.kappa_sq,
+                      ws_.medium.gamma, ws_.tt.tau, ws_.tt.grad1, ws_.tt.grad2, ws_.tt.lap, ws_.bc)
+        with threadpool_limits(1):
+            t0 = time.perf_counter()
+            _, _, r = O.solve_upwind(p, tol=args.tol, maxiter=6)
+            tc = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": gg.n_nodes * r.iterations / tc / 1e6, "unit": "Mdof*iter/s", "cores": 1,
+                               "kind": "port", "sample": f"oracle on cfg3_513 (1025x513): assembly + hierarchy + "
+                                                         f"{r.iterations} outer iterations ({tc:.1f} s)"}
+    elif not args.no_cpu_baseline and rank == 0:
         from threadpoolctl import threadpool_limits
 
         from oracle import hadr_oracle_nd as ND
@@ -483,6 +518,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extra-3d", type=int, default=513, help="also run BASELINE config 4 at this n (0: skip)")
     ap.add_argument("--steps-3d", type=int, default=2)
+    ap.add_argument("--extra-cfg3", type=int, default=2049, help="also run BASELINE config 3 at this n (0: skip)")
     args = ap.parse_args()
     ws, rank, local, dist = dist_init()
     if args.impl == "reference":

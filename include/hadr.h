@@ -164,6 +164,15 @@ int hadr_dist_plan(int n1, int n2, int n3, int max_levels, int* bounds, int* n_d
 /* pure host helper: split n1 planes into `size` slabs with interior bounds multiples of `align` */
 int hadr_slab_bounds(int n1, int size, int align, int* bounds /* size + 1 */);
 
+/* ---- travel time (setup, host; the amplitude solve takes tau as an input) ----
+ * Factored-eikonal fast marching (helmadr/_fmm.py:22-331 via helmadr/eikonal.py:72-99): tau = tau0 * tau1
+ * with tau0 = |x - x0| and its gradient g0 (AnalyticBase), kappa = slowness; order 1 or 2.
+ * Writes tau1 (N doubles); *n_accepted = N on success (fewer: disconnected / heap overflow).
+ * dim 2 reproduces the reference; dim 3 is this build's extension (g03 used). No device needed. */
+int hadr_fast_march(int dim, const int* n, const double* h, const double* tau0, const double* g01,
+                    const double* g02, const double* g03, const double* kappa, const int* src, int order,
+                    double* tau1, long long* n_accepted);
+
 /* ---- Krylov (helmadr/krylov.py) ---- */
 /* _gmres_relax_pre / gmres_relax (helmadr/krylov.py:82-119) */
 int hadr_gmres_relax(hadr_op A, const double* b, const double* x, int steps, double* x_out, int on_device);

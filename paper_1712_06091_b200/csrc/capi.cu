@@ -68,6 +68,11 @@ struct DevVec {
 
 static hadr_op wrap(Op* op, bool own = true) { return new hadr_op_s{op, own}; }
 
+namespace hadr {
+int64_t fast_march(int dim, const int* n, const double* h, const double* tau0, const double* const* g0,
+                   const double* kappa, const int* src, int order, double* tau1_out);  // eikonal.cpp
+}
+
 // Multi-GPU solve_adr_upwind: slab assembly, slab hierarchy with agglomerated coarse
 // levels, distributed FGMRES; every rank passes the global inputs and receives the
 // global amplitude (rows gathered from their owners).
@@ -563,6 +568,19 @@ int hadr_slab_bounds(int n1, int size, int align, int* bounds) {
     const std::vector<int> b = slab_bounds(n1, size, align);
     if (b.empty()) throw ValueError("cannot split the axis into slabs");
     for (size_t i = 0; i < b.size(); ++i) bounds[i] = b[i];
+  });
+}
+
+int hadr_fast_march(int dim, const int* n, const double* h, const double* tau0, const double* g01,
+                    const double* g02, const double* g03, const double* kappa, const int* src, int order,
+                    double* tau1, long long* n_accepted) {
+  return guarded([&] {
+    const double* g0[3] = {g01, g02, g03};
+    try {
+      *n_accepted = (long long)hadr::fast_march(dim, n, h, tau0, g0, kappa, src, order, tau1);
+    } catch (const std::invalid_argument& e) {
+      throw ValueError(e.what());
+    }
   });
 }
 

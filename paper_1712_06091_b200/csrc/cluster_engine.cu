@@ -310,7 +310,7 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
       ce_allreduce<1>(c, v);
       {
         CEProfScope prof_(c, 3);
-        if (threadIdx.x == 0) relax_step(R, j, v[0]);
+        if (threadIdx.x == 0) relax_step_sm(R, j, v[0]);
         __syncthreads();
       }
     }
@@ -432,7 +432,7 @@ __device__ __noinline__ void ce_arnoldi(CEC& c, FgCtl2* f, const CELevel& L, int
       f->reo = (f->wn < kReorthRatio * f->w0) ? 1 : 0;  // helmadr/krylov.py:178-179
       if (!f->reo) {
         CEProfScope prof_(c, 3);
-        fg_post(f, j);
+        fg_post_sm(f, j);
       }
     }
     __syncthreads();
@@ -464,7 +464,7 @@ __device__ __noinline__ void ce_arnoldi(CEC& c, FgCtl2* f, const CELevel& L, int
     ce_allreduce<1>(c, v);
     if (threadIdx.x == 0) {
       f->wn = sqrt(v[0]);
-      fg_post(f, j);
+      fg_post_sm(f, j);
     }
     __syncthreads();
   }

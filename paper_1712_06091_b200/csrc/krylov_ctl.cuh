@@ -122,6 +122,71 @@ static __device__ void relax_step(RelaxCtl* c, int j, double ss) {
   backsolve<RMAX>(c->R, c->g, c->y, j + 1);
 }
 
+// ---- the same control with the state in SHARED memory (cluster engine) ----
+// No local copies (the local-array versions above cost a 6 KB stack frame and
+// L1/L2 round trips per element); identical arithmetic in identical order, so
+// the results are bit-identical to givens_col / backsolve.
+template <int LD>
+__device__ __forceinline__ void givens_col_sm(const cplx* H, cplx* R, const cplx* cs, const cplx* sn, cplx hnext,
+                                              cplx& csj, cplx& snj, cplx& gj, cplx& gj1, int j) {
+  // column j of H (rows 0..j; row j+1 = hnext), rotated by cs/sn[0..j-1] into R
+  cplx a = H[j];  // H[0 * LD + j]
+  for (int i = 0; i < j; ++i) {
+    const cplx b = H[(i + 1) * LD + j];
+    const cplx ci = cs[i], si = sn[i];
+    const cplx t = cadd(cmul_sp(ci, a), cmul_sp(si, b));
+    a = cadd(cmul_sp(cneg(cconj(si)), a), cmul_sp(cconj(ci), b));
+    R[i * LD + j] = t;
+  }
+  const cplx b = hnext;
+  const double aa = cabs_d(a), bb = cabs_d(b);
+  const double den = sqrt(aa * aa + bb * bb);
+  if (den == 0.0) {
+    csj = mk(1.0, 0.0);
+    snj = mk(0.0, 0.0);
+  } else {
+    csj = cdiv_np(cconj(a), mk(den, 0.0));
+    snj = cdiv_np(cconj(b), mk(den, 0.0));
+  }
+  R[j * LD + j] = cadd(cmul_sp(csj, a), cmul_sp(snj, b));
+  R[(j + 1) * LD + j] = mk(0.0, 0.0);
+  const cplx g = gj;
+  gj1 = cmul_sp(cneg(cconj(snj)), g);
+  gj = cmul_sp(csj, g);
+}
+
+template <int LD>
+__device__ void backsolve_sm(const cplx* R, const cplx* g, cplx* y, int k) {
+  for (int i = 0; i < k; ++i) y[i] = g[i];
+  for (int j = k - 1; j >= 0; --j) {
+    const cplx yj = cdiv_np(y[j], R[j * LD + j]);
+    y[j] = yj;
+    for (int i = 0; i < j; ++i) y[i] = csub(y[i], cmul_sp(yj, R[i * LD + j]));
+  }
+}
+
+static __device__ void relax_step_sm(RelaxCtl* c, int j, double ss) {
+  const double hn = sqrt(ss);
+  const double beta = c->beta;
+  const int steps = c->steps;
+  c->H[(j + 1) * RMAX + j] = mk(hn, 0.0);
+  cplx gj = c->g[j], gj1, csj, snj;
+  givens_col_sm<RMAX>(c->H, c->R, c->cs, c->sn, mk(hn, 0.0), csj, snj, gj, gj1, j);
+  c->cs[j] = csj;
+  c->sn[j] = snj;
+  c->g[j] = gj;
+  c->g[j + 1] = gj1;
+  c->k = j + 1;
+  const bool stop = (hn <= kBreakdownEps * beta) || (j + 1 >= steps);  // helmadr/krylov.py:113-114
+  if (!stop) {
+    c->inv_hn = 1.0 / hn;
+    c->cur = j + 1;
+    return;
+  }
+  c->cur = kStopped;
+  backsolve_sm<RMAX>(c->R, c->g, c->y, j + 1);
+}
+
 // ---- inner FGMRES(2) control (helmadr/krylov.py:142-231, helmadr/multigrid.py:159-167) ----
 template <class F>
 __device__ void fg_init(F* f, double ss) {
@@ -197,6 +262,44 @@ __device__ void fg_post(F* f, int j) {
     }
   }
   fg_solve_y(f);
+  f->path = (f->cycle == 0 && j == 0) ? FG_BRK : FG_FIN;
+}
+
+// fg_post with shared-memory state: H is rotated in place (R == H), as the reference does
+template <class F>
+__device__ void fg_post_sm(F* f, int j) {
+  constexpr int LD = F::LD;
+  f->reo = 0;
+  const double wn = f->wn;
+  f->H[(j + 1) * LD + j] = mk(wn, 0.0);
+  if (!isfinite(wn)) {  // helmadr/krylov.py:186-190
+    f->note = 1;
+    f->broke = 1;
+    f->k = j;
+  } else {
+    const bool lucky = wn <= kBreakdownEps * fmax(f->bnorm, 1e-300);
+    if (!lucky) f->inv_w = 1.0 / wn;
+    cplx gj = f->g[j], gj1, csj, snj;
+    givens_col_sm<LD>(f->H, f->H, f->cs, f->sn, mk(wn, 0.0), csj, snj, gj, gj1, j);
+    f->cs[j] = csj;
+    f->sn[j] = snj;
+    f->g[j] = gj;
+    f->g[j + 1] = gj1;
+    f->it += 1;
+    f->k = j + 1;
+    const double h = cabs_d(gj1);
+    if (f->nhist < 8) f->hist[f->nhist++] = h;
+    const bool stop = lucky || h <= f->target;
+    if (f->cycle == 0 && j == 0 && !stop) {  // m = 2: second iteration of the first cycle
+      f->path = FG_CONT;
+      return;
+    }
+  }
+  const int k = f->k;
+  if (k == 1)
+    f->y[0] = cdiv_np(f->g[0], f->H[0]);
+  else if (k > 1)
+    backsolve_sm<LD>(f->H, f->g, f->y, k);
   f->path = (f->cycle == 0 && j == 0) ? FG_BRK : FG_FIN;
 }
 

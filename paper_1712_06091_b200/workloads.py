@@ -8,6 +8,9 @@ are not facts of the reference are marked.
          tau = kappa*r (tau1 = 1), all-Sommerfeld.
 * cfg2 : 1025^2, v = 1.5 + 2.5 x2, 12 ppw at v_min, source (0.5, 0.05),
          20-cell layer, analytic linear-gradient tau, all-Sommerfeld.
+* cfg3 : 4097 x 2049, seeded smooth layered velocity, surface source, tau from
+         the fast-marching restatement (csrc/eikonal.cpp), Neumann top.
+* cfg4 : 3D 513^2 x 257, linear gradient, analytic tau.
 Both accept ``n=`` for down-scaled parity cases (same physics, ppw kept).
 
 The coefficient fields grad(tau), lap(tau) follow the reference's
@@ -215,8 +218,52 @@ def cfg4(n: int = 513, ppw: float = 10.0, layer: int | None = None) -> Workload:
     return Workload(f"cfg4_{n}", grid, med, src, tt, bc)
 
 
+def cfg3_medium(grid: GridSpec, sigma_cells: float) -> np.ndarray:
+    """Seeded smooth layered velocity (SURVEY.md §8(d) config 3 recipe): 8 random planar
+    interfaces, 9 layer velocities in [1.5, 4.5], Gaussian smoothing sigma (cells),
+    affine rescale to [1.5, 4.5]."""
+    from scipy.ndimage import gaussian_filter
+
+    rng = np.random.default_rng(1712)
+    z0 = np.sort(rng.uniform(0.08, 0.95, 8))
+    slope = rng.uniform(-0.15, 0.15, 8)
+    vel = rng.uniform(1.5, 4.5, 9)
+    x1, x2 = grid.coords()
+    layer = np.zeros(grid.shape, dtype=np.int64)
+    for k in range(8):
+        layer += (x2 > z0[k] + slope[k] * (x1 - 1.0)).astype(np.int64)
+    v = gaussian_filter(vel[layer], sigma=sigma_cells, mode="nearest")
+    vmin, vmax = v.min(), v.max()
+    return 1.5 + 3.0 * (v - vmin) / (vmax - vmin)
+
+
+def cfg3(n: int = 2049, ppw: float = 10.0, layer: int | None = None, tt=None) -> Workload:
+    """BASELINE config 3 (n=2049): 4097 x 2049 on [0,2] x [0,1], h = 1/2048, seeded smooth
+    layered velocity 1.5-4.5, 10 ppw at v = 1.5, source at the top centre (2048, 0),
+    tau from fast marching (eikonal.compute_travel_time, setup), reference default
+    boundary (Neumann top, Sommerfeld elsewhere) with the 20-cell layer on the bottom,
+    left and right.  ``n`` scales the grid (2n-1) x n, smoothing and
+    layer in proportion."""
+    from .eikonal import compute_travel_time
+
+    grid = GridSpec(2 * (n - 1) + 1, n, 2.0, 1.0)
+    h = grid.h1
+    omega = 2.0 * np.pi * 1.5 / (ppw * h)
+    scale = (n - 1) / 2048
+    layer = layer if layer is not None else max(2, round(20 * scale))
+    src = SourceSpec((grid.n1 - 1) // 2, 0, omega)
+    v = cfg3_medium(grid, max(1.0, 20.0 * scale))
+    ksq = 1.0 / v**2
+    gam = cell_layer_gamma(grid, omega, layer, ("bottom", "left", "right"))
+    med = Medium(grid, ksq, gam)
+    if tt is None:
+        tt = compute_travel_time(med, grid, src, "second")
+    bc = ("neumann", "sommerfeld", "sommerfeld", "sommerfeld")  # reference BCSpec() default
+    return Workload(f"cfg3_{n}", grid, med, src, tt, bc)
+
+
 def by_name(name: str, n: int | None = None) -> Workload:
-    builders = {"cfg1": cfg1, "cfg2": cfg2, "cfg4": cfg4}
+    builders = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4}
     if name not in builders:
         raise ValueError(f"unknown workload {name!r}; known: {sorted(builders)}")
     return builders[name]() if n is None else builders[name](n)

@@ -65,3 +65,8 @@ def g65():
 @pytest.fixture(scope="session")
 def gcfg1():
     return load_golden("cfg1_129")
+
+
+@pytest.fixture(scope="session")
+def gcfg3():
+    return load_golden("cfg3_65")

@@ -138,14 +138,14 @@ def _floor(p, O, tol):
     return worst, a0, r0
 
 
-@pytest.mark.parametrize("case", ["g33", "g65", "gcfg1"])
+@pytest.mark.parametrize("case", ["g33", "g65", "gcfg1", "gcfg3"])
 def test_solve_upwind_vs_oracle(hadr, case, request, engine):
     from oracle import hadr_oracle as O
     from paper_1712_06091_b200 import workloads
 
     g = request.getfixturevalue(case)
     wl = {"g33": lambda: workloads.cfg1(33), "g65": lambda: workloads.cfg2(65),
-          "gcfg1": lambda: workloads.cfg1(129)}[case]()
+          "gcfg1": lambda: workloads.cfg1(129), "gcfg3": lambda: workloads.cfg3(65)}[case]()
     p = oracle_problem(wl)
     floor, a_or, r_or = _floor(p, O, 1e-6)
     assert r_or.iterations == int(g["upwind_iterations"])
@@ -266,6 +266,18 @@ def test_drivers_end_to_end(hadr, case, request):
     u, a, rep = drivers.solve_adr_central(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
     assert rep.converged and abs(rep.iterations - int(g["central_iterations"])) <= 1
     assert rel(u, g["central_u"]) <= 1e-6
+
+
+def test_drivers_cfg3(hadr, gcfg3):
+    """Config-3 recipe (non-square 129 x 65, Neumann top, surface source, fast-marching
+    travel time) through the public driver."""
+    from paper_1712_06091_b200 import drivers, workloads
+
+    wl = workloads.cfg3(65)
+    cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=1e-6, max_iter=1000)
+    u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
+    assert rep.converged and abs(rep.iterations - int(gcfg3["upwind_iterations"])) <= 1
+    assert rel(a, gcfg3["upwind_a"]) <= 1e-6
 
 
 @pytest.mark.parametrize("case", ["g65", "gcfg1"])

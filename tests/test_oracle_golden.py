@@ -101,6 +101,29 @@ def test_strategies_bitexact(case, request):
     assert np.array_equal(u, g["central_u"])
 
 
+def test_cfg3_recipe_bitexact(gcfg3):
+    """Config-3 recipe at 129 x 65 (layered medium, surface source, Neumann top, travel
+    time from the fast-marching restatement == the reference's, checked when the fixture
+    was made): fields, fine operators, hierarchy and the upwind solve are bit-exact."""
+    g = gcfg3
+    wl = workloads.cfg3(65)
+    assert np.array_equal(wl.tt.tau1, g["tau1"])
+    for k in ("grad1", "grad2", "lap", "tau"):
+        assert np.array_equal(getattr(wl.tt, k), g[k]), k
+    assert np.array_equal(wl.medium.kappa_sq, g["kappa_sq"]) and np.array_equal(wl.medium.gamma, g["gamma"])
+    p = oracle_problem(wl)
+    H2, H1 = O.adr_of(p, "upwind2"), O.adr_of(p, "upwind1")
+    _same_csr(H2, g, "H2up")
+    B = (0.75 * H2 + 0.25 * H1).tocsr()
+    _same_csr(B, g, "blend")
+    Hi = O.hierarchy(B, (p.n1, p.n2), 5)
+    for l, A in enumerate(Hi.ops):
+        _same_csr(A, g, f"lev{l}")
+    u, a, rep = O.solve_upwind(p, tol=1e-6, maxiter=1000)
+    assert rep.iterations == int(g["upwind_iterations"])
+    assert np.array_equal(a, g["upwind_a"])
+
+
 def test_cfg1_iteration_counts_match_survey(gcfg1):
     # SURVEY.md §6 measured-here table: upwind 18, central 19, standard 20
     assert int(gcfg1["upwind_iterations"]) == 18

@@ -61,7 +61,7 @@ def main() -> None:
             "levels": nl, "iterations": rep.iterations, "iterations_single": rep1.iterations,
             "converged": bool(rep.converged), "final_relres": rep.final_relres, "rel_l2_vs_single": rel,
             "history": [float(h) for h in rep.history], "history_single": [float(h) for h in rep1.history],
-            "device_time_s": rep.device_time,
+            "device_time_s": rep.device_time, "device_time_single_s": rep1.device_time,
         }
         line = json.dumps(out)
         print(line, flush=True)
