@@ -568,6 +568,7 @@ __device__ void ce_kcycle(CEC& c, int l, const cplx* b, cplx* xo) {
 __global__ void __launch_bounds__(CE_THREADS, 1)
     k_cluster_engine(const CEDesc* __restrict__ d, int mode, int l0, const cplx* b, cplx* xo, const int* active,
                      int prof) {
+  pdl_enter();
   if (active && *((volatile const int*)active) == 0) return;
   __shared__ CEShared S;
   // level descriptors into shared memory
@@ -638,13 +639,15 @@ void launch_cluster_engine(cudaStream_t s, const CEDesc* d, int mode, int l0, co
   cfg.blockDim = dim3(CE_THREADS);
   cfg.dynamicSmemBytes = tile_bytes;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = ctas;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g_pdl ? 2 : 1;
   cudaLaunchKernelEx(&cfg, k_cluster_engine, d, mode, l0, b, xo, active, g_ce_prof_on);
 }
 

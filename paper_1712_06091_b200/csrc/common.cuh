@@ -157,6 +157,15 @@ __device__ __forceinline__ bool grid_sum(double (&v)[NV], RedScratch rs, double 
   return true;
 }
 
+// Programmatic dependent launch (PDL): solve-phase kernels are launched with
+// programmatic stream serialization, so the next kernel of the chain is scheduled
+// while this one runs; every such kernel first waits for its predecessor's
+// completion (griddepcontrol.wait: full completion + memory visibility) and then
+// allows its own successor to launch.  Both are no-ops without the attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
+}
+
 #define HADR_CUDA(call)                                                     \
   do {                                                                      \
     cudaError_t e_ = (call);                                                \

@@ -120,6 +120,7 @@ __device__ __forceinline__ void finish(double (&v)[NV], const RedScratch& rs, co
 
 template <int NV>
 __global__ void __launch_bounds__(kThreads) k_finalize(RedScratch rs, int nblocks, Gate g, Epi e) {
+  pdl_enter();
   if (!gate_open(g)) return;
   __shared__ double sm[NV * 32];
   double acc[NV];
@@ -163,10 +164,31 @@ static int blocks_for(const LaunchCfg& lc, long n) {
   return (int)b;
 }
 
+int g_pdl = 1;  // programmatic dependent launch of the solve-phase kernels (option "pdl")
+
+static inline int pdl_attr(cudaLaunchAttribute* at) {
+  if (!g_pdl) return 0;
+  at->id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at->val.programmaticStreamSerializationAllowed = 1;
+  return 1;
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kern)(KArgs...), int blocks, int threads, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  cfg.numAttrs = pdl_attr(at);
+  cfg.attrs = at;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <typename... KArgs, typename... Args>
 static void launch_geo(void (*kern)(KArgs...), const Geo& geo, cudaStream_t s, Args&&... args) {
   if (!geo.cluster) {
-    kern<<<geo.blocks, kThreads, 0, s>>>(std::forward<Args>(args)...);
+    launch_k(kern, geo.blocks, kThreads, s, std::forward<Args>(args)...);
     return;
   }
   if (geo.cluster > 8) {  // non-portable cluster sizes must be enabled per kernel
@@ -181,13 +203,13 @@ static void launch_geo(void (*kern)(KArgs...), const Geo& geo, cudaStream_t s, A
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = geo.cluster;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 1 + pdl_attr(at + 1);
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -195,6 +217,7 @@ static void launch_geo(void (*kern)(KArgs...), const Geo& geo, cudaStream_t s, A
 // rank order (so every rank holds bit-identical control state), then the epilogue.
 template <int NV>
 __global__ void k_epi_gathered(const double* all, int size, Gate g, Epi e) {
+  pdl_enter();
   if (!gate_open(g)) return;
   double t[NV];
 #pragma unroll
@@ -211,14 +234,14 @@ static void launch_finalize(const LaunchCfg& lc, const Geo& geo, Gate g, RedScra
   if (geo.cluster) return;
   ++g_launch_count;
   if (!lc.dist) {
-    k_finalize<NV><<<1, kThreads, 0, lc.stream>>>(rs, geo.blocks, g, e);
+    launch_k(k_finalize<NV>, 1, kThreads, lc.stream, rs, geo.blocks, g, e);
     return;
   }
   const DistRed& d = *lc.dist;
-  k_finalize<NV><<<1, kThreads, 0, lc.stream>>>(rs, geo.blocks, g, epi_store(d.buf));
+  launch_k(k_finalize<NV>, 1, kThreads, lc.stream, rs, geo.blocks, g, epi_store(d.buf));
   d.gather(d.ctx, lc.stream);
   ++g_launch_count;
-  k_epi_gathered<NV><<<1, 1, 0, lc.stream>>>(d.all, d.size, g, e);
+  launch_k(k_epi_gathered<NV>, 1, 1, lc.stream, (const double*)d.all, d.size, g, e);
 }
 
 // ---------------------------------------------------------------------------
@@ -262,6 +285,7 @@ __device__ __forceinline__ void stencil_chunk(const StencilArgs& a, int o0, int 
 
 template <int INM, int OUTM, int RED, int NO, int CL>
 __global__ void __launch_bounds__(kThreads, 4) k_stencil(StencilArgs a) {
+  pdl_enter();
   if (!gate_open(a.gate)) return;
   const int n1 = a.A.n1, n2 = a.A.n2, n3 = a.A.n3, nofs = a.A.nofs;
   const int n23 = n2 * n3;
@@ -377,6 +401,7 @@ template <int RED, int CL>
 __global__ void __launch_bounds__(kThreads) k_axpy_red(long n, cplx* __restrict__ w, const cplx* h,
                                                          const cplx* __restrict__ v, const cplx* __restrict__ u,
                                                          Gate g, RedScratch rs, Epi e) {
+  pdl_enter();
   if (!gate_open(g)) return;
   const cplx hh = *h;
   constexpr int NV = (RED == RED_NORM) ? 1 : 2;
@@ -420,6 +445,7 @@ void launch_axpy_red(const LaunchCfg& lc, long n, cplx* w, const cplx* h, const 
 template <int CL>
 __global__ void __launch_bounds__(kThreads) k_dot(long n, const cplx* __restrict__ u, const cplx* __restrict__ w,
                                                     Gate g, RedScratch rs, Epi e) {
+  pdl_enter();
   if (!gate_open(g)) return;
   double red[2] = {0.0, 0.0};
   const long stride = (long)gridDim.x * blockDim.x;
@@ -444,6 +470,7 @@ void launch_dot(const LaunchCfg& lc, long n, const cplx* u, const cplx* w, Gate 
 template <int RED, int CL>
 __global__ void __launch_bounds__(kThreads) k_scale(long n, const cplx* __restrict__ in, const double* s,
                                                       cplx* __restrict__ out, Gate g, RedScratch rs, Epi e) {
+  pdl_enter();
   if (!gate_open(g)) return;
   const double sc = s ? *s : 1.0;
   double red[1] = {0.0};
@@ -468,22 +495,24 @@ void launch_scale(const LaunchCfg& lc, long n, const cplx* in, const double* s, 
       launch_geo(k_scale<1, 0>, geo, lc.stream, n, in, s, out, g, rs, e);
     launch_finalize<1>(lc, geo, g, rs, e);
   } else {
-    k_scale<0, 0><<<blocks_for(lc, n), kThreads, 0, lc.stream>>>(n, in, s, out, g, rs, e);
+    launch_k(k_scale<0, 0>, blocks_for(lc, n), kThreads, lc.stream, n, in, s, out, g, rs, e);
   }
 }
 
 __global__ void k_zero(long n, cplx* out, Gate g) {
+  pdl_enter();
   if (!gate_open(g)) return;
   const long stride = (long)gridDim.x * blockDim.x;
   for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) out[k] = mk(0.0, 0.0);
 }
 void launch_zero(const LaunchCfg& lc, long n, cplx* out, Gate g) {
   ++g_launch_count;
-  k_zero<<<blocks_for(lc, n), kThreads, 0, lc.stream>>>(n, out, g);
+  launch_k(k_zero, blocks_for(lc, n), kThreads, lc.stream, n, out, g);
 }
 
 // K5: out = base + [dinv (.)] sum_i v_i y_i
 __global__ void __launch_bounds__(kThreads) k_lincomb(long n, LinComb c, Gate g) {
+  pdl_enter();
   if (!gate_open(g)) return;
   const int k = c.kptr ? *c.kptr : c.kfix;
   cplx y[MMAX];
@@ -499,7 +528,7 @@ __global__ void __launch_bounds__(kThreads) k_lincomb(long n, LinComb c, Gate g)
 }
 void launch_lincomb(const LaunchCfg& lc, long n, const LinComb& c, Gate g) {
   ++g_launch_count;
-  k_lincomb<<<blocks_for(lc, n), kThreads, 0, lc.stream>>>(n, c, g);
+  launch_k(k_lincomb, blocks_for(lc, n), kThreads, lc.stream, n, c, g);
 }
 
 // brk_stage 1: first-cycle early exit, x = 0 + Z0*y0 (k<=1)
@@ -507,6 +536,7 @@ void launch_lincomb(const LaunchCfg& lc, long n, const LinComb& c, Gate g) {
 __global__ void __launch_bounds__(kThreads) k_fg_finalize(long n, FgCtl* f, const cplx* __restrict__ Z0,
                                                             const cplx* __restrict__ Z1, cplx* x, Gate g,
                                                             int brk_stage) {
+  pdl_enter();
   if (!gate_open(g)) return;
   const int path = f->path, k = f->k, cyc = f->cycle;
   const cplx y0 = f->y[0], y1 = f->y[1];
@@ -531,7 +561,7 @@ __global__ void __launch_bounds__(kThreads) k_fg_finalize(long n, FgCtl* f, cons
 void launch_fg_finalize(const LaunchCfg& lc, long n, FgCtl* f, const cplx* Z0, const cplx* Z1, cplx* x, Gate g,
                         int brk_stage) {
   ++g_launch_count;
-  k_fg_finalize<<<blocks_for(lc, n), kThreads, 0, lc.stream>>>(n, f, Z0, Z1, x, g, brk_stage);
+  launch_k(k_fg_finalize, blocks_for(lc, n), kThreads, lc.stream, n, f, Z0, Z1, x, g, brk_stage);
 }
 
 // ---------------------------------------------------------------------------
@@ -546,6 +576,7 @@ __device__ __forceinline__ int coarse_n(int n) { return (n - 1) / 2 + 1; }
 
 __global__ void __launch_bounds__(kThreads) k_restrict(int n1f, int n2f, int n3f, int p0f, int q0, int nq,
                                                          const cplx* __restrict__ r, cplx* __restrict__ rc, Gate g) {
+  pdl_enter();
   // coarse planes [q0, q0 + nq) (rc points at plane q0); r points at fine plane p0f (halo at < 0)
   if (!gate_open(g)) return;
   const int n2c = coarse_n(n2f), n3c = coarse_n(n3f);
@@ -584,7 +615,7 @@ void launch_restrict(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cplx*
   ++g_launch_count;
   if (nq < 0) nq = (n1f - 1) / 2 + 1;
   const long Nc = (long)nq * ((n2f - 1) / 2 + 1) * ((n3f - 1) / 2 + 1);
-  k_restrict<<<blocks_for(lc, Nc), kThreads, 0, lc.stream>>>(n1f, n2f, n3f, p0f, q0, nq, r, rc, g);
+  launch_k(k_restrict, blocks_for(lc, Nc), kThreads, lc.stream, n1f, n2f, n3f, p0f, q0, nq, r, rc, g);
 }
 
 __device__ __forceinline__ int parents(int f, int* p, double& w) {
@@ -602,6 +633,7 @@ __device__ __forceinline__ int parents(int f, int* p, double& w) {
 
 __global__ void __launch_bounds__(kThreads) k_prolong_add(int n1f, int n2f, int n3f, int p0f, int nf, int q0c,
                                                             const cplx* __restrict__ ec, cplx* __restrict__ x, Gate g) {
+  pdl_enter();
   // fine planes [p0f, p0f + nf) (x points at plane p0f); ec points at coarse plane q0c
   if (!gate_open(g)) return;
   const int n2c = coarse_n(n2f), n3c = coarse_n(n3f);
@@ -628,33 +660,38 @@ void launch_prolong_add(const LaunchCfg& lc, int n1f, int n2f, int n3f, const cp
                         int nf, int q0c) {
   ++g_launch_count;
   if (nf < 0) nf = n1f;
-  k_prolong_add<<<blocks_for(lc, (long)nf * n2f * n3f), kThreads, 0, lc.stream>>>(n1f, n2f, n3f, p0f, nf, q0c, ec,
-                                                                                   x, g);
+  launch_k(k_prolong_add, blocks_for(lc, (long)nf * n2f * n3f), kThreads, lc.stream, n1f, n2f, n3f, p0f, nf, q0c,
+           ec, x, g);
 }
 
 // ---------------------------------------------------------------------------
 // gates and control initialisation (single thread)
 // ---------------------------------------------------------------------------
-__global__ void k_set_gate(int* dst, Gate g) { *dst = gate_open(g) ? 1 : 0; }
+__global__ void k_set_gate(int* dst, Gate g) {
+  pdl_enter();
+  *dst = gate_open(g) ? 1 : 0;
+}
 void launch_set_gate(cudaStream_t s, int* dst, Gate g) {
-  ++g_launch_count; k_set_gate<<<1, 1, 0, s>>>(dst, g); }
+  ++g_launch_count; launch_k(k_set_gate, 1, 1, s, dst, g); }
 
 __global__ void k_relax_init(RelaxCtl* c, int steps, Gate g) {
+  pdl_enter();
   if (!gate_open(g)) return;
   c->steps = steps;
   c->k = 0;
   c->cur = kStopped;
 }
 void launch_relax_init(cudaStream_t s, RelaxCtl* c, int steps, Gate g) {
-  ++g_launch_count; k_relax_init<<<1, 1, 0, s>>>(c, steps, g); }
+  ++g_launch_count; launch_k(k_relax_init, 1, 1, s, c, steps, g); }
 
 __global__ void k_fg_setup(FgCtl* f, double tol, Gate g) {
+  pdl_enter();
   if (!gate_open(g)) return;
   f->tol = tol;
   f->reo = 0;
 }
 void launch_fg_setup(cudaStream_t s, FgCtl* f, double tol, Gate g) {
-  ++g_launch_count; k_fg_setup<<<1, 1, 0, s>>>(f, tol, g); }
+  ++g_launch_count; launch_k(k_fg_setup, 1, 1, s, f, tol, g); }
 
 // ---------------------------------------------------------------------------
 // operator construction (setup; not on the solve's inner loop)

@@ -1,6 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -m gpu -x -q -k "cfg3 or upwind_vs_oracle" 2>&1 | tail -3
-timeout 900 python bench.py --steps 2 --warmup 3 --extra-3d 0 > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err
-tail -3 gpurun_out/bench_cfg3.err
-python -c "
-import json; d=json.load(open('gpurun_out/bench_cfg3.json')); c=d['config_3']; c.pop('t_krylov_ms',None); print(json.dumps(c)); print(d['value'], d['ms_per_step'])"
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for p in 1 0 1 0; do echo "pdl=$p: $(HADR_PDL=$p python tools/prof_solve.py --n 1025 --its 1000 2>&1 | tail -1)"; done
+for p in 1 0; do echo "cfg4 257 pdl=$p: $(HADR_PDL=$p HADR_WORKLOAD=cfg4 python tools/prof_solve.py --n 257 --its 1000 2>&1 | tail -1)"; done
+for p in 1 0; do echo "cfg3 1025 pdl=$p: $(HADR_PDL=$p HADR_WORKLOAD=cfg3 python tools/prof_solve.py --n 1025 --its 1000 2>&1 | tail -1)"; done
