@@ -130,8 +130,9 @@ void hadr_hier_destroy(hadr_hier h);
  * (mixed precision: K-cycle operators c64, vectors / reductions / outer FGMRES c128) */
 int hadr_set_option(const char* name, double value);
 /* cluster-engine phase counters (enable with hadr_set_option("ce_profile", 1)): cycles seen by CTA 0
- * [total, allreduce, n_allreduce, scalar epilogue, n_epilogue, stencil, n_stencil, launches] */
-int hadr_ce_profile(unsigned long long* out8, int reset);
+ * [total, allreduce, n, epilogue, n, stencil, n, launches, vector ops, n, barriers, n, transfers, n,
+ *  relaxation update, n] */
+int hadr_ce_profile(unsigned long long* out16, int reset);
 /* microbenchmark of the stencil kernel K1 on device vectors x, y: `reps` back-to-back launches timed
  * with CUDA events on the library stream; variant 0 = y = A x, 1 = the relaxation's fused
  * y = A(D^-1 s x) + basis write + <V0, y>.  *avg_ms = mean launch duration (incl. any finalize). */

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhadr.so")
+LIB_PATH = os.environ.get("HADR_LIB_PATH") or os.path.join(_HERE, "libhadr.so")
 
 HADR_OK, HADR_EVALUE, HADR_ERUNTIME, HADR_ECUDA = 0, 1, 2, 3
 

@@ -42,7 +42,7 @@ struct CEC {
 };
 
 // Phase profile of the engine (hadr_ce_profile): cycles seen by CTA 0 thread 0.
-__device__ unsigned long long g_ce_prof[8];
+__device__ unsigned long long g_ce_prof[16];
 struct CEProfScope {
   unsigned long long* p;
   int slot;
@@ -61,6 +61,12 @@ struct CEProfScope {
 __device__ __forceinline__ void ce_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
+// standalone barrier between vector ops (profiled as slot 10)
+#define CE_SYNC(c)                 \
+  do {                             \
+    CEProfScope prof_sync_(c, 10); \
+    ce_sync();                     \
+  } while (0)
 __device__ __forceinline__ double ce_remote(const double* p, unsigned rank) {
   unsigned long long in = reinterpret_cast<unsigned long long>(p), out;
   asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(in), "r"(rank));
@@ -217,6 +223,7 @@ __device__ __noinline__ void ce_stencil(CEC& c, const StencilDev& A, const cplx*
 // w -= h*v ; RED_DOT: <u, w> ; RED_NORM: ||w||^2
 template <int RED>
 __device__ void ce_axpy(CEC& c, long n, cplx* w, cplx h, const cplx* v, const cplx* u, double (&red)[2]) {
+  CEProfScope prof_(c, 8);
   red[0] = red[1] = 0.0;
   for (long k = c.gtid; k < n; k += c.gstride) {
     const cplx y = csub(ldm(w, k), cmul_np(h, ldm(v, k)));
@@ -232,6 +239,7 @@ __device__ void ce_axpy(CEC& c, long n, cplx* w, cplx h, const cplx* v, const cp
 }
 
 __device__ void ce_dot(CEC& c, long n, const cplx* u, const cplx* w, double (&red)[2]) {
+  CEProfScope prof_(c, 8);
   red[0] = red[1] = 0.0;
   for (long k = c.gtid; k < n; k += c.gstride) {
     const cplx uu = ldm(u, k), y = ldm(w, k);
@@ -242,6 +250,7 @@ __device__ void ce_dot(CEC& c, long n, const cplx* u, const cplx* w, double (&re
 
 // out = in * s (s < 0: copy) ; returns ||out||^2 partial
 __device__ double ce_scale(CEC& c, long n, const cplx* in, double s, bool scaled, cplx* out) {
+  CEProfScope prof_(c, 8);
   double r = 0.0;
   for (long k = c.gtid; k < n; k += c.gstride) {
     cplx y = ldm(in, k);
@@ -317,19 +326,21 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
   }
   // xo = x + dinv (.) (V[:k]^T y)
   const int k = R->k;
+  CEProfScope prof_lc_(c, 14);
   for (long p = c.gtid; p < n; p += c.gstride) {
     cplx t = mk(0.0, 0.0);
     for (int i = 0; i < k; ++i) t = cadd(t, cmul_np(ldm(L.V[i], p), R->y[i]));
     t = cmul_np(ldk(L.dinv, p), t);
     xo[p] = x ? cadd(ldm(x, p), t) : cadd(mk(0.0, 0.0), t);
   }
-  ce_sync();
+  CE_SYNC(c);
 }
 
 // ---------------------------------------------------------------------------
 // transfer operators (bit-exact orders, see kernels.cu)
 // ---------------------------------------------------------------------------
 __device__ __noinline__ void ce_restrict(CEC& c, int n1f, int n2f, int n3f, const cplx* r, cplx* rc) {
+  CEProfScope prof_(c, 12);
   const int n1c = (n1f - 1) / 2 + 1, n2c = (n2f - 1) / 2 + 1, n3c = (n3f - 1) / 2 + 1;
   const long Nc = (long)n1c * n2c * n3c;
   const int c3lo = n3f > 1 ? -1 : 0, c3hi = n3f > 1 ? 1 : 0;
@@ -372,6 +383,7 @@ __device__ __forceinline__ int ce_parents(int f, int* p, double& w) {
 }
 
 __device__ __noinline__ void ce_prolong_add(CEC& c, int n1f, int n2f, int n3f, const cplx* ec, cplx* x) {
+  CEProfScope prof_(c, 12);
   const int n2c = (n2f - 1) / 2 + 1, n3c = (n3f - 1) / 2 + 1;
   const int n23 = n2f * n3f;
   const long Nf = (long)n1f * n23;
@@ -488,11 +500,11 @@ __device__ void ce_inner(CEC& c, int ci) {
   }
   if (f->path == FG_ZERO) {
     for (long p = c.gtid; p < n; p += c.gstride) C.fx[p] = mk(0.0, 0.0);
-    ce_sync();
+    CE_SYNC(c);
     return;
   }
   ce_scale(c, n, C.fb, f->inv_r, true, C.fV0);
-  ce_sync();
+  CE_SYNC(c);
   ce_kcycle<D>(c, ci, C.fV0, C.fZ0);
   ce_arnoldi(c, f, C, 0, C.fZ0, C.fV0, nullptr);
   if (f->path == FG_BRK) {  // early exit after iteration 1: x = Z0 y0, r = b - A x
@@ -500,7 +512,7 @@ __device__ void ce_inner(CEC& c, int ci) {
     const cplx y0 = f->y[0];
     for (long p = c.gtid; p < n; p += c.gstride)
       C.fx[p] = (k >= 1) ? cadd(mk(0.0, 0.0), cmul_np(ldm(C.fZ0, p), y0)) : mk(0.0, 0.0);
-    ce_sync();
+    CE_SYNC(c);
     double red[3];
     ce_stencil<IN_PLAIN, OUT_RESID, RED_NORM>(c, C.A, C.fx, 1.0, nullptr, nullptr, C.fb, C.fr, nullptr, red);
     double v[1] = {red[0]};
@@ -514,7 +526,7 @@ __device__ void ce_inner(CEC& c, int ci) {
       ce_scale(c, n, C.fw, f->inv_w, true, C.fu);
     else
       ce_scale(c, n, C.fr, f->inv_r, true, C.fu);
-    ce_sync();
+    CE_SYNC(c);
     ce_kcycle<D>(c, ci, C.fu, C.fZ1);
     if (path == FG_CONT)
       ce_arnoldi(c, f, C, 1, C.fZ1, C.fV0, C.fu);
@@ -537,7 +549,7 @@ __device__ void ce_inner(CEC& c, int ci) {
       }
       C.fx[p] = out;
     }
-    ce_sync();
+    CE_SYNC(c);
   }
 }
 
@@ -551,16 +563,16 @@ __device__ void ce_kcycle(CEC& c, int l, const cplx* b, cplx* xo) {
     {
       double red[3];
       ce_stencil<IN_PLAIN, OUT_RESID, RED_NONE>(c, L.A, xo, 1.0, nullptr, nullptr, b, L.r, nullptr, red);
-      ce_sync();
+      CE_SYNC(c);
     }
     ce_restrict(c, L.A.n1, L.A.n2, L.A.n3, L.r, C.fb);
-    ce_sync();
+    CE_SYNC(c);
     if (l + 1 == S->nlev - 1)
       ce_relax(c, C, C.fb, nullptr, C.fx, S->coarse_steps);
     else
       ce_inner<D + 1>(c, l + 1);
     ce_prolong_add(c, L.A.n1, L.A.n2, L.A.n3, C.fx, xo);
-    ce_sync();
+    CE_SYNC(c);
     ce_relax(c, L, b, xo, xo, L.s);
   }
 }
@@ -609,10 +621,10 @@ __global__ void __launch_bounds__(CE_THREADS, 1)
 }
 
 int ce_profile_read(unsigned long long* out, int reset) {
-  cudaError_t e = cudaMemcpyFromSymbol(out, g_ce_prof, sizeof(unsigned long long) * 8);
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_ce_prof, sizeof(unsigned long long) * 16);
   if (e != cudaSuccess) return (int)e;
   if (reset) {
-    unsigned long long z[8] = {0};
+    unsigned long long z[16] = {0};
     e = cudaMemcpyToSymbol(g_ce_prof, z, sizeof(z));
   }
   return (int)e;

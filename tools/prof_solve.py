@@ -67,14 +67,17 @@ def ce_breakdown(n=1025, its=1000):
 
     L = _lib.lib()
     _lib.set_option("ce_profile", 1)
-    out = (C.c_ulonglong * 8)()
+    out = (C.c_ulonglong * 16)()
     L.hadr_ce_profile(out, 1)
     sys.argv = [sys.argv[0], "--n", str(n), "--its", str(its), "--warm", "0"]
     main()
     L.hadr_ce_profile(out, 1)
-    tot, ar, nar, ep, nep, st, nst, launches = list(out)
-    print(f"CE launches={launches} total={tot/1.9e3:.0f}us  allreduce={ar/1.9e3:.0f}us n={nar} ({ar/max(nar,1)/1.9:.0f} ns/op)  "
-          f"epilogue={ep/1.9e3:.0f}us n={nep} ({ep/max(nep,1)/1.9:.0f} ns)  stencil={st/1.9e3:.0f}us n={nst} ({st/max(nst,1)/1.9:.0f} ns)")
+    v = list(out)
+    f = 1.9e3  # cycles per us
+    print(f"CE launches={v[7]} total={v[0]/f:.0f}us")
+    for name, i in (("allreduce", 1), ("epilogue", 3), ("stencil", 5), ("vector ops", 8), ("barriers", 10),
+                    ("transfers", 12), ("relax update", 14)):
+        print(f"  {name:13s} {v[i]/f:9.0f} us  n={v[i+1]:7d}  {v[i]/max(v[i+1],1)/1.9:7.0f} ns/op")
 
 
 def sweep_ce(n=1025, values=(0, 32768, 70000, 270000)):
