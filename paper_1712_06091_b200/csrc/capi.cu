@@ -498,10 +498,10 @@ int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, 
   });
 }
 
-int hadr_ce_profile(unsigned long long* out8, int reset) {
+int hadr_ce_profile(unsigned long long* out16, int reset) {
   return guarded([&] {
     Ctx::get().sync();
-    if (ce_profile_read(out8, reset)) throw std::runtime_error("ce_profile_read failed");
+    if (ce_profile_read(out16, reset)) throw std::runtime_error("ce_profile_read failed");
   });
 }
 
