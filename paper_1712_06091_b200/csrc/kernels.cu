@@ -343,6 +343,161 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(StencilArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1 tiled: the same stencil with the (transformed) input staged in shared memory.
+// A block owns a tile of tp planes x ty rows x tx columns (3D: 2 x 4 x 32, 2D:
+// 8 x 32) and stages it with a 2-point halo on every stencilled axis, applying
+// the scale / D^-1 transform once per staged point.  Neighbour reads are LDS;
+// the coefficient planes stream from HBM exactly once.  Arithmetic and
+// accumulation order are identical to k_stencil (bit-identical outputs).
+// ---------------------------------------------------------------------------
+struct TileCfg {
+  int tp, ty, tx, hy;    // tile extents, halo rows (2 in 3D, 0 in 2D)
+  int ntp, nty, ntx;     // tile counts per axis
+};
+
+template <int CH, bool C32>
+__device__ __forceinline__ void tile_chunk(const StencilArgs& a, const cplx* tl, int o0, int nofs, long k, int i1,
+                                           int i2, int i3, int n1, int n2, int n3, long N, int tidx, int sP, int sY,
+                                           bool d3, cplx& acc) {
+  cplx cv[CH];
+  int ti[CH];
+  bool ok[CH];
+#pragma unroll
+  for (int q = 0; q < CH; ++q) {
+    const int o = o0 + q;
+    const bool live = o < nofs;
+    const int oo = live ? o : 0;
+    const int d1 = a.A.d1[oo], d2 = a.A.d2[oo], dd3 = a.A.d3[oo];
+    const int j1 = i1 + d1, j2 = i2 + d2, j3 = i3 + dd3;
+    ok[q] = live && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2 && j3 >= 0 && j3 < n3;
+    ti[q] = ok[q] ? tidx + d1 * sP + (d3 ? d2 * sY + dd3 : d2) : tidx;
+    cv[q] = C32 ? ld_c64(a.A, live ? (long)o * N + k : k) : ldc(a.A.coef, live ? (long)o * N + k : k);
+  }
+#pragma unroll
+  for (int q = 0; q < CH; ++q) {
+    const cplx t = cadd(acc, cmul_sp(cv[q], tl[ti[q]]));
+    acc = ok[q] ? t : acc;
+  }
+}
+
+template <int INM, int OUTM, int RED, int NO>
+__global__ void __launch_bounds__(kThreads, 4) k_stencil_tile(StencilArgs a, TileCfg t) {
+  pdl_enter();
+  if (!gate_open(a.gate)) return;
+  extern __shared__ cplx tl[];
+  const int n1 = a.A.n1, n2 = a.A.n2, n3 = a.A.n3, nofs = a.A.nofs;
+  const long N = a.A.pstride;
+  const int n1own = a.A.n1own, p0 = a.A.p0;
+  const bool d3 = n3 > 1;
+  const int nY = d3 ? n2 : 1, nX = d3 ? n3 : n2;
+  const double s = (INM & IN_SCALE) ? *a.scale : 1.0;
+  const bool c32 = a.A.coef32 != nullptr;
+  const int sY = t.tx + 4, sP = (t.ty + 2 * t.hy) * sY, tsize = (t.tp + 4) * sP;
+  const long ntiles = (long)t.ntp * t.nty * t.ntx;
+  const int px = threadIdx.x % t.tx, py = (threadIdx.x / t.tx) % t.ty, pp = threadIdx.x / (t.tx * t.ty);
+  constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & (RED_DOT | RED_DOT_CENTER)) ? 2 : 0);
+  double red[NV > 0 ? NV : 1];
+#pragma unroll
+  for (int q = 0; q < (NV > 0 ? NV : 1); ++q) red[q] = 0.0;
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int bx = (int)(tile % t.ntx), by = (int)((tile / t.ntx) % t.nty), bp = (int)(tile / ((long)t.ntx * t.nty));
+    const int P0 = bp * t.tp, Y0 = by * t.ty, X0 = bx * t.tx;
+    for (int e = threadIdx.x; e < tsize; e += blockDim.x) {
+      const int ep = e / sP, r = e - ep * sP, ey = r / sY, ex = r - ey * sY;
+      const int gp = P0 - 2 + ep, gy = Y0 - t.hy + ey, gx = X0 - 2 + ex;
+      cplx v = mk(0.0, 0.0);
+      if (gp + p0 >= 0 && gp + p0 < n1 && gp < n1own + 2 && gy >= 0 && gy < nY && gx >= 0 && gx < nX) {
+        const long kk = ((long)gp * nY + gy) * nX + gx;
+        v = ldc(a.x, kk);
+        if (INM & IN_SCALE) v = cscale(v, s);
+        if (INM & IN_JAC) v = cmul_np(ldc(a.dinv, kk), v);
+      }
+      tl[e] = v;
+    }
+    __syncthreads();
+    const int il = P0 + pp, y = Y0 + py, x = X0 + px;
+    if (pp < t.tp && il < n1own && y < nY && x < nX) {
+      const long k = ((long)il * nY + y) * nX + x;
+      const int i1 = il + p0, i2 = d3 ? y : x, i3 = d3 ? x : 0;
+      const int tidx = (pp + 2) * sP + (py + t.hy) * sY + (px + 2);
+      cplx acc = mk(0.0, 0.0);
+      if constexpr (NO > 0) {
+        if (c32)
+          tile_chunk<NO, true>(a, tl, 0, nofs, k, i1, i2, i3, n1, n2, n3, N, tidx, sP, sY, d3, acc);
+        else
+          tile_chunk<NO, false>(a, tl, 0, nofs, k, i1, i2, i3, n1, n2, n3, N, tidx, sP, sY, d3, acc);
+      } else {
+        for (int o0 = 0; o0 < nofs; o0 += 9) {
+          if (c32)
+            tile_chunk<9, true>(a, tl, o0, nofs, k, i1, i2, i3, n1, n2, n3, N, tidx, sP, sY, d3, acc);
+          else
+            tile_chunk<9, false>(a, tl, o0, nofs, k, i1, i2, i3, n1, n2, n3, N, tidx, sP, sY, d3, acc);
+        }
+      }
+      cplx vc = mk(0.0, 0.0);
+      if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) {
+        vc = ldc(a.x, k);
+        if (INM & IN_SCALE) vc = cscale(vc, s);
+        if (INM & IN_WRITEV) a.vout[k] = vc;
+      }
+      cplx yv = (OUTM == OUT_RESID) ? csub(ldc(a.b, k), acc) : acc;
+      a.y[k] = yv;
+      if (RED & RED_NORM) red[0] += yv.x * yv.x + yv.y * yv.y;
+      if (RED & (RED_DOT | RED_DOT_CENTER)) {
+        const cplx u = (RED & RED_DOT_CENTER) ? vc : ldc(a.u, k);
+        constexpr int o = (RED & RED_NORM) ? 1 : 0;
+        red[o] += u.x * yv.x + u.y * yv.y;
+        red[o + 1] += u.x * yv.y - u.y * yv.x;
+      }
+    }
+    __syncthreads();  // the tile is restaged for the next tile
+  }
+  if constexpr (NV > 0) {
+    double v[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v[q] = red[q];
+    finish<NV, 0>(v, a.rs, a.epi);
+  }
+}
+
+int g_stencil_tile = 1;  // option "stencil_tile": 0 off, 1 policy (2D wide stencils), 2 always
+
+template <int INM, int OUTM, int RED, int NO>
+static void launch_tile_no(const LaunchCfg& lc, const StencilArgs& a, const TileCfg& t, int blocks) {
+  const size_t smem = (size_t)(t.tp + 4) * (t.ty + 2 * t.hy) * (t.tx + 4) * sizeof(cplx);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = lc.stream;
+  cudaLaunchAttribute at[1];
+  cfg.numAttrs = pdl_attr(at);
+  cfg.attrs = at;
+  cudaLaunchKernelEx(&cfg, k_stencil_tile<INM, OUTM, RED, NO>, a, t);
+}
+
+template <int INM, int OUTM, int RED>
+static void dispatch_tile(const LaunchCfg& lc, const StencilArgs& a, const TileCfg& t, int blocks) {
+  const int n = a.A.nofs;
+  if (n == 5)
+    launch_tile_no<INM, OUTM, RED, 5>(lc, a, t, blocks);
+  else if (n == 9)
+    launch_tile_no<INM, OUTM, RED, 9>(lc, a, t, blocks);
+  else if (n == 21)
+    launch_tile_no<INM, OUTM, RED, 21>(lc, a, t, blocks);
+  else if (n <= 7)
+    launch_tile_no<INM, OUTM, RED, 7>(lc, a, t, blocks);
+  else if (n <= 13)
+    launch_tile_no<INM, OUTM, RED, 13>(lc, a, t, blocks);
+  else if (n <= 25)
+    launch_tile_no<INM, OUTM, RED, 25>(lc, a, t, blocks);
+  else
+    launch_tile_no<INM, OUTM, RED, 0>(lc, a, t, blocks);
+  constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & (RED_DOT | RED_DOT_CENTER)) ? 2 : 0);
+  if constexpr (NV > 0) launch_finalize<NV>(lc, Geo{blocks, 0}, a.gate, a.rs, a.epi);
+}
+
 template <int INM, int OUTM, int RED, int NO>
 static void launch_stencil_no(const LaunchCfg& lc, const StencilArgs& a, const Geo& geo) {
   if (geo.cluster)
@@ -377,6 +532,37 @@ void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const Stenc
   const long N = (long)a.A.n1own * a.A.n2 * a.A.n3;  // points computed (owned slab)
   const Geo geo = red ? geo_for(lc, N) : Geo{blocks_for(lc, N), 0};
   constexpr int J = IN_SCALE | IN_JAC | IN_WRITEV;
+  // tiled kernel where it measured faster (B200): 2D operators with wide (Galerkin)
+  // stencils; the 3D and 9-point fine-level sweeps keep the flat kernel, whose
+  // neighbour re-reads L1 already absorbs (tools/prof_solve.py A/B)
+  if (g_stencil_tile && !geo.cluster && a.A.n1own >= 2 &&
+      (g_stencil_tile > 1 || (a.A.n3 == 1 && a.A.nofs > 9))) {
+    const bool d3 = a.A.n3 > 1;
+    TileCfg t{};
+    t.tp = d3 ? 2 : 8;
+    t.ty = d3 ? 4 : 1;
+    t.tx = d3 ? 32 : 32;
+    t.hy = d3 ? 2 : 0;
+    const int nY = d3 ? a.A.n2 : 1, nX = d3 ? a.A.n3 : a.A.n2;
+    t.ntp = (a.A.n1own + t.tp - 1) / t.tp;
+    t.nty = (nY + t.ty - 1) / t.ty;
+    t.ntx = (nX + t.tx - 1) / t.tx;
+    const long ntiles = (long)t.ntp * t.nty * t.ntx;
+    const int blocks = (int)(ntiles < lc.max_blocks ? ntiles : lc.max_blocks);
+#define HADR_TCASE(I, O, R)                          \
+  if (inm == (I) && outm == (O) && red == (R)) {     \
+    dispatch_tile<I, O, R>(lc, a, t, blocks);        \
+    return;                                          \
+  }
+    HADR_TCASE(IN_PLAIN, OUT_APPLY, RED_NONE)
+    HADR_TCASE(IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT)
+    HADR_TCASE(IN_PLAIN, OUT_RESID, RED_NONE)
+    HADR_TCASE(IN_PLAIN, OUT_RESID, RED_NORM)
+    HADR_TCASE(J, OUT_APPLY, RED_DOT_CENTER)
+    HADR_TCASE(J, OUT_APPLY, RED_DOT)
+    HADR_TCASE(IN_JAC, OUT_APPLY, RED_NONE)
+#undef HADR_TCASE
+  }
 #define HADR_CASE(I, O, R)                       \
   if (inm == (I) && outm == (O) && red == (R)) { \
     dispatch_no<I, O, R>(lc, a, geo);            \

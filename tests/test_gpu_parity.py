@@ -52,6 +52,22 @@ def test_spmv_bitexact(hadr, g33, key):
     assert (abs(B - A)).max() == 0
 
 
+@pytest.mark.parametrize("tile", [0, 2])
+def test_stencil_kernels_bitexact_2d(hadr, g65, tile):
+    """Flat and shared-memory-tiled stencil kernels (stencil_tile 0 / 2) reproduce
+    csr_matvec bit for bit on the fine 9-offset and the coarse 21-offset operators."""
+    hadr._lib.set_option("stencil_tile", tile)
+    try:
+        rng = np.random.default_rng(11)
+        for key, shape in (("blend", (65, 65)), ("lev1", (33, 33))):
+            A = csr_from(g65, key)
+            op = hadr.StencilOperator.from_csr(A, shape)
+            x = rng.standard_normal(A.shape[0]) + 1j * rng.standard_normal(A.shape[0])
+            assert np.array_equal(op @ x, A @ x), key
+    finally:
+        hadr._lib.set_option("stencil_tile", 1)
+
+
 def test_spmv_golden(hadr, g65):
     A = csr_from(g65, "blend")
     op = hadr.StencilOperator.from_csr(A, _shape(g65))

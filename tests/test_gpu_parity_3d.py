@@ -59,6 +59,30 @@ def test_spmv_and_transfer_bitexact_3d(hadr, case3d):
     assert np.array_equal(op1 @ x1, A1 @ x1)
 
 
+@pytest.mark.parametrize("tile", [0, 2])
+def test_stencil_kernels_bitexact_3d(hadr, case3d, tile):
+    """Flat and shared-memory-tiled stencil kernels (option stencil_tile 0 / 2 = always)
+    both reproduce csr_matvec bit for bit, fine 13-offset and coarse 81-offset."""
+    from oracle import hadr_oracle as O
+
+    hadr._lib.set_option("stencil_tile", tile)
+    hadr._lib.set_option("ce_max_n", 0)
+    try:
+        rng = np.random.default_rng(7)
+        for l in (0, 1):
+            A = case3d["Hi"].ops[l] if l else case3d["H2"]
+            op = hadr.StencilOperator.from_csr(A, case3d["Hi"].shapes[l])
+            x = rng.standard_normal(A.shape[0]) + 1j * rng.standard_normal(A.shape[0])
+            assert np.array_equal(op @ x, A @ x), l
+        Hi = case3d["Hi"]
+        H = hadr.hierarchy_from_ops(Hi.ops, shapes=Hi.shapes)
+        b = rng.standard_normal(Hi.ops[0].shape[0]) + 1j * rng.standard_normal(Hi.ops[0].shape[0])
+        assert rel(hadr.make_kcycle_preconditioner(H)(b), O.kcycle(Hi, 1, b, np.zeros_like(b))) <= 1e-12
+    finally:
+        hadr._lib.set_option("stencil_tile", 1)
+        hadr._lib.set_option("ce_max_n", 32768)
+
+
 def test_device_assembly_3d(hadr, case3d):
     from paper_1712_06091_b200 import operators
 
