@@ -512,6 +512,13 @@ int hadr_set_option(const char* name, double value) {
       g_ce_prof_on = value != 0.0;
     } else if (n == "kcycle_c64") {
       g_kcycle_c64 = value != 0.0;
+    } else if (n == "ce_smem_relax") {
+      g_ce_smem_relax = value != 0.0;
+      for (;;) {
+        Hier* h = hier_pool_pop();
+        if (!h) break;
+        delete h;
+      }
     } else if (n == "stencil_tile") {
       g_stencil_tile = (int)value;
       for (;;) {

@@ -337,6 +337,197 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
 }
 
 // ---------------------------------------------------------------------------
+// The same relaxation with every vector of it in shared memory: CTA r keeps its
+// own rows of the basis V[0..s] and of the Arnoldi vector w (double-buffered);
+// the stencil input tile takes its halo rows from the neighbouring CTAs' w over
+// DSMEM.  Only the right-hand side, the starting guess and the result touch
+// global memory.  Element formulas are those of ce_relax (the reductions sum in
+// a different order: rounding-level differences only).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ cplx ce_remote_c(const cplx* p, unsigned rank) {
+  unsigned long long in = reinterpret_cast<unsigned long long>(p), out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(in), "r"(rank));
+  return *reinterpret_cast<const cplx*>(out);
+}
+
+template <int NO, bool C32>
+__device__ __forceinline__ void sm_stencil_rows(CEC& c, const StencilDev& A, const cplx* tile, int r0, int r1,
+                                                int t0, cplx* w, const cplx* v0, double (&red)[2]) {
+  const int n1 = A.n1, n2 = A.n2, n3 = A.n3, nofs = A.nofs;
+  const int n23 = n2 * n3;
+  const long N = (long)n1 * n23;
+  const long own0 = (long)r0 * n23, own1 = (long)r1 * n23;
+  for (long k = own0 + threadIdx.x; k < own1; k += blockDim.x) {
+    const int i1 = (int)(k / n23);
+    const int rem = (int)(k - (long)i1 * n23);
+    const int i2 = rem / n3, i3 = rem - (rem / n3) * n3;
+    cplx acc = mk(0.0, 0.0);
+    constexpr int CH = NO > 0 ? NO : 9;
+    const int nch = NO > 0 ? 1 : (nofs + CH - 1) / CH;
+    for (int ch = 0; ch < nch; ++ch) {
+      const int o0 = ch * CH;
+      cplx cv[CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int o = o0 + q;
+        const long ci = o < nofs ? (long)o * N + k : k;
+        cv[q] = C32 ? ld_c64(A, ci) : ldk(A.coef, ci);
+      }
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int o = o0 + q;
+        const int oo = o < nofs ? o : 0;
+        const int j1 = i1 + A.d1[oo], j2 = i2 + A.d2[oo], j3 = i3 + A.d3[oo];
+        const bool ok = o < nofs && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2 && j3 >= 0 && j3 < n3;
+        const cplx v = tile[ok ? ((long)(j1 - t0) * n2 + j2) * n3 + j3 : 0];
+        const cplx t = cadd(acc, cmul_sp(cv[q], v));
+        acc = ok ? t : acc;
+      }
+    }
+    const long p = k - own0;
+    w[p] = acc;
+    const cplx u = v0[p];
+    red[0] += u.x * acc.x + u.y * acc.y;
+    red[1] += u.x * acc.y - u.y * acc.x;
+  }
+}
+
+__device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b, const cplx* x, cplx* xo, int s) {
+  RelaxCtl* R = &c.S->rc;
+  const int n1 = L.A.n1, n23 = L.A.n2 * L.A.n3;
+  const int rows = (n1 + (int)c.C - 1) / (int)c.C;
+  const int r0 = min(n1, (int)c.rank * rows), r1 = min(n1, r0 + rows);
+  const int t0 = max(0, r0 - 2), t1 = min(n1, r1 + 2);
+  const long np = (long)(r1 - r0) * n23, own0 = (long)r0 * n23;
+  const long rs = (long)rows * n23;  // per-buffer stride (same layout in every CTA)
+  cplx* tile = ce_tile;                        // (rows + 4) * n23
+  cplx* Vb = ce_tile + (long)(rows + 4) * n23;  // V[i] = Vb + i * rs, i <= s
+  cplx* wb = Vb + (long)(s + 1) * rs;           // w[0], w[1]
+  if (threadIdx.x == 0) {
+    R->steps = s;
+    R->k = 0;
+    R->cur = kStopped;
+  }
+  {
+    double v[1];
+    const cplx* src = b;
+    if (x) {
+      double red[3];
+      ce_stencil<IN_PLAIN, OUT_RESID, RED_NORM>(c, L.A, x, 1.0, nullptr, nullptr, b, L.w[1], nullptr, red);
+      v[0] = red[0];
+      src = L.w[1];  // written by this CTA's own rows (row partition of ce_stencil)
+    }
+    double nn = 0.0;
+    for (long p = threadIdx.x; p < np; p += blockDim.x) {
+      const cplx y = ldm(src, own0 + p);
+      wb[rs + p] = y;  // w[1] = r : the "previous" buffer of step 0
+      nn += y.x * y.x + y.y * y.y;
+    }
+    if (!x) v[0] = nn;
+    ce_allreduce<1>(c, v);
+    if (threadIdx.x == 0) relax_beta(R, v[0]);
+    __syncthreads();
+  }
+  for (int j = 0; j < s; ++j) {
+    if (R->cur != j) break;
+    const double sc = (j == 0) ? R->inv_beta : R->inv_hn;
+    cplx* wp = wb + (long)((j + 1) % 2) * rs;  // previous Arnoldi vector (step 0: r)
+    cplx* w = wb + (long)(j % 2) * rs;
+    cplx* Vj = Vb + (long)j * rs;
+    {
+      CEProfScope prof_(c, 5);
+      // V[j] = wp * sc (own rows); tile = D^-1 (.) (wp * sc) on rows [t0, t1)
+      const long tn = (long)(t1 - t0) * n23;
+      for (long q = threadIdx.x; q < tn; q += blockDim.x) {
+        const int row = t0 + (int)(q / n23);
+        const long col = q - (long)(row - t0) * n23;
+        cplx v;
+        if (row >= r0 && row < r1) {
+          v = cscale(wp[(long)(row - r0) * n23 + col], sc);
+          Vj[(long)(row - r0) * n23 + col] = v;
+        } else {  // halo row owned by a neighbouring CTA: its previous w over DSMEM
+          const int owner = row / rows;
+          const cplx* rw = wb + (long)((j + 1) % 2) * rs + (long)(row - owner * rows) * n23 + col;
+          v = cscale(ce_remote_c(rw, owner), sc);
+        }
+        tile[q] = cmul_np(ldk(L.dinv, (long)row * n23 + col), v);
+      }
+      __syncthreads();
+      double red[2] = {0.0, 0.0};
+      const cplx* V0 = Vb;
+      if (L.A.coef32) {
+        if (L.A.nofs == 21)
+          sm_stencil_rows<21, true>(c, L.A, tile, r0, r1, t0, w, V0, red);
+        else
+          sm_stencil_rows<0, true>(c, L.A, tile, r0, r1, t0, w, V0, red);
+      } else {
+        switch (L.A.nofs) {
+          case 5: sm_stencil_rows<5, false>(c, L.A, tile, r0, r1, t0, w, V0, red); break;
+          case 9: sm_stencil_rows<9, false>(c, L.A, tile, r0, r1, t0, w, V0, red); break;
+          case 21: sm_stencil_rows<21, false>(c, L.A, tile, r0, r1, t0, w, V0, red); break;
+          default: sm_stencil_rows<0, false>(c, L.A, tile, r0, r1, t0, w, V0, red); break;
+        }
+      }
+      double v[2] = {red[0], red[1]};
+      ce_allreduce<2>(c, v);
+      if (threadIdx.x == 0) R->H[0 * RMAX + j] = mk(v[0], v[1]);
+      __syncthreads();
+    }
+    for (int i = 0; i < j; ++i) {
+      const cplx h = R->H[i * RMAX + j];
+      const cplx* Vi = Vb + (long)i * rs;
+      const cplx* Vi1 = Vb + (long)(i + 1) * rs;
+      double v[2] = {0.0, 0.0};
+      for (long p = threadIdx.x; p < np; p += blockDim.x) {
+        const cplx y = csub(w[p], cmul_np(h, Vi[p]));
+        w[p] = y;
+        const cplx uu = Vi1[p];
+        v[0] += uu.x * y.x + uu.y * y.y;
+        v[1] += uu.x * y.y - uu.y * y.x;
+      }
+      ce_allreduce<2>(c, v);
+      if (threadIdx.x == 0) R->H[(i + 1) * RMAX + j] = mk(v[0], v[1]);
+      __syncthreads();
+    }
+    {
+      const cplx h = R->H[j * RMAX + j];
+      double v[1] = {0.0};
+      for (long p = threadIdx.x; p < np; p += blockDim.x) {
+        const cplx y = csub(w[p], cmul_np(h, Vj[p]));
+        w[p] = y;
+        v[0] += y.x * y.x + y.y * y.y;
+      }
+      ce_allreduce<1>(c, v);
+      {
+        CEProfScope prof_(c, 3);
+        if (threadIdx.x == 0) relax_step_sm(R, j, v[0]);
+        __syncthreads();
+      }
+    }
+  }
+  // xo = x + dinv (.) (V[:k]^T y)   (own rows)
+  const int k = R->k;
+  {
+    CEProfScope prof_lc_(c, 14);
+    for (long p = threadIdx.x; p < np; p += blockDim.x) {
+      cplx t = mk(0.0, 0.0);
+      for (int i = 0; i < k; ++i) t = cadd(t, cmul_np(Vb[(long)i * rs + p], R->y[i]));
+      t = cmul_np(ldk(L.dinv, own0 + p), t);
+      xo[own0 + p] = x ? cadd(ldm(x, own0 + p), t) : cadd(mk(0.0, 0.0), t);
+    }
+  }
+  CE_SYNC(c);
+}
+
+__device__ __forceinline__ void ce_relax_any(CEC& c, const CELevel& L, const cplx* b, const cplx* x, cplx* xo,
+                                             int s) {
+  if (L.smr)
+    ce_relax_sm(c, L, b, x, xo, s);
+  else
+    ce_relax(c, L, b, x, xo, s);
+}
+
+// ---------------------------------------------------------------------------
 // transfer operators (bit-exact orders, see kernels.cu)
 // ---------------------------------------------------------------------------
 __device__ __noinline__ void ce_restrict(CEC& c, int n1f, int n2f, int n3f, const cplx* r, cplx* rc) {
@@ -559,7 +750,7 @@ __device__ void ce_kcycle(CEC& c, int l, const cplx* b, cplx* xo) {
     CEShared* S = c.S;
     const CELevel& L = S->lv[l];
     const CELevel& C = S->lv[l + 1];
-    ce_relax(c, L, b, nullptr, xo, L.s);
+    ce_relax_any(c, L, b, nullptr, xo, L.s);
     {
       double red[3];
       ce_stencil<IN_PLAIN, OUT_RESID, RED_NONE>(c, L.A, xo, 1.0, nullptr, nullptr, b, L.r, nullptr, red);
@@ -568,12 +759,12 @@ __device__ void ce_kcycle(CEC& c, int l, const cplx* b, cplx* xo) {
     ce_restrict(c, L.A.n1, L.A.n2, L.A.n3, L.r, C.fb);
     CE_SYNC(c);
     if (l + 1 == S->nlev - 1)
-      ce_relax(c, C, C.fb, nullptr, C.fx, S->coarse_steps);
+      ce_relax_any(c, C, C.fb, nullptr, C.fx, S->coarse_steps);
     else
       ce_inner<D + 1>(c, l + 1);
     ce_prolong_add(c, L.A.n1, L.A.n2, L.A.n3, C.fx, xo);
     CE_SYNC(c);
-    ce_relax(c, L, b, xo, xo, L.s);
+    ce_relax_any(c, L, b, xo, xo, L.s);
   }
 }
 
@@ -611,7 +802,7 @@ __global__ void __launch_bounds__(CE_THREADS, 1)
     ce_inner<0>(c, l0);
   } else {
     const CELevel& C = S.lv[l0];
-    ce_relax(c, C, C.fb, nullptr, C.fx, S.coarse_steps);
+    ce_relax_any(c, C, C.fb, nullptr, C.fx, S.coarse_steps);
   }
   ce_sync();  // no CTA exits while another may still read its shared memory
   if (c.prof) {

@@ -13,8 +13,8 @@ struct CELevel {
   StencilDev A;
   const cplx* dinv;
   long N;
-  int s;  // relaxation length
-  int pad_;
+  int s;    // relaxation length
+  int smr;  // 1: the relaxation runs out of shared memory (ce_relax_sm; see ce_relax_sm_bytes)
   cplx* r;
   cplx* V[RMAX + 1];
   cplx* w[2];
@@ -40,5 +40,12 @@ void launch_cluster_engine(cudaStream_t s, const CEDesc* d, int mode, int l0, co
 inline size_t ce_tile_bytes(int n1, int n2, int ctas) {
   return (size_t)((n1 + ctas - 1) / ctas + 4) * n2 * sizeof(cplx);
 }
+// shared-memory relaxation of a level with n1 rows of n23 points and s steps: per CTA the
+// input tile (rows + 4 halo rows), the basis V[0..s] and two w buffers of its own rows
+inline size_t ce_relax_sm_bytes(int n1, long n23, int s, int ctas) {
+  const long rows = (n1 + ctas - 1) / ctas;
+  return (size_t)(rows * (s + 3) + rows + 4) * n23 * sizeof(cplx);
+}
+constexpr size_t CE_SMEM_BUDGET = 190 * 1024;  // dynamic shared memory the engine may request
 
 }  // namespace hadr

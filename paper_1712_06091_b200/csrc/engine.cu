@@ -652,9 +652,20 @@ Hier::~Hier() {
   dfree(ce_desc);
 }
 
+int g_ce_smem_relax = 1;
+
+// the level's relaxation fits the engine's shared memory (ce_relax_sm)
+static bool level_smr(const Level& L) {
+  return g_ce_smem_relax && !L.dist &&
+         ce_relax_sm_bytes(L.n1, (long)L.n2 * L.n3, L.s, CE_CTAS) <= CE_SMEM_BUDGET;
+}
+
 size_t Hier::ce_tile(int li) const {
-  size_t m = 0;  // the engine touches levels li .. coarsest; the finest of them is the largest
-  for (int i = li; i < (int)lv.size(); ++i) m = std::max(m, ce_tile_bytes(lv[i].n1, lv[i].n2 * lv[i].n3, CE_CTAS));
+  size_t m = 0;  // the engine touches levels li .. coarsest
+  for (int i = li; i < (int)lv.size(); ++i) {
+    m = std::max(m, ce_tile_bytes(lv[i].n1, lv[i].n2 * lv[i].n3, CE_CTAS));
+    if (level_smr(lv[i])) m = std::max(m, ce_relax_sm_bytes(lv[i].n1, (long)lv[i].n2 * lv[i].n3, lv[i].s, CE_CTAS));
+  }
   return m;
 }
 
@@ -729,6 +740,7 @@ void Hier::alloc_workspace() {
       d.dinv = L.dinv;
       d.N = L.N;
       d.s = L.s;
+      d.smr = level_smr(L) ? 1 : 0;
       d.r = L.r;
       for (int j = 0; j <= RMAX; ++j) d.V[j] = L.V[j];
       d.w[0] = L.w[0];

@@ -149,6 +149,7 @@ struct Hier {
 // runtime options (hadr_set_option)
 extern long g_ce_max_n;  // levels with N <= this run inside the cluster engine (0 disables)
 extern int g_kcycle_c64; // build hierarchies with complex64 operator storage (mixed-precision K-cycle)
+extern int g_ce_smem_relax;  // engine relaxations out of shared memory where they fit
 
 Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol);
 void hier_release(Hier* h);  // recycle (workspace + captured graphs) or delete

@@ -102,13 +102,16 @@ def test_galerkin_device(hadr, case, request):
         assert err <= 1e-12 * abs(ref).max(), (l, err)
 
 
-@pytest.fixture(params=["cluster", "graph"])
+@pytest.fixture(params=["cluster", "cluster_gmem", "graph"])
 def engine(request, hadr):
-    """Run a test with the coarse levels in the single-cluster engine (default)
+    """Run a test with the coarse levels in the single-cluster engine (default: relaxations
+    out of shared memory where they fit), in the engine with global-memory relaxations,
     and with every operation as its own kernel (ce_max_n = 0)."""
-    hadr._lib.set_option("ce_max_n", 32768 if request.param == "cluster" else 0)
+    hadr._lib.set_option("ce_max_n", 0 if request.param == "graph" else 32768)
+    hadr._lib.set_option("ce_smem_relax", 0 if request.param == "cluster_gmem" else 1)
     yield request.param
     hadr._lib.set_option("ce_max_n", 32768)
+    hadr._lib.set_option("ce_smem_relax", 1)
 
 
 @pytest.mark.parametrize("case", ["g33", "g65"])

@@ -103,11 +103,12 @@ def test_galerkin_3d(hadr, case3d):
         assert err <= 1e-12 * abs(ref).max(), (l, err)
 
 
-@pytest.mark.parametrize("engine", ["cluster", "graph"])
+@pytest.mark.parametrize("engine", ["cluster", "cluster_gmem", "graph"])
 def test_kcycle_3d(hadr, case3d, engine):
     from oracle import hadr_oracle as O
 
-    hadr._lib.set_option("ce_max_n", 32768 if engine == "cluster" else 0)
+    hadr._lib.set_option("ce_max_n", 0 if engine == "graph" else 32768)
+    hadr._lib.set_option("ce_smem_relax", 0 if engine == "cluster_gmem" else 1)
     try:
         Hi = case3d["Hi"]
         H = hadr.hierarchy_from_ops(Hi.ops, shapes=Hi.shapes)
@@ -119,6 +120,7 @@ def test_kcycle_3d(hadr, case3d, engine):
         assert rel(hadr.make_kcycle_preconditioner(H)(b), ref) <= 1e-12
     finally:
         hadr._lib.set_option("ce_max_n", 32768)
+        hadr._lib.set_option("ce_smem_relax", 1)
 
 
 def test_solve_upwind_3d(hadr, case3d):
