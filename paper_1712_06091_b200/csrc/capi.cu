@@ -519,6 +519,13 @@ int hadr_set_option(const char* name, double value) {
         if (!h) break;
         delete h;
       }
+    } else if (n == "cl_max_n") {
+      g_cl_max_n = (long)value;
+      for (;;) {
+        Hier* h = hier_pool_pop();
+        if (!h) break;
+        delete h;
+      }
     } else if (n == "stencil_tile") {
       g_stencil_tile = (int)value;
       for (;;) {

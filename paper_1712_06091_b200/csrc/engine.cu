@@ -400,17 +400,26 @@ static Mask125 galerkin_mask(const Op& A) {
   return m;
 }
 
-static void galerkin_write(const Op& A, Op& C) {  // C's offsets define the planes
+// C's offsets define the planes.  check_mask: the same pass also ORs the non-zero
+// pattern; returns false when it is not C's layout (the caller rebuilds).
+static bool galerkin_write(const Op& A, Op& C, bool check_mask = false) {
   Ctx& c = Ctx::get();
   int* dslot = dalloc<int>(125);
   int slot[125];
   for (int q = 0; q < 125; ++q) slot[q] = -1;
   for (int o = 0; o < C.nofs; ++o) slot[slot125(C.d1[o], C.d2[o], C.d3[o])] = o;
   HADR_CUDA(cudaMemcpyAsync(dslot, slot, sizeof(slot), cudaMemcpyHostToDevice, c.stream));
-  launch_galerkin(c.stream, A.dev(), C.n1, C.n2, C.n3, nullptr, dslot, C.coef);
+  unsigned long long* dmask = check_mask ? (unsigned long long*)(c.dscal + 40) : nullptr;
+  if (dmask) HADR_CUDA(cudaMemsetAsync(dmask, 0, 2 * sizeof(unsigned long long), c.stream));
+  launch_galerkin(c.stream, A.dev(), C.n1, C.n2, C.n3, dmask, dslot, C.coef);
   HADR_CUDA(cudaGetLastError());
+  Mask125 m{{0ull, 0ull}};
+  if (dmask) HADR_CUDA(cudaMemcpyAsync(m.w, dmask, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
   c.sync();
   dfree(dslot);
+  if (!check_mask) return true;
+  mask_set(m, slot125(0, 0, 0));
+  return mask_eq(m, layout_mask(C));
 }
 
 Op* op_galerkin(const Op& A) {
@@ -787,8 +796,7 @@ static bool hier_refresh(Hier* h, const Op& fine) {
   for (size_t l = 1; l < h->lv.size(); ++l) {
     Op& F = *h->lv[l - 1].A;
     Op& C = *h->lv[l].A;
-    if (!mask_eq(galerkin_mask(F), layout_mask(C))) return false;
-    galerkin_write(F, C);
+    if (!galerkin_write(F, C, true)) return false;  // one pass: values + pattern check
   }
   for (auto& L : h->lv) {
     L.A->refresh_inv_diag();

@@ -138,7 +138,7 @@ __device__ __forceinline__ cplx ldc(const cplx* p, long i) { return __ldg(p + i)
 
 // Launch geometry of one vector op: a single cluster for small levels, else a
 // grid capped at a multiple of the SM count (+ a finalize kernel when reducing).
-constexpr long kClusterMaxN = 32768;
+long g_cl_max_n = 32768;  // option "cl_max_n": vector ops up to this size reduce inside one cluster
 constexpr int kClusterMaxCTAs = 16;
 
 struct Geo {
@@ -148,7 +148,7 @@ struct Geo {
 
 static Geo geo_for(const LaunchCfg& lc, long n) {
   long b = (n + kThreads - 1) / kThreads;
-  if (n <= kClusterMaxN && !lc.dist) {  // distributed sums finish through the communicator
+  if (n <= g_cl_max_n && !lc.dist) {  // distributed sums finish through the communicator
     if (b > kClusterMaxCTAs) b = kClusterMaxCTAs;
     if (b < 1) b = 1;
     return Geo{(int)b, (int)b};

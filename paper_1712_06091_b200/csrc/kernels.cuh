@@ -6,7 +6,8 @@ namespace hadr {
 
 extern long long g_launch_count;
 extern int g_pdl;  // programmatic dependent launch of the solve-phase kernels
-extern int g_stencil_tile;  // shared-memory tiled stencil kernel on the graph path
+extern int g_stencil_tile;
+extern long g_cl_max_n;  // single-cluster reductions (in-kernel epilogue) up to this many points  // shared-memory tiled stencil kernel on the graph path
 
 // Structured 2D/3D stencil in union-offset, plane-major layout (2D: n3 = 1, d3 = 0):
 //   k = (i1*n2 + i2)*n3 + i3,  coef[o*N + k] multiplies x[k + (d1*n2 + d2)*n3 + d3],
