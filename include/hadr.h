@@ -165,6 +165,12 @@ int hadr_dist_plan(int n1, int n2, int n3, int max_levels, int* bounds, int* n_d
 /* pure host helper: split n1 planes into `size` slabs with interior bounds multiples of `align` */
 int hadr_slab_bounds(int n1, int size, int align, int* bounds /* size + 1 */);
 
+/* out = q (.) exp(sign * i * omega * tau), sign = +1 (to_adr) / -1 (to_helmholtz): the phase transforms
+ * of helmadr/operators.py:269-278 (rhs_transform) and compose_waveform (helmadr/drivers.py:171-173) on the
+ * device; tau real.  cos/sin are the device's (within an ulp of numpy's). */
+int hadr_phase_transform(long long n, const double* q, const double* tau, double omega, int sign, double* out,
+                         int on_device);
+
 /* ---- travel time (setup, host; the amplitude solve takes tau as an input) ----
  * Factored-eikonal fast marching (helmadr/_fmm.py:22-331 via helmadr/eikonal.py:72-99): tau = tau0 * tau1
  * with tau0 = |x - x0| and its gradient g0 (AnalyticBase), kappa = slowness; order 1 or 2.

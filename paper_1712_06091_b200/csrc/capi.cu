@@ -163,10 +163,31 @@ int hadr_init(int device) {
 int hadr_device_sync(void) { return guarded([&] { Ctx::get().sync(); }); }
 
 int hadr_device_malloc(void** ptr, size_t bytes) {
-  return guarded([&] { HADR_CUDA(cudaMalloc(ptr, bytes)); });
+  return guarded([&] { *ptr = pool_alloc(bytes); });  // caching allocator: repeated solves do not cudaMalloc
 }
 int hadr_device_free(void* ptr) {
-  return guarded([&] { HADR_CUDA(cudaFree(ptr)); });
+  return guarded([&] { pool_free(ptr); });
+}
+
+int hadr_phase_transform(long long n, const double* q, const double* tau, double omega, int sign, double* out,
+                         int on_device) {
+  return guarded([&] {
+    if (sign != 1 && sign != -1) throw ValueError("sign must be +1 (to_adr) or -1 (to_helmholtz)");
+    Ctx& c = Ctx::get();
+    DevVec dq(q, n, on_device, true), dout(out, n, on_device, false);
+    const double* dt = tau;
+    double* tmp = nullptr;
+    if (!on_device) {
+      tmp = dalloc<double>(n);
+      HADR_CUDA(cudaMemcpyAsync(tmp, tau, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+      dt = tmp;
+    }
+    launch_phase(c.stream, n, dq.p, dt, omega, sign, dout.p);
+    HADR_CUDA(cudaGetLastError());
+    dout.copy_out(out);
+    c.sync();
+    dfree(tmp);
+  });
 }
 int hadr_memcpy(void* dst, const void* src, size_t bytes, int kind) {
   return guarded([&] {

@@ -1320,6 +1320,24 @@ void launch_assemble(cudaStream_t s, int dim, int n1, int n2, int n3, double h1,
 namespace hadr {
 
 // complex128 -> complex64 (round to nearest) for the mixed-precision K-cycle operators
+// out = q (.) exp(sign * i * omega * tau)  (helmadr/operators.py:269-278 rhs_transform; numpy's
+// complex product formula; cos/sin are CUDA's, within an ulp of the host libm's)
+__global__ void k_phase(long n, const cplx* __restrict__ q, const double* __restrict__ tau, double omega, int sign,
+                        cplx* __restrict__ out) {
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    double sn, cs;
+    sincos(omega * tau[k], &sn, &cs);
+    out[k] = cmul_np(q[k], mk(cs, sign > 0 ? sn : -sn));
+  }
+}
+void launch_phase(cudaStream_t s, long n, const cplx* q, const double* tau, double omega, int sign, cplx* out) {
+  ++g_launch_count;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) return;
+  k_phase<<<blocks, 256, 0, s>>>(n, q, tau, omega, sign, out);
+}
+
 __global__ void k_to_c64(long n, const cplx* __restrict__ in, float2* __restrict__ out) {
   for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
     const cplx v = in[k];

@@ -165,6 +165,7 @@ void launch_assemble(cudaStream_t s, int dim, int n1, int n2, int n3, double h1,
                      const double* g1, const double* g2, const double* g3, const double* lap, cplx* coefp,
                      unsigned* mask, int r0 = 0, int nr = -1, long pstride = -1);
 void launch_to_c64(cudaStream_t s, long n, const cplx* in, float2* out);
+void launch_phase(cudaStream_t s, long n, const cplx* q, const double* tau, double omega, int sign, cplx* out);
 void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, int n3c, unsigned long long* mask,
                      const int* slot_of, cplx* coef_c, int q0 = 0, int nq = -1, long cstride = -1);
 

@@ -165,11 +165,16 @@ def rhs_transform(q: np.ndarray, tt, omega: float, direction: str) -> np.ndarray
     """helmadr/operators.py:269-278."""
     if q.shape != tt.tau.shape:
         raise ValueError("field/travel-time grid mismatch")
-    if direction == "to_adr":
-        return q * np.exp(1j * omega * tt.tau)
-    if direction == "to_helmholtz":
-        return q * np.exp(-1j * omega * tt.tau)
-    raise ValueError(f"direction {direction!r} not in ('to_adr', 'to_helmholtz')")
+    if direction not in ("to_adr", "to_helmholtz"):
+        raise ValueError(f"direction {direction!r} not in ('to_adr', 'to_helmholtz')")
+    j = 1j if direction == "to_adr" else -1j
+    nz = np.flatnonzero(q)
+    if nz.size * 8 < q.size:  # a point source: the phase only where q is non-zero (same values there)
+        out = np.zeros(q.shape, dtype=np.result_type(q.dtype, np.complex128))
+        qf, tf, of = q.reshape(-1), tt.tau.reshape(-1), out.reshape(-1)
+        of[nz] = qf[nz] * np.exp(j * omega * tf[nz])
+        return out
+    return q * np.exp(j * omega * tt.tau)
 
 
 def max_nnz_per_row(A) -> int:
