@@ -66,6 +66,10 @@ int hadr_op_from_csr(int n1, int n2, int n3, int64_t nnz, const int64_t* indptr,
 int hadr_op_from_planes(int n1, int n2, int n3, int n_offsets, const int* offsets, const double* coef, hadr_op* out);
 int hadr_op_info(hadr_op op, int* n1, int* n2, int* n3, int* n_offsets, int* offsets /* 3*125 */);
 int hadr_op_export(hadr_op op, double* coef /* n_offsets*N complex */);
+/* storage of the operator's stencil kernel: *n_slots = coefficient planes the apply reads from the
+ * pair-compressed copy (fine upwind operators: 2D 7, 3D 10), 0 = union planes (n_offsets). Built lazily
+ * by the first apply / solve (option "pair_compress"); no reference counterpart (layout only). */
+int hadr_op_storage(hadr_op op, int* n_slots);
 /* y = A x  (helmadr/krylov.py:60-65 spmv; scipy csr_matvec order, bit-exact) */
 int hadr_op_apply(hadr_op op, const double* x, double* y, int on_device);
 /* z = r / diag(A)  (helmadr/krylov.py:68-73 jacobi_apply) */
@@ -179,6 +183,17 @@ int hadr_phase_transform(long long n, const double* q, const double* tau, double
 int hadr_fast_march(int dim, const int* n, const double* h, const double* tau0, const double* g01,
                     const double* g02, const double* g03, const double* kappa, const int* src, int order,
                     double* tau1, long long* n_accepted);
+
+/* ---- accuracy workflow (helmadr/grid.py:175-191 relative_error_map; helmadr/drivers.py:176-196
+ * accuracy_compare) ----
+ * err = |u - u_ref| / max(|u_ref|, floor) over n complex points (err may be NULL); floor < 0 selects the
+ * reference default 1e-12 * max|u_ref|, written back to *floor_used.  The nodes with |u_ref| >= floor are
+ * the statistics mask: *count receives their number and vals[q] the idx[q]-th smallest masked error
+ * (ascending order, idx clipped to [0, count-1]) for q < nidx, from which the host shim forms numpy's
+ * median / linear-interpolated percentile.  on_device: u, u_ref, err are device pointers. */
+int hadr_relative_error(long long n, const double* u, const double* u_ref, double floor, double* err,
+                        double* floor_used, long long* count, const long long* idx, int nidx, double* vals,
+                        int on_device);
 
 /* ---- Krylov (helmadr/krylov.py) ---- */
 /* _gmres_relax_pre / gmres_relax (helmadr/krylov.py:82-119) */

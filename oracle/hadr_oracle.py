@@ -613,3 +613,46 @@ def solve_central(p: Problem, alpha=0.2, s1_cycles=5, s1_tol=1e-2, restart=5, to
     rep = Report(r1.iterations + r2.iterations, r2.history, r2.converged, el, r2.bnorm,
                  r2.final_relres, stage1=r1, stage2=r2)
     return u.reshape(p.n1, p.n2), a, rep
+
+
+# --------------------------------------------------------------------------
+# accuracy workflow and field dumps
+
+def error_map(u, u_ref, floor=None):
+    """helmadr/grid.py:175-191: |u - u_ref| / max(|u_ref|, floor), floor default
+    1e-12 max|u_ref|."""
+    u = np.asarray(u)
+    u_ref = np.asarray(u_ref)
+    if u.shape != u_ref.shape:
+        raise ValueError("grid mismatch")
+    mag = np.abs(u_ref)
+    fl = 1e-12 * float(mag.max()) if floor is None else floor
+    if fl < 0:
+        raise ValueError("floor must be non-negative")
+    return np.abs(u - u_ref) / np.where(mag < fl, fl, mag)
+
+
+def compare(solutions, u_ref, floor=None):
+    """helmadr/drivers.py:176-196: median / p95 / max of the error map over |u_ref| >= floor."""
+    u_ref = np.asarray(u_ref)
+    fl = 1e-12 * float(np.abs(u_ref).max()) if floor is None else floor
+    keep = np.abs(u_ref) >= fl
+    res = {}
+    for name, u in solutions:
+        e = error_map(u, u_ref, fl)
+        v = e[keep]
+        res[name] = {"median": float(np.median(v)), "p95": float(np.percentile(v, 95)), "max": float(v.max()),
+                     "error_map": e}
+    return res
+
+
+def dump_bytes(values):
+    """helmadr/models.py:100-113 payload: little-endian float64, complex as (re, im) pairs."""
+    values = np.asarray(values)
+    if np.iscomplexobj(values):
+        flat = np.empty(2 * values.size)
+        flat[0::2] = values.real.reshape(-1)
+        flat[1::2] = values.imag.reshape(-1)
+    else:
+        flat = values.astype(np.float64).reshape(-1)
+    return flat.astype("<f8").tobytes()

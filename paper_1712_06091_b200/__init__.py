@@ -14,10 +14,12 @@ from .multigrid import (COARSE_FGMRES_TOL, COARSE_GMRES_STEPS, KCyclePreconditio
                         build_hierarchy, build_prolongation, coarsenable_levels, galerkin_coarsen,
                         hierarchy_from_ops, k_cycle, make_kcycle_preconditioner)
 from .stencil import Prolongation, StencilOperator, as_operator
+from .accuracy import accuracy_compare, read_field, read_meta, relative_error_map, write_field, write_meta
 
 __all__ = [
     "KrylovConfig", "SolveReport", "fgmres", "fgmres_device", "gmres_relax", "jacobi_apply", "spmv", "launch_count",
     "COARSE_FGMRES_TOL", "COARSE_GMRES_STEPS", "KCyclePreconditioner", "MGHierarchy", "build_hierarchy",
     "build_prolongation", "coarsenable_levels", "galerkin_coarsen", "hierarchy_from_ops", "k_cycle",
     "make_kcycle_preconditioner", "Prolongation", "StencilOperator", "as_operator",
+    "accuracy_compare", "read_field", "read_meta", "relative_error_map", "write_field", "write_meta",
 ]

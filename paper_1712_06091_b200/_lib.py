@@ -27,7 +27,8 @@ EXPORTS = (
     "hadr_fgmres", "hadr_launch_count", "hadr_assemble", "hadr_solve_adr_upwind", "hadr_pool_trim",
     "hadr_stream_timer", "hadr_set_option", "hadr_ce_profile", "hadr_op_bench",
     "hadr_dist_nccl_id", "hadr_dist_init_nccl", "hadr_dist_init_host", "hadr_dist_finalize", "hadr_dist_info",
-    "hadr_dist_plan", "hadr_slab_bounds", "hadr_fast_march", "hadr_phase_transform",
+    "hadr_dist_plan", "hadr_slab_bounds", "hadr_fast_march", "hadr_phase_transform", "hadr_op_storage",
+    "hadr_relative_error",
 )
 
 # host-communicator callbacks (include/hadr.h hadr_host_*)
@@ -97,6 +98,9 @@ _SIGS = {
     "hadr_slab_bounds": (_i, [_i, _i, _i, _vp]),
     "hadr_fast_march": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, C.POINTER(C.c_longlong)]),
     "hadr_phase_transform": (_i, [C.c_longlong, _vp, _vp, _d, _i, _vp, _i]),
+    "hadr_op_storage": (_i, [_vp, C.POINTER(_i)]),
+    "hadr_relative_error": (_i, [C.c_longlong, _vp, _vp, _d, _vp, C.POINTER(_d), C.POINTER(C.c_longlong), _vp, _i,
+                                 _vp, _i]),
 }
 
 _lib = None

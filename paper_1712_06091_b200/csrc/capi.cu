@@ -69,6 +69,8 @@ struct DevVec {
 static hadr_op wrap(Op* op, bool own = true) { return new hadr_op_s{op, own}; }
 
 namespace hadr {
+void accuracy_stats(long n, const cplx* u, const cplx* ref, double floor_in, double* err_dev, double* floor_out,
+                    long long* count_out, const long long* idx, int nidx, double* vals_out);  // accuracy.cu
 int64_t fast_march(int dim, const int* n, const double* h, const double* tau0, const double* const* g0,
                    const double* kappa, const int* src, int order, double* tau1_out);  // eikonal.cpp
 }
@@ -237,13 +239,18 @@ int hadr_op_export(hadr_op h, double* coef) {
 
 int hadr_op_apply(hadr_op h, const double* x, double* y, int on_device) {
   return guarded([&] {
-    const Op* op = h->op;
+    Op* op = h->op;
+    if (g_pair_compress && !op->pc_tried) op->pair_compress();  // the fine-level kernel the solver runs
     DevVec dx(x, op->N, on_device, true), dy(y, op->N, on_device, false);
     op_apply(*op, dx.p, dy.p);
     HADR_CUDA(cudaGetLastError());
     dy.copy_out(y);
     Ctx::get().sync();
   });
+}
+
+int hadr_op_storage(hadr_op h, int* n_slots) {
+  return guarded([&] { *n_slots = h->op->pcode ? h->op->nslot : 0; });
 }
 
 int hadr_op_jacobi(hadr_op h, const double* r, double* z, int on_device) {
@@ -477,6 +484,7 @@ int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, 
   return guarded([&] {
     Ctx& c = Ctx::get();
     Op* op = h->op;
+    if (g_pair_compress && !op->pc_tried) op->pair_compress();  // as the hierarchy's fine level
     const cplx* xd = (const cplx*)x;
     cplx* yd = (cplx*)y;
     cplx* vtmp = dalloc<cplx>(op->N);
@@ -549,6 +557,13 @@ int hadr_set_option(const char* name, double value) {
       }
     } else if (n == "stencil_tile") {
       g_stencil_tile = (int)value;
+      for (;;) {
+        Hier* h = hier_pool_pop();
+        if (!h) break;
+        delete h;
+      }
+    } else if (n == "pair_compress") {
+      g_pair_compress = value != 0.0;
       for (;;) {
         Hier* h = hier_pool_pop();
         if (!h) break;
@@ -629,6 +644,25 @@ int hadr_fast_march(int dim, const int* n, const double* h, const double* tau0, 
       *n_accepted = (long long)hadr::fast_march(dim, n, h, tau0, g0, kappa, src, order, tau1);
     } catch (const std::invalid_argument& e) {
       throw ValueError(e.what());
+    }
+  });
+}
+
+int hadr_relative_error(long long n, const double* u, const double* u_ref, double floor, double* err,
+                        double* floor_used, long long* count, const long long* idx, int nidx, double* vals,
+                        int on_device) {
+  return guarded([&] {
+    if (n <= 0) throw ValueError("relative_error: empty field");
+    if (nidx < 0 || (nidx > 0 && (!idx || !vals))) throw ValueError("relative_error: bad order-statistic request");
+    Ctx& c = Ctx::get();
+    DevVec du(u, n, on_device, true), dr(u_ref, n, on_device, true);
+    double* derr = nullptr;
+    if (err) derr = on_device ? err : dalloc<double>(n);
+    accuracy_stats(n, du.p, dr.p, floor, derr, floor_used, count, idx, nidx, vals);
+    if (err && !on_device) {
+      HADR_CUDA(cudaMemcpyAsync(err, derr, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      dfree(derr);
     }
   });
 }

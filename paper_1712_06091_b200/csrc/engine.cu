@@ -99,11 +99,79 @@ Op::~Op() {
   dfree(coef);
   dfree(coef32);
   dfree(dinv);
+  dfree(pcode);
+  dfree(pcoef);
+  dfree(pcoef32);
 }
 
 void Op::make_c64() {
   if (!coef32) coef32 = dalloc<float2>((size_t)alloc_len()) + base_off();
   launch_to_c64(Ctx::get().stream, alloc_len(), coef - base_off(), coef32 - base_off());
+  if (pcode) {
+    if (!pcoef32) pcoef32 = dalloc<float2>((size_t)nslot * nloc());
+    launch_to_c64(Ctx::get().stream, (long)nslot * nloc(), pcoef, pcoef32);
+  }
+}
+
+int g_pair_compress = 1;
+
+bool Op::pair_compress() {
+  pc_tried = true;
+  auto drop = [&] {
+    dfree(pcode);
+    dfree(pcoef);
+    dfree(pcoef32);
+    pcode = nullptr;
+    pcoef = nullptr;
+    pcoef32 = nullptr;
+    nslot = 0;
+    return false;
+  };
+  // exactly the plus-radius-2 union in sorted order: centre, +-1 and +-2 along each axis
+  const int dim = n3 > 1 ? 3 : 2;
+  if (nofs != (dim == 2 ? 9 : 13)) return drop();
+  {
+    int k = 0;
+    bool ok = true;
+    for (int a1 = -2; a1 <= 2; ++a1)
+      for (int a2 = -2; a2 <= 2; ++a2)
+        for (int a3 = (dim == 3 ? -2 : 0); a3 <= (dim == 3 ? 2 : 0); ++a3) {
+          if ((a1 != 0) + (a2 != 0) + (a3 != 0) > 1) continue;
+          ok = ok && k < nofs && d1[k] == a1 && d2[k] == a2 && d3[k] == a3;
+          ++k;
+        }
+    if (!ok || k != nofs) return drop();
+  }
+  int pos_a[HADR_MAX_OFS], pos_b[HADR_MAX_OFS], bit[HADR_MAX_OFS];
+  const int ns = pair_layout(nofs, pos_a, pos_b, bit);
+  if (ns == 0) return drop();
+  const long n = nloc();
+  if (pcode && nslot != ns) drop();
+  if (!pcode) {
+    pcode = dalloc<uint8_t>(n);
+    pcoef = dalloc<cplx>((size_t)ns * n);
+  }
+  nslot = ns;
+  Ctx& c = Ctx::get();
+  int* flag = (int*)c.dscal + 33;
+  HADR_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), c.stream));
+  StencilDev A = dev();
+  launch_pair_compress(c.stream, A, ns, pos_a, pos_b, bit, pcoef, n, pcode, flag);
+  HADR_CUDA(cudaGetLastError());
+  int conflict = 0;
+  HADR_CUDA(cudaMemcpyAsync(&conflict, flag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  if (slab()) {  // every rank must take the same kernel path (identical graphs, no divergence)
+    unsigned long long f = (unsigned long long)conflict;
+    dist_comm()->allreduce_or_u64(&f, 1, c.stream);
+    conflict = f != 0;
+  }
+  if (conflict) return drop();
+  if (coef32) {  // mixed precision: complex64 copy of the compressed planes as well
+    if (!pcoef32) pcoef32 = dalloc<float2>((size_t)nslot * n);
+    launch_to_c64(c.stream, (long)nslot * n, pcoef, pcoef32);
+  }
+  return true;
 }
 
 StencilDev Op::dev() const {
@@ -122,6 +190,10 @@ StencilDev Op::dev() const {
   }
   s.coef = coef;
   s.coef32 = coef32;
+  s.pcode = pcode;
+  s.pcoef = pcoef;
+  s.pcoef32 = pcoef32;
+  s.pstr = nloc();
   return s;
 }
 
@@ -793,6 +865,7 @@ static bool hier_refresh(Hier* h, const Op& fine) {
     return false;
   HADR_CUDA(cudaMemcpyAsync(L0.coef, fine.coef, (size_t)fine.nofs * fine.N * sizeof(cplx), cudaMemcpyDeviceToDevice,
                             c.stream));
+  if (L0.pcode && !L0.pair_compress()) return false;  // kernel path captured in the graphs changed
   for (size_t l = 1; l < h->lv.size(); ++l) {
     Op& F = *h->lv[l - 1].A;
     Op& C = *h->lv[l].A;
@@ -840,6 +913,7 @@ Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol) 
       L.own = true;
       h->lv.push_back(L);
     }
+    if (g_pair_compress && h->lv[0].A->nloc() > g_cl_max_n) h->lv[0].A->pair_compress();
     h->alloc_workspace();
   } catch (...) {
     delete h;
@@ -937,6 +1011,7 @@ Hier* hier_build_dist(Op* fine, const SlabPlan& plan, int coarse_steps, double c
       L.own = true;
       h->lv.push_back(L);
     }
+    if (g_pair_compress) h->lv[0].A->pair_compress();
     h->alloc_workspace();
   } catch (...) {
     delete h;
@@ -1307,6 +1382,7 @@ void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart,
     if (A.slab()) dist_comm()->halo((void*)v, A.n23() * sizeof(cplx), A.own(), kHalo, c.stream);
   };
   OuterWS* ws = outer_ws(N, restart, A.slab() ? (long)kHalo * A.n23() : 0);
+  if (g_pair_compress && !A.pc_tried && N > g_cl_max_n) A.pair_compress();
   const StencilDev Ad = A.dev();
   auto norm2 = [&](const cplx* v) -> double {
     launch_scale(lcd, N, v, nullptr, nullptr, RED_NORM, gate_always(), c.rs, epi_store(c.dscal));

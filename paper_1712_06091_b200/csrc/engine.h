@@ -63,8 +63,17 @@ struct Op {
   cplx* coef = nullptr;
   float2* coef32 = nullptr;  // complex64 copy used by the K-cycle in mixed precision (null: c128)
   cplx* dinv = nullptr;      // lazily computed inverse diagonal
+  // pair-compressed copy of the owned rows (StencilDev::pcode), read by the flat stencil kernel
+  uint8_t* pcode = nullptr;
+  cplx* pcoef = nullptr;
+  float2* pcoef32 = nullptr;
+  int nslot = 0;
+  bool pc_tried = false;
   ~Op();
-  void make_c64();           // (re)build coef32 from coef
+  void make_c64();           // (re)build coef32 (and pcoef32) from coef (pcoef)
+  // (re)build the pair-compressed copy from coef; false (and no copy) when no +-2 pair
+  // exists or a row holds both members.  Reuses its buffers when refreshing.
+  bool pair_compress();
   StencilDev dev() const;
   int center() const;
   const cplx* inv_diag();  // computes on first use; throws ValueError on a zero diagonal
@@ -150,6 +159,7 @@ struct Hier {
 extern long g_ce_max_n;  // levels with N <= this run inside the cluster engine (0 disables)
 extern int g_kcycle_c64; // build hierarchies with complex64 operator storage (mixed-precision K-cycle)
 extern int g_ce_smem_relax;  // engine relaxations out of shared memory where they fit
+extern int g_pair_compress;  // pair-compress fine operators (outer A, hierarchy level 0)
 
 Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol);
 void hier_release(Hier* h);  // recycle (workspace + captured graphs) or delete

@@ -283,8 +283,139 @@ __device__ __forceinline__ void stencil_chunk(const StencilArgs& a, int o0, int 
   }
 }
 
-template <int INM, int OUTM, int RED, int NO, int CL>
-__global__ void __launch_bounds__(kThreads, 4) k_stencil(StencilArgs a) {
+// Pair-compressed fine operator (StencilDev::pcode): the union is exactly the
+// plus-radius-2 set (centre, +-1 and +-2 along each of D axes; 2D 9, 3D 13 offsets
+// in sorted order) and the two +-2 offsets of an axis share one coefficient plane.
+// One load per slot (2D 7, 3D 10 instead of 9 / 13); the far term of axis d is
+// computed once and added at the position of whichever member the row holds, so
+// the accumulation order (ascending column) and rounding equal the union kernel's.
+//   2D union positions: 0 (-2,0) 1 (-1,0) 2 (0,-2) 3 (0,-1) 4 centre 5 (0,1) 6 (0,2) 7 (1,0) 8 (2,0)
+//   3D: 0 (-2,0,0) 1 (-1,0,0) 2 (0,-2,0) 3 (0,-1,0) 4 (0,0,-2) 5 (0,0,-1) 6 centre
+//       7 (0,0,1) 8 (0,0,2) 9 (0,1,0) 10 (0,2,0) 11 (1,0,0) 12 (2,0,0)
+template <int NO>
+struct PcLayout;
+template <>
+struct PcLayout<9> {
+  static constexpr int NS = 7;
+  // slot of each union position; pair (axis) of a position or -1; member: 0 minus, 1 plus
+  __host__ __device__ static constexpr int slot(int p) {
+    constexpr int t[9] = {0, 1, 2, 3, 4, 5, 2, 6, 0};
+    return t[p];
+  }
+  __host__ __device__ static constexpr int pair(int p) {
+    constexpr int t[9] = {0, -1, 1, -1, -1, -1, 1, -1, 0};
+    return t[p];
+  }
+  __host__ __device__ static constexpr int plus_pos(int q) {  // slot -> union position of its plus member
+    constexpr int t[7] = {8, -1, 6, -1, -1, -1, -1};
+    return t[q];
+  }
+  __host__ __device__ static constexpr int first_pos(int q) {  // slot -> union position (minus member)
+    constexpr int t[7] = {0, 1, 2, 3, 4, 5, 7};
+    return t[q];
+  }
+  __host__ __device__ static constexpr int axis(int q) {  // slot -> axis of its offset (-1: centre)
+    constexpr int t[7] = {0, 0, 1, 1, -1, 1, 0};
+    return t[q];
+  }
+  __host__ __device__ static constexpr int delta(int q) {  // slot -> offset along that axis (pairs: -2)
+    constexpr int t[7] = {-2, -1, -2, -1, 0, 1, 1};
+    return t[q];
+  }
+};
+template <>
+struct PcLayout<13> {
+  static constexpr int NS = 10;
+  __host__ __device__ static constexpr int slot(int p) {
+    constexpr int t[13] = {0, 1, 2, 3, 4, 5, 6, 7, 4, 8, 2, 9, 0};
+    return t[p];
+  }
+  __host__ __device__ static constexpr int pair(int p) {
+    constexpr int t[13] = {0, -1, 1, -1, 2, -1, -1, -1, 2, -1, 1, -1, 0};
+    return t[p];
+  }
+  __host__ __device__ static constexpr int plus_pos(int q) {
+    constexpr int t[10] = {12, -1, 10, -1, 8, -1, -1, -1, -1, -1};
+    return t[q];
+  }
+  __host__ __device__ static constexpr int first_pos(int q) {
+    constexpr int t[10] = {0, 1, 2, 3, 4, 5, 6, 7, 9, 11};
+    return t[q];
+  }
+  __host__ __device__ static constexpr int axis(int q) {
+    constexpr int t[10] = {0, 0, 1, 1, 2, 2, -1, 2, 1, 0};
+    return t[q];
+  }
+  __host__ __device__ static constexpr int delta(int q) {
+    constexpr int t[10] = {-2, -1, -2, -1, -2, -1, 0, 1, 1, 1};
+    return t[q];
+  }
+};
+
+template <int NO, int INM, bool C32>
+__device__ __forceinline__ void stencil_pc(const StencilArgs& a, long k, int i1, int i2, int i3, int n1, int n2,
+                                           int n3, double s, unsigned code, cplx& acc) {
+  // Branch-free: the slot geometry is compile-time (PcLayout, verified on the host by
+  // Op::pair_compress), so every load is in one basic block and issues back to back.
+  using Lay = PcLayout<NO>;
+  constexpr int NS = Lay::NS;
+  const int crd[3] = {i1, i2, i3};
+  const int ext[3] = {n1, n2, n3};
+  const long str[3] = {(long)n2 * n3, (long)n3, 1};
+  cplx cv[NS], xv[NS], dv[NS];
+  bool ok[NS];
+  const long ps = a.A.pstr;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    const int ax = Lay::axis(q);
+    int dl = Lay::delta(q);
+    if (Lay::plus_pos(q) >= 0) dl = ((code >> Lay::pair(Lay::first_pos(q))) & 1u) ? 2 : -2;
+    long jj = k;
+    ok[q] = true;
+    if (ax >= 0) {
+      ok[q] = (unsigned)(crd[ax] + dl) < (unsigned)ext[ax];
+      jj = ok[q] ? k + dl * str[ax] : k;  // owned-relative (slab halos at < 0)
+    }
+    if constexpr (C32) {
+      const float2 c = __ldg(a.A.pcoef32 + (long)q * ps + k);
+      cv[q] = make_double2((double)c.x, (double)c.y);
+    } else {
+      cv[q] = ldc(a.A.pcoef, (long)q * ps + k);
+    }
+    xv[q] = ldc(a.x, jj);
+    if (INM & IN_JAC) dv[q] = ldc(a.dinv, jj);
+  }
+  cplx tv[NS];
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    cplx v = xv[q];
+    if (INM & IN_SCALE) v = cscale(v, s);
+    if (INM & IN_JAC) v = cmul_np(dv[q], v);
+    tv[q] = cmul_sp(cv[q], v);
+  }
+#pragma unroll
+  for (int p = 0; p < NO; ++p) {
+    const int q = Lay::slot(p);
+    bool live = ok[q];
+    if (Lay::pair(p) >= 0) {
+      const unsigned member = (Lay::plus_pos(q) == p) ? 1u : 0u;
+      live = live && ((code >> Lay::pair(p)) & 1u) == member;
+    }
+    const cplx t = cadd(acc, tv[q]);
+    acc = live ? t : acc;
+  }
+}
+
+// Resident CTAs per SM: the pair-compressed relaxation variant (IN_JAC: 21 loads per
+// point in 2D) gets 128 registers so all of a point's loads issue back to back
+// (B200, 1025^2 fine sweep: 50.6 us union / 44.1 us at 4 CTAs / 41.4 us at 2 CTAs);
+// plain applies keep 4 CTAs (26.3 us vs 30.6 us at 2).
+template <int INM, bool PC>
+constexpr int stencil_min_blocks() {
+  return (PC && (INM & IN_JAC)) ? 2 : 4;
+}
+template <int INM, int OUTM, int RED, int NO, int CL, bool PC = false>
+__global__ void __launch_bounds__(kThreads, stencil_min_blocks<INM, PC>()) k_stencil(StencilArgs a) {
   pdl_enter();
   if (!gate_open(a.gate)) return;
   const int n1 = a.A.n1, n2 = a.A.n2, n3 = a.A.n3, nofs = a.A.nofs;
@@ -306,7 +437,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(StencilArgs a) {
     const int i2 = rem / n3;
     const int i3 = rem - i2 * n3;
     cplx acc = mk(0.0, 0.0);
-    if constexpr (NO > 0) {
+    if constexpr (PC) {
+      const unsigned code = __ldg(a.A.pcode + k);
+      if (a.A.pcoef32)
+        stencil_pc<NO, INM, true>(a, k, i1, i2, i3, n1, n2, n3, s, code, acc);
+      else
+        stencil_pc<NO, INM, false>(a, k, i1, i2, i3, n1, n2, n3, s, code, acc);
+    } else if constexpr (NO > 0) {
       if (c32)
         stencil_chunk<NO, INM, true>(a, 0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
       else
@@ -509,7 +646,12 @@ static void launch_stencil_no(const LaunchCfg& lc, const StencilArgs& a, const G
 template <int INM, int OUTM, int RED>
 static void dispatch_no(const LaunchCfg& lc, const StencilArgs& a, const Geo& geo) {
   const int n = a.A.nofs;
-  if (n == 5)
+  if (a.A.pcode && !geo.cluster && (n == 9 || n == 13)) {  // pair-compressed fine operator
+    if (n == 9)
+      launch_geo(k_stencil<INM, OUTM, RED, 9, 0, true>, geo, lc.stream, a);
+    else
+      launch_geo(k_stencil<INM, OUTM, RED, 13, 0, true>, geo, lc.stream, a);
+  } else if (n == 5)
     launch_stencil_no<INM, OUTM, RED, 5>(lc, a, geo);
   else if (n == 9)
     launch_stencil_no<INM, OUTM, RED, 9>(lc, a, geo);
@@ -535,7 +677,7 @@ void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const Stenc
   // tiled kernel where it measured faster (B200): 2D operators with wide (Galerkin)
   // stencils; the 3D and 9-point fine-level sweeps keep the flat kernel, whose
   // neighbour re-reads L1 already absorbs (tools/prof_solve.py A/B)
-  if (g_stencil_tile && !geo.cluster && a.A.n1own >= 2 &&
+  if (g_stencil_tile && !geo.cluster && a.A.n1own >= 2 && !a.A.pcode &&
       (g_stencil_tile > 1 || (a.A.n3 == 1 && a.A.nofs > 9))) {
     const bool d3 = a.A.n3 > 1;
     TileCfg t{};
@@ -1336,6 +1478,76 @@ void launch_phase(cudaStream_t s, long n, const cplx* q, const double* tau, doub
   if (blocks > 4096) blocks = 4096;
   if (blocks < 1) return;
   k_phase<<<blocks, 256, 0, s>>>(n, q, tau, omega, sign, out);
+}
+
+struct PairTab {
+  int pos_a[HADR_MAX_OFS], pos_b[HADR_MAX_OFS], bit[HADR_MAX_OFS];
+  int nslot;
+};
+// Pair compression (setup): one pass over the owned rows of the union planes.
+// Slot q holds union plane pos_a[q], or for a pair (pos_b[q] >= 0) whichever of
+// pos_a / pos_b is non-zero in the row, with code bit bit[q] set for pos_b.
+__global__ void k_pair_compress(StencilDev A, PairTab t, cplx* __restrict__ pcoef, long pstr,
+                                uint8_t* __restrict__ pcode, int* conflict) {
+  const long n = (long)A.n1own * A.n2 * A.n3;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    unsigned code = 0;
+    int bad = 0;
+    for (int q = 0; q < t.nslot; ++q) {
+      const cplx ca = A.coef[(long)t.pos_a[q] * A.pstride + k];
+      cplx v = ca;
+      if (t.pos_b[q] >= 0) {
+        const cplx cb = A.coef[(long)t.pos_b[q] * A.pstride + k];
+        const bool nza = ca.x != 0.0 || ca.y != 0.0, nzb = cb.x != 0.0 || cb.y != 0.0;
+        bad |= nza && nzb;
+        if (nzb) {
+          code |= 1u << t.bit[q];
+          v = cb;
+        }
+      }
+      pcoef[(long)q * pstr + k] = v;
+    }
+    pcode[k] = (uint8_t)code;
+    if (bad) atomicOr(conflict, 1);
+  }
+}
+
+void launch_pair_compress(cudaStream_t s, const StencilDev& A, int nslot, const int* pos_a, const int* pos_b,
+                          const int* bit, cplx* pcoef, long pstr, uint8_t* pcode, int* conflict) {
+  PairTab t{};
+  for (int q = 0; q < nslot; ++q) {
+    t.pos_a[q] = pos_a[q];
+    t.pos_b[q] = pos_b[q];
+    t.bit[q] = bit[q];
+  }
+  t.nslot = nslot;
+  const long n = (long)A.n1own * A.n2 * A.n3;
+  long b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  k_pair_compress<<<(int)b, 256, 0, s>>>(A, t, pcoef, pstr, pcode, conflict);
+}
+
+// slot layout of the pair-compressed plus-radius-2 union (nofs 9 or 13), see PcLayout
+int pair_layout(int nofs, int* pos_a, int* pos_b, int* bit) {
+  if (nofs == 9) {
+    using L = PcLayout<9>;
+    for (int q = 0; q < L::NS; ++q) {
+      pos_a[q] = L::first_pos(q);
+      pos_b[q] = L::plus_pos(q);
+      bit[q] = L::pair(L::first_pos(q));
+    }
+    return L::NS;
+  }
+  if (nofs == 13) {
+    using L = PcLayout<13>;
+    for (int q = 0; q < L::NS; ++q) {
+      pos_a[q] = L::first_pos(q);
+      pos_b[q] = L::plus_pos(q);
+      bit[q] = L::pair(L::first_pos(q));
+    }
+    return L::NS;
+  }
+  return 0;
 }
 
 __global__ void k_to_c64(long n, const cplx* __restrict__ in, float2* __restrict__ out) {

@@ -28,6 +28,14 @@ struct StencilDev {
   int8_t d3[HADR_MAX_OFS];
   const cplx* coef;
   const float2* coef32;  // non-null: apply with complex64-stored coefficients (mixed-precision K-cycle)
+  // Pair-compressed copy (fine upwind operators, plus-radius-2 union): the offsets +-2
+  // along one axis are never both non-zero in a row (the upwind side), so they share
+  // one plane; bit d of pcode[k] is set when row k holds the +2 member of axis d.
+  // Slot planes (kernels.cu PcLayout) are pstr apart and cover the owned points only.
+  const uint8_t* pcode;
+  const cplx* pcoef;
+  const float2* pcoef32;
+  long pstr;
 };
 
 // coefficient from complex64 storage, widened to complex128 for the arithmetic
@@ -165,6 +173,12 @@ void launch_assemble(cudaStream_t s, int dim, int n1, int n2, int n3, double h1,
                      const double* g1, const double* g2, const double* g3, const double* lap, cplx* coefp,
                      unsigned* mask, int r0 = 0, int nr = -1, long pstride = -1);
 void launch_to_c64(cudaStream_t s, long n, const cplx* in, float2* out);
+// pair compression of the owned rows of a plus-radius-2 union (kernels.cu PcLayout):
+// pair_layout fills the slot table (returns the slot count, 0 if nofs is not 9 / 13);
+// *conflict |= 1 where a row holds both members of a pair
+int pair_layout(int nofs, int* pos_a, int* pos_b, int* bit);
+void launch_pair_compress(cudaStream_t s, const StencilDev& A, int nslot, const int* pos_a, const int* pos_b,
+                          const int* bit, cplx* pcoef, long pstr, uint8_t* pcode, int* conflict);
 void launch_phase(cudaStream_t s, long n, const cplx* q, const double* tau, double omega, int sign, cplx* out);
 void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, int n3c, unsigned long long* mask,
                      const int* slot_of, cplx* coef_c, int q0 = 0, int nq = -1, long cstride = -1);

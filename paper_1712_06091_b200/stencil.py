@@ -88,6 +88,16 @@ class StencilOperator:
     def dtype(self):
         return np.dtype(np.complex128)
 
+    @property
+    def storage_slots(self) -> int:
+        """Coefficient planes the stencil kernel reads from the pair-compressed copy
+        (0: the union planes).  Built by the first apply / solve."""
+        import ctypes as C
+
+        n = C.c_int()
+        check(_lib.lib().hadr_op_storage(self._h, C.byref(n)))
+        return n.value
+
     def planes(self) -> np.ndarray:
         n = self.shape[0]
         out = np.empty((len(self.offsets), n), dtype=np.complex128)

@@ -262,8 +262,82 @@ def cfg3(n: int = 2049, ppw: float = 10.0, layer: int | None = None, tt=None) ->
     return Workload(f"cfg3_{n}", grid, med, src, tt, bc)
 
 
+def _lerp_axis(a: np.ndarray, m: int, ax: int) -> np.ndarray:
+    """Nodal linear interpolation by an integer factor m along one axis: coarse node j
+    lands on fine node j*m (exact nodal alignment)."""
+    if m == 1:
+        return a
+    nc = a.shape[ax]
+    nf = (nc - 1) * m + 1
+    pos = np.arange(nf) / m
+    j0 = np.minimum(np.floor(pos).astype(np.int64), nc - 2)
+    t = pos - j0
+    shp = [1] * a.ndim
+    shp[ax] = nf
+    t = t.reshape(shp)
+    return np.take(a, j0, axis=ax) * (1.0 - t) + np.take(a, j0 + 1, axis=ax) * t
+
+
+def cfg5_medium(grid, corr_cells: float, vmin: float = 2.0, vmax: float = 4.0) -> np.ndarray:
+    """Seeded smooth Gaussian random velocity (BASELINE config 5): white noise
+    (numpy default_rng(1712)) filtered by a Gaussian of sigma = corr/2 cells, whose
+    autocorrelation exp(-r^2 / (4 sigma^2)) falls to 1/e at corr cells (decision), then
+    an affine map to [vmin, vmax].  The noise lives on a lattice m = (n1-1)//128 fine
+    cells apart (m = 8 at 1025^2 x 513; sigma/m = 2.5 lattice cells, smooth at that
+    scale) and is interpolated trilinearly to the grid, so building the 539 M-node field
+    costs seconds instead of a 539 M-point filter."""
+    from scipy.ndimage import gaussian_filter
+
+    m = max(1, (grid.n1 - 1) // 128)
+    while any((n - 1) % m for n in grid.shape):
+        m //= 2
+    cshape = tuple((n - 1) // m + 1 for n in grid.shape)
+    rng = np.random.default_rng(1712)
+    w = rng.standard_normal(cshape)
+    f = gaussian_filter(w, sigma=0.5 * corr_cells / m, mode="reflect")
+    for ax in range(f.ndim):
+        f = _lerp_axis(f, m, ax)
+    lo, hi = f.min(), f.max()
+    return vmin + (vmax - vmin) * (f - lo) / (hi - lo)
+
+
+def cfg5(n: int = 1025, ppw: float = 10.0, layer: int | None = None, tt=None) -> Workload:
+    """BASELINE config 5 (n=1025): 1025 x 1025 x 513 on [0,1]^2 x [0,0.5], h = 1/1024,
+    seeded Gaussian random velocity 2-4 km/s with a 40-cell correlation length
+    (cfg5_medium), 10 ppw at v = 2 (decision), source (0.5, 0.5, 0.05), 16-cell layer
+    on all six faces, all-Sommerfeld, tau from the 3D fast marcher at setup.  Solved
+    with adr_upwind and with standard_sl at alpha = 0.5 ("shift 1+0.5i", SURVEY.md
+    Appendix B4).  ``n`` scales grid, correlation length and layer in proportion."""
+    from .eikonal import compute_travel_time
+    from .fields import GridSpec3, SourceSpec3
+
+    n3 = (n - 1) // 2 + 1
+    grid = GridSpec3(n, n, n3, 1.0, 1.0, 0.5)
+    h = grid.h1
+    vmin = 2.0
+    omega = 2.0 * np.pi * vmin / (ppw * h)
+    scale = (n - 1) / 1024
+    layer = layer if layer is not None else max(2, round(16 * scale))
+    i3 = max(layer + 2, round(0.05 / grid.h3))
+    src = SourceSpec3((n - 1) // 2, (n - 1) // 2, i3, omega)
+    v = cfg5_medium(grid, max(2.0, 40.0 * scale))
+    ksq = 1.0 / v**2
+    X = grid.coords()
+    gam = np.zeros(grid.shape)
+    for ax in range(3):
+        wl = layer * grid.hs[ax]
+        for depth in (wl - X[ax], X[ax] - (grid.Ls[ax] - wl)):
+            d = np.clip(depth, 0.0, wl)
+            gam = np.maximum(gam, omega * (d / wl) ** 2)
+    med = Medium(grid, ksq, gam)
+    if tt is None:
+        tt = compute_travel_time(med, grid, src, "second")
+    bc = ("sommerfeld",) * 6
+    return Workload(f"cfg5_{n}", grid, med, src, tt, bc)
+
+
 def by_name(name: str, n: int | None = None) -> Workload:
-    builders = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4}
+    builders = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
     if name not in builders:
         raise ValueError(f"unknown workload {name!r}; known: {sorted(builders)}")
     return builders[name]() if n is None else builders[name](n)

@@ -68,6 +68,61 @@ def test_stencil_kernels_bitexact_2d(hadr, g65, tile):
         hadr._lib.set_option("stencil_tile", 1)
 
 
+@pytest.mark.parametrize("key", ["H2up", "blend"])
+def test_pair_compressed_stencil_bitexact(hadr, g65, key):
+    """Fine upwind operators stored pair-compressed (the +-2 offsets of an axis share
+    one plane, 9 -> 7 planes) still reproduce csr_matvec bit for bit, and equal the
+    union-plane kernel."""
+    A = csr_from(g65, key)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(A.shape[0]) + 1j * rng.standard_normal(A.shape[0])
+    ys = {}
+    try:
+        for pc in (0, 1):
+            hadr._lib.set_option("pair_compress", pc)
+            op = hadr.StencilOperator.from_csr(A, (65, 65))
+            ys[pc] = op @ x
+            assert op.storage_slots == (7 if pc else 0)
+    finally:
+        hadr._lib.set_option("pair_compress", 1)
+    assert np.array_equal(ys[1], A @ x)
+    assert np.array_equal(ys[0], ys[1])
+
+
+@pytest.mark.parametrize("c64", [0, 1])
+def test_pair_compressed_solve_identical(hadr, c64):
+    """Whole solves with the pair-compressed fine level (outer A and the K-cycle's fine
+    operator; cl_max_n lowered so the 65^2 fine level takes the grid path) are bit-identical
+    to the union-plane solve, complex128 and mixed precision."""
+    from oracle import hadr_oracle as O
+    from paper_1712_06091_b200 import workloads
+
+    p = oracle_problem(workloads.cfg2(65))
+    q = O.delta_source(p.n1, p.n2, p.h1, p.h2, p.src)
+    qh = O.to_adr(q, p.tau, p.omega).reshape(-1)
+    H2 = O.adr_of(p, "upwind2")
+    B = (0.75 * H2 + 0.25 * O.adr_of(p, "upwind1")).tocsr()
+    out = {}
+    hadr._lib.set_option("cl_max_n", 1000)
+    hadr._lib.set_option("kcycle_c64", c64)
+    try:
+        for pc in (0, 1):
+            hadr._lib.set_option("pair_compress", pc)
+            A = hadr.StencilOperator.from_csr(H2, (p.n1, p.n2))
+            Hh = hadr.build_hierarchy(B, (p.n1, p.n2), 5)
+            a, rep = hadr.fgmres(A, qh, None, hadr.make_kcycle_preconditioner(Hh),
+                                 hadr.KrylovConfig(restart=5, maxiter=1000, tol=1e-6))
+            assert A.storage_slots == (7 if pc else 0)
+            out[pc] = (a, rep.iterations, list(rep.history))
+    finally:
+        hadr._lib.set_option("pair_compress", 1)
+        hadr._lib.set_option("cl_max_n", 32768)
+        hadr._lib.set_option("kcycle_c64", 0)
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][2] == out[1][2]
+
+
 def test_spmv_golden(hadr, g65):
     A = csr_from(g65, "blend")
     op = hadr.StencilOperator.from_csr(A, _shape(g65))

@@ -59,6 +59,18 @@ def test_spmv_and_transfer_bitexact_3d(hadr, case3d):
     assert np.array_equal(op1 @ x1, A1 @ x1)
 
 
+def test_pair_compressed_stencil_bitexact_3d(hadr, case3d):
+    """3D fine upwind operators pair-compressed (13 -> 10 planes) reproduce csr_matvec."""
+    rng = np.random.default_rng(9)
+    for key in ("H2", "B"):
+        A = case3d[key]
+        x = rng.standard_normal(A.shape[0]) + 1j * rng.standard_normal(A.shape[0])
+        op = hadr.StencilOperator.from_csr(A, case3d["shape"])
+        y = op @ x
+        assert op.storage_slots == 10, key
+        assert np.array_equal(y, A @ x), key
+
+
 @pytest.mark.parametrize("tile", [0, 2])
 def test_stencil_kernels_bitexact_3d(hadr, case3d, tile):
     """Flat and shared-memory-tiled stencil kernels (option stencil_tile 0 / 2 = always)

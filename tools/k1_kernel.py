@@ -44,7 +44,10 @@ if __name__ == "__main__":
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--variant", type=int, default=1)
     ap.add_argument("--size", type=int, default=1025)
+    ap.add_argument("--pc", type=int, default=1, help="option pair_compress")
     a = ap.parse_args()
-    from paper_1712_06091_b200 import workloads
+    from paper_1712_06091_b200 import _lib, workloads
+
+    _lib.set_option("pair_compress", a.pc)
 
     print(json.dumps(k1_measure(workloads.cfg2(a.size), a.reps, a.variant)))
