@@ -286,6 +286,8 @@ def run_ours(args, ws, rank, local, dist):
         out["config_4_3d"] = run_3d(args, L, local, dist, ws, rank)
     if args.extra_cfg3:
         out["config_3"] = run_3d(args, L, local, dist, 1, rank, which="cfg3")
+    if args.extra_cfg5:
+        out["config_5"] = run_3d(args, L, local, dist, 1, rank, which="cfg5")
     return out
 
 
@@ -310,6 +312,9 @@ def run_3d(args, L, local, dist, ws=1, rank=0, which="cfg4"):
     t_fm = None
     if which == "cfg3":
         wl = workloads.cfg3(args.extra_cfg3)
+        t_fm = wl.tt.fm_time
+    elif which == "cfg5":
+        wl = workloads.cfg5(args.extra_cfg5)
         t_fm = wl.tt.fm_time
     else:
         wl = workloads.cfg4(args.extra_3d)
@@ -364,8 +369,10 @@ def run_3d(args, L, local, dist, ws=1, rank=0, which="cfg4"):
     hbm, srcp = peaks()
     t_k = max_over_ranks(sum(tk) / len(tk), dist)
     bw = b_op * N * (sum(its) / len(its)) / t_k / 1e9 / ws  # per-GPU bytes
-    label = (f"BASELINE configs[2], 2D {n1}x{n2}, layered medium, fast-marching tau" if which == "cfg3"
-             else f"BASELINE configs[3], 3D {n1}x{n2}x{n3}")
+    label = {"cfg3": f"BASELINE configs[2], 2D {n1}x{n2}, layered medium, fast-marching tau",
+             "cfg5": f"BASELINE configs[4] recipe at {n1}x{n2}x{n3} (full 1025^2x513 needs 8 GPUs), Gaussian random "
+                     f"medium, 3D fast-marching tau, adr_upwind",
+             "cfg4": f"BASELINE configs[3], 3D {n1}x{n2}x{n3}"}[which]
     out = {"workload": f"{wl.name} ({label}, c128, {ws} GPU)",
            "value": N * sum(its) / t_dev / 1e6, "unit": "Mdof*iter/s", "outer_iterations": its,
            "n_gpus": ws, "scaling": "strong" if ws > 1 else None,
@@ -379,7 +386,26 @@ def run_3d(args, L, local, dist, ws=1, rank=0, which="cfg4"):
         out["note"] = "travel time from the fast-marching restatement at setup (host, untimed, t_fast_march_s)"
     del fields, q_d, a_d
     torch.cuda.empty_cache()
-    if not args.no_cpu_baseline and rank == 0 and which == "cfg3":
+    if which == "cfg5":
+        out["standard_sl"] = run_cfg5_sl(args, L, wl)
+    if not args.no_cpu_baseline and rank == 0 and which == "cfg5":
+        from threadpoolctl import threadpool_limits
+
+        from oracle import hadr_oracle_nd as ND
+
+        w5 = workloads.cfg5(65)
+        gg = w5.grid
+        bc = ND.bc_dict(3, w5.bc)
+        grads, lap, tau = ND.tau_fields(w5.tt.tau1, gg.Ls, w5.source.index)
+        with threadpool_limits(1):
+            t0 = time.perf_counter()
+            _, r = ND.solve_upwind(gg.shape, gg.hs, w5.omega, w5.source.index, w5.medium.kappa_sq, w5.medium.gamma,
+                                   grads, lap, tau, bc, maxiter=3)
+            tc = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": gg.n_nodes * r.iterations / tc / 1e6, "unit": "Mdof*iter/s", "cores": 1,
+                               "kind": "port", "sample": f"nd oracle on cfg5_65 (65x65x33): assembly + hierarchy + "
+                                                         f"{r.iterations} outer iterations ({tc:.1f} s)"}
+    elif not args.no_cpu_baseline and rank == 0 and which == "cfg3":
         from threadpoolctl import threadpool_limits
 
         from oracle import hadr_oracle as O
@@ -412,6 +438,38 @@ def run_3d(args, L, local, dist, ws=1, rank=0, which="cfg4"):
                                "kind": "port", "sample": f"nd oracle on cfg4_65 (65x65x33): assembly + hierarchy + "
                                                          f"{r.iterations} outer iterations ({tc:.1f} s)"}
     return out
+
+
+B_OP_3D_SL_C128 = 5006.0  # 3D standard_sl c128 (7 / 7 / 27 non-zeros)
+
+
+def run_cfg5_sl(args, L, wl):
+    """Config 5's second solver: standard_sl (shift alpha = 0.5 on the 7-point Helmholtz
+    operator, helmadr/drivers.py:57-67) through the public API; the reference times the
+    FGMRES only (helmadr/drivers.py:63-66), so does this line (device time of fgmres)."""
+    from paper_1712_06091_b200 import drivers, operators
+    from paper_1712_06091_b200.fields import point_source
+
+    g = wl.grid
+    N = g.n_nodes
+    H = operators.assemble_helmholtz(wl.medium, g, wl.omega, wl.bc)
+    q = point_source(g, wl.source)
+    cfg = drivers.StrategyConfig(strategy="standard_sl", alpha=0.5, tol=args.tol, max_iter=args.maxiter)
+    drivers.solve_standard(H, q, wl.medium, wl.omega, cfg)
+    its, tk = [], []
+    for _ in range(args.steps_3d):
+        _, rep = drivers.solve_standard(H, q, wl.medium, wl.omega, cfg)
+        its.append(rep.iterations)
+        tk.append(rep.device_time)
+    t = sum(tk) / len(tk)
+    hbm, srcp = peaks()
+    bw = B_OP_3D_SL_C128 * N * (sum(its) / len(its)) / t / 1e9
+    return {"value": N * sum(its) / sum(tk) / 1e6, "unit": "Mdof*iter/s", "outer_iterations": its,
+            "ms_per_step": t * 1e3, "alpha": 0.5,
+            "solve_roofline": {"bound": "hbm", "model_bytes_per_dof_iter": B_OP_3D_SL_C128, "achieved": bw,
+                               "peak": hbm, "unit": "GB/s", "frac": bw / hbm, "peak_source": srcp},
+            "note": "FGMRES device time per solve (the reference's standard_sl timing); K-cycle on H - 0.5i w^2 "
+                    "diag(kappa^2), the 'shift 1+0.5i' of BASELINE config 5"}
 
 
 def kernel_roofline(H, L, wl, cfg, args):
@@ -520,6 +578,8 @@ def main():
     ap.add_argument("--extra-3d", type=int, default=513, help="also run BASELINE config 4 at this n (0: skip)")
     ap.add_argument("--steps-3d", type=int, default=2)
     ap.add_argument("--extra-cfg3", type=int, default=2049, help="also run BASELINE config 3 at this n (0: skip)")
+    ap.add_argument("--extra-cfg5", type=int, default=257,
+                    help="also run BASELINE config 5's recipe at this n (0: skip; full size 1025 needs 8 GPUs)")
     args = ap.parse_args()
     ws, rank, local, dist = dist_init()
     if args.impl == "reference":

@@ -275,3 +275,16 @@ def solve_upwind(shape, hs, omega, src, kappa_sq, gamma, grads, lap, tau, bc, be
     Hi = hierarchy(B, shape, levels)
     a, rep = fgmres(H2, qh, None, kcycle_precond(Hi), 5, maxiter, tol)
     return a.reshape(shape), rep
+
+
+def solve_sl(shape, hs, omega, src, kappa_sq, gamma, bc, alpha=0.5, tol=1e-6, maxiter=1000, levels=5):
+    """helmadr/drivers.py:57-67 (standard_sl) in any dimension: FGMRES on the standard
+    Helmholtz operator preconditioned by K-cycles on H - i alpha w^2 diag(kappa^2)
+    (helmadr/operators.py:237-244).  Returns (u, report)."""
+    from .hadr_oracle import fgmres, kcycle_precond, shifted
+
+    H = helmholtz_csr(shape, hs, omega, kappa_sq, gamma, bc)
+    Hi = hierarchy(shifted(H, alpha, omega, kappa_sq), shape, levels)
+    q = delta_source(shape, hs, src).reshape(-1)
+    u, rep = fgmres(H, q, None, kcycle_precond(Hi), 5, maxiter, tol)
+    return u.reshape(shape), rep

@@ -146,3 +146,61 @@ def test_solve_upwind_3d(hadr, case3d):
     u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
     assert rep.converged and abs(rep.iterations - rep_ref.iterations) <= 1
     assert rel(a, a_ref) <= 1e-6
+
+
+@pytest.fixture(scope="module")
+def cfg5_small():
+    """BASELINE config 5 recipe at 33 x 33 x 17: Gaussian random medium, tau from the 3D
+    fast marcher (setup), all-Sommerfeld, 2-cell layer."""
+    from oracle import hadr_oracle_nd as ND
+    from paper_1712_06091_b200 import workloads
+
+    wl = workloads.cfg5(33)
+    g = wl.grid
+    grads, lap, tau = ND.tau_fields(wl.tt.tau1, g.Ls, wl.source.index)
+    return dict(wl=wl, shape=g.shape, hs=g.hs, src=wl.source.index, bc=ND.bc_dict(3, wl.bc), grads=grads, lap=lap,
+                tau=tau)
+
+
+def test_device_assembly_helmholtz_3d(hadr, cfg5_small):
+    """3D standard Helmholtz (7-point) and its shift on the device equal the ND oracle."""
+    from oracle import hadr_oracle as O
+    from oracle import hadr_oracle_nd as ND
+    from paper_1712_06091_b200 import operators
+
+    c = cfg5_small
+    wl = c["wl"]
+    ref = ND.helmholtz_csr(c["shape"], c["hs"], wl.omega, wl.medium.kappa_sq, wl.medium.gamma, c["bc"])
+    H = operators.assemble_helmholtz(wl.medium, wl.grid, wl.omega, wl.bc)
+    got = H.tocsr()
+    assert np.array_equal(got.indptr, ref.indptr) and np.array_equal(got.indices, ref.indices)
+    assert np.abs(got.data - ref.data).max() <= 4e-16 * np.abs(ref.data).max()
+    Hs = operators.shift_operator(H, 0.5, wl.omega, wl.medium).tocsr()
+    Hs_ref = O.shifted(ref, 0.5, wl.omega, wl.medium.kappa_sq)
+    assert np.abs(Hs - Hs_ref).max() <= 4e-16 * np.abs(Hs_ref).max()
+
+
+def test_cfg5_recipe_solves(hadr, cfg5_small):
+    """Config 5's two solvers on its recipe (fast-marching tau, random medium):
+    adr_upwind and standard_sl with alpha = 0.5 vs the ND oracle — iterations within 1,
+    amplitude / wavefield within 1e-6 (upwind; as test_solve_upwind_3d) and 1e-8 (SL)."""
+    from oracle import hadr_oracle_nd as ND
+    from paper_1712_06091_b200 import drivers, operators
+    from paper_1712_06091_b200.fields import point_source
+
+    c = cfg5_small
+    wl = c["wl"]
+    a_ref, rep_ref = ND.solve_upwind(c["shape"], c["hs"], wl.omega, c["src"], wl.medium.kappa_sq, wl.medium.gamma,
+                                     c["grads"], c["lap"], c["tau"], c["bc"])
+    cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=1e-6, max_iter=1000)
+    u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
+    assert rep.converged and abs(rep.iterations - rep_ref.iterations) <= 1
+    assert rel(a, a_ref) <= 1e-6
+    u_ref, rs_ref = ND.solve_sl(c["shape"], c["hs"], wl.omega, c["src"], wl.medium.kappa_sq, wl.medium.gamma, c["bc"],
+                                alpha=0.5)
+    H = operators.assemble_helmholtz(wl.medium, wl.grid, wl.omega, wl.bc)
+    q = point_source(wl.grid, wl.source)
+    cfg_sl = drivers.StrategyConfig(strategy="standard_sl", alpha=0.5, tol=1e-6, max_iter=1000)
+    u_sl, rs = drivers.solve_standard(H, q, wl.medium, wl.omega, cfg_sl)
+    assert rs.converged and abs(rs.iterations - rs_ref.iterations) <= 1
+    assert rel(u_sl, u_ref) <= 1e-8
