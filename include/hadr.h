@@ -67,9 +67,11 @@ int hadr_op_from_planes(int n1, int n2, int n3, int n_offsets, const int* offset
 int hadr_op_info(hadr_op op, int* n1, int* n2, int* n3, int* n_offsets, int* offsets /* 3*125 */);
 int hadr_op_export(hadr_op op, double* coef /* n_offsets*N complex */);
 /* storage of the operator's stencil kernel: *n_slots = coefficient planes the apply reads from the
- * pair-compressed copy (fine upwind operators: 2D 7, 3D 10), 0 = union planes (n_offsets). Built lazily
- * by the first apply / solve (option "pair_compress"); no reference counterpart (layout only). */
-int hadr_op_storage(hadr_op op, int* n_slots);
+ * pair-compressed copy (fine upwind operators: 2D 7, 3D 10) or the class-compressed copy (coarse upwind
+ * Galerkin operators: 2D 15, 3D 54), 0 = union planes (n_offsets).  Built lazily by the first apply /
+ * solve (options "pair_compress", "class_compress"); no reference counterpart (layout only). */
+int hadr_op_storage(hadr_op op, int* n_slots, long long* overflow_rows /* class-compressed rows applied
+                                                                           from the union planes */);
 /* y = A x  (helmadr/krylov.py:60-65 spmv; scipy csr_matvec order, bit-exact) */
 int hadr_op_apply(hadr_op op, const double* x, double* y, int on_device);
 /* z = r / diag(A)  (helmadr/krylov.py:68-73 jacobi_apply) */

@@ -98,7 +98,7 @@ _SIGS = {
     "hadr_slab_bounds": (_i, [_i, _i, _i, _vp]),
     "hadr_fast_march": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, C.POINTER(C.c_longlong)]),
     "hadr_phase_transform": (_i, [C.c_longlong, _vp, _vp, _d, _i, _vp, _i]),
-    "hadr_op_storage": (_i, [_vp, C.POINTER(_i)]),
+    "hadr_op_storage": (_i, [_vp, C.POINTER(_i), C.POINTER(C.c_longlong)]),
     "hadr_relative_error": (_i, [C.c_longlong, _vp, _vp, _d, _vp, C.POINTER(_d), C.POINTER(C.c_longlong), _vp, _i,
                                  _vp, _i]),
 }

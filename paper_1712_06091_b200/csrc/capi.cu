@@ -241,6 +241,8 @@ int hadr_op_apply(hadr_op h, const double* x, double* y, int on_device) {
   return guarded([&] {
     Op* op = h->op;
     if (g_pair_compress && !op->pc_tried) op->pair_compress();  // the fine-level kernel the solver runs
+    if (!op->pcode && g_class_compress > (op->n3 > 1 ? 0 : 1) && !op->cc_tried && op->nofs > 13)
+      op->class_compress();  // the coarse-level kernel of the hierarchy's graph path
     DevVec dx(x, op->N, on_device, true), dy(y, op->N, on_device, false);
     op_apply(*op, dx.p, dy.p);
     HADR_CUDA(cudaGetLastError());
@@ -249,8 +251,11 @@ int hadr_op_apply(hadr_op h, const double* x, double* y, int on_device) {
   });
 }
 
-int hadr_op_storage(hadr_op h, int* n_slots) {
-  return guarded([&] { *n_slots = h->op->pcode ? h->op->nslot : 0; });
+int hadr_op_storage(hadr_op h, int* n_slots, long long* overflow_rows) {
+  return guarded([&] {
+    *n_slots = h->op->pcode ? h->op->nslot : h->op->ccode ? h->op->nsl : 0;
+    if (overflow_rows) *overflow_rows = h->op->ccode ? h->op->overflow_rows : 0;
+  });
 }
 
 int hadr_op_jacobi(hadr_op h, const double* r, double* z, int on_device) {
@@ -485,6 +490,8 @@ int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, 
     Ctx& c = Ctx::get();
     Op* op = h->op;
     if (g_pair_compress && !op->pc_tried) op->pair_compress();  // as the hierarchy's fine level
+    if (!op->pcode && g_class_compress > (op->n3 > 1 ? 0 : 1) && !op->cc_tried && op->nofs > 13)
+      op->class_compress();  // as the hierarchy's coarse graph-path levels
     const cplx* xd = (const cplx*)x;
     cplx* yd = (cplx*)y;
     cplx* vtmp = dalloc<cplx>(op->N);
@@ -557,6 +564,13 @@ int hadr_set_option(const char* name, double value) {
       }
     } else if (n == "stencil_tile") {
       g_stencil_tile = (int)value;
+      for (;;) {
+        Hier* h = hier_pool_pop();
+        if (!h) break;
+        delete h;
+      }
+    } else if (n == "class_compress") {
+      g_class_compress = (int)value;
       for (;;) {
         Hier* h = hier_pool_pop();
         if (!h) break;

@@ -5,7 +5,10 @@
 namespace hadr {
 
 constexpr int CE_MAXLEV = 6;      // levels a single engine launch may span
-constexpr int CE_THREADS = 512;   // threads per CTA
+#ifndef HADR_CE_THREADS
+#define HADR_CE_THREADS 512
+#endif
+constexpr int CE_THREADS = HADR_CE_THREADS;  // threads per CTA
 constexpr int CE_CTAS = 16;       // CTAs in the (single, non-portable) cluster
 
 // Device-resident description of one multigrid level for the engine.

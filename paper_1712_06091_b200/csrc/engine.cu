@@ -102,6 +102,10 @@ Op::~Op() {
   dfree(pcode);
   dfree(pcoef);
   dfree(pcoef32);
+  dfree(ccode);
+  dfree(ccoef);
+  dfree(ccoef32);
+  dfree(ctab);
 }
 
 void Op::make_c64() {
@@ -111,6 +115,96 @@ void Op::make_c64() {
     if (!pcoef32) pcoef32 = dalloc<float2>((size_t)nslot * nloc());
     launch_to_c64(Ctx::get().stream, (long)nslot * nloc(), pcoef, pcoef32);
   }
+  if (ccode) {
+    if (!ccoef32) ccoef32 = dalloc<float2>((size_t)nsl * nloc());
+    launch_to_c64(Ctx::get().stream, (long)nsl * nloc(), ccoef, ccoef32);
+  }
+}
+
+int g_class_compress = 2;
+
+bool Op::class_compress() {
+  cc_tried = true;
+  auto drop = [&] {
+    dfree(ccode);
+    dfree(ccoef);
+    dfree(ccoef32);
+    dfree(ctab);
+    ccode = nullptr;
+    ccoef = nullptr;
+    ccoef32 = nullptr;
+    ctab = nullptr;
+    nsl = 0;
+    return false;
+  };
+  const int dim = n3 > 1 ? 3 : 2;
+  for (int o = 0; o < nofs; ++o) {
+    const int a[3] = {d1[o], d2[o], d3[o]};
+    int far = 0;
+    for (int ax = 0; ax < 3; ++ax) {
+      if (a[ax] < -2 || a[ax] > 2) return drop();
+      far += (a[ax] == 2 || a[ax] == -2);
+    }
+    if (far > 1) return drop();
+  }
+  const int ncls = 1 << dim;
+  unsigned long long live[16] = {0};
+  int tab[8 * 64];
+  int ns = 0;
+  std::vector<std::vector<int>> sl(ncls);
+  for (int c = 0; c < ncls; ++c) {
+    for (int o = 0; o < nofs; ++o) {
+      const int a[3] = {d1[o], d2[o], d3[o]};
+      bool in = true;
+      for (int ax = 0; ax < dim; ++ax)
+        if (a[ax] == 2 || a[ax] == -2) in = in && ((a[ax] > 0) == (((c >> ax) & 1) != 0));
+      if (!in) continue;
+      sl[c].push_back(o);
+      live[2 * c + (o >> 6)] |= 1ull << (o & 63);
+    }
+    ns = std::max(ns, (int)sl[c].size());
+  }
+  if (ns > 64 || ns * 5 > nofs * 4) return drop();  // < 20% of the planes saved
+  for (int c = 0; c < ncls; ++c)
+    for (int q = 0; q < ns; ++q) tab[c * ns + q] = q < (int)sl[c].size() ? sl[c][q] : -1;
+  const long n = nloc();
+  if (ccode && nsl != ns) drop();
+  if (!ccode) {
+    ccode = dalloc<uint8_t>(n);
+    ccoef = dalloc<cplx>((size_t)ns * n);
+    ctab = dalloc<int4>((size_t)ncls * ns);
+  }
+  nsl = ns;
+  std::vector<int4> ht((size_t)ncls * ns);
+  for (int c = 0; c < ncls; ++c)
+    for (int q = 0; q < ns; ++q) {
+      const int o = tab[c * ns + q];
+      ht[(size_t)c * ns + q] =
+          o >= 0 ? make_int4((int)(((long)d1[o] * n2 + d2[o]) * n3 + d3[o]), d1[o], d2[o], d3[o]) : make_int4(0, 0, 0, 0);
+    }
+  Ctx& cx = Ctx::get();
+  HADR_CUDA(cudaMemcpyAsync(ctab, ht.data(), ht.size() * sizeof(int4), cudaMemcpyHostToDevice, cx.stream));
+  unsigned long long* cnt = (unsigned long long*)(cx.dscal + 48);
+  HADR_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), cx.stream));
+  StencilDev A = dev();
+  launch_class_compress(cx.stream, A, ncls, live, ns, tab, ccoef, n, ccode, cnt);
+  HADR_CUDA(cudaGetLastError());
+  unsigned long long ov[2] = {0, 0};
+  HADR_CUDA(cudaMemcpyAsync(ov, cnt, sizeof(ov), cudaMemcpyDeviceToHost, cx.stream));
+  cx.sync();
+  overflow_rows = (long)ov[0];
+  // warps that hold an overflow row run both paths: measured on B200, 5.5% overflow rows
+  // scattered by a random medium (config 5) made the apply 30% slower than the union planes
+  unsigned long long bad = (long)ov[1] * 32 * 20 > n ? 1ull : 0ull;  // > 5% of the warps
+  if (slab()) {  // every rank takes the same kernel path
+    dist_comm()->allreduce_or_u64(&bad, 1, cx.stream);
+  }
+  if (bad) return drop();
+  if (coef32) {
+    if (!ccoef32) ccoef32 = dalloc<float2>((size_t)nsl * n);
+    launch_to_c64(cx.stream, (long)nsl * n, ccoef, ccoef32);
+  }
+  return true;
 }
 
 int g_pair_compress = 1;
@@ -194,6 +288,12 @@ StencilDev Op::dev() const {
   s.pcoef = pcoef;
   s.pcoef32 = pcoef32;
   s.pstr = nloc();
+  s.ccode = ccode;
+  s.ccoef = ccoef;
+  s.ccoef32 = ccoef32;
+  s.ctab = ctab;
+  s.cstr = nloc();
+  s.nsl = nsl;
   return s;
 }
 
@@ -870,6 +970,7 @@ static bool hier_refresh(Hier* h, const Op& fine) {
     Op& F = *h->lv[l - 1].A;
     Op& C = *h->lv[l].A;
     if (!galerkin_write(F, C, true)) return false;  // one pass: values + pattern check
+    if (C.ccode && !C.class_compress()) return false;  // kernel path captured in the graphs changed
   }
   for (auto& L : h->lv) {
     L.A->refresh_inv_diag();
@@ -914,6 +1015,10 @@ Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol) 
       h->lv.push_back(L);
     }
     if (g_pair_compress && h->lv[0].A->nloc() > g_cl_max_n) h->lv[0].A->pair_compress();
+    for (size_t l = 1; l < h->lv.size(); ++l) {
+      Op& C = *h->lv[l].A;
+      if (g_class_compress > (C.n3 > 1 ? 0 : 1) && C.nloc() > g_cl_max_n) C.class_compress();
+    }
     h->alloc_workspace();
   } catch (...) {
     delete h;
@@ -1012,6 +1117,10 @@ Hier* hier_build_dist(Op* fine, const SlabPlan& plan, int coarse_steps, double c
       h->lv.push_back(L);
     }
     if (g_pair_compress) h->lv[0].A->pair_compress();
+    for (size_t l = 1; l < h->lv.size(); ++l) {  // slab levels and the replicated graph-path levels
+      Op& C = *h->lv[l].A;
+      if (g_class_compress > (C.n3 > 1 ? 0 : 1) && (C.slab() || C.nloc() > g_cl_max_n)) C.class_compress();
+    }
     h->alloc_workspace();
   } catch (...) {
     delete h;

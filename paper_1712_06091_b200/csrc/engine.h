@@ -69,11 +69,22 @@ struct Op {
   float2* pcoef32 = nullptr;
   int nslot = 0;
   bool pc_tried = false;
+  // class-compressed copy of the owned rows (StencilDev::ccode), coarse upwind Galerkin operators
+  uint8_t* ccode = nullptr;
+  cplx* ccoef = nullptr;
+  float2* ccoef32 = nullptr;
+  int4* ctab = nullptr;
+  int nsl = 0;
+  long overflow_rows = 0;
+  bool cc_tried = false;
   ~Op();
   void make_c64();           // (re)build coef32 (and pcoef32) from coef (pcoef)
   // (re)build the pair-compressed copy from coef; false (and no copy) when no +-2 pair
   // exists or a row holds both members.  Reuses its buffers when refreshing.
   bool pair_compress();
+  // (re)build the class-compressed copy; false (and no copy) when the union is not an upwind
+  // reach-2 set, compression would save < 20% of the planes, or > 5% of the warps hold overflow rows
+  bool class_compress();
   StencilDev dev() const;
   int center() const;
   const cplx* inv_diag();  // computes on first use; throws ValueError on a zero diagonal
@@ -160,6 +171,7 @@ extern long g_ce_max_n;  // levels with N <= this run inside the cluster engine 
 extern int g_kcycle_c64; // build hierarchies with complex64 operator storage (mixed-precision K-cycle)
 extern int g_ce_smem_relax;  // engine relaxations out of shared memory where they fit
 extern int g_pair_compress;  // pair-compress fine operators (outer A, hierarchy level 0)
+extern int g_class_compress;  // class-compress coarse graph-path levels: 0 off, 1 3D, 2 2D and 3D
 
 Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol);
 void hier_release(Hier* h);  // recycle (workspace + captured graphs) or delete

@@ -406,6 +406,47 @@ __device__ __forceinline__ void stencil_pc(const StencilArgs& a, long k, int i1,
   }
 }
 
+// Class-compressed coarse operator: slots of the row's class in ascending union order,
+// chunks of CH slots, every load of a chunk independent (table -> coefficient, x, D^-1).
+template <int CH, int INM, bool C32>
+__device__ __forceinline__ void stencil_cc(const StencilArgs& a, int cls, long k, int i1, int i2, int i3, int n1,
+                                           int n2, int n3, double s, cplx& acc) {
+  const int nsl = a.A.nsl;
+  const long cs = a.A.cstr;
+  const int4* tab = a.A.ctab + (long)cls * nsl;
+  for (int q0 = 0; q0 < nsl; q0 += CH) {
+    int4 t[CH];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) t[q] = __ldg(tab + (q0 + q < nsl ? q0 + q : 0));
+    cplx cv[CH], xv[CH], dv[CH];
+    bool ok[CH];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      const bool live = q0 + q < nsl;
+      const int j1 = i1 + t[q].y, j2 = i2 + t[q].z, j3 = i3 + t[q].w;
+      ok[q] = live && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2 && j3 >= 0 && j3 < n3;
+      const long jj = ok[q] ? k + t[q].x : k;
+      const long ci = (long)(live ? q0 + q : 0) * cs + k;
+      if constexpr (C32) {
+        const float2 c = __ldg(a.A.ccoef32 + ci);
+        cv[q] = make_double2((double)c.x, (double)c.y);
+      } else {
+        cv[q] = ldc(a.A.ccoef, ci);
+      }
+      xv[q] = ldc(a.x, jj);
+      if (INM & IN_JAC) dv[q] = ldc(a.dinv, jj);
+    }
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      cplx v = xv[q];
+      if (INM & IN_SCALE) v = cscale(v, s);
+      if (INM & IN_JAC) v = cmul_np(dv[q], v);
+      const cplx tt = cadd(acc, cmul_sp(cv[q], v));
+      acc = ok[q] ? tt : acc;
+    }
+  }
+}
+
 // Resident CTAs per SM: the pair-compressed relaxation variant (IN_JAC: 21 loads per
 // point in 2D) gets 128 registers so all of a point's loads issue back to back
 // (B200, 1025^2 fine sweep: 50.6 us union / 44.1 us at 4 CTAs / 41.4 us at 2 CTAs);
@@ -414,7 +455,7 @@ template <int INM, bool PC>
 constexpr int stencil_min_blocks() {
   return (PC && (INM & IN_JAC)) ? 2 : 4;
 }
-template <int INM, int OUTM, int RED, int NO, int CL, bool PC = false>
+template <int INM, int OUTM, int RED, int NO, int CL, bool PC = false, bool CC = false>
 __global__ void __launch_bounds__(kThreads, stencil_min_blocks<INM, PC>()) k_stencil(StencilArgs a) {
   pdl_enter();
   if (!gate_open(a.gate)) return;
@@ -443,6 +484,21 @@ __global__ void __launch_bounds__(kThreads, stencil_min_blocks<INM, PC>()) k_ste
         stencil_pc<NO, INM, true>(a, k, i1, i2, i3, n1, n2, n3, s, code, acc);
       else
         stencil_pc<NO, INM, false>(a, k, i1, i2, i3, n1, n2, n3, s, code, acc);
+    } else if constexpr (CC) {
+      const int cls = __ldg(a.A.ccode + k);
+      if (cls != 0xFF) {
+        if (a.A.ccoef32)
+          stencil_cc<9, INM, true>(a, cls, k, i1, i2, i3, n1, n2, n3, s, acc);
+        else
+          stencil_cc<9, INM, false>(a, cls, k, i1, i2, i3, n1, n2, n3, s, acc);
+      } else {  // overflow row: union planes
+        for (int o0 = 0; o0 < nofs; o0 += 9) {
+          if (c32)
+            stencil_chunk<9, INM, true>(a, o0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
+          else
+            stencil_chunk<9, INM, false>(a, o0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
+        }
+      }
     } else if constexpr (NO > 0) {
       if (c32)
         stencil_chunk<NO, INM, true>(a, 0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
@@ -651,6 +707,8 @@ static void dispatch_no(const LaunchCfg& lc, const StencilArgs& a, const Geo& ge
       launch_geo(k_stencil<INM, OUTM, RED, 9, 0, true>, geo, lc.stream, a);
     else
       launch_geo(k_stencil<INM, OUTM, RED, 13, 0, true>, geo, lc.stream, a);
+  } else if (a.A.ccode && !geo.cluster) {  // class-compressed coarse operator
+    launch_geo(k_stencil<INM, OUTM, RED, 0, 0, false, true>, geo, lc.stream, a);
   } else if (n == 5)
     launch_stencil_no<INM, OUTM, RED, 5>(lc, a, geo);
   else if (n == 9)
@@ -677,7 +735,7 @@ void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const Stenc
   // tiled kernel where it measured faster (B200): 2D operators with wide (Galerkin)
   // stencils; the 3D and 9-point fine-level sweeps keep the flat kernel, whose
   // neighbour re-reads L1 already absorbs (tools/prof_solve.py A/B)
-  if (g_stencil_tile && !geo.cluster && a.A.n1own >= 2 && !a.A.pcode &&
+  if (g_stencil_tile && !geo.cluster && a.A.n1own >= 2 && !a.A.pcode && !a.A.ccode &&
       (g_stencil_tile > 1 || (a.A.n3 == 1 && a.A.nofs > 9))) {
     const bool d3 = a.A.n3 > 1;
     TileCfg t{};
@@ -1525,6 +1583,63 @@ void launch_pair_compress(cudaStream_t s, const StencilDev& A, int nslot, const 
   long b = (n + 255) / 256;
   if (b > 148 * 16) b = 148 * 16;
   k_pair_compress<<<(int)b, 256, 0, s>>>(A, t, pcoef, pstr, pcode, conflict);
+}
+
+struct ClassTab {
+  unsigned long long live[8][2];
+  int tab[8 * 64];
+};
+__global__ void k_class_compress(StencilDev A, int ncls, int nsl, ClassTab t, cplx* __restrict__ ccoef, long cstr,
+                                 uint8_t* __restrict__ ccode, unsigned long long* overflow) {
+  const long n = (long)A.n1own * A.n2 * A.n3;
+  unsigned long long cnt = 0;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    unsigned long long m0 = 0, m1 = 0;
+    for (int o = 0; o < A.nofs; ++o) {
+      const cplx c = A.coef[(long)o * A.pstride + k];
+      if (c.x != 0.0 || c.y != 0.0) {
+        if (o < 64)
+          m0 |= 1ull << o;
+        else
+          m1 |= 1ull << (o - 64);
+      }
+    }
+    int cls = 0xFF;
+    for (int c = 0; c < ncls; ++c)
+      if ((m0 & ~t.live[c][0]) == 0 && (m1 & ~t.live[c][1]) == 0) {
+        cls = c;
+        break;
+      }
+    ccode[k] = (uint8_t)cls;
+    // a warp's 32 consecutive rows diverge into the union path if any of them overflows
+    const unsigned any = __ballot_sync(__activemask(), cls == 0xFF);
+    if (cls == 0xFF) {
+      ++cnt;
+    } else {
+      for (int q = 0; q < nsl; ++q) {
+        const int o = t.tab[cls * nsl + q];  // -1: padding slot (zero coefficient)
+        ccoef[(long)q * cstr + k] = o >= 0 ? A.coef[(long)o * A.pstride + k] : mk(0.0, 0.0);
+      }
+    }
+    if (any && (threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(overflow + 1, 1ull);
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(overflow, cnt);
+}
+
+void launch_class_compress(cudaStream_t s, const StencilDev& A, int ncls, const unsigned long long* live,
+                           int nsl, const int* tab, cplx* ccoef, long cstr, uint8_t* ccode,
+                           unsigned long long* overflow) {
+  ClassTab t{};
+  for (int c = 0; c < ncls; ++c) {
+    t.live[c][0] = live[2 * c];
+    t.live[c][1] = live[2 * c + 1];
+    for (int q = 0; q < nsl; ++q) t.tab[c * nsl + q] = tab[c * nsl + q];
+  }
+  const long n = (long)A.n1own * A.n2 * A.n3;
+  long b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  k_class_compress<<<(int)b, 256, 0, s>>>(A, ncls, nsl, t, ccoef, cstr, ccode, overflow);
 }
 
 // slot layout of the pair-compressed plus-radius-2 union (nofs 9 or 13), see PcLayout

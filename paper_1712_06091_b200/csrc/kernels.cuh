@@ -36,6 +36,18 @@ struct StencilDev {
   const cplx* pcoef;
   const float2* pcoef32;
   long pstr;
+  // Class-compressed copy (coarse Galerkin operators of upwind fine operators): a row's
+  // non-zeros fit one of the 2^dim upwind sign classes (box offsets |d| <= 1 plus the
+  // +-2 offsets on each axis's upwind side); class c keeps nsl slot planes whose union
+  // offsets ctab[c * nsl + q] ascend.  ccode[k] = class, or 0xFF: the row overflows
+  // every class and is applied from the union planes.  Slot planes cstr apart, owned
+  // points only.
+  const uint8_t* ccode;
+  const cplx* ccoef;
+  const float2* ccoef32;
+  const int4* ctab;  // {linear displacement, d1, d2, d3} per (class, slot)
+  long cstr;
+  int nsl;
 };
 
 // coefficient from complex64 storage, widened to complex128 for the arithmetic
@@ -179,6 +191,12 @@ void launch_to_c64(cudaStream_t s, long n, const cplx* in, float2* out);
 int pair_layout(int nofs, int* pos_a, int* pos_b, int* bit);
 void launch_pair_compress(cudaStream_t s, const StencilDev& A, int nslot, const int* pos_a, const int* pos_b,
                           const int* bit, cplx* pcoef, long pstr, uint8_t* pcode, int* conflict);
+// class compression of the owned rows: live[c] = 2 x u64 offset bitset of class c, tab[c*nsl + q]
+// = union offset of slot q; writes ccode / ccoef; overflow[0] += overflow rows, overflow[1] += warps
+// (32 consecutive rows) holding at least one
+void launch_class_compress(cudaStream_t s, const StencilDev& A, int ncls, const unsigned long long* live,
+                           int nsl, const int* tab, cplx* ccoef, long cstr, uint8_t* ccode,
+                           unsigned long long* overflow);
 void launch_phase(cudaStream_t s, long n, const cplx* q, const double* tau, double omega, int sign, cplx* out);
 void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, int n3c, unsigned long long* mask,
                      const int* slot_of, cplx* coef_c, int q0 = 0, int nq = -1, long cstride = -1);

@@ -95,8 +95,17 @@ class StencilOperator:
         import ctypes as C
 
         n = C.c_int()
-        check(_lib.lib().hadr_op_storage(self._h, C.byref(n)))
+        check(_lib.lib().hadr_op_storage(self._h, C.byref(n), None))
         return n.value
+
+    @property
+    def overflow_rows(self) -> int:
+        """Rows of a class-compressed operator applied from the union planes."""
+        import ctypes as C
+
+        n, ov = C.c_int(), C.c_longlong()
+        check(_lib.lib().hadr_op_storage(self._h, C.byref(n), C.byref(ov)))
+        return ov.value
 
     def planes(self) -> np.ndarray:
         n = self.shape[0]

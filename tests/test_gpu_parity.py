@@ -123,6 +123,22 @@ def test_pair_compressed_solve_identical(hadr, c64):
     assert out[0][2] == out[1][2]
 
 
+def test_class_compressed_coarse_bitexact_2d(hadr, g65):
+    """2D coarse 21-offset operators class-compressed (option class_compress 2: rows fit
+    one of 4 upwind sign classes, 15 slot planes) reproduce csr_matvec bit for bit."""
+    A = csr_from(g65, "lev1")
+    rng = np.random.default_rng(17)
+    x = rng.standard_normal(A.shape[0]) + 1j * rng.standard_normal(A.shape[0])
+    try:
+        hadr._lib.set_option("class_compress", 2)
+        op = hadr.StencilOperator.from_csr(A, (33, 33))
+        y = op @ x
+        assert op.storage_slots == 15
+    finally:
+        hadr._lib.set_option("class_compress", 2)
+    assert np.array_equal(y, A @ x)
+
+
 def test_spmv_golden(hadr, g65):
     A = csr_from(g65, "blend")
     op = hadr.StencilOperator.from_csr(A, _shape(g65))

@@ -204,3 +204,52 @@ def test_cfg5_recipe_solves(hadr, cfg5_small):
     u_sl, rs = drivers.solve_standard(H, q, wl.medium, wl.omega, cfg_sl)
     assert rs.converged and abs(rs.iterations - rs_ref.iterations) <= 1
     assert rel(u_sl, u_ref) <= 1e-8
+
+
+def test_class_compressed_coarse_bitexact_3d(hadr, case3d):
+    """Coarse 81-offset Galerkin operators stored class-compressed (rows fit one of 8
+    upwind sign classes: 54 slot planes; overflow rows from the union planes) reproduce
+    csr_matvec bit for bit, and equal the union-plane kernel."""
+    A1 = case3d["Hi"].ops[1]
+    shape1 = case3d["Hi"].shapes[1]
+    rng = np.random.default_rng(13)
+    x = rng.standard_normal(A1.shape[0]) + 1j * rng.standard_normal(A1.shape[0])
+    ys = {}
+    try:
+        for cc in (0, 1):
+            hadr._lib.set_option("class_compress", cc)
+            op = hadr.StencilOperator.from_csr(A1, shape1)
+            ys[cc] = op @ x
+            assert op.storage_slots == (54 if cc else 0)
+    finally:
+        hadr._lib.set_option("class_compress", 2)
+    assert np.array_equal(ys[1], A1 @ x)
+    assert np.array_equal(ys[0], ys[1])
+
+
+@pytest.mark.parametrize("c64", [0, 1])
+def test_compressed_solve_identical_3d(hadr, c64):
+    """A 3D solve whose coarse levels take the graph path (cl_max_n lowered) with the
+    pair-compressed fine and class-compressed coarse operators is bit-identical to the
+    union-plane solve (complex128 and mixed precision)."""
+    from paper_1712_06091_b200 import drivers, workloads
+
+    wl = workloads.cfg4(33)
+    cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=1e-6, max_iter=1000)
+    out = {}
+    hadr._lib.set_option("cl_max_n", 1000)
+    hadr._lib.set_option("ce_max_n", 1000)
+    hadr._lib.set_option("kcycle_c64", c64)
+    try:
+        for cmp in (0, 1):
+            hadr._lib.set_option("class_compress", cmp)
+            hadr._lib.set_option("pair_compress", cmp)
+            u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
+            out[cmp] = (a, rep.iterations, list(rep.history))
+    finally:
+        for k, v in (("class_compress", 2), ("pair_compress", 1), ("cl_max_n", 32768), ("ce_max_n", 32768),
+                     ("kcycle_c64", 0)):
+            hadr._lib.set_option(k, v)
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][2] == out[1][2]
