@@ -495,6 +495,8 @@ int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, 
     const cplx* xd = (const cplx*)x;
     cplx* yd = (cplx*)y;
     cplx* vtmp = dalloc<cplx>(op->N);
+    cplx* utmp = dalloc<cplx>(op->N);  // dot partner V0: its own stream, as in the relaxation
+    HADR_CUDA(cudaMemsetAsync(utmp, 0, op->N * sizeof(cplx), c.stream));
     double* sc = c.dscal + 56;
     const double one = 1.0;
     HADR_CUDA(cudaMemcpyAsync(sc, &one, sizeof(double), cudaMemcpyHostToDevice, c.stream));
@@ -512,7 +514,7 @@ int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, 
         a.scale = sc;
         a.dinv = op->inv_diag();
         a.vout = vtmp;
-        a.u = xd;
+        a.u = utmp;
         a.epi = epi_store(c.dscal);
         launch_stencil(c.lc, IN_SCALE | IN_JAC | IN_WRITEV, OUT_APPLY, RED_DOT, a);
       }
@@ -531,6 +533,7 @@ int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, 
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     dfree(vtmp);
+    dfree(utmp);
   });
 }
 

@@ -478,6 +478,12 @@ __global__ void __launch_bounds__(kThreads, stencil_min_blocks<INM, PC>()) k_ste
     const int i2 = rem / n3;
     const int i3 = rem - i2 * n3;
     cplx acc = mk(0.0, 0.0);
+    // the point's own streams (centre, residual rhs, dot partner) are loaded up front with
+    // the stencil's loads rather than after the accumulation (one memory round trip less)
+    cplx xc = mk(0.0, 0.0), bk = mk(0.0, 0.0), uk = mk(0.0, 0.0);
+    if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) xc = ldc(a.x, k);
+    if (OUTM == OUT_RESID) bk = ldc(a.b, k);
+    if (RED & RED_DOT) uk = ldc(a.u, k);
     if constexpr (PC) {
       const unsigned code = __ldg(a.A.pcode + k);
       if (a.A.pcoef32)
@@ -514,15 +520,15 @@ __global__ void __launch_bounds__(kThreads, stencil_min_blocks<INM, PC>()) k_ste
     }
     cplx vc = mk(0.0, 0.0);
     if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) {
-      vc = ldc(a.x, k);
+      vc = xc;
       if (INM & IN_SCALE) vc = cscale(vc, s);
       if (INM & IN_WRITEV) a.vout[k] = vc;
     }
-    cplx y = (OUTM == OUT_RESID) ? csub(ldc(a.b, k), acc) : acc;
+    cplx y = (OUTM == OUT_RESID) ? csub(bk, acc) : acc;
     a.y[k] = y;
     if (RED & RED_NORM) red[0] += y.x * y.x + y.y * y.y;
     if (RED & (RED_DOT | RED_DOT_CENTER)) {
-      const cplx u = (RED & RED_DOT_CENTER) ? vc : ldc(a.u, k);
+      const cplx u = (RED & RED_DOT_CENTER) ? vc : uk;
       constexpr int o = (RED & RED_NORM) ? 1 : 0;
       red[o] += u.x * y.x + u.y * y.y;
       red[o + 1] += u.x * y.y - u.y * y.x;
@@ -615,6 +621,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_tile(StencilArgs a, Til
       const int i1 = il + p0, i2 = d3 ? y : x, i3 = d3 ? x : 0;
       const int tidx = (pp + 2) * sP + (py + t.hy) * sY + (px + 2);
       cplx acc = mk(0.0, 0.0);
+      cplx xc = mk(0.0, 0.0), bk = mk(0.0, 0.0), uk = mk(0.0, 0.0);  // issued with the stencil's loads
+      if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) xc = ldc(a.x, k);
+      if (OUTM == OUT_RESID) bk = ldc(a.b, k);
+      if (RED & RED_DOT) uk = ldc(a.u, k);
       if constexpr (NO > 0) {
         if (c32)
           tile_chunk<NO, true>(a, tl, 0, nofs, k, i1, i2, i3, n1, n2, n3, N, tidx, sP, sY, d3, acc);
@@ -630,15 +640,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_tile(StencilArgs a, Til
       }
       cplx vc = mk(0.0, 0.0);
       if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) {
-        vc = ldc(a.x, k);
+        vc = xc;
         if (INM & IN_SCALE) vc = cscale(vc, s);
         if (INM & IN_WRITEV) a.vout[k] = vc;
       }
-      cplx yv = (OUTM == OUT_RESID) ? csub(ldc(a.b, k), acc) : acc;
+      cplx yv = (OUTM == OUT_RESID) ? csub(bk, acc) : acc;
       a.y[k] = yv;
       if (RED & RED_NORM) red[0] += yv.x * yv.x + yv.y * yv.y;
       if (RED & (RED_DOT | RED_DOT_CENTER)) {
-        const cplx u = (RED & RED_DOT_CENTER) ? vc : ldc(a.u, k);
+        const cplx u = (RED & RED_DOT_CENTER) ? vc : uk;
         constexpr int o = (RED & RED_NORM) ? 1 : 0;
         red[o] += u.x * yv.x + u.y * yv.y;
         red[o + 1] += u.x * yv.y - u.y * yv.x;
