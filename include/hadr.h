@@ -66,12 +66,12 @@ int hadr_op_from_csr(int n1, int n2, int n3, int64_t nnz, const int64_t* indptr,
 int hadr_op_from_planes(int n1, int n2, int n3, int n_offsets, const int* offsets, const double* coef, hadr_op* out);
 int hadr_op_info(hadr_op op, int* n1, int* n2, int* n3, int* n_offsets, int* offsets /* 3*125 */);
 int hadr_op_export(hadr_op op, double* coef /* n_offsets*N complex */);
-/* storage of the operator's stencil kernel: *n_slots = coefficient planes the apply reads from the
- * pair-compressed copy (fine upwind operators: 2D 7, 3D 10) or the class-compressed copy (coarse upwind
- * Galerkin operators: 2D 15, 3D 54), 0 = union planes (n_offsets).  Built lazily by the first apply /
+/* storage of the operator's stencil kernel: *n_slots = coefficient planes stored in the pair-compressed
+ * copy (fine upwind operators: 2D 7, 3D 10) or the class-compressed copy (coarse upwind Galerkin
+ * operators: the largest class present; interior rows read 2D 15, 3D 54), 0 = union planes (n_offsets).  Built lazily by the first apply /
  * solve (options "pair_compress", "class_compress"); no reference counterpart (layout only). */
-int hadr_op_storage(hadr_op op, int* n_slots, long long* overflow_rows /* class-compressed rows applied
-                                                                           from the union planes */);
+int hadr_op_storage(hadr_op op, int* n_slots, long long* mixed_rows /* class-compressed rows whose class
+                                                                        holds both +-2 sides of an axis */);
 /* y = A x  (helmadr/krylov.py:60-65 spmv; scipy csr_matvec order, bit-exact) */
 int hadr_op_apply(hadr_op op, const double* x, double* y, int on_device);
 /* z = r / diag(A)  (helmadr/krylov.py:68-73 jacobi_apply) */

@@ -254,7 +254,7 @@ int hadr_op_apply(hadr_op h, const double* x, double* y, int on_device) {
 int hadr_op_storage(hadr_op h, int* n_slots, long long* overflow_rows) {
   return guarded([&] {
     *n_slots = h->op->pcode ? h->op->nslot : h->op->ccode ? h->op->nsl : 0;
-    if (overflow_rows) *overflow_rows = h->op->ccode ? h->op->overflow_rows : 0;
+    if (overflow_rows) *overflow_rows = h->op->ccode ? h->op->mixed_rows : 0;
   });
 }
 

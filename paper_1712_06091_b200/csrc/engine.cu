@@ -106,6 +106,7 @@ Op::~Op() {
   dfree(ccoef);
   dfree(ccoef32);
   dfree(ctab);
+  dfree(cnsl);
 }
 
 void Op::make_c64() {
@@ -130,10 +131,12 @@ bool Op::class_compress() {
     dfree(ccoef);
     dfree(ccoef32);
     dfree(ctab);
+    dfree(cnsl);
     ccode = nullptr;
     ccoef = nullptr;
     ccoef32 = nullptr;
     ctab = nullptr;
+    cnsl = nullptr;
     nsl = 0;
     return false;
   };
@@ -147,59 +150,86 @@ bool Op::class_compress() {
     }
     if (far > 1) return drop();
   }
-  const int ncls = 1 << dim;
-  unsigned long long live[16] = {0};
-  int tab[8 * 64];
-  int ns = 0;
-  std::vector<std::vector<int>> sl(ncls);
+  // classes: per axis '-' (only the -2 side), '+' or both; ordered by size so the
+  // classifier's first fit is the smallest class that covers the row
+  int ncls = 1;
+  for (int ax = 0; ax < dim; ++ax) ncls *= 3;
+  struct Cls {
+    std::vector<int> offs;
+    int mixed;
+  };
+  std::vector<Cls> cl;
   for (int c = 0; c < ncls; ++c) {
+    int st[3] = {0, 0, 0}, cc = c, mixed = 0;
+    for (int ax = 0; ax < dim; ++ax) {
+      st[ax] = cc % 3;
+      cc /= 3;
+      mixed |= st[ax] == 2;
+    }
+    Cls k{{}, mixed};
     for (int o = 0; o < nofs; ++o) {
       const int a[3] = {d1[o], d2[o], d3[o]};
       bool in = true;
       for (int ax = 0; ax < dim; ++ax)
-        if (a[ax] == 2 || a[ax] == -2) in = in && ((a[ax] > 0) == (((c >> ax) & 1) != 0));
-      if (!in) continue;
-      sl[c].push_back(o);
-      live[2 * c + (o >> 6)] |= 1ull << (o & 63);
+        if (a[ax] == 2 || a[ax] == -2) in = in && (st[ax] == 2 || (a[ax] > 0) == (st[ax] == 1));
+      if (in) k.offs.push_back(o);
     }
-    ns = std::max(ns, (int)sl[c].size());
+    cl.push_back(k);
   }
-  if (ns > 64 || ns * 5 > nofs * 4) return drop();  // < 20% of the planes saved
-  for (int c = 0; c < ncls; ++c)
-    for (int q = 0; q < ns; ++q) tab[c * ns + q] = q < (int)sl[c].size() ? sl[c][q] : -1;
-  const long n = nloc();
-  if (ccode && nsl != ns) drop();
-  if (!ccode) {
-    ccode = dalloc<uint8_t>(n);
-    ccoef = dalloc<cplx>((size_t)ns * n);
-    ctab = dalloc<int4>((size_t)ncls * ns);
+  std::stable_sort(cl.begin(), cl.end(), [](const Cls& x, const Cls& y) { return x.offs.size() < y.offs.size(); });
+  std::vector<unsigned long long> live(2 * ncls, 0ull);
+  std::vector<int> hn(ncls), hm(ncls);
+  for (int c = 0; c < ncls; ++c) {
+    for (int o : cl[c].offs) live[2 * c + (o >> 6)] |= 1ull << (o & 63);
+    hn[c] = (int)cl[c].offs.size();
+    hm[c] = cl[c].mixed;
   }
-  nsl = ns;
-  std::vector<int4> ht((size_t)ncls * ns);
-  for (int c = 0; c < ncls; ++c)
-    for (int q = 0; q < ns; ++q) {
-      const int o = tab[c * ns + q];
-      ht[(size_t)c * ns + q] =
-          o >= 0 ? make_int4((int)(((long)d1[o] * n2 + d2[o]) * n3 + d3[o]), d1[o], d2[o], d3[o]) : make_int4(0, 0, 0, 0);
-    }
+  if (hn[0] * 5 > nofs * 4) return drop();  // even the smallest class saves < 20% of the planes
   Ctx& cx = Ctx::get();
-  HADR_CUDA(cudaMemcpyAsync(ctab, ht.data(), ht.size() * sizeof(int4), cudaMemcpyHostToDevice, cx.stream));
-  unsigned long long* cnt = (unsigned long long*)(cx.dscal + 48);
-  HADR_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), cx.stream));
+  const long n = nloc();
+  const bool refresh = ccode != nullptr;
+  if (!ccode) ccode = dalloc<uint16_t>(n);
+  if (!cnsl) cnsl = dalloc<int>(ncls);
+  unsigned long long* dlive = dalloc<unsigned long long>(2 * ncls);
+  int* dmix = dalloc<int>(ncls);
+  HADR_CUDA(cudaMemcpyAsync(dlive, live.data(), live.size() * 8, cudaMemcpyHostToDevice, cx.stream));
+  HADR_CUDA(cudaMemcpyAsync(cnsl, hn.data(), ncls * sizeof(int), cudaMemcpyHostToDevice, cx.stream));
+  HADR_CUDA(cudaMemcpyAsync(dmix, hm.data(), ncls * sizeof(int), cudaMemcpyHostToDevice, cx.stream));
+  unsigned long long* st = (unsigned long long*)(cx.dscal + 48);
+  HADR_CUDA(cudaMemsetAsync(st, 0, 3 * sizeof(unsigned long long), cx.stream));
   StencilDev A = dev();
-  launch_class_compress(cx.stream, A, ncls, live, ns, tab, ccoef, n, ccode, cnt);
+  launch_class_classify(cx.stream, A, ncls, dlive, cnsl, dmix, ccode, st);
   HADR_CUDA(cudaGetLastError());
-  unsigned long long ov[2] = {0, 0};
-  HADR_CUDA(cudaMemcpyAsync(ov, cnt, sizeof(ov), cudaMemcpyDeviceToHost, cx.stream));
+  unsigned long long hs[3] = {0, 0, 0};
+  HADR_CUDA(cudaMemcpyAsync(hs, st, sizeof(hs), cudaMemcpyDeviceToHost, cx.stream));
   cx.sync();
-  overflow_rows = (long)ov[0];
-  // warps that hold an overflow row run both paths: measured on B200, 5.5% overflow rows
-  // scattered by a random medium (config 5) made the apply 30% slower than the union planes
-  unsigned long long bad = (long)ov[1] * 32 * 20 > n ? 1ull : 0ull;  // > 5% of the warps
-  if (slab()) {  // every rank takes the same kernel path
-    dist_comm()->allreduce_or_u64(&bad, 1, cx.stream);
-  }
+  dfree(dlive);
+  dfree(dmix);
+  mixed_rows = (long)hs[2];
+  const int used = (int)hs[1];
+  // worth it only if the rows read clearly fewer planes than the union on average
+  unsigned long long bad = (hs[0] * 100 > (unsigned long long)n * nofs * 85) ? 1ull : 0ull;
+  if (refresh && used != nsl) bad = 1;  // the captured graphs hold the old layout
+  if (slab()) dist_comm()->allreduce_or_u64(&bad, 1, cx.stream);  // every rank takes the same path
   if (bad) return drop();
+  if (!ccoef) ccoef = dalloc<cplx>((size_t)used * n);
+  if (!ctab) ctab = dalloc<int4>((size_t)ncls * used);
+  nsl = used;
+  std::vector<int> otab((size_t)ncls * used, 0);
+  std::vector<int4> ht((size_t)ncls * used, make_int4(0, 0, 0, 0));
+  for (int c = 0; c < ncls; ++c)
+    for (int q = 0; q < std::min(hn[c], used); ++q) {
+      const int o = cl[c].offs[q];
+      otab[(size_t)c * used + q] = o;
+      ht[(size_t)c * used + q] = make_int4((int)(((long)d1[o] * n2 + d2[o]) * n3 + d3[o]), d1[o], d2[o], d3[o]);
+    }
+  int* dot = dalloc<int>(otab.size());
+  HADR_CUDA(cudaMemcpyAsync(dot, otab.data(), otab.size() * sizeof(int), cudaMemcpyHostToDevice, cx.stream));
+  HADR_CUDA(cudaMemcpyAsync(ctab, ht.data(), ht.size() * sizeof(int4), cudaMemcpyHostToDevice, cx.stream));
+  launch_class_fill(cx.stream, A, ccode, cnsl, dot, used, ccoef, n);
+  HADR_CUDA(cudaGetLastError());
+  cx.sync();
+  dfree(dot);
   if (coef32) {
     if (!ccoef32) ccoef32 = dalloc<float2>((size_t)nsl * n);
     launch_to_c64(cx.stream, (long)nsl * n, ccoef, ccoef32);
@@ -292,6 +322,7 @@ StencilDev Op::dev() const {
   s.ccoef = ccoef;
   s.ccoef32 = ccoef32;
   s.ctab = ctab;
+  s.cnsl = cnsl;
   s.cstr = nloc();
   s.nsl = nsl;
   return s;

@@ -70,12 +70,13 @@ struct Op {
   int nslot = 0;
   bool pc_tried = false;
   // class-compressed copy of the owned rows (StencilDev::ccode), coarse upwind Galerkin operators
-  uint8_t* ccode = nullptr;
+  uint16_t* ccode = nullptr;
   cplx* ccoef = nullptr;
   float2* ccoef32 = nullptr;
   int4* ctab = nullptr;
+  int* cnsl = nullptr;
   int nsl = 0;
-  long overflow_rows = 0;
+  long mixed_rows = 0;  // rows whose class holds both +-2 sides of some axis
   bool cc_tried = false;
   ~Op();
   void make_c64();           // (re)build coef32 (and pcoef32) from coef (pcoef)
@@ -83,7 +84,7 @@ struct Op {
   // exists or a row holds both members.  Reuses its buffers when refreshing.
   bool pair_compress();
   // (re)build the class-compressed copy; false (and no copy) when the union is not an upwind
-  // reach-2 set, compression would save < 20% of the planes, or > 5% of the warps hold overflow rows
+  // reach-2 set or the rows would read more than 85% of the union's planes on average
   bool class_compress();
   StencilDev dev() const;
   int center() const;

@@ -408,21 +408,24 @@ __device__ __forceinline__ void stencil_pc(const StencilArgs& a, long k, int i1,
 
 // Class-compressed coarse operator: slots of the row's class in ascending union order,
 // chunks of CH slots, every load of a chunk independent (table -> coefficient, x, D^-1).
+// Class-compressed coarse operator: the row's class slots in ascending union order, chunks
+// of CH slots, every load of a chunk independent (table -> coefficient, x, D^-1).
 template <int CH, int INM, bool C32>
-__device__ __forceinline__ void stencil_cc(const StencilArgs& a, int cls, long k, int i1, int i2, int i3, int n1,
-                                           int n2, int n3, double s, cplx& acc) {
-  const int nsl = a.A.nsl;
+__device__ __forceinline__ void stencil_cc(const StencilArgs& a, int cls, int nslc, long k, int i1, int i2, int i3,
+                                           int n1, int n2, int n3, double s, cplx& acc) {
+  // warp-uniform trip count (the warp's largest class); slots past a row's own class are dead
+  const int nsw = __reduce_max_sync(__activemask(), (unsigned)nslc);
   const long cs = a.A.cstr;
-  const int4* tab = a.A.ctab + (long)cls * nsl;
-  for (int q0 = 0; q0 < nsl; q0 += CH) {
+  const int4* tab = a.A.ctab + (long)cls * a.A.nsl;
+  for (int q0 = 0; q0 < nsw; q0 += CH) {
     int4 t[CH];
 #pragma unroll
-    for (int q = 0; q < CH; ++q) t[q] = __ldg(tab + (q0 + q < nsl ? q0 + q : 0));
+    for (int q = 0; q < CH; ++q) t[q] = __ldg(tab + (q0 + q < nslc ? q0 + q : 0));
     cplx cv[CH], xv[CH], dv[CH];
     bool ok[CH];
 #pragma unroll
     for (int q = 0; q < CH; ++q) {
-      const bool live = q0 + q < nsl;
+      const bool live = q0 + q < nslc;
       const int j1 = i1 + t[q].y, j2 = i2 + t[q].z, j3 = i3 + t[q].w;
       ok[q] = live && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2 && j3 >= 0 && j3 < n3;
       const long jj = ok[q] ? k + t[q].x : k;
@@ -451,12 +454,13 @@ __device__ __forceinline__ void stencil_cc(const StencilArgs& a, int cls, long k
 // point in 2D) gets 128 registers so all of a point's loads issue back to back
 // (B200, 1025^2 fine sweep: 50.6 us union / 44.1 us at 4 CTAs / 41.4 us at 2 CTAs);
 // plain applies keep 4 CTAs (26.3 us vs 30.6 us at 2).
-template <int INM, bool PC>
+// (the class-compressed kernel measured fastest at 4 CTAs/SM in every variant)
+template <int INM, bool PC, bool CC>
 constexpr int stencil_min_blocks() {
   return (PC && (INM & IN_JAC)) ? 2 : 4;
 }
 template <int INM, int OUTM, int RED, int NO, int CL, bool PC = false, bool CC = false>
-__global__ void __launch_bounds__(kThreads, stencil_min_blocks<INM, PC>()) k_stencil(StencilArgs a) {
+__global__ void __launch_bounds__(kThreads, stencil_min_blocks<INM, PC, CC>()) k_stencil(StencilArgs a) {
   pdl_enter();
   if (!gate_open(a.gate)) return;
   const int n1 = a.A.n1, n2 = a.A.n2, n3 = a.A.n3, nofs = a.A.nofs;
@@ -491,20 +495,12 @@ __global__ void __launch_bounds__(kThreads, stencil_min_blocks<INM, PC>()) k_ste
       else
         stencil_pc<NO, INM, false>(a, k, i1, i2, i3, n1, n2, n3, s, code, acc);
     } else if constexpr (CC) {
-      const int cls = __ldg(a.A.ccode + k);
-      if (cls != 0xFF) {
-        if (a.A.ccoef32)
-          stencil_cc<9, INM, true>(a, cls, k, i1, i2, i3, n1, n2, n3, s, acc);
-        else
-          stencil_cc<9, INM, false>(a, cls, k, i1, i2, i3, n1, n2, n3, s, acc);
-      } else {  // overflow row: union planes
-        for (int o0 = 0; o0 < nofs; o0 += 9) {
-          if (c32)
-            stencil_chunk<9, INM, true>(a, o0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
-          else
-            stencil_chunk<9, INM, false>(a, o0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
-        }
-      }
+      const unsigned cw = __ldg(a.A.ccode + k);
+      const int cls = (int)(cw & 0xFFu);
+      if (a.A.ccoef32)
+        stencil_cc<9, INM, true>(a, cls, (int)(cw >> 8), k, i1, i2, i3, n1, n2, n3, s, acc);
+      else
+        stencil_cc<9, INM, false>(a, cls, (int)(cw >> 8), k, i1, i2, i3, n1, n2, n3, s, acc);
     } else if constexpr (NO > 0) {
       if (c32)
         stencil_chunk<NO, INM, true>(a, 0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
@@ -1595,14 +1591,12 @@ void launch_pair_compress(cudaStream_t s, const StencilDev& A, int nslot, const 
   k_pair_compress<<<(int)b, 256, 0, s>>>(A, t, pcoef, pstr, pcode, conflict);
 }
 
-struct ClassTab {
-  unsigned long long live[8][2];
-  int tab[8 * 64];
-};
-__global__ void k_class_compress(StencilDev A, int ncls, int nsl, ClassTab t, cplx* __restrict__ ccoef, long cstr,
-                                 uint8_t* __restrict__ ccode, unsigned long long* overflow) {
+__global__ void k_class_classify(StencilDev A, int ncls, const unsigned long long* __restrict__ live,
+                                 const int* __restrict__ cnsl, const int* __restrict__ mixed,
+                                 uint16_t* __restrict__ ccode, unsigned long long* stats) {
   const long n = (long)A.n1own * A.n2 * A.n3;
-  unsigned long long cnt = 0;
+  unsigned long long slots = 0, nmix = 0;
+  int mx = 0;
   for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
     unsigned long long m0 = 0, m1 = 0;
     for (int o = 0; o < A.nofs; ++o) {
@@ -1614,42 +1608,55 @@ __global__ void k_class_compress(StencilDev A, int ncls, int nsl, ClassTab t, cp
           m1 |= 1ull << (o - 64);
       }
     }
-    int cls = 0xFF;
+    int cls = ncls - 1;  // the last class (every axis 'both') is the whole union
     for (int c = 0; c < ncls; ++c)
-      if ((m0 & ~t.live[c][0]) == 0 && (m1 & ~t.live[c][1]) == 0) {
+      if ((m0 & ~live[2 * c]) == 0 && (m1 & ~live[2 * c + 1]) == 0) {
         cls = c;
         break;
       }
-    ccode[k] = (uint8_t)cls;
-    // a warp's 32 consecutive rows diverge into the union path if any of them overflows
-    const unsigned any = __ballot_sync(__activemask(), cls == 0xFF);
-    if (cls == 0xFF) {
-      ++cnt;
-    } else {
-      for (int q = 0; q < nsl; ++q) {
-        const int o = t.tab[cls * nsl + q];  // -1: padding slot (zero coefficient)
-        ccoef[(long)q * cstr + k] = o >= 0 ? A.coef[(long)o * A.pstride + k] : mk(0.0, 0.0);
-      }
-    }
-    if (any && (threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(overflow + 1, 1ull);
+    ccode[k] = (uint16_t)(cls | (cnsl[cls] << 8));
+    slots += cnsl[cls];
+    nmix += mixed[cls];
+    mx = max(mx, cnsl[cls]);
   }
-  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(overflow, cnt);
+  for (int o = 16; o > 0; o >>= 1) {
+    slots += __shfl_xor_sync(0xffffffffu, slots, o);
+    nmix += __shfl_xor_sync(0xffffffffu, nmix, o);
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(stats, slots);
+    atomicMax(stats + 1, (unsigned long long)mx);
+    atomicAdd(stats + 2, nmix);
+  }
 }
 
-void launch_class_compress(cudaStream_t s, const StencilDev& A, int ncls, const unsigned long long* live,
-                           int nsl, const int* tab, cplx* ccoef, long cstr, uint8_t* ccode,
-                           unsigned long long* overflow) {
-  ClassTab t{};
-  for (int c = 0; c < ncls; ++c) {
-    t.live[c][0] = live[2 * c];
-    t.live[c][1] = live[2 * c + 1];
-    for (int q = 0; q < nsl; ++q) t.tab[c * nsl + q] = tab[c * nsl + q];
-  }
+__global__ void k_class_fill(StencilDev A, const uint16_t* __restrict__ ccode, const int* __restrict__ cnsl,
+                             const int* __restrict__ otab, int nsl, cplx* __restrict__ ccoef, long cstr) {
   const long n = (long)A.n1own * A.n2 * A.n3;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    const int c = ccode[k] & 0xFF;
+    const int m = cnsl[c];
+    for (int q = 0; q < m; ++q) ccoef[(long)q * cstr + k] = A.coef[(long)otab[c * nsl + q] * A.pstride + k];
+  }
+}
+
+static int setup_blocks(long n) {
   long b = (n + 255) / 256;
   if (b > 148 * 16) b = 148 * 16;
-  k_class_compress<<<(int)b, 256, 0, s>>>(A, ncls, nsl, t, ccoef, cstr, ccode, overflow);
+  return (int)(b < 1 ? 1 : b);
+}
+
+void launch_class_classify(cudaStream_t s, const StencilDev& A, int ncls, const unsigned long long* live_dev,
+                           const int* cnsl_dev, const int* mixed_dev, uint16_t* ccode, unsigned long long* stats) {
+  const long n = (long)A.n1own * A.n2 * A.n3;
+  k_class_classify<<<setup_blocks(n), 256, 0, s>>>(A, ncls, live_dev, cnsl_dev, mixed_dev, ccode, stats);
+}
+
+void launch_class_fill(cudaStream_t s, const StencilDev& A, const uint16_t* ccode, const int* cnsl_dev,
+                       const int* otab_dev, int nsl, cplx* ccoef, long cstr) {
+  const long n = (long)A.n1own * A.n2 * A.n3;
+  k_class_fill<<<setup_blocks(n), 256, 0, s>>>(A, ccode, cnsl_dev, otab_dev, nsl, ccoef, cstr);
 }
 
 // slot layout of the pair-compressed plus-radius-2 union (nofs 9 or 13), see PcLayout

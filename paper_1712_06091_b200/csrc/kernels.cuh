@@ -37,17 +37,19 @@ struct StencilDev {
   const float2* pcoef32;
   long pstr;
   // Class-compressed copy (coarse Galerkin operators of upwind fine operators): a row's
-  // non-zeros fit one of the 2^dim upwind sign classes (box offsets |d| <= 1 plus the
-  // +-2 offsets on each axis's upwind side); class c keeps nsl slot planes whose union
-  // offsets ctab[c * nsl + q] ascend.  ccode[k] = class, or 0xFF: the row overflows
-  // every class and is applied from the union planes.  Slot planes cstr apart, owned
-  // points only.
-  const uint8_t* ccode;
+  // class fixes, per axis, which +-2 offsets it may hold (the upwind side '-' or '+',
+  // or both where the upwind direction changes) — 3^dim classes.  Class c lists its
+  // cnsl[c] live union offsets in ascending order (ctab[c * nsl + q] = {linear
+  // displacement, d1, d2, d3}); a row reads only its class's slots, planes cstr apart
+  // (owned points only), so a row in an interior class streams 15 (2D) / 54 (3D)
+  // planes instead of the union's 21 / 81.
+  const uint16_t* ccode;  // class | (slots of the class << 8)
   const cplx* ccoef;
   const float2* ccoef32;
-  const int4* ctab;  // {linear displacement, d1, d2, d3} per (class, slot)
+  const int4* ctab;
+  const int* cnsl;
   long cstr;
-  int nsl;
+  int nsl;  // table row stride = slot planes stored
 };
 
 // coefficient from complex64 storage, widened to complex128 for the arithmetic
@@ -191,12 +193,15 @@ void launch_to_c64(cudaStream_t s, long n, const cplx* in, float2* out);
 int pair_layout(int nofs, int* pos_a, int* pos_b, int* bit);
 void launch_pair_compress(cudaStream_t s, const StencilDev& A, int nslot, const int* pos_a, const int* pos_b,
                           const int* bit, cplx* pcoef, long pstr, uint8_t* pcode, int* conflict);
-// class compression of the owned rows: live[c] = 2 x u64 offset bitset of class c, tab[c*nsl + q]
-// = union offset of slot q; writes ccode / ccoef; overflow[0] += overflow rows, overflow[1] += warps
-// (32 consecutive rows) holding at least one
-void launch_class_compress(cudaStream_t s, const StencilDev& A, int ncls, const unsigned long long* live,
-                           int nsl, const int* tab, cplx* ccoef, long cstr, uint8_t* ccode,
-                           unsigned long long* overflow);
+// class compression of the owned rows (Op::class_compress): pass 1 classifies every row into
+// the first class (ascending size) whose live bitset (live[2c], live[2c+1]) covers its
+// non-zeros, ccode[k] = c, and accumulates stats[0] += slots read, stats[1] = max class size,
+// stats[2] += rows of mixed classes; pass 2 fills slot q < cnsl[c] of row k from union
+// plane otab[c * nsl + q]
+void launch_class_classify(cudaStream_t s, const StencilDev& A, int ncls, const unsigned long long* live_dev,
+                           const int* cnsl_dev, const int* mixed_dev, uint16_t* ccode, unsigned long long* stats);
+void launch_class_fill(cudaStream_t s, const StencilDev& A, const uint16_t* ccode, const int* cnsl_dev,
+                       const int* otab_dev, int nsl, cplx* ccoef, long cstr);
 void launch_phase(cudaStream_t s, long n, const cplx* q, const double* tau, double omega, int sign, cplx* out);
 void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, int n3c, unsigned long long* mask,
                      const int* slot_of, cplx* coef_c, int q0 = 0, int nq = -1, long cstride = -1);

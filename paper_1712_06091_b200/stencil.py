@@ -99,8 +99,8 @@ class StencilOperator:
         return n.value
 
     @property
-    def overflow_rows(self) -> int:
-        """Rows of a class-compressed operator applied from the union planes."""
+    def mixed_rows(self) -> int:
+        """Rows of a class-compressed operator whose class holds both +-2 sides of an axis."""
         import ctypes as C
 
         n, ov = C.c_int(), C.c_longlong()

@@ -207,9 +207,9 @@ def test_cfg5_recipe_solves(hadr, cfg5_small):
 
 
 def test_class_compressed_coarse_bitexact_3d(hadr, case3d):
-    """Coarse 81-offset Galerkin operators stored class-compressed (rows fit one of 8
-    upwind sign classes: 54 slot planes; overflow rows from the union planes) reproduce
-    csr_matvec bit for bit, and equal the union-plane kernel."""
+    """Coarse 81-offset Galerkin operators stored class-compressed (each row reads the
+    slots of its upwind sign class: 54 planes in the interior, more where the upwind
+    side changes) reproduce csr_matvec bit for bit, and equal the union-plane kernel."""
     A1 = case3d["Hi"].ops[1]
     shape1 = case3d["Hi"].shapes[1]
     rng = np.random.default_rng(13)
@@ -220,7 +220,7 @@ def test_class_compressed_coarse_bitexact_3d(hadr, case3d):
             hadr._lib.set_option("class_compress", cc)
             op = hadr.StencilOperator.from_csr(A1, shape1)
             ys[cc] = op @ x
-            assert op.storage_slots == (54 if cc else 0)
+            assert (54 <= op.storage_slots <= 81) if cc else op.storage_slots == 0
     finally:
         hadr._lib.set_option("class_compress", 2)
     assert np.array_equal(ys[1], A1 @ x)

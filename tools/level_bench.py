@@ -51,7 +51,7 @@ def main():
             planes = op.storage_slots or len(op.offsets)
             lay = (planes + per) * N * 16
             alg = (nnz + per * N) * 16
-            out.append({"level": lev, "N": N, "offsets": len(op.offsets), "slots": op.storage_slots, "overflow": op.overflow_rows,
+            out.append({"level": lev, "N": N, "offsets": len(op.offsets), "slots": op.storage_slots, "mixed": op.mixed_rows,
                         "nnz_per_row": nnz / N, "variant": var, "us": ms.value * 1e3,
                         "layout_GBs": lay / ms.value / 1e6, "alg_GBs": alg / ms.value / 1e6})
             print(json.dumps(out[-1]))
