@@ -364,6 +364,22 @@ def run_3d(args, L, local, dist, ws=1, rank=0, which="cfg4"):
         its.append(i)
         tk.append(t)
     t_dev = max_over_ranks(L.hadr_stream_timer(0) * 1e-3, dist)
+    c64 = None
+    if which == "cfg4":  # BASELINE config 4 names complex64 too: the mixed-precision K-cycle
+        _lib.set_option("kcycle_c64", 1)
+        try:
+            step()
+            its64 = []
+            L.hadr_stream_timer(1)
+            for _ in range(args.steps_3d):
+                its64.append(step()[0])
+            t64 = max_over_ranks(L.hadr_stream_timer(0) * 1e-3, dist)
+        finally:
+            _lib.set_option("kcycle_c64", 0)
+        c64 = {"value": N * sum(its64) / t64 / 1e6, "unit": "Mdof*iter/s", "outer_iterations": its64,
+               "ms_per_step": t64 / len(its64) * 1e3,
+               "note": "K-cycle operators stored complex64 (widened to c128 arithmetic); vectors, reductions and "
+                       "the outer FGMRES complex128 (SURVEY.md §7.3 item 5); parity <= 1e-4 in tests"}
     if slab is not None:
         D.finalize()
     hbm, srcp = peaks()
@@ -381,6 +397,8 @@ def run_3d(args, L, local, dist, ws=1, rank=0, which="cfg4"):
            "solve_roofline": {"bound": "hbm", "model_bytes_per_dof_iter": b_op, "achieved": bw,
                               "peak": hbm, "unit": "GB/s", "frac": bw / hbm, "peak_source": srcp,
                               "note": "per GPU" if ws > 1 else ""}}
+    if c64 is not None:
+        out["complex64_mixed"] = c64
     if t_fm is not None:
         out["t_fast_march_s"] = t_fm
         out["note"] = "travel time from the fast-marching restatement at setup (host, untimed, t_fast_march_s)"

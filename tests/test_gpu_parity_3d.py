@@ -253,3 +253,23 @@ def test_compressed_solve_identical_3d(hadr, c64):
     assert out[0][1] == out[1][1]
     assert np.array_equal(out[0][0], out[1][0])
     assert out[0][2] == out[1][2]
+
+
+def test_solve_upwind_3d_c64_mixed(hadr, case3d):
+    """BASELINE config 4's complex64 variant (mixed precision: complex64 K-cycle operators,
+    complex128 vectors and outer FGMRES) vs the complex128 ND oracle: iterations within 1,
+    amplitude within 1e-4 (north_star's complex64 bar)."""
+    from oracle import hadr_oracle_nd as ND
+    from paper_1712_06091_b200 import drivers
+
+    wl = case3d["wl"]
+    a_ref, rep_ref = ND.solve_upwind(case3d["shape"], case3d["hs"], wl.omega, case3d["src"], wl.medium.kappa_sq,
+                                     wl.medium.gamma, case3d["grads"], case3d["lap"], case3d["tau"], case3d["bc"])
+    cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=1e-6, max_iter=1000)
+    hadr._lib.set_option("kcycle_c64", 1)
+    try:
+        u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
+    finally:
+        hadr._lib.set_option("kcycle_c64", 0)
+    assert rep.converged and abs(rep.iterations - rep_ref.iterations) <= 1
+    assert rel(a, a_ref) <= 1e-4
