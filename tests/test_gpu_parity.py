@@ -404,3 +404,47 @@ def test_solve_upwind_c64_mixed(hadr, case, request):
         hadr._lib.set_option("kcycle_c64", 0)
     assert rep.converged and abs(rep.iterations - int(g["upwind_iterations"])) <= 1
     assert rel(a, g["upwind_a"]) <= 1e-4
+
+
+def test_error_behaviour_matches_reference(hadr, g33):
+    """The drop-in raises where the reference raises (ValueError: helmadr/krylov.py:63-64,
+    71-72, 86-87; helmadr/multigrid.py:51-52, 79-80, 116-122, 141-142), treats steps < 1 /
+    beta = 0 as no-ops (krylov.py:96-97), reports non-convergence in the report instead of
+    raising (krylov.py:231), and never mutates its inputs (krylov.py:93, 138)."""
+    import scipy.sparse as sp
+
+    A = csr_from(g33, "blend")
+    n = A.shape[0]
+    op = hadr.StencilOperator.from_csr(A, (33, 33))
+    rng = np.random.default_rng(21)
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    with pytest.raises(ValueError):
+        hadr.spmv(op, b[:-1])
+    Z = A.tolil()
+    Z[5, 5] = 0.0
+    Z = Z.tocsr()
+    Z.eliminate_zeros()
+    zop = hadr.StencilOperator.from_csr(Z, (33, 33))
+    with pytest.raises(ValueError):
+        hadr.jacobi_apply(zop, b)
+    with pytest.raises(ValueError):
+        hadr.gmres_relax(zop, b, np.zeros(n, complex), 2)
+    x = rng.standard_normal(n) + 0j
+    x_keep = x.copy()
+    assert np.array_equal(hadr.gmres_relax(op, b, x, 0), x)
+    assert np.array_equal(hadr.gmres_relax(op, A @ x, x, 3), x)  # beta = 0: x returned as is
+    assert np.array_equal(x, x_keep)
+    with pytest.raises(ValueError):
+        hadr.build_hierarchy(A, (33, 34), 5)
+    with pytest.raises(ValueError):
+        hadr.build_hierarchy(sp.identity(32 * 32, format="csr", dtype=complex), (32, 32), 5)
+    H = hadr.build_hierarchy(A, (33, 33), 5)
+    for bad in (0, H.n_levels + 1):
+        with pytest.raises(ValueError):
+            hadr.k_cycle(H, bad, b, np.zeros_like(b))
+    b_keep = b.copy()
+    x0 = np.zeros(n, complex)
+    xs, rep = hadr.fgmres(op, b, x0, hadr.make_kcycle_preconditioner(H), hadr.KrylovConfig(restart=5, maxiter=2,
+                                                                                         tol=1e-12))
+    assert not rep.converged and rep.iterations == 2 and len(rep.history) == 3
+    assert np.array_equal(b, b_keep) and not np.any(x0)
