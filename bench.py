@@ -366,6 +366,7 @@ def run_3d(args, L, local, dist, ws=1, rank=0, which="cfg4"):
     t_dev = max_over_ranks(L.hadr_stream_timer(0) * 1e-3, dist)
     c64 = None
     if which == "cfg4":  # BASELINE config 4 names complex64 too: the mixed-precision K-cycle
+        L.hadr_pool_trim()  # release the recycled complex128 hierarchy before building the mixed one
         _lib.set_option("kcycle_c64", 1)
         try:
             step()
@@ -376,6 +377,7 @@ def run_3d(args, L, local, dist, ws=1, rank=0, which="cfg4"):
             t64 = max_over_ranks(L.hadr_stream_timer(0) * 1e-3, dist)
         finally:
             _lib.set_option("kcycle_c64", 0)
+            L.hadr_pool_trim()
         c64 = {"value": N * sum(its64) / t64 / 1e6, "unit": "Mdof*iter/s", "outer_iterations": its64,
                "ms_per_step": t64 / len(its64) * 1e3,
                "note": "K-cycle operators stored complex64 (widened to c128 arithmetic); vectors, reductions and "

@@ -455,6 +455,14 @@ __device__ __forceinline__ void stencil_cc(const StencilArgs& a, int cls, int ns
 // (B200, 1025^2 fine sweep: 50.6 us union / 44.1 us at 4 CTAs / 41.4 us at 2 CTAs);
 // plain applies keep 4 CTAs (26.3 us vs 30.6 us at 2).
 // (the class-compressed kernel measured fastest at 4 CTAs/SM in every variant)
+// Class-compressed chunk (slots whose loads are issued together): measured on B200 at
+// 4 CTAs/SM, the Jacobi variant (coefficient, x, D^-1 per slot) is fastest at 9, the
+// plain apply (coefficient, x) at 6 (3D level-2 apply 1524 -> 1309 us); 3 CTAs/SM and
+// chunks of 12 were slower in every variant.
+template <int INM>
+__host__ __device__ constexpr int cc_chunk() {
+  return (INM & IN_JAC) ? 9 : 6;
+}
 template <int INM, bool PC, bool CC>
 constexpr int stencil_min_blocks() {
   return (PC && (INM & IN_JAC)) ? 2 : 4;
@@ -498,9 +506,9 @@ __global__ void __launch_bounds__(kThreads, stencil_min_blocks<INM, PC, CC>()) k
       const unsigned cw = __ldg(a.A.ccode + k);
       const int cls = (int)(cw & 0xFFu);
       if (a.A.ccoef32)
-        stencil_cc<9, INM, true>(a, cls, (int)(cw >> 8), k, i1, i2, i3, n1, n2, n3, s, acc);
+        stencil_cc<cc_chunk<INM>(), INM, true>(a, cls, (int)(cw >> 8), k, i1, i2, i3, n1, n2, n3, s, acc);
       else
-        stencil_cc<9, INM, false>(a, cls, (int)(cw >> 8), k, i1, i2, i3, n1, n2, n3, s, acc);
+        stencil_cc<cc_chunk<INM>(), INM, false>(a, cls, (int)(cw >> 8), k, i1, i2, i3, n1, n2, n3, s, acc);
     } else if constexpr (NO > 0) {
       if (c32)
         stencil_chunk<NO, INM, true>(a, 0, nofs, k, i1, i2, i3, n1, n2, n3, N, s, acc);
