@@ -283,12 +283,39 @@ def run_ours(args, ws, rank, local, dist):
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, args, sample_its=args.cpu_its, threads_one=True)
     if args.extra_3d:
-        out["config_4_3d"] = run_3d(args, L, local, dist, ws, rank)
+        out["config_4_3d"] = guarded_slab_run(lambda: run_3d(args, L, local, dist, ws, rank), out, ws, rank,
+                                              args.slab_timeout)
     if args.extra_cfg3:
         out["config_3"] = run_3d(args, L, local, dist, 1, rank, which="cfg3")
     if args.extra_cfg5:
         out["config_5"] = run_3d(args, L, local, dist, 1, rank, which="cfg5")
     return out
+
+
+def guarded_slab_run(fn, out, ws, rank, timeout_s):
+    """The N > 1 config-4 line is ONE solve split over the ranks (NCCL inside the K-cycle
+    graphs).  If it fails or stalls, the headline line must still be printed: a watchdog
+    prints what was measured so far (rank 0) and ends the process after timeout_s."""
+    if ws == 1:
+        return fn()
+    import threading
+
+    def fire():
+        if rank == 0:
+            res = dict(out)
+            res["config_4_3d"] = {"error": f"slab solve did not finish within {timeout_s:.0f} s"}
+            print(json.dumps(res), flush=True)
+        os._exit(0)
+
+    timer = threading.Timer(timeout_s, fire)
+    timer.daemon = True
+    timer.start()
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001 - recorded in the JSON line, the headline stands
+        return {"error": f"{type(e).__name__}: {e}"}
+    finally:
+        timer.cancel()
 
 
 B_OP_3D_UPWIND_C128 = 6788.0  # SURVEY.md §8(d): 3D adr_upwind c128 (10 / 10 / 54 non-zeros)
@@ -597,6 +624,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extra-3d", type=int, default=513, help="also run BASELINE config 4 at this n (0: skip)")
     ap.add_argument("--steps-3d", type=int, default=2)
+    ap.add_argument("--slab-timeout", type=float, default=600.0,
+                    help="N > 1: watchdog on the multi-GPU config-4 solve (the headline is printed regardless)")
     ap.add_argument("--extra-cfg3", type=int, default=2049, help="also run BASELINE config 3 at this n (0: skip)")
     ap.add_argument("--extra-cfg5", type=int, default=257,
                     help="also run BASELINE config 5's recipe at this n (0: skip; full size 1025 needs 8 GPUs)")
