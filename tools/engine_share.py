@@ -18,12 +18,13 @@ import numpy as np  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=1025)
+    ap.add_argument("--workload", default="cfg2")
     ap.add_argument("--mhz", type=float, default=1965.0)
     a, extra = ap.parse_known_args()
     from paper_1712_06091_b200 import _lib, drivers, workloads
 
     L = _lib.lib()
-    wl = workloads.cfg2(a.n)
+    wl = workloads.by_name(a.workload, a.n)
     cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=1e-6, max_iter=1000)
     for opt in extra:
         if "=" in opt and not opt.startswith("--"):
