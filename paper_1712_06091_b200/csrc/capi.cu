@@ -572,6 +572,13 @@ int hadr_set_option(const char* name, double value) {
         if (!h) break;
         delete h;
       }
+    } else if (n == "relax_split") {
+      g_relax_split = (long)value;
+      for (;;) {
+        Hier* h = hier_pool_pop();
+        if (!h) break;
+        delete h;
+      }
     } else if (n == "class_compress") {
       g_class_compress = (int)value;
       for (;;) {

@@ -123,6 +123,7 @@ void Op::make_c64() {
 }
 
 int g_class_compress = 2;
+long g_relax_split = 1L << 20;
 
 bool Op::class_compress() {
   cc_tried = true;
@@ -855,6 +856,7 @@ Hier::~Hier() {
     for (auto* v : L.V) dfree(v);
     dfree(L.w[0]);
     dfree(L.w[1]);
+    dfree(L.z);
     dfree(L.rctl);
     dfree(L.fb), dfree(L.fx), dfree(L.fV0), dfree(L.fu), dfree(L.fZ0), dfree(L.fZ1), dfree(L.fw), dfree(L.fr);
     dfree(L.fctl);
@@ -919,6 +921,7 @@ void Hier::alloc_workspace() {
     L.w[0] = valloc(L);
     L.w[1] = valloc(L);
     L.r = valloc(L);
+    if (g_relax_split > 0 && L.n3 > 1 && L.N >= g_relax_split) L.z = valloc(L);
     L.rctl = dalloc<RelaxCtl>(1);
     HADR_CUDA(cudaMemset(L.rctl, 0, sizeof(RelaxCtl)));
     if (i >= 1) {
@@ -1201,8 +1204,17 @@ void Hier::emit_relax(Level& L, const cplx* b, const cplx* x, cplx* xo, int s, G
     a.gate = gj;
     a.rs = c.rs;
     a.epi = epi(EPI_RELAX_H, rc, 0, j);
-    xchg(L, a.x);
-    launch_stencil(lc0, IN_SCALE | IN_JAC | IN_WRITEV, OUT_APPLY, j == 0 ? RED_DOT_CENTER : RED_DOT, a);
+    if (L.z) {
+      // large 3D level: V[j] = s w and z = D^-1 V[j] once per point, then a plain stencil on z
+      // (the fused form re-derives D^-1 (s w) for each of a point's 10-54 neighbours)
+      launch_scale_jac(lc0, L.N, a.x, a.scale, L.dinv, L.V[j], L.z, gj);
+      a.x = L.z;
+      xchg(L, L.z);
+      launch_stencil(lc0, IN_PLAIN, OUT_APPLY, RED_DOT, a);
+    } else {
+      xchg(L, a.x);
+      launch_stencil(lc0, IN_SCALE | IN_JAC | IN_WRITEV, OUT_APPLY, j == 0 ? RED_DOT_CENTER : RED_DOT, a);
+    }
     for (int i = 0; i < j; ++i)
       launch_axpy_red(lc0, L.N, w, &rc->H[i * RMAX + j], L.V[i], RED_DOT, L.V[i + 1], gj, c.rs,
                       epi(EPI_RELAX_H, rc, i + 1, j));

@@ -131,6 +131,7 @@ struct Level {
   cplx* r = nullptr;
   cplx* V[RMAX + 1] = {nullptr};
   cplx* w[2] = {nullptr, nullptr};
+  cplx* z = nullptr;         // split relaxation input D^-1 (s w) (large 3D levels, g_relax_split)
   RelaxCtl* rctl = nullptr;
   // inner-FGMRES workspace (levels >= 2)
   cplx *fb = nullptr, *fx = nullptr, *fV0 = nullptr, *fu = nullptr, *fZ0 = nullptr, *fZ1 = nullptr,
@@ -172,6 +173,7 @@ extern long g_ce_max_n;  // levels with N <= this run inside the cluster engine 
 extern int g_kcycle_c64; // build hierarchies with complex64 operator storage (mixed-precision K-cycle)
 extern int g_ce_smem_relax;  // engine relaxations out of shared memory where they fit
 extern int g_pair_compress;  // pair-compress fine operators (outer A, hierarchy level 0)
+extern long g_relax_split;   // 3D levels with at least this many points form D^-1 (s w) once per point
 extern int g_class_compress;  // class-compress coarse graph-path levels: 0 off, 1 3D, 2 2D and 3D
 
 Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol);

@@ -797,6 +797,7 @@ void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const Stenc
   }
     HADR_TCASE(IN_PLAIN, OUT_APPLY, RED_NONE)
     HADR_TCASE(IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT)
+  HADR_TCASE(IN_PLAIN, OUT_APPLY, RED_DOT)
     HADR_TCASE(IN_PLAIN, OUT_RESID, RED_NONE)
     HADR_TCASE(IN_PLAIN, OUT_RESID, RED_NORM)
     HADR_TCASE(J, OUT_APPLY, RED_DOT_CENTER)
@@ -811,6 +812,7 @@ void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const Stenc
   }
   HADR_CASE(IN_PLAIN, OUT_APPLY, RED_NONE)
   HADR_CASE(IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT)
+  HADR_CASE(IN_PLAIN, OUT_APPLY, RED_DOT)
   HADR_CASE(IN_PLAIN, OUT_RESID, RED_NONE)
   HADR_CASE(IN_PLAIN, OUT_RESID, RED_NORM)
   HADR_CASE(J, OUT_APPLY, RED_DOT_CENTER)
@@ -932,6 +934,28 @@ __global__ void k_zero(long n, cplx* out, Gate g) {
   const long stride = (long)gridDim.x * blockDim.x;
   for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) out[k] = mk(0.0, 0.0);
 }
+// Relaxation step input, split out of the stencil on large 3D levels (Hier::emit_relax):
+// v = s x (the new basis vector) and z = D^-1 (.) v — the values the fused stencil would
+// form per neighbour, formed once per point.
+__global__ void __launch_bounds__(kThreads) k_scale_jac(long n, const cplx* __restrict__ in, const double* s,
+                                                        const cplx* __restrict__ dinv, cplx* __restrict__ v,
+                                                        cplx* __restrict__ z, Gate g) {
+  pdl_enter();
+  if (!gate_open(g)) return;
+  const double sc = *s;
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    const cplx a = cscale(ldc(in, k), sc);
+    v[k] = a;
+    z[k] = cmul_np(ldc(dinv, k), a);
+  }
+}
+
+void launch_scale_jac(const LaunchCfg& lc, long n, const cplx* in, const double* s, const cplx* dinv, cplx* v,
+                      cplx* z, Gate g) {
+  ++g_launch_count;
+  launch_k(k_scale_jac, blocks_for(lc, n), kThreads, lc.stream, n, in, s, dinv, v, z, g);
+}
+
 void launch_zero(const LaunchCfg& lc, long n, cplx* out, Gate g) {
   ++g_launch_count;
   launch_k(k_zero, blocks_for(lc, n), kThreads, lc.stream, n, out, g);

@@ -136,6 +136,9 @@ void launch_dot(const LaunchCfg& lc, long n, const cplx* u, const cplx* w, Gate 
 void launch_scale(const LaunchCfg& lc, long n, const cplx* in, const double* s, cplx* out, int red, Gate g,
                   RedScratch rs, Epi e);
 void launch_zero(const LaunchCfg& lc, long n, cplx* out, Gate g);
+// v = (*s) in ; z = dinv (.) v   (the relaxation step's input, split out of the stencil)
+void launch_scale_jac(const LaunchCfg& lc, long n, const cplx* in, const double* s, const cplx* dinv, cplx* v,
+                      cplx* z, Gate g);
 
 // out = base + [dinv (.)] sum_{i<k} v_i * y_i ; k = *kptr if kptr else kfix ; base may be null (zero)
 struct LinComb {
