@@ -11,7 +11,7 @@ hierarchy, FGMRES to 1e-6.
   value : inputs (medium, tau fields, transformed source) resident in HBM;
           CUDA events on the library stream around the K steps.
   e2e   : the public API drivers.solve_adr_upwind(...) with numpy inputs in
-          pinned host memory: source phase transform (host, sparse), H2D of the
+          pinned host memory: the point source's phase value (host), H2D of the
           fields, the solve, the waveform u = a exp(-i w tau) on the device, D2H
           of a and u — wall clock.
 Metric: Mdof*iter/s = N * outer_iterations / t / 1e6.
@@ -243,7 +243,7 @@ def run_ours(args, ws, rank, local, dist):
     t_e2e = max_over_ranks(time.perf_counter() - t0, dist)
     e2e_value = sum_over_ranks(N * e2e_its / 1e6, dist) / t_e2e
     h2d = (3 + dim) * 8 * N  # kappa^2, gamma, grad(tau) per axis, lap(tau)
-    h2d += 16 * N + 8 * N    # transformed source qhat, tau (device waveform composition)
+    h2d += 8 * N + 16        # tau (device waveform composition), the point source's one value
     d2h = 2 * 16 * N         # amplitude a and waveform u
     agree = float(np.linalg.norm(a.reshape(-1) - a_dev) / np.linalg.norm(a_dev))
 

@@ -56,6 +56,8 @@ int hadr_device_malloc(void** ptr, size_t bytes);
 int hadr_device_free(void* ptr);
 /* kind: 1 host->device, 2 device->host, 3 device->device */
 int hadr_memcpy(void* dst, const void* src, size_t bytes, int kind);
+/* device memset (byte value), stream-ordered and synchronised like hadr_memcpy */
+int hadr_memset(void* dst, int value, size_t bytes);
 
 /* ---- operators (helmadr/operators.py CSR matrices, as structured stencils) ---- */
 /* From a canonical CSR matrix on the (n1, n2) grid; replaces the scipy CSR consumed by

@@ -28,7 +28,7 @@ EXPORTS = (
     "hadr_stream_timer", "hadr_set_option", "hadr_ce_profile", "hadr_op_bench",
     "hadr_dist_nccl_id", "hadr_dist_init_nccl", "hadr_dist_init_host", "hadr_dist_finalize", "hadr_dist_info",
     "hadr_dist_plan", "hadr_slab_bounds", "hadr_fast_march", "hadr_phase_transform", "hadr_op_storage",
-    "hadr_relative_error",
+    "hadr_relative_error", "hadr_memset",
 )
 
 # host-communicator callbacks (include/hadr.h hadr_host_*)
@@ -99,6 +99,7 @@ _SIGS = {
     "hadr_fast_march": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, C.POINTER(C.c_longlong)]),
     "hadr_phase_transform": (_i, [C.c_longlong, _vp, _vp, _d, _i, _vp, _i]),
     "hadr_op_storage": (_i, [_vp, C.POINTER(_i), C.POINTER(C.c_longlong)]),
+    "hadr_memset": (_i, [_vp, _i, C.c_size_t]),
     "hadr_relative_error": (_i, [C.c_longlong, _vp, _vp, _d, _vp, C.POINTER(_d), C.POINTER(C.c_longlong), _vp, _i,
                                  _vp, _i]),
 }

@@ -200,6 +200,14 @@ int hadr_memcpy(void* dst, const void* src, size_t bytes, int kind) {
   });
 }
 
+int hadr_memset(void* dst, int value, size_t bytes) {
+  return guarded([&] {
+    Ctx& c = Ctx::get();
+    HADR_CUDA(cudaMemsetAsync(dst, value, bytes, c.stream));
+    c.sync();
+  });
+}
+
 int hadr_op_from_csr(int n1, int n2, int n3, int64_t nnz, const int64_t* indptr, const int32_t* indices,
                      const double* data, hadr_op* out) {
   return guarded([&] {
