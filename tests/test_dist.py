@@ -144,3 +144,25 @@ def test_host_communicator_callbacks_gloo(world):
         assert o["above"] == ([r + 1 + 0.25, r + 1 + 0.5] if r < world - 1 else [-1.0, -1.0])
         assert o["below"] == ([r - 1 + 0.75, r - 1 + 0.875] if r > 0 else [-1.0, -1.0])
         assert o["bcast"] == [7.0, 8.0, 9.0]
+
+
+def test_bench_slab_watchdog_prints_headline():
+    """bench.py's multi-GPU config-4 line runs under a watchdog: if the slab solve stalls,
+    rank 0 still prints the JSON line measured so far (with the stall recorded) and the
+    process exits 0; an exception is recorded instead of propagating."""
+    import json
+    import subprocess
+
+    code = ("import sys, time; sys.path.insert(0, %r); import bench; "
+            "bench.guarded_slab_run(lambda: time.sleep(30), {'metric': 'm', 'value': 1.0}, 2, 0, 1.0)") % REPO
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0, p.stderr
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["value"] == 1.0 and "error" in line["config_4_3d"]
+    sys.path.insert(0, REPO)
+    import bench
+
+    def boom():
+        raise RuntimeError("nccl")
+
+    assert "nccl" in bench.guarded_slab_run(boom, {}, 2, 0, 60.0)["error"]
