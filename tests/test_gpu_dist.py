@@ -26,6 +26,7 @@ CASES = [
     (1, ["--case", "cfg1:65", "--backend", "nccl"]),                      # NCCL, captured in the K-cycle graph
     (2, ["--case", "cfg4:65", "--backend", "host", "--levels", "2", "--c64", "1"]),  # mixed precision
     (2, ["--case", "cfg3:65", "--backend", "host", "--levels", "2"]),     # Neumann top, non-square, FM tau
+    (2, ["--case", "cfg4:33", "--backend", "host", "--levels", "2", "--opt", "relax_split=1000"]),  # split relax, z halos
 ]
 
 

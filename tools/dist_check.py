@@ -28,6 +28,7 @@ def main() -> None:
     ap.add_argument("--levels", type=int, default=0)
     ap.add_argument("--min-planes", type=int, default=16)
     ap.add_argument("--c64", type=int, default=0)
+    ap.add_argument("--opt", action="append", default=[], help="library option name=value (repeatable)")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
 
@@ -48,6 +49,9 @@ def main() -> None:
     D.set_policy(min_planes=args.min_planes, levels=args.levels)
     if args.c64:
         H._lib.set_option("kcycle_c64", 1)
+    for o in args.opt:
+        k, v = o.split("=")
+        H._lib.set_option(k, float(v))
     bounds, nd, nl = D.plan(wl.grid.shape, 5)
     cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=1e-6, max_iter=1000)
     u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
