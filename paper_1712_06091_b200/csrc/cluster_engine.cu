@@ -130,6 +130,43 @@ __device__ void ce_allreduce(CEC& c, double (&v)[NV]) {
 // The (transformed) input rows [r0-2, r1+2) are staged once in shared memory,
 // so every neighbour is an LDS instead of an L2 round trip; D^-1 and the scale
 // are applied once per point (same values as applying them per neighbour).
+// Class-compressed row (StencilDev::ccode, kernels.cu stencil_cc; 3D engine levels): the
+// row's class slots in ascending union order; neighbours from the staged tile (linear
+// index k - tbase + displacement).
+template <bool C32>
+__device__ __forceinline__ cplx ce_cc_row(const StencilDev& A, const cplx* tile, long k, long tbase, int i1, int i2,
+                                          int i3, int n1, int n2, int n3) {
+  const unsigned cw = __ldg(A.ccode + k);
+  const int nslc = (int)(cw >> 8);
+  const int4* tab = A.ctab + (long)(cw & 0xFFu) * A.nsl;
+  cplx acc = mk(0.0, 0.0);
+  for (int q0 = 0; q0 < nslc; q0 += 9) {
+    int4 t[9];
+    cplx cv[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const bool live = q0 + q < nslc;
+      t[q] = __ldg(tab + (live ? q0 + q : 0));
+      const long ci = (long)(live ? q0 + q : 0) * A.cstr + k;
+      if constexpr (C32) {
+        const float2 f = __ldg(A.ccoef32 + ci);
+        cv[q] = make_double2((double)f.x, (double)f.y);
+      } else {
+        cv[q] = __ldg(A.ccoef + ci);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const int j1 = i1 + t[q].y, j2 = i2 + t[q].z, j3 = i3 + t[q].w;
+      const bool ok = q0 + q < nslc && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2 && j3 >= 0 && j3 < n3;
+      const cplx v = tile[ok ? k - tbase + t[q].x : 0];
+      const cplx tt = cadd(acc, cmul_sp(cv[q], v));
+      acc = ok ? tt : acc;
+    }
+  }
+  return acc;
+}
+
 extern __shared__ cplx ce_tile[];
 
 template <int NO, int INM, int OUTM, int RED, bool C32>
@@ -156,7 +193,8 @@ __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double
     const int i2 = rem / n3, i3 = rem - (rem / n3) * n3;
     cplx acc = mk(0.0, 0.0);
     constexpr int CH = NO > 0 ? NO : 9;
-    const int nch = NO > 0 ? 1 : (nofs + CH - 1) / CH;
+    const int nch = (NO == 0 && A.ccode) ? 0 : NO > 0 ? 1 : (nofs + CH - 1) / CH;
+    if (NO == 0 && A.ccode) acc = ce_cc_row<C32>(A, ce_tile, k, base, i1, i2, i3, n1, n2, n3);
     for (int ch = 0; ch < nch; ++ch) {
       const int o0 = ch * CH;
       cplx cv[CH];
@@ -363,7 +401,8 @@ __device__ __forceinline__ void sm_stencil_rows(CEC& c, const StencilDev& A, con
     const int i2 = rem / n3, i3 = rem - (rem / n3) * n3;
     cplx acc = mk(0.0, 0.0);
     constexpr int CH = NO > 0 ? NO : 9;
-    const int nch = NO > 0 ? 1 : (nofs + CH - 1) / CH;
+    const int nch = (NO == 0 && A.ccode) ? 0 : NO > 0 ? 1 : (nofs + CH - 1) / CH;
+    if (NO == 0 && A.ccode) acc = ce_cc_row<C32>(A, tile, k, (long)t0 * n23, i1, i2, i3, n1, n2, n3);
     for (int ch = 0; ch < nch; ++ch) {
       const int o0 = ch * CH;
       cplx cv[CH];

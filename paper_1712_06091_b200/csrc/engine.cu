@@ -1049,9 +1049,9 @@ Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol) 
       h->lv.push_back(L);
     }
     if (g_pair_compress && h->lv[0].A->nloc() > g_cl_max_n) h->lv[0].A->pair_compress();
-    for (size_t l = 1; l < h->lv.size(); ++l) {
+    for (size_t l = 1; l < h->lv.size(); ++l) {  // graph-path levels; in 3D the cluster-engine levels too
       Op& C = *h->lv[l].A;
-      if (g_class_compress > (C.n3 > 1 ? 0 : 1) && C.nloc() > g_cl_max_n) C.class_compress();
+      if (g_class_compress > (C.n3 > 1 ? 0 : 1) && (C.nloc() > g_cl_max_n || C.n3 > 1)) C.class_compress();
     }
     h->alloc_workspace();
   } catch (...) {
