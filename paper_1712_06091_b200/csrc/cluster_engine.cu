@@ -447,6 +447,9 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
     R->k = 0;
     R->cur = kStopped;
   }
+  double beta = 0.0, sc_next = 0.0;
+  int cur = kStopped;
+  cplx hcol = mk(0.0, 0.0);
   {
     double v[1];
     const cplx* src = b;
@@ -465,11 +468,16 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
     if (!x) v[0] = nn;
     ce_allreduce<1>(c, v);
     if (threadIdx.x == 0) relax_beta(R, v[0]);
-    __syncthreads();
+    // every thread holds the all-reduced value: the branch state and the scale are formed
+    // locally (the same IEEE operations as relax_beta / relax_step_sm), so no thread waits
+    // for thread 0's control update — it is read back only after the loop
+    beta = sqrt(v[0]);
+    cur = (beta == 0.0 || s < 1) ? kStopped : 0;
+    sc_next = 1.0 / beta;
   }
   for (int j = 0; j < s; ++j) {
-    if (R->cur != j) break;
-    const double sc = (j == 0) ? R->inv_beta : R->inv_hn;
+    if (cur != j) break;
+    const double sc = sc_next;
     cplx* wp = wb + (long)((j + 1) % 2) * rs;  // previous Arnoldi vector (step 0: r)
     cplx* w = wb + (long)(j % 2) * rs;
     cplx* Vj = Vb + (long)j * rs;
@@ -509,11 +517,11 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       }
       double v[2] = {red[0], red[1]};
       ce_allreduce<2>(c, v);
-      if (threadIdx.x == 0) R->H[0 * RMAX + j] = mk(v[0], v[1]);
-      __syncthreads();
+      hcol = mk(v[0], v[1]);
+      if (threadIdx.x == 0) R->H[0 * RMAX + j] = hcol;
     }
     for (int i = 0; i < j; ++i) {
-      const cplx h = R->H[i * RMAX + j];
+      const cplx h = hcol;  // H[i][j], the previous all-reduce
       const cplx* Vi = Vb + (long)i * rs;
       const cplx* Vi1 = Vb + (long)(i + 1) * rs;
       double v[2] = {0.0, 0.0};
@@ -525,11 +533,11 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
         v[1] += uu.x * y.y - uu.y * y.x;
       }
       ce_allreduce<2>(c, v);
-      if (threadIdx.x == 0) R->H[(i + 1) * RMAX + j] = mk(v[0], v[1]);
-      __syncthreads();
+      hcol = mk(v[0], v[1]);
+      if (threadIdx.x == 0) R->H[(i + 1) * RMAX + j] = hcol;
     }
     {
-      const cplx h = R->H[j * RMAX + j];
+      const cplx h = hcol;  // H[j][j]
       double v[1] = {0.0};
       for (long p = threadIdx.x; p < np; p += blockDim.x) {
         const cplx y = csub(w[p], cmul_np(h, Vj[p]));
@@ -539,11 +547,15 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       ce_allreduce<1>(c, v);
       {
         CEProfScope prof_(c, 3);
-        if (threadIdx.x == 0) relax_step_sm(R, j, v[0]);
-        __syncthreads();
+        if (threadIdx.x == 0) relax_step_sm(R, j, v[0]);  // Givens, least squares (thread 0)
       }
+      const double hn = sqrt(v[0]);
+      const bool stop = (hn <= kBreakdownEps * beta) || (j + 1 >= s);  // helmadr/krylov.py:113-114
+      cur = stop ? kStopped : j + 1;
+      sc_next = 1.0 / hn;
     }
   }
+  __syncthreads();  // thread 0's y / k
   // xo = x + dinv (.) (V[:k]^T y)   (own rows)
   const int k = R->k;
   {
