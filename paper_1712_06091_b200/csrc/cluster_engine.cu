@@ -310,6 +310,10 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
     R->k = 0;
     R->cur = kStopped;
   }
+  // branch state and scales formed locally from the all-reduced values (see ce_relax_sm)
+  double beta = 0.0, sc_next = 0.0;
+  int cur = kStopped;
+  cplx hcol = mk(0.0, 0.0);
   const cplx* r = b;
   {
     double v[1];
@@ -323,13 +327,15 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
     }
     ce_allreduce<1>(c, v);
     if (threadIdx.x == 0) relax_beta(R, v[0]);
-    __syncthreads();
+    beta = sqrt(v[0]);
+    cur = (beta == 0.0 || s < 1) ? kStopped : 0;
+    sc_next = 1.0 / beta;
   }
   for (int j = 0; j < s; ++j) {
-    if (R->cur != j) break;
+    if (cur != j) break;
     cplx* w = L.w[j % 2];
     const cplx* src = (j == 0) ? r : L.w[(j - 1) % 2];
-    const double sc = (j == 0) ? R->inv_beta : R->inv_hn;
+    const double sc = sc_next;
     {
       double red[3];
       if (j == 0)
@@ -340,28 +346,32 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
                                                                       L.V[0], red);
       double v[2] = {red[0], red[1]};
       ce_allreduce<2>(c, v);
-      if (threadIdx.x == 0) R->H[0 * RMAX + j] = mk(v[0], v[1]);
-      __syncthreads();
+      hcol = mk(v[0], v[1]);
+      if (threadIdx.x == 0) R->H[0 * RMAX + j] = hcol;
     }
     for (int i = 0; i < j; ++i) {
       double v[2];
-      ce_axpy<RED_DOT>(c, n, w, R->H[i * RMAX + j], L.V[i], L.V[i + 1], v);
+      ce_axpy<RED_DOT>(c, n, w, hcol, L.V[i], L.V[i + 1], v);  // h = H[i][j]
       ce_allreduce<2>(c, v);
-      if (threadIdx.x == 0) R->H[(i + 1) * RMAX + j] = mk(v[0], v[1]);
-      __syncthreads();
+      hcol = mk(v[0], v[1]);
+      if (threadIdx.x == 0) R->H[(i + 1) * RMAX + j] = hcol;
     }
     {
       double v2[2];
-      ce_axpy<RED_NORM>(c, n, w, R->H[j * RMAX + j], L.V[j], nullptr, v2);
+      ce_axpy<RED_NORM>(c, n, w, hcol, L.V[j], nullptr, v2);  // h = H[j][j]
       double v[1] = {v2[0]};
       ce_allreduce<1>(c, v);
       {
         CEProfScope prof_(c, 3);
         if (threadIdx.x == 0) relax_step_sm(R, j, v[0]);
-        __syncthreads();
       }
+      const double hn = sqrt(v[0]);
+      const bool stop = (hn <= kBreakdownEps * beta) || (j + 1 >= s);  // helmadr/krylov.py:113-114
+      cur = stop ? kStopped : j + 1;
+      sc_next = 1.0 / hn;
     }
   }
+  __syncthreads();  // thread 0's y / k
   // xo = x + dinv (.) (V[:k]^T y)
   const int k = R->k;
   CEProfScope prof_lc_(c, 14);
