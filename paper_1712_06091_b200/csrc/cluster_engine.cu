@@ -305,7 +305,11 @@ __device__ double ce_scale(CEC& c, long n, const cplx* in, double s, bool scaled
 __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, const cplx* x, cplx* xo, int s) {
   RelaxCtl* R = &c.S->rc;
   const long n = L.N;
-  if (threadIdx.x == 0) {
+  // the control thread: the CTA's last, whose share of the vector work is the smallest
+  // (none at all on the coarsest grids), so the Givens updates run beside the other
+  // threads' work instead of ahead of it
+  const bool ctl = threadIdx.x == blockDim.x - 1;
+  if (ctl) {
     R->steps = s;
     R->k = 0;
     R->cur = kStopped;
@@ -326,7 +330,7 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
       v[0] = ce_scale(c, n, b, 1.0, false, nullptr);
     }
     ce_allreduce<1>(c, v);
-    if (threadIdx.x == 0) relax_beta(R, v[0]);
+    if (ctl) relax_beta(R, v[0]);
     beta = sqrt(v[0]);
     cur = (beta == 0.0 || s < 1) ? kStopped : 0;
     sc_next = 1.0 / beta;
@@ -347,14 +351,14 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
       double v[2] = {red[0], red[1]};
       ce_allreduce<2>(c, v);
       hcol = mk(v[0], v[1]);
-      if (threadIdx.x == 0) R->H[0 * RMAX + j] = hcol;
+      if (ctl) R->H[0 * RMAX + j] = hcol;
     }
     for (int i = 0; i < j; ++i) {
       double v[2];
       ce_axpy<RED_DOT>(c, n, w, hcol, L.V[i], L.V[i + 1], v);  // h = H[i][j]
       ce_allreduce<2>(c, v);
       hcol = mk(v[0], v[1]);
-      if (threadIdx.x == 0) R->H[(i + 1) * RMAX + j] = hcol;
+      if (ctl) R->H[(i + 1) * RMAX + j] = hcol;
     }
     {
       double v2[2];
@@ -363,7 +367,7 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
       ce_allreduce<1>(c, v);
       {
         CEProfScope prof_(c, 3);
-        if (threadIdx.x == 0) relax_step_sm(R, j, v[0]);
+        if (ctl) relax_step_sm(R, j, v[0]);
       }
       const double hn = sqrt(v[0]);
       const bool stop = (hn <= kBreakdownEps * beta) || (j + 1 >= s);  // helmadr/krylov.py:113-114
@@ -371,7 +375,7 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
       sc_next = 1.0 / hn;
     }
   }
-  __syncthreads();  // thread 0's y / k
+  __syncthreads();  // the control thread's y / k
   // xo = x + dinv (.) (V[:k]^T y)
   const int k = R->k;
   CEProfScope prof_lc_(c, 14);
@@ -452,7 +456,11 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
   cplx* tile = ce_tile;                        // (rows + 4) * n23
   cplx* Vb = ce_tile + (long)(rows + 4) * n23;  // V[i] = Vb + i * rs, i <= s
   cplx* wb = Vb + (long)(s + 1) * rs;           // w[0], w[1]
-  if (threadIdx.x == 0) {
+  // the control thread: the CTA's last, whose share of the vector work is the smallest
+  // (none at all on the coarsest grids), so the Givens updates run beside the other
+  // threads' work instead of ahead of it
+  const bool ctl = threadIdx.x == blockDim.x - 1;
+  if (ctl) {
     R->steps = s;
     R->k = 0;
     R->cur = kStopped;
@@ -477,7 +485,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
     }
     if (!x) v[0] = nn;
     ce_allreduce<1>(c, v);
-    if (threadIdx.x == 0) relax_beta(R, v[0]);
+    if (ctl) relax_beta(R, v[0]);
     // every thread holds the all-reduced value: the branch state and the scale are formed
     // locally (the same IEEE operations as relax_beta / relax_step_sm), so no thread waits
     // for thread 0's control update — it is read back only after the loop
@@ -528,7 +536,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       double v[2] = {red[0], red[1]};
       ce_allreduce<2>(c, v);
       hcol = mk(v[0], v[1]);
-      if (threadIdx.x == 0) R->H[0 * RMAX + j] = hcol;
+      if (ctl) R->H[0 * RMAX + j] = hcol;
     }
     for (int i = 0; i < j; ++i) {
       const cplx h = hcol;  // H[i][j], the previous all-reduce
@@ -544,7 +552,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       }
       ce_allreduce<2>(c, v);
       hcol = mk(v[0], v[1]);
-      if (threadIdx.x == 0) R->H[(i + 1) * RMAX + j] = hcol;
+      if (ctl) R->H[(i + 1) * RMAX + j] = hcol;
     }
     {
       const cplx h = hcol;  // H[j][j]
@@ -557,7 +565,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       ce_allreduce<1>(c, v);
       {
         CEProfScope prof_(c, 3);
-        if (threadIdx.x == 0) relax_step_sm(R, j, v[0]);  // Givens, least squares (thread 0)
+        if (ctl) relax_step_sm(R, j, v[0]);  // Givens, least squares (thread 0)
       }
       const double hn = sqrt(v[0]);
       const bool stop = (hn <= kBreakdownEps * beta) || (j + 1 >= s);  // helmadr/krylov.py:113-114
@@ -565,7 +573,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       sc_next = 1.0 / hn;
     }
   }
-  __syncthreads();  // thread 0's y / k
+  __syncthreads();  // the control thread's y / k
   // xo = x + dinv (.) (V[:k]^T y)   (own rows)
   const int k = R->k;
   {
