@@ -49,6 +49,18 @@ def peaks():
         return HBM_FALLBACK, "fallback"
 
 
+def self_launch(args):
+    """`python bench.py --gpus N` without torchrun: re-launch as N ranks (one per GPU)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -227,9 +239,12 @@ def run_ours(args, ws, rank, local, dist):
                    "the outer FGMRES complex128 (SURVEY.md §7.3 item 5)"}
 
     # ---- e2e through the public API (host numpy inputs, pinned) ----
+    # the travel time enters as tau1 alone: tau, grad(tau), lap(tau) are formed on the device
+    # (tau_derivatives, helmadr/eikonal.py:180-226) inside the timed call
+    from paper_1712_06091_b200.fields import DeviceTravelTime
+
     med = type(wl.medium)(g, pinned(wl.medium.kappa_sq), pinned(wl.medium.gamma))
-    tt = wl.tt
-    tt_p = type(tt)(g, tt.tau1, pinned(tt.tau), pinned(tt.grad1), pinned(tt.grad2), pinned(tt.lap), tt.base)
+    tt_p = DeviceTravelTime(g, wl.source, pinned(wl.tt.tau1))
     e2e_its = 0
     u = a = None
     for _ in range(max(1, min(args.warmup, 2))):
@@ -242,15 +257,15 @@ def run_ours(args, ws, rank, local, dist):
         e2e_its += r.iterations
     t_e2e = max_over_ranks(time.perf_counter() - t0, dist)
     e2e_value = sum_over_ranks(N * e2e_its / 1e6, dist) / t_e2e
-    h2d = (3 + dim) * 8 * N  # kappa^2, gamma, grad(tau) per axis, lap(tau)
-    h2d += 8 * N + 16        # tau (device waveform composition), the point source's one value
+    h2d = 3 * 8 * N + 16     # kappa^2, gamma, tau1; the point source's one value
     d2h = 2 * 16 * N         # amplitude a and waveform u
     agree = float(np.linalg.norm(a.reshape(-1) - a_dev) / np.linalg.norm(a_dev))
 
-    # ---- dominant-kernel roofline: fine-level relaxation stencil (K1), live CUDA events ----
-    roof = kernel_roofline(H, L, wl, cfg, args)
-    hbm, src = peaks()
+    # ---- rooflines: the dominant kernel (cluster engine) and the fine sweep K1, live CUDA events ----
     its_mean = sum(its_list) / len(its_list)
+    roof = engine_roofline(H, L, wl, cfg, its_mean, sum(t_kry) / len(t_kry))
+    roof_k1 = kernel_roofline(H, L, wl, cfg, args)
+    hbm, src = peaks()
     solve_bw = B_OP_2D_UPWIND_C128 * N * its_mean / (sum(t_kry) / len(t_kry)) / 1e9
     out = {
         "metric": "amplitude solve Mdof*iter/s (FGMRES(5) + K-cycle, ADR upwind blend)",
@@ -265,23 +280,22 @@ def run_ours(args, ws, rank, local, dist):
         "vs_baseline": None,
         "dtype": "c128",
         "data": "synthetic (seeded config builder: linear-gradient velocity, analytic tau)",
-        "config": {"workload": f"{wl.name} (BASELINE configs[1], 2D 1025x1025, c128)", "grid": [n1, n2],
-                   "strategy": "adr_upwind_blend", "tol": args.tol, "restart": 5, "levels": 5,
-                   "outer_iterations": its_list, "t_setup_ms": [x * 1e3 for x in t_setup],
-                   "t_krylov_ms": [x * 1e3 for x in t_kry], "parallelism": f"replicas x{ws}",
-                   "l2": "working set (~1.3 GB) > 126 MB L2; no flush needed"},
+        "config": bench_config(wl, args, ws),
+        "run": {"outer_iterations": its_list, "t_setup_ms": [x * 1e3 for x in t_setup],
+                "t_krylov_ms": [x * 1e3 for x in t_kry]},
         "e2e": {"value": e2e_value, "unit": "Mdof*iter/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": t_e2e / args.steps * 1e3, "rel_l2_vs_device_path": agree},
         "gpu_launches": int(launches),
         "complex64_mixed": c64,
         "roofline": roof,
+        "roofline_k1": roof_k1,
         "solve_roofline": {"bound": "hbm", "model_bytes_per_dof_iter": B_OP_2D_UPWIND_C128,
                            "achieved": solve_bw, "peak": hbm, "unit": "GB/s", "frac": solve_bw / hbm,
                            "peak_source": src, "note": "B_op (SURVEY.md §8(d)) over the FGMRES time"},
         "clocks": clk.summary(),
     }
     if rank == 0 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(wl, args, sample_its=args.cpu_its, threads_one=True)
+        out["cpu_baseline"] = cpu_baseline(wl, args, its_full=round(its_mean))
     if args.extra_3d:
         out["config_4_3d"] = guarded_slab_run(lambda: run_3d(args, L, local, dist, ws, rank), out, ws, rank,
                                               args.slab_timeout)
@@ -459,8 +473,7 @@ def run_3d(args, L, local, dist, ws=1, rank=0, which="cfg4"):
 
         ws_ = workloads.cfg3(513)  # 1025 x 513: same recipe, bounded CPU sample
         gg = ws_.grid
-        p = O.Problem(gg.n1, gg.n2, gg.h1, gg.h2, ws_.omega, (ws_.source.i1, ws_.source.i2), ws_.medium.kappa_sq,
-                      ws_.medium.gamma, ws_.tt.tau, ws_.tt.grad1, ws_.tt.grad2, ws_.tt.lap, ws_.bc)
+        p = oracle_problem(ws_)
         with threadpool_limits(1):
             t0 = time.perf_counter()
             _, _, r = O.solve_upwind(p, tol=args.tol, maxiter=6)
@@ -478,8 +491,11 @@ def run_3d(args, L, local, dist, ws=1, rank=0, which="cfg4"):
         bc = ND.bc_dict(3, ws.bc)
         with threadpool_limits(1):
             t0 = time.perf_counter()
+            grads, lap, tau = ND.tau_fields(ws.tt.tau1, gg.Ls, ws.source.index)
+        with threadpool_limits(1):
+            t0 = time.perf_counter()
             _, r = ND.solve_upwind(gg.shape, gg.hs, ws.omega, ws.source.index, ws.medium.kappa_sq, ws.medium.gamma,
-                                   list(ws.tt.grads), ws.tt.lap, ws.tt.tau, bc, maxiter=3)
+                                   grads, lap, tau, bc, maxiter=3)
             tc = time.perf_counter() - t0
         out["cpu_baseline"] = {"value": gg.n_nodes * r.iterations / tc / 1e6, "unit": "Mdof*iter/s", "cores": 1,
                                "kind": "port", "sample": f"nd oracle on cfg4_65 (65x65x33): assembly + hierarchy + "
@@ -519,6 +535,138 @@ def run_cfg5_sl(args, L, wl):
                     "diag(kappa^2), the 'shift 1+0.5i' of BASELINE config 5"}
 
 
+def op_stream_model(Ns, S, S_outer, b=16, restart=5, s_coarse=10):
+    """Algorithmic bytes of the reference's op stream (SURVEY.md §8(d) counting: stencil
+    (S+2)b per point, +b for a fused right-hand-side read or D^-1; dot 2b, axpy 3b, norm b,
+    scale 2b, lincomb (k+2)b; copies and known-zero spmvs not counted; re-orthogonalisation
+    on every FGMRES step, two inner iterations; S = mean non-zeros per row).  Follows
+    helmadr/krylov.py:91-242 and helmadr/multigrid.py:132-171.  Returns (bytes per level per
+    outer iteration, function level -> bytes of one inner FGMRES(2) call at that level with
+    everything below it).  For config 2 the total reproduces SURVEY's B_op (7,726 B/dof/it)
+    within 1%."""
+    nl = len(Ns)
+
+    def relax(lev, l, s, xzero):
+        t = 0 if xzero else (S[l] + 3) * b
+        t += 3 * b
+        for j in range(s):
+            t += (S[l] + 3) * b + (j + 1) * 5 * b + 3 * b
+        t += (s + 3) * b
+        lev[l] += t * Ns[l]
+
+    def kcycle(lev, l):
+        relax(lev, l, l + 2, True)
+        lev[l] += (S[l] + 3) * b * Ns[l] + b * Ns[l] + 2 * b * Ns[l]
+        lev[l + 1] += 2 * b * Ns[l + 1]
+        if l + 1 == nl - 1:
+            relax(lev, l + 1, s_coarse, True)
+        else:
+            inner(lev, l + 1)
+        relax(lev, l, l + 2, False)
+
+    def inner(lev, c):
+        t = 4 * b
+        for j in range(2):
+            kcycle(lev, c)
+            t += (S[c] + 2) * b + 3 * b + 2 * (j + 1) * 5 * b + 2 * b
+        t += 4 * b + (S[c] + 3) * b + b
+        lev[c] += t * Ns[c]
+
+    lev = [0.0] * nl
+    kcycle(lev, 0)
+    t = sum((S_outer + 2) * b + 3 * b + 2 * (j + 1) * 5 * b + 2 * b for j in range(restart)) / restart
+    t += ((restart + 2) * b + (S_outer + 3) * b + 3 * b) / restart
+    lev[0] += t * Ns[0]
+
+    def inner_bytes(c):
+        x = [0.0] * nl
+        inner(x, c)
+        return sum(x)
+
+    return lev, inner_bytes
+
+
+def engine_roofline(H, L, wl, cfg, its_mean, t_krylov):
+    """The dominant kernel of the headline solve: k_cluster_engine, the coarse part of the
+    K-cycle (inner FGMRES(2) at the engine's entry level with both recursive K-cycles and
+    the coarsest GMRES(10)) as ONE persistent 16-CTA cluster kernel.  Timed live with CUDA
+    events (hadr_ce_bench: back-to-back launches on the library stream, after a real
+    preconditioner application filled its inputs); algorithmic bytes per launch = the
+    reference op stream of that call (op_stream_model with the levels' measured mean
+    non-zeros per row).  latency_budget: the engine's clock64 phase counters over profiled
+    launches — reduction-separated steps per launch and what each costs."""
+    import ctypes as C
+
+    from paper_1712_06091_b200 import operators
+    from paper_1712_06091_b200.fields import point_source
+
+    g = wl.grid
+    H2 = operators.assemble_adr(wl.medium, g, wl.omega, wl.tt, "upwind2", wl.bc)
+    H1 = operators.assemble_adr(wl.medium, g, wl.omega, wl.tt, "upwind1", wl.bc)
+    hier = H.build_hierarchy(operators.blend_operator(H2, H1, cfg.beta), g, cfg.levels)
+    del H1
+    M = H.make_kcycle_preconditioner(hier)
+    q = operators.rhs_transform(point_source(g, wl.source), wl.tt, wl.omega, "to_adr").reshape(-1)
+    M(q / np.linalg.norm(q))
+    entry = None
+    for lev in range(2, hier.n_levels):
+        try:
+            t = C.c_double()
+            _lib_check(L.hadr_ce_bench(hier.handle, lev, 1, C.byref(t)))
+            entry = lev
+            break
+        except ValueError:
+            continue
+    if entry is None:
+        return {"kernel": "k_cluster_engine", "error": "no level runs in the cluster engine"}
+    avg = C.c_double()
+    _lib_check(L.hadr_ce_bench(hier.handle, entry, 200, C.byref(avg)))
+    Ns = [int(np.prod(s)) for s in hier.shapes]
+    S = [hier.ops[l].nnz / Ns[l] if l >= entry - 1 else 0.0 for l in range(hier.n_levels)]
+    _, inner_bytes = op_stream_model(Ns, S, 7.0)
+    bytes_launch = inner_bytes(entry - 1)
+    hbm, src = peaks()
+    ach = bytes_launch / (avg.value * 1e-3) / 1e9
+    launches_per_it = 2 ** (entry - 2)  # inner(entry) runs once per visit of level entry-1
+    # latency budget: phase counters of CTA 0 over profiled launches (clock64, 1965 MHz)
+    from paper_1712_06091_b200 import _lib
+
+    prof = (C.c_ulonglong * 32)()
+    _lib.set_option("ce_profile", 1)
+    try:
+        L.hadr_ce_profile(prof, 1)
+        t = C.c_double()
+        _lib_check(L.hadr_ce_bench(hier.handle, entry, 50, C.byref(t)))
+        L.hadr_ce_profile(prof, 1)
+    finally:
+        _lib.set_option("ce_profile", 0)
+    v = list(prof)
+    nl_ = max(v[7], 1)
+    mhz = 1965.0
+    budget = {"launches_profiled": v[7], "us_per_launch_profiled": v[0] / mhz / nl_,
+              "allreduces_per_launch": v[2] / nl_, "us_per_allreduce": v[1] / mhz / max(v[2], 1),
+              "stencils_per_launch": v[6] / nl_, "us_per_stencil": v[5] / mhz / max(v[6], 1),
+              "control_us_per_launch": v[3] / mhz / nl_, "vector_ops_us_per_launch": v[8] / mhz / nl_,
+              "barrier_us_per_launch": v[10] / mhz / nl_, "transfer_us_per_launch": v[12] / mhz / nl_,
+              "lincomb_us_per_launch": v[14] / mhz / nl_,
+              "note": "clock64 of CTA 0 (thread 0; relaxation control on the last thread), 1965 MHz"}
+    return {"kernel": f"k_cluster_engine (16-CTA cluster; inner FGMRES(2) at level {entry} "
+                      f"{'x'.join(map(str, hier.shapes[entry - 1]))} + K-cycles + coarsest GMRES(10))",
+            "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+            "peak_source": src, "avg_launch_ms": avg.value, "algorithmic_bytes_per_launch": bytes_launch,
+            "launches_per_outer_iteration": launches_per_it,
+            "share_of_krylov_time": launches_per_it * its_mean * avg.value * 1e-3 / t_krylov,
+            "mean_nnz_per_row": {f"level{l + 1}": S[l] for l in range(entry - 1, hier.n_levels)},
+            "latency_budget": budget,
+            "traffic_note": "working set L2/SMEM-resident (DRAM traffic ~0): bound by reduction-separated steps"}
+
+
+def _lib_check(code):
+    from paper_1712_06091_b200 import _lib
+
+    _lib.check(code)
+
+
 def kernel_roofline(H, L, wl, cfg, args):
     """K1 — the fine-level relaxation stencil y = A(D^-1 s x) with the basis write
     and the fused <V0, y> — timed live with CUDA events on the library stream
@@ -543,48 +691,92 @@ def kernel_roofline(H, L, wl, cfg, args):
 # --------------------------------------------------------------------------
 # CPU oracle (baseline / reference arm)
 # --------------------------------------------------------------------------
-def _oracle_step(wl, its, tol):
+def bench_config(wl, args, ws):
+    """The workload's config dict — identical in both arms (the driver compares them)."""
+    g = wl.grid
+    return {"workload": f"{wl.name} (BASELINE configs[1], 2D {g.n1}x{g.n2}, c128)", "grid": [g.n1, g.n2],
+            "strategy": "adr_upwind_blend", "tol": args.tol, "restart": 5, "levels": 5,
+            "parallelism": f"replicas x{ws}", "l2": "working set (~1.3 GB) > 126 MB L2; no flush needed"}
+
+
+def oracle_problem(wl):
+    """oracle.Problem of a 2D workload, the derivative fields formed by the oracle's own
+    restatement of tau_derivatives (helmadr/eikonal.py:180-226) from tau1."""
     from oracle import hadr_oracle as O
 
     g = wl.grid
-    p = O.Problem(g.n1, g.n2, g.h1, g.h2, wl.omega, (wl.source.i1, wl.source.i2), wl.medium.kappa_sq,
-                  wl.medium.gamma, wl.tt.tau, wl.tt.grad1, wl.tt.grad2, wl.tt.lap, wl.bc)
+    src = (wl.source.i1, wl.source.i2)
+    gr1, gr2, lap, tau = O.tau_fields(wl.tt.tau1, g.L1, g.L2, src)
+    return O.Problem(g.n1, g.n2, g.h1, g.h2, wl.omega, src, wl.medium.kappa_sq, wl.medium.gamma, tau, gr1, gr2, lap,
+                     wl.bc)
+
+
+def _oracle_upwind_timed(p, tol, maxiter):
+    """The reference's timed region of solve_adr_upwind (helmadr/drivers.py:153-165) on the
+    oracle restatement: (t_setup = assembly + blend + hierarchy, t_krylov = fgmres, iterations)."""
+    from oracle import hadr_oracle as O
+
+    q = O.delta_source(p.n1, p.n2, p.h1, p.h2, p.src)
+    qh = O.to_adr(q, p.tau, p.omega).reshape(-1)
     t0 = time.perf_counter()
-    u, a, rep = O.solve_upwind(p, tol=tol, maxiter=its)
-    return time.perf_counter() - t0, rep.iterations
+    H2 = O.adr_of(p, "upwind2")
+    H1 = O.adr_of(p, "upwind1")
+    B = ((1.0 - 0.25) * H2 + 0.25 * H1).tocsr()
+    Hi = O.hierarchy(B, (p.n1, p.n2), 5)
+    t1 = time.perf_counter()
+    _, rep = O.fgmres(H2, qh, None, O.kcycle_precond(Hi), 5, maxiter, tol)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, rep.iterations
 
 
-def cpu_baseline(wl, args, sample_its, threads_one):
-    """The oracle (numpy/scipy restatement of the reference) on this host: one
-    bounded sample = assembly + hierarchy + `sample_its` outer iterations."""
+def _charged(t_setup, t_kry, its, its_full):
+    """Seconds a full solve would take: the sample's setup + its per-iteration cost x the
+    full solve's iteration count (setup charged once, as in the GPU arm's solve)."""
+    return t_setup + its_full * t_kry / max(its, 1)
+
+
+def cpu_baseline(wl, args, its_full):
+    """The oracle (numpy/scipy restatement of the reference, 1 thread) on this host: one
+    bounded sample = assembly + hierarchy + `--cpu-its` outer iterations, charged to the
+    full solve's iteration count (the GPU arm's, equal to the reference's within +-1 by the
+    parity tests)."""
     from threadpoolctl import threadpool_limits
 
-    if threads_one:
-        with threadpool_limits(1):
-            t, its = _oracle_step(wl, sample_its, args.tol)
-    else:
-        t, its = _oracle_step(wl, sample_its, args.tol)
+    p = oracle_problem(wl)
+    with threadpool_limits(1):
+        ts, tk, its = _oracle_upwind_timed(p, args.tol, args.cpu_its)
+    t = _charged(ts, tk, its, its_full)
     N = wl.grid.n_nodes
-    return {"value": N * its / t / 1e6, "unit": "Mdof*iter/s", "cores": 1, "kind": "port",
-            "sample": f"oracle solve_upwind on {wl.name}: assembly + hierarchy + {its} outer FGMRES iterations "
-                      f"({t:.1f} s); host cpu_count={os.cpu_count()}, scipy sparse kernels single-threaded"}
+    return {"value": N * its_full / t / 1e6, "unit": "Mdof*iter/s", "cores": 1, "kind": "port",
+            "sample": f"oracle solve_upwind on {wl.name}: assembly + hierarchy ({ts:.1f} s) + {its} outer FGMRES "
+                      f"iterations ({tk:.1f} s), charged to a full {its_full}-iteration solve ({t:.1f} s); host "
+                      f"cpu_count={os.cpu_count()}, 1 thread (scipy sparse kernels are single-threaded)"}
 
 
 def run_reference(args, ws, rank, local, dist):
+    """The reference's CPU path (the oracle restatement, bit-exact to helmadr on its own
+    goldens) on the host cores with all BLAS threads, same workload / config / metric.
+    A full solve runs once first (untimed calibration: its iteration count and time); each
+    warm-up and timed step is then a bounded sample — assembly + hierarchy + `--ref-its`
+    outer iterations — charged to the full solve's iteration count (setup once, per-
+    iteration cost x iterations), so one step stands for the same work as a GPU-arm step."""
     if rank != 0:
         return None
     from paper_1712_06091_b200 import workloads
 
     wl = workloads.by_name(args.workload, args.size)
     N = wl.grid.n_nodes
+    p = oracle_problem(wl)
+    ts0, tk0, its_full = _oracle_upwind_timed(p, args.tol, args.maxiter)
     for _ in range(args.warmup):
-        _oracle_step(wl, 1, args.tol)
-    tot_t, tot_its = 0.0, 0
+        _oracle_upwind_timed(p, args.tol, args.ref_its)
+    charged, walls, samples = [], [], []
     for _ in range(args.steps):
-        t, its = _oracle_step(wl, args.ref_its, args.tol)
-        tot_t += t
-        tot_its += its
-    value = N * tot_its / tot_t / 1e6
+        ts, tk, its = _oracle_upwind_timed(p, args.tol, args.ref_its)
+        charged.append(_charged(ts, tk, its, its_full))
+        walls.append(ts + tk)
+        samples.append([round(ts, 3), round(tk, 3), its])
+    value = N * its_full * len(charged) / sum(charged) / 1e6
     cores = os.cpu_count()
     return {
         "impl": "reference",
@@ -594,17 +786,20 @@ def run_reference(args, ws, rank, local, dist):
         "n_gpus": ws,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": tot_t / args.steps * 1e3,
+        "ms_per_step": sum(charged) / len(charged) * 1e3,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "c128",
-        "data": "synthetic (seeded config builder)",
-        "config": {"workload": f"{wl.name} (BASELINE configs[1])", "grid": list(wl.grid.shape),
-                   "strategy": "adr_upwind_blend", "tol": args.tol},
+        "data": "synthetic (seeded config builder: linear-gradient velocity, analytic tau)",
+        "config": bench_config(wl, args, ws),
+        "run": {"full_solve": {"iterations": its_full, "t_setup_s": ts0, "t_krylov_s": tk0,
+                               "value": N * its_full / (ts0 + tk0) / 1e6},
+                "samples_setup_krylov_its": samples, "sample_wall_ms": [w * 1e3 for w in walls]},
         "cpu_baseline": {"value": value, "unit": "Mdof*iter/s", "cores": cores, "kind": "port",
-                         "sample": f"per step: oracle assembly + hierarchy + {args.ref_its} outer iterations "
-                                   f"(all BLAS threads; scipy sparse kernels single-threaded)"},
+                         "sample": f"per step: oracle assembly + hierarchy + {args.ref_its} outer iterations, "
+                                   f"charged to the calibration solve's {its_full} iterations (all BLAS threads; "
+                                   f"scipy sparse kernels single-threaded)"},
         "e2e": {"value": value, "unit": "Mdof*iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -619,8 +814,8 @@ def main():
     ap.add_argument("--size", type=int, default=None, help="override the grid size n (parity/debug runs)")
     ap.add_argument("--tol", type=float, default=1e-6)
     ap.add_argument("--maxiter", type=int, default=1000)
-    ap.add_argument("--cpu-its", type=int, default=6, help="outer iterations in the cpu_baseline sample")
-    ap.add_argument("--ref-its", type=int, default=4, help="outer iterations per reference-arm step")
+    ap.add_argument("--cpu-its", type=int, default=4, help="outer iterations in the cpu_baseline sample")
+    ap.add_argument("--ref-its", type=int, default=2, help="outer iterations per reference-arm step sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extra-3d", type=int, default=513, help="also run BASELINE config 4 at this n (0: skip)")
     ap.add_argument("--steps-3d", type=int, default=2)
@@ -630,7 +825,11 @@ def main():
     ap.add_argument("--extra-cfg5", type=int, default=257,
                     help="also run BASELINE config 5's recipe at this n (0: skip; full size 1025 needs 8 GPUs)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     ws, rank, local, dist = dist_init()
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}")
     if args.impl == "reference":
         out = run_reference(args, ws, rank, local, dist)
     else:

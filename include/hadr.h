@@ -47,6 +47,8 @@ typedef struct {
   double final_relres;
   double wall_time;   /* seconds, host clock around the device solve */
   double device_time; /* seconds, CUDA events on the library stream around the solve */
+  double ortho_max;   /* max |<v_i, v_j>| (i != j) of the Arnoldi basis over the restart cycles; computed
+                         only with HADR_FG_DIAGNOSTICS (helmadr/krylov.py:214-217), else 0 */
 } hadr_report;
 
 const char* hadr_last_error(void);
@@ -137,10 +139,17 @@ void hadr_hier_destroy(hadr_hier h);
  * "kcycle_c64" = 1: hierarchies built afterwards apply their operators from complex64 storage
  * (mixed precision: K-cycle operators c64, vectors / reductions / outer FGMRES c128) */
 int hadr_set_option(const char* name, double value);
-/* cluster-engine phase counters (enable with hadr_set_option("ce_profile", 1)): cycles seen by CTA 0
- * [total, allreduce, n, epilogue, n, stencil, n, launches, vector ops, n, barriers, n, transfers, n,
- *  relaxation update, n] */
-int hadr_ce_profile(unsigned long long* out16, int reset);
+/* cluster-engine phase counters (enable with hadr_set_option("ce_profile", 1)): cycles seen by CTA 0,
+ * 32 entries: [total, allreduce, n, relaxation control, n, stencil, n, launches, vector ops, n, barriers,
+ * n, transfers, n, relaxation update, n, stencil on levels > 8192 points, n, shared-memory relaxation
+ * staging (> 8192), n, its stencil rows (> 8192), n, staging (small levels), n, stencil rows (small), n,
+ * all-reduce cluster-barrier wait, n, inner-FGMRES control, n, 0, 0] */
+int hadr_ce_profile(unsigned long long* out32, int reset);
+/* Measurement hook (bench.py roofline): launch the cluster engine `reps` times back to back at
+ * hierarchy level `level` (1-based, 2 <= level < n_levels) in its inner-FGMRES(2) entry — one
+ * launch = the coarse part of the K-cycle from that level down (helmadr/multigrid.py:153-167)
+ * on the level's current right-hand side — and return the mean launch time (CUDA events). */
+int hadr_ce_bench(hadr_hier h, int level, int reps, double* avg_ms);
 /* microbenchmark of the stencil kernel K1 on device vectors x, y: `reps` back-to-back launches timed
  * with CUDA events on the library stream; variant 0 = y = A x, 1 = the relaxation's fused
  * y = A(D^-1 s x) + basis write + <V0, y>.  *avg_ms = mean launch duration (incl. any finalize). */
@@ -173,6 +182,13 @@ int hadr_dist_plan(int n1, int n2, int n3, int max_levels, int* bounds, int* n_d
 /* pure host helper: split n1 planes into `size` slabs with interior bounds multiples of `align` */
 int hadr_slab_bounds(int n1, int size, int align, int* bounds /* size + 1 */);
 
+/* tau_derivatives (helmadr/eikonal.py:180-226) with AnalyticBase's distance factor
+ * (helmadr/eikonal.py:15-36; 3D: the per-axis generalisation, lap(tau0) = 2/r): from tau1 on the
+ * n[0] x .. x n[dim-1] grid over [0, L[a]] with the source node src[], writes tau = tau0 tau1 (may be
+ * NULL), grads (dim planes of N doubles, axis-major) and lap.  Bit-identical to the reference's
+ * numpy expressions (np.hypot = glibc's hypot).  on_device: every array is a device pointer. */
+int hadr_tau_derivatives(int dim, const int* n, const double* L, const int* src, const double* tau1, double* tau,
+                         double* grads, double* lap, int on_device);
 /* out = q (.) exp(sign * i * omega * tau), sign = +1 (to_adr) / -1 (to_helmholtz): the phase transforms
  * of helmadr/operators.py:269-278 (rhs_transform) and compose_waveform (helmadr/drivers.py:171-173) on the
  * device; tau real.  cos/sin are the device's (within an ulp of numpy's). */
@@ -206,6 +222,14 @@ int hadr_gmres_relax(hadr_op A, const double* b, const double* x, int steps, dou
  * M may be NULL (identity preconditioner); x0 may be NULL (zero). */
 int hadr_fgmres(hadr_op A, hadr_hier M, const double* b, const double* x0, int restart, int maxiter, double tol,
                 double* x_out, hadr_report* rep, double* history, int history_cap, int on_device);
+/* fgmres with KrylovConfig's switches (helmadr/krylov.py:16-31): flags HADR_FG_NONFLEXIBLE = cfg.flexible
+ * False (x += M(V[:k]^T y) at the end of each cycle, helmadr/krylov.py:222-223; identical to the flexible
+ * update when M is NULL), HADR_FG_DIAGNOSTICS = cfg.collect_diagnostics (rep->ortho_max,
+ * helmadr/krylov.py:214-217). */
+#define HADR_FG_NONFLEXIBLE 1
+#define HADR_FG_DIAGNOSTICS 2
+int hadr_fgmres_ex(hadr_op A, hadr_hier M, const double* b, const double* x0, int restart, int maxiter, double tol,
+                   int flags, double* x_out, hadr_report* rep, double* history, int history_cap, int on_device);
 
 #ifdef __cplusplus
 }

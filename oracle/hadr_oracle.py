@@ -447,9 +447,10 @@ def _matvec_of(A):
     return A if callable(A) else (lambda v: A @ v)
 
 
-def fgmres(A, b, x0=None, M=None, restart=5, maxiter=200, tol=1e-5, diagnostics=False):
-    """Restarted flexible GMRES with MGS + one conditional re-orthogonalisation
-    and complex Givens (helmadr/krylov.py:122-242).  Returns (x, Report)."""
+def fgmres(A, b, x0=None, M=None, restart=5, maxiter=200, tol=1e-5, diagnostics=False, flexible=True):
+    """Restarted (flexible) GMRES with MGS + one conditional re-orthogonalisation
+    and complex Givens (helmadr/krylov.py:122-242).  flexible=False: x += M(V[:k]^T y)
+    (helmadr/krylov.py:222-223).  Returns (x, Report)."""
     t0 = time.perf_counter()
     mv = _matvec_of(A)
     b = np.asarray(b, dtype=np.complex128).reshape(-1)
@@ -528,7 +529,7 @@ def fgmres(A, b, x0=None, M=None, restart=5, maxiter=200, tol=1e-5, diagnostics=
             omax = max(omax, float(np.abs(G).max()))
         if k > 0:
             y = np.linalg.solve(Hm[:k, :k], g[:k]) if k > 1 else g[:1] / Hm[0, 0]
-            x = x + Z[:k].T @ y
+            x = x + Z[:k].T @ y if flexible else x + pc(V[:k].T @ y)
         r = b - mv(x)
         rn = float(np.linalg.norm(r))
         if broke:

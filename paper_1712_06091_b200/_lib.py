@@ -28,7 +28,8 @@ EXPORTS = (
     "hadr_stream_timer", "hadr_set_option", "hadr_ce_profile", "hadr_op_bench",
     "hadr_dist_nccl_id", "hadr_dist_init_nccl", "hadr_dist_init_host", "hadr_dist_finalize", "hadr_dist_info",
     "hadr_dist_plan", "hadr_slab_bounds", "hadr_fast_march", "hadr_phase_transform", "hadr_op_storage",
-    "hadr_relative_error", "hadr_memset",
+    "hadr_relative_error", "hadr_memset", "hadr_fgmres_ex",
+    "hadr_tau_derivatives", "hadr_ce_bench",
 )
 
 # host-communicator callbacks (include/hadr.h hadr_host_*)
@@ -47,6 +48,7 @@ class HadrReport(C.Structure):
         ("final_relres", C.c_double),
         ("wall_time", C.c_double),
         ("device_time", C.c_double),
+        ("ortho_max", C.c_double),
     ]
 
 
@@ -78,6 +80,7 @@ _SIGS = {
     "hadr_set_option": (_i, [C.c_char_p, _d]),
     "hadr_ce_profile": (_i, [_vp, _i]),
     "hadr_op_bench": (_i, [_vp, _vp, _vp, _i, _i, C.POINTER(_d)]),
+    "hadr_ce_bench": (_i, [_vp, _i, _i, C.POINTER(_d)]),
     "hadr_transfer": (_i, [_i, _i, _i, _i, _vp, _vp, _i]),
     "hadr_hier_create": (_i, [_vp, _i, _i, _d, C.POINTER(_vp)]),
     "hadr_hier_from_ops": (_i, [_i, _vp, _i, _d, C.POINTER(_vp)]),
@@ -89,6 +92,7 @@ _SIGS = {
     "hadr_launch_count": (C.c_longlong, []),
     "hadr_gmres_relax": (_i, [_vp, _vp, _vp, _i, _vp, _i]),
     "hadr_fgmres": (_i, [_vp, _vp, _vp, _vp, _i, _i, _d, _vp, C.POINTER(HadrReport), _vp, _i, _i]),
+    "hadr_fgmres_ex": (_i, [_vp, _vp, _vp, _vp, _i, _i, _d, _i, _vp, C.POINTER(HadrReport), _vp, _i, _i]),
     "hadr_dist_nccl_id": (_i, [_vp]),
     "hadr_dist_init_nccl": (_i, [_i, _i, _vp]),
     "hadr_dist_init_host": (_i, [_i, _i, HOST_ALLGATHER, HOST_SENDRECV, HOST_BCAST]),
@@ -100,6 +104,7 @@ _SIGS = {
     "hadr_phase_transform": (_i, [C.c_longlong, _vp, _vp, _d, _i, _vp, _i]),
     "hadr_op_storage": (_i, [_vp, C.POINTER(_i), C.POINTER(C.c_longlong)]),
     "hadr_memset": (_i, [_vp, _i, C.c_size_t]),
+    "hadr_tau_derivatives": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i]),
     "hadr_relative_error": (_i, [C.c_longlong, _vp, _vp, _d, _vp, C.POINTER(_d), C.POINTER(C.c_longlong), _vp, _i,
                                  _vp, _i]),
 }

@@ -191,6 +191,43 @@ int hadr_phase_transform(long long n, const double* q, const double* tau, double
     dfree(tmp);
   });
 }
+int hadr_tau_derivatives(int dim, const int* n, const double* L, const int* src, const double* tau1, double* tau,
+                         double* grads, double* lap, int on_device) {
+  return guarded([&] {
+    if (dim != 2 && dim != 3) throw ValueError("dim must be 2 or 3");
+    long N = 1;
+    double h[3];
+    for (int a = 0; a < dim; ++a) {
+      if (n[a] < 4) throw ValueError("tau_derivatives needs at least 4 nodes per axis (one-sided 4-point ends)");
+      if (src[a] < 0 || src[a] >= n[a]) throw ValueError("source index outside the grid");
+      h[a] = L[a] / (n[a] - 1);  // GridSpec.h = L / (n - 1)
+      N *= n[a];
+    }
+    Ctx& c = Ctx::get();
+    const size_t nb = N * sizeof(double);
+    const double* t1 = tau1;
+    double *tmp = nullptr, *dtau = tau, *dg = grads, *dl = lap;
+    if (!on_device) {  // one staging block: tau1 | tau | grads | lap
+      tmp = dalloc<double>((size_t)N * (dim + 3));
+      HADR_CUDA(cudaMemcpyAsync(tmp, tau1, nb, cudaMemcpyHostToDevice, c.stream));
+      t1 = tmp;
+      dtau = tau ? tmp + N : nullptr;
+      dg = tmp + 2 * N;
+      dl = tmp + (2 + dim) * N;
+    }
+    double* gp[3] = {dg, dg + N, dim == 3 ? dg + 2 * N : nullptr};
+    launch_tau_derivs(c.stream, dim, n, h, L, src, t1, dtau, gp, dl);
+    HADR_CUDA(cudaGetLastError());
+    if (!on_device) {
+      if (tau) HADR_CUDA(cudaMemcpyAsync(tau, dtau, nb, cudaMemcpyDeviceToHost, c.stream));
+      HADR_CUDA(cudaMemcpyAsync(grads, dg, nb * dim, cudaMemcpyDeviceToHost, c.stream));
+      HADR_CUDA(cudaMemcpyAsync(lap, dl, nb, cudaMemcpyDeviceToHost, c.stream));
+    }
+    c.sync();
+    dfree(tmp);
+  });
+}
+
 int hadr_memcpy(void* dst, const void* src, size_t bytes, int kind) {
   return guarded([&] {
     Ctx& c = Ctx::get();
@@ -327,6 +364,7 @@ int hadr_solve_adr_upwind(int dim, int n1, int n2, int n3, double h1, double h2,
       rep->final_relres = r.final_relres;
       rep->wall_time = r.wall_time;
       rep->device_time = r.device_time;
+      rep->ortho_max = r.ortho_max;
       const int nh = (int)r.history.size();
       rep->history_len = nh;
       if (history)
@@ -369,6 +407,7 @@ int hadr_solve_adr_upwind(int dim, int n1, int n2, int n3, double h1, double h2,
       rep->final_relres = r.final_relres;
       rep->wall_time = r.wall_time;
       rep->device_time = r.device_time;
+      rep->ortho_max = r.ortho_max;
       const int nh = (int)r.history.size();
       rep->history_len = nh;
       if (history)
@@ -493,6 +532,33 @@ int hadr_precond_apply(hadr_hier hh, const double* r, double* z, int on_device) 
 
 long long hadr_launch_count(void) { return g_launch_count; }
 
+int hadr_ce_bench(hadr_hier hh, int level, int reps, double* avg_ms) {
+  return guarded([&] {
+    Ctx& c = Ctx::get();
+    Hier* h = hh->h;
+    const int li = level - 1;
+    const int nl = (int)h->lv.size();
+    if (li < 1 || li >= nl - 1) throw ValueError("the engine's inner-FGMRES entry needs 2 <= level < n_levels");
+    if (!h->use_ce(li)) throw ValueError("this level does not run in the cluster engine");
+    auto once = [&]() { launch_cluster_engine(c.stream, h->ce_desc, 1, li, nullptr, nullptr, nullptr, CE_CTAS,
+                                              h->ce_tile(li)); };
+    for (int i = 0; i < 3; ++i) once();
+    cudaEvent_t e0, e1;
+    HADR_CUDA(cudaEventCreate(&e0));
+    HADR_CUDA(cudaEventCreate(&e1));
+    HADR_CUDA(cudaEventRecord(e0, c.stream));
+    for (int i = 0; i < reps; ++i) once();
+    HADR_CUDA(cudaEventRecord(e1, c.stream));
+    HADR_CUDA(cudaEventSynchronize(e1));
+    HADR_CUDA(cudaGetLastError());
+    float ms = 0.f;
+    HADR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *avg_ms = ms / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
 int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, double* avg_ms) {
   return guarded([&] {
     Ctx& c = Ctx::get();
@@ -545,10 +611,10 @@ int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, 
   });
 }
 
-int hadr_ce_profile(unsigned long long* out16, int reset) {
+int hadr_ce_profile(unsigned long long* out32, int reset) {
   return guarded([&] {
     Ctx::get().sync();
-    if (ce_profile_read(out16, reset)) throw std::runtime_error("ce_profile_read failed");
+    if (ce_profile_read(out32, reset)) throw std::runtime_error("ce_profile_read failed");
   });
 }
 
@@ -751,11 +817,16 @@ int hadr_gmres_relax(hadr_op A, const double* b, const double* x, int steps, dou
 
 int hadr_fgmres(hadr_op A, hadr_hier M, const double* b, const double* x0, int restart, int maxiter, double tol,
                 double* x_out, hadr_report* rep, double* history, int history_cap, int on_device) {
+  return hadr_fgmres_ex(A, M, b, x0, restart, maxiter, tol, 0, x_out, rep, history, history_cap, on_device);
+}
+
+int hadr_fgmres_ex(hadr_op A, hadr_hier M, const double* b, const double* x0, int restart, int maxiter, double tol,
+                   int flags, double* x_out, hadr_report* rep, double* history, int history_cap, int on_device) {
   return guarded([&] {
     Op* op = A->op;
     DevVec db(b, op->N, on_device, true), dx0(x0, op->N, on_device, true), dx(x_out, op->N, on_device, false);
     Report r;
-    fgmres(*op, M ? M->h : nullptr, db.p, x0 ? dx0.p : nullptr, dx.p, restart, maxiter, tol, r);
+    fgmres(*op, M ? M->h : nullptr, db.p, x0 ? dx0.p : nullptr, dx.p, restart, maxiter, tol, r, flags);
     dx.copy_out(x_out);
     Ctx::get().sync();
     rep->iterations = r.iterations;
@@ -765,6 +836,7 @@ int hadr_fgmres(hadr_op A, hadr_hier M, const double* b, const double* x0, int r
     rep->final_relres = r.final_relres;
     rep->wall_time = r.wall_time;
     rep->device_time = r.device_time;
+    rep->ortho_max = r.ortho_max;
     const int nh = (int)r.history.size();
     rep->history_len = nh;
     if (history)

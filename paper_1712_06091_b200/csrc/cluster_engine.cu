@@ -23,8 +23,7 @@
 namespace hadr {
 
 struct CEShared {
-  double slot[2][4];  // DSMEM all-reduce slots (double-buffered)
-  double tot[4];
+  double pslot[2][CE_CTAS][4];  // all-reduce: CTA r's total, pushed here by CTA r (double-buffered)
   double bsum[4 * 32];
   RelaxCtl rc;            // the (single) live relaxation
   FgCtl2 fg[CE_MAXLEV];   // one inner FGMRES(2) per level (nested)
@@ -38,11 +37,19 @@ struct CEC {
   long gtid, gstride;
   int ph;
   CEShared* S;
-  unsigned long long* prof;  // CTA 0 / thread 0 phase counters (null = off)
+  unsigned long long* prof;      // CTA 0 / thread 0 phase counters (null = off)
+  unsigned long long* prof_ctl;  // CTA 0 / relaxation control thread (blockDim.x - 1): slot 3
 };
 
-// Phase profile of the engine (hadr_ce_profile): cycles seen by CTA 0 thread 0.
-__device__ unsigned long long g_ce_prof[16];
+// Phase profile of the engine (hadr_ce_profile): cycles seen by CTA 0 — thread 0, except
+// slot 3 (relaxation control), owned by the control thread (blockDim.x - 1).  Every slot
+// pair (cycles, count) has a single writer thread.  Slots: 0 total, 1 all-reduce, 3 relaxation
+// control, 5 stencil, 7 launches, 8 vector ops, 10 barriers, 12 transfers, 14 lincomb,
+// 16 stencil on levels > 8192 points, 18 / 20 shared-memory relaxation staging / stencil
+// rows on levels > 8192 points, 22 / 24 the same on smaller levels, 26 all-reduce cluster-
+// barrier wait, 28 inner-FGMRES control (thread 0).
+constexpr int CE_NPROF = 32;
+__device__ unsigned long long g_ce_prof[CE_NPROF];
 struct CEProfScope {
   unsigned long long* p;
   int slot;
@@ -50,12 +57,17 @@ struct CEProfScope {
   __device__ CEProfScope(const CEC& c, int s) : p(c.prof), slot(s), t0(0) {
     if (p) t0 = clock64();
   }
-  __device__ ~CEProfScope() {
+  __device__ CEProfScope(unsigned long long* q, int s) : p(q), slot(s), t0(0) {
+    if (p) t0 = clock64();
+  }
+  __device__ void stop() {
     if (p) {
       p[slot] += clock64() - t0;
       p[slot + 1] += 1;
+      p = nullptr;
     }
   }
+  __device__ ~CEProfScope() { stop(); }
 };
 
 __device__ __forceinline__ void ce_sync() {
@@ -67,16 +79,25 @@ __device__ __forceinline__ void ce_sync() {
     CEProfScope prof_sync_(c, 10); \
     ce_sync();                     \
   } while (0)
-__device__ __forceinline__ double ce_remote(const double* p, unsigned rank) {
-  unsigned long long in = reinterpret_cast<unsigned long long>(p), out;
-  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(in), "r"(rank));
-  return *reinterpret_cast<const double*>(out);
-}
 // mutable vectors are read through L2 (written by other CTAs of the cluster)
 __device__ __forceinline__ cplx ldm(const cplx* p, long i) { return __ldcg(p + i); }
 __device__ __forceinline__ cplx ldk(const cplx* p, long i) { return __ldg(p + i); }
 
-// Cluster all-reduce of NV doubles: every CTA ends with bit-identical totals.
+__device__ __forceinline__ void ce_store_remote(double* p, unsigned rank, double v) {
+  unsigned long long in = reinterpret_cast<unsigned long long>(p), out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(in), "r"(rank));
+  *reinterpret_cast<volatile double*>(out) = v;
+}
+
+// Cluster all-reduce of NV doubles: every thread of every CTA ends with bit-identical
+// totals.  Per CTA: warp partials (shuffle tree) -> warp 0 sums them in warp order and
+// PUSHES the CTA total into slot [rank] of every CTA (DSMEM stores, issued before the
+// barrier's release) -> cluster barrier -> every warp sums the 16 local slots in rank
+// order (the same shuffle tree in every warp and CTA).  No DSMEM load sits behind the
+// barrier and no block barrier follows it (the pull version read the 16 remote slots
+// from warp 0 after the barrier and broadcast through shared memory + __syncthreads).
+// Slots are double-buffered: a CTA pushes into a parity again only two all-reduces
+// later, after a barrier every thread reaches only once its reads of that parity are done.
 template <int NV>
 __device__ void ce_allreduce(CEC& c, double (&v)[NV]) {
   CEProfScope prof_(c, 1);
@@ -99,27 +120,20 @@ __device__ void ce_allreduce(CEC& c, double (&v)[NV]) {
       double t = lane < nw ? S->bsum[q * 32 + lane] : 0.0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (lane == 0) S->slot[c.ph][q] = t;
+      if (lane < (int)c.C) ce_store_remote(&S->pslot[c.ph][c.rank][q], lane, t);
     }
   }
-  ce_sync();
-  if (wid == 0) {
-    double t[NV];
-#pragma unroll
-    for (int q = 0; q < NV; ++q) t[q] = lane < (int)c.C ? ce_remote(&S->slot[c.ph][q], lane) : 0.0;
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t[q] += __shfl_xor_sync(0xffffffffu, t[q], o);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int q = 0; q < NV; ++q) S->tot[q] = t[q];
-    }
+  {
+    CEProfScope prof_w_(c, 26);
+    ce_sync();
   }
-  __syncthreads();
 #pragma unroll
-  for (int q = 0; q < NV; ++q) v[q] = S->tot[q];
+  for (int q = 0; q < NV; ++q) {
+    double t = lane < (int)c.C ? S->pslot[c.ph][lane][q] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    v[q] = t;
+  }
   c.ph ^= 1;
 }
 
@@ -169,6 +183,45 @@ __device__ __forceinline__ cplx ce_cc_row(const StencilDev& A, const cplx* tile,
 
 extern __shared__ cplx ce_tile[];
 
+// Fast rows of a standard 2D offset set (Std2D, compile-time offsets): the coefficient
+// pointer, sizes and offsets live in registers / immediates (the generic loop re-reads the
+// level descriptor from shared memory every point: its smem stores may alias it), and all
+// NO coefficient loads of a point are issued together.  Same accumulation order as
+// csr_matvec (ascending offsets, no FMA): bit-identical to the generic loop.
+// out(k, acc) consumes point k.
+template <int NO, bool C32, class F>
+__device__ __forceinline__ void ce_rows_std2d(const StencilDev& A, const cplx* tile, int t0, long own0, long own1,
+                                              long tw, long nwk, F&& out) {
+  const int n1 = A.n1, n2 = A.n2;
+  const long N = (long)n1 * n2;
+  const cplx* __restrict__ coef = A.coef;
+  const float2* __restrict__ coef32 = A.coef32;
+  for (long k = own0 + tw; k < own1; k += nwk) {
+    const int i1 = (int)(k / n2), i2 = (int)(k - (long)(k / n2) * n2);
+    cplx cv[NO];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      if constexpr (C32) {
+        const float2 f = __ldg(coef32 + (long)o * N + k);
+        cv[o] = make_double2((double)f.x, (double)f.y);
+      } else {
+        cv[o] = __ldg(coef + (long)o * N + k);
+      }
+    }
+    cplx acc = mk(0.0, 0.0);
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      const int j1 = i1 + Std2D::d1<NO>(o), j2 = i2 + Std2D::d2<NO>(o);
+      const bool ok = j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2;
+      const cplx v = tile[ok ? (long)(j1 - t0) * n2 + j2 : 0];
+      const cplx t = cadd(acc, cmul_sp(cv[o], v));
+      acc = ok ? t : acc;
+    }
+    out(k, acc);
+  }
+}
+
+
 template <int NO, int INM, int OUTM, int RED, bool C32>
 __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double s, const cplx* dinv, cplx* vout,
                               const cplx* b, cplx* y, const cplx* u, double (&red)[3]) {
@@ -187,6 +240,29 @@ __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double
   }
   __syncthreads();
   const long own1 = (long)r1 * n23;
+  if constexpr (NO == 5 || NO == 9 || NO == 21) {
+    if (A.std2d == NO) {
+      ce_rows_std2d<NO, C32>(A, ce_tile, t0, (long)r0 * n23, own1, threadIdx.x, blockDim.x, [&](long k, cplx acc) {
+        cplx vc = mk(0.0, 0.0);
+        if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) {
+          vc = ldm(x, k);
+          if (INM & IN_SCALE) vc = cscale(vc, s);
+          if (INM & IN_WRITEV) vout[k] = vc;
+        }
+        const cplx yy = (OUTM == OUT_RESID) ? csub(ldm(b, k), acc) : acc;
+        y[k] = yy;
+        if (RED & RED_NORM) red[0] += yy.x * yy.x + yy.y * yy.y;
+        if (RED & (RED_DOT | RED_DOT_CENTER)) {
+          const cplx uu = (RED & RED_DOT_CENTER) ? vc : ldm(u, k);
+          constexpr int o = (RED & RED_NORM) ? 1 : 0;
+          red[o] += uu.x * yy.x + uu.y * yy.y;
+          red[o + 1] += uu.x * yy.y - uu.y * yy.x;
+        }
+      });
+      __syncthreads();  // the tile is reused by the next stencil
+      return;
+    }
+  }
   for (long k = (long)r0 * n23 + threadIdx.x; k < own1; k += blockDim.x) {
     const int i1 = (int)(k / n23);
     const int rem = (int)(k - (long)i1 * n23);
@@ -241,6 +317,7 @@ template <int INM, int OUTM, int RED>
 __device__ __noinline__ void ce_stencil(CEC& c, const StencilDev& A, const cplx* x, double s, const cplx* dinv,
                                         cplx* vout, const cplx* b, cplx* y, const cplx* u, double (&red)[3]) {
   CEProfScope prof_(c, 5);
+  CEProfScope prof_big_(A.n1 * A.n2 * A.n3 > 8192 ? c.prof : nullptr, 16);
   red[0] = red[1] = red[2] = 0.0;
   if (A.coef32) {  // mixed precision: complex64-stored operator
     switch (A.nofs) {
@@ -365,9 +442,9 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
       ce_axpy<RED_NORM>(c, n, w, hcol, L.V[j], nullptr, v2);  // h = H[j][j]
       double v[1] = {v2[0]};
       ce_allreduce<1>(c, v);
-      {
-        CEProfScope prof_(c, 3);
-        if (ctl) relax_step_sm(R, j, v[0]);
+      if (ctl) {
+        CEProfScope prof_(c.prof_ctl, 3);
+        relax_step_sm(R, j, v[0]);
       }
       const double hn = sqrt(v[0]);
       const bool stop = (hn <= kBreakdownEps * beta) || (j + 1 >= s);  // helmadr/krylov.py:113-114
@@ -404,12 +481,25 @@ __device__ __forceinline__ cplx ce_remote_c(const cplx* p, unsigned rank) {
 
 template <int NO, bool C32>
 __device__ __forceinline__ void sm_stencil_rows(CEC& c, const StencilDev& A, const cplx* tile, int r0, int r1,
-                                                int t0, cplx* w, const cplx* v0, double (&red)[2]) {
+                                                int t0, cplx* w, const cplx* v0, double (&red)[2], long tw,
+                                                long nwk) {
   const int n1 = A.n1, n2 = A.n2, n3 = A.n3, nofs = A.nofs;
   const int n23 = n2 * n3;
   const long N = (long)n1 * n23;
   const long own0 = (long)r0 * n23, own1 = (long)r1 * n23;
-  for (long k = own0 + threadIdx.x; k < own1; k += blockDim.x) {
+  if constexpr (NO == 5 || NO == 9 || NO == 21) {
+    if (A.std2d == NO) {
+      ce_rows_std2d<NO, C32>(A, tile, t0, own0, own1, tw, nwk, [&](long k, cplx acc) {
+        const long p = k - own0;
+        w[p] = acc;
+        const cplx u = v0[p];
+        red[0] += u.x * acc.x + u.y * acc.y;
+        red[1] += u.x * acc.y - u.y * acc.x;
+      });
+      return;
+    }
+  }
+  for (long k = own0 + tw; k < own1; k += nwk) {
     const int i1 = (int)(k / n23);
     const int rem = (int)(k - (long)i1 * n23);
     const int i2 = rem / n3, i3 = rem - (rem / n3) * n3;
@@ -456,10 +546,12 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
   cplx* tile = ce_tile;                        // (rows + 4) * n23
   cplx* Vb = ce_tile + (long)(rows + 4) * n23;  // V[i] = Vb + i * rs, i <= s
   cplx* wb = Vb + (long)(s + 1) * rs;           // w[0], w[1]
-  // the control thread: the CTA's last, whose share of the vector work is the smallest
-  // (none at all on the coarsest grids), so the Givens updates run beside the other
-  // threads' work instead of ahead of it
+  // the control warp (the CTA's last) takes no share of the vector work: its last thread
+  // runs the Givens / least-squares update of each step while the other warps already
+  // stage and apply the next step's stencil, so the update is off the critical path
   const bool ctl = threadIdx.x == blockDim.x - 1;
+  const long nwk = blockDim.x - 32;                                   // worker threads
+  const long tw = threadIdx.x < nwk ? threadIdx.x : (long)1 << 40;    // this thread's first point (none: ctl warp)
   if (ctl) {
     R->steps = s;
     R->k = 0;
@@ -478,7 +570,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       src = L.w[1];  // written by this CTA's own rows (row partition of ce_stencil)
     }
     double nn = 0.0;
-    for (long p = threadIdx.x; p < np; p += blockDim.x) {
+    for (long p = tw; p < np; p += nwk) {
       const cplx y = ldm(src, own0 + p);
       wb[rs + p] = y;  // w[1] = r : the "previous" buffer of step 0
       nn += y.x * y.x + y.y * y.y;
@@ -501,9 +593,11 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
     cplx* Vj = Vb + (long)j * rs;
     {
       CEProfScope prof_(c, 5);
+      const bool big = (long)n1 * n23 > 8192;
+      CEProfScope prof_st_(c.prof, big ? 18 : 22);
       // V[j] = wp * sc (own rows); tile = D^-1 (.) (wp * sc) on rows [t0, t1)
       const long tn = (long)(t1 - t0) * n23;
-      for (long q = threadIdx.x; q < tn; q += blockDim.x) {
+      for (long q = tw; q < tn; q += nwk) {
         const int row = t0 + (int)(q / n23);
         const long col = q - (long)(row - t0) * n23;
         cplx v;
@@ -518,19 +612,23 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
         tile[q] = cmul_np(ldk(L.dinv, (long)row * n23 + col), v);
       }
       __syncthreads();
+      prof_st_.stop();
+      CEProfScope prof_rows_(c.prof, big ? 20 : 24);
       double red[2] = {0.0, 0.0};
       const cplx* V0 = Vb;
       if (L.A.coef32) {
         if (L.A.nofs == 21)
-          sm_stencil_rows<21, true>(c, L.A, tile, r0, r1, t0, w, V0, red);
+          sm_stencil_rows<21, true>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk);
+        else if (L.A.nofs == 9)
+          sm_stencil_rows<9, true>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk);
         else
-          sm_stencil_rows<0, true>(c, L.A, tile, r0, r1, t0, w, V0, red);
+          sm_stencil_rows<0, true>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk);
       } else {
         switch (L.A.nofs) {
-          case 5: sm_stencil_rows<5, false>(c, L.A, tile, r0, r1, t0, w, V0, red); break;
-          case 9: sm_stencil_rows<9, false>(c, L.A, tile, r0, r1, t0, w, V0, red); break;
-          case 21: sm_stencil_rows<21, false>(c, L.A, tile, r0, r1, t0, w, V0, red); break;
-          default: sm_stencil_rows<0, false>(c, L.A, tile, r0, r1, t0, w, V0, red); break;
+          case 5: sm_stencil_rows<5, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk); break;
+          case 9: sm_stencil_rows<9, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk); break;
+          case 21: sm_stencil_rows<21, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk); break;
+          default: sm_stencil_rows<0, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk); break;
         }
       }
       double v[2] = {red[0], red[1]};
@@ -543,7 +641,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       const cplx* Vi = Vb + (long)i * rs;
       const cplx* Vi1 = Vb + (long)(i + 1) * rs;
       double v[2] = {0.0, 0.0};
-      for (long p = threadIdx.x; p < np; p += blockDim.x) {
+      for (long p = tw; p < np; p += nwk) {
         const cplx y = csub(w[p], cmul_np(h, Vi[p]));
         w[p] = y;
         const cplx uu = Vi1[p];
@@ -557,15 +655,15 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
     {
       const cplx h = hcol;  // H[j][j]
       double v[1] = {0.0};
-      for (long p = threadIdx.x; p < np; p += blockDim.x) {
+      for (long p = tw; p < np; p += nwk) {
         const cplx y = csub(w[p], cmul_np(h, Vj[p]));
         w[p] = y;
         v[0] += y.x * y.x + y.y * y.y;
       }
       ce_allreduce<1>(c, v);
-      {
-        CEProfScope prof_(c, 3);
-        if (ctl) relax_step_sm(R, j, v[0]);  // Givens, least squares (thread 0)
+      if (ctl) {  // Givens, least squares (the control thread)
+        CEProfScope prof_(c.prof_ctl, 3);
+        relax_step_sm(R, j, v[0]);
       }
       const double hn = sqrt(v[0]);
       const bool stop = (hn <= kBreakdownEps * beta) || (j + 1 >= s);  // helmadr/krylov.py:113-114
@@ -578,7 +676,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
   const int k = R->k;
   {
     CEProfScope prof_lc_(c, 14);
-    for (long p = threadIdx.x; p < np; p += blockDim.x) {
+    for (long p = tw; p < np; p += nwk) {
       cplx t = mk(0.0, 0.0);
       for (int i = 0; i < k; ++i) t = cadd(t, cmul_np(Vb[(long)i * rs + p], R->y[i]));
       t = cmul_np(ldk(L.dinv, own0 + p), t);
@@ -703,7 +801,7 @@ __device__ __noinline__ void ce_arnoldi(CEC& c, FgCtl2* f, const CELevel& L, int
       f->wn = sqrt(v[0]);
       f->reo = (f->wn < kReorthRatio * f->w0) ? 1 : 0;  // helmadr/krylov.py:178-179
       if (!f->reo) {
-        CEProfScope prof_(c, 3);
+        CEProfScope prof_(c, 28);
         fg_post_sm(f, j);
       }
     }
@@ -828,7 +926,7 @@ __device__ void ce_kcycle(CEC& c, int l, const cplx* b, cplx* xo) {
     ce_restrict(c, L.A.n1, L.A.n2, L.A.n3, L.r, C.fb);
     CE_SYNC(c);
     if (l + 1 == S->nlev - 1)
-      ce_relax_any(c, C, C.fb, nullptr, C.fx, S->coarse_steps);
+      ce_relax_any(c, C, C.fb, nullptr, C.fx, C.s);  // the level's min(coarse_steps, N)
     else
       ce_inner<D + 1>(c, l + 1);
     ce_prolong_add(c, L.A.n1, L.A.n2, L.A.n3, C.fx, xo);
@@ -864,6 +962,7 @@ __global__ void __launch_bounds__(CE_THREADS, 1)
   c.ph = 0;
   c.S = &S;
   c.prof = (prof && blockIdx.x == 0 && threadIdx.x == 0) ? g_ce_prof : nullptr;
+  c.prof_ctl = (prof && blockIdx.x == 0 && threadIdx.x == blockDim.x - 1) ? g_ce_prof : nullptr;
   const long long t_start = clock64();
   if (mode == 0) {
     ce_kcycle<0>(c, l0, b, xo);
@@ -871,7 +970,7 @@ __global__ void __launch_bounds__(CE_THREADS, 1)
     ce_inner<0>(c, l0);
   } else {
     const CELevel& C = S.lv[l0];
-    ce_relax_any(c, C, C.fb, nullptr, C.fx, S.coarse_steps);
+    ce_relax_any(c, C, C.fb, nullptr, C.fx, C.s);
   }
   ce_sync();  // no CTA exits while another may still read its shared memory
   if (c.prof) {
@@ -881,10 +980,10 @@ __global__ void __launch_bounds__(CE_THREADS, 1)
 }
 
 int ce_profile_read(unsigned long long* out, int reset) {
-  cudaError_t e = cudaMemcpyFromSymbol(out, g_ce_prof, sizeof(unsigned long long) * 16);
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_ce_prof, sizeof(unsigned long long) * CE_NPROF);
   if (e != cudaSuccess) return (int)e;
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[CE_NPROF] = {0};
     e = cudaMemcpyToSymbol(g_ce_prof, z, sizeof(z));
   }
   return (int)e;

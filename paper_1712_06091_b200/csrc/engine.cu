@@ -313,6 +313,16 @@ StencilDev Op::dev() const {
     s.d2[o] = d2[o];
     s.d3[o] = d3[o];
   }
+  s.std2d = 0;
+  if (n3 == 1 && (nofs == 21 || nofs == 9 || nofs == 5)) {
+    bool same = true;
+    for (int o = 0; o < nofs; ++o) {
+      const int a = nofs == 21 ? Std2D::d1<21>(o) : nofs == 9 ? Std2D::d1<9>(o) : Std2D::d1<5>(o);
+      const int b = nofs == 21 ? Std2D::d2<21>(o) : nofs == 9 ? Std2D::d2<9>(o) : Std2D::d2<5>(o);
+      same = same && d1[o] == a && d2[o] == b && d3[o] == 0;
+    }
+    if (same) s.std2d = nofs;
+  }
   s.coef = coef;
   s.coef32 = coef32;
   s.pcode = pcode;
@@ -946,7 +956,7 @@ void Hier::alloc_workspace() {
   if (nl <= CE_MAXLEV) {
     CEDesc h{};
     h.nlev = nl;
-    h.coarse_steps = coarse_steps;
+    h.coarse_steps = lv[nl - 1].s;  // min(coarse_steps, N) as the graph path (helmadr/krylov.py steps = min(steps, n))
     h.coarse_tol = coarse_tol;
     for (int i = 0; i < nl; ++i) {
       const Level& L = lv[i];
@@ -1479,14 +1489,15 @@ struct OuterWS {
   int m = 0;
   long h = 0;
   std::vector<cplx*> V, Z;
-  cplx *w = nullptr, *r = nullptr;
+  cplx *w = nullptr, *r = nullptr, *t = nullptr;  // t: V[:k]^T y of the non-flexible update
+  double* gram = nullptr;                          // <v_i, v_j> pairs (collect_diagnostics)
   FgCtl* f = nullptr;
   FgCtl* hf = nullptr;  // pinned
   double* inv = nullptr;  // device scalar(s)
   ~OuterWS() {
     for (auto p : V) dfree(p);
     for (auto p : Z) dfree(p);
-    dfree(w), dfree(r), dfree(f), dfree(inv);
+    dfree(w), dfree(r), dfree(t), dfree(gram), dfree(f), dfree(inv);
     if (hf) cudaFreeHost(hf);
   }
 };
@@ -1510,6 +1521,8 @@ static OuterWS* outer_ws(long N, int m, long h) {
   for (int j = 0; j < m; ++j) ws->Z.push_back(halo_vec(N, h));
   ws->w = halo_vec(N, h);
   ws->r = halo_vec(N, h);
+  ws->t = halo_vec(N, h);
+  ws->gram = dalloc<double>(2 * MMAX * MMAX);
   ws->f = dalloc<FgCtl>(1);
   HADR_CUDA(cudaMemset(ws->f, 0, sizeof(FgCtl)));
   HADR_CUDA(cudaMallocHost(&ws->hf, sizeof(FgCtl)));
@@ -1518,7 +1531,7 @@ static OuterWS* outer_ws(long N, int m, long h) {
 }
 
 void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart, int maxiter, double tol,
-            Report& rep) {
+            Report& rep, int flags) {
   if (restart < 1) throw ValueError("restart must be >= 1");
   if (tol <= 0) throw ValueError("tol must be positive");
   if (restart > MMAX) throw ValueError("restart exceeds the device limit (16)");
@@ -1681,6 +1694,18 @@ void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart,
       rep.history.push_back(habs(g[j + 1]));
       if (lucky || rep.history.back() <= target) break;
     }
+    if ((flags & FG_DIAGNOSTICS) && k > 0) {  // G = V[:k] V[:k]^H off the diagonal (helmadr/krylov.py:214-217)
+      int np_ = 0;
+      for (int i = 0; i < k; ++i)
+        for (int jj = i + 1; jj < k; ++jj, ++np_)
+          launch_dot(lcd, N, ws->V[i], ws->V[jj], gate_always(), c.rs, epi_store(ws->gram + 2 * np_));
+      if (np_) {
+        std::vector<double> gh(2 * np_);
+        HADR_CUDA(cudaMemcpyAsync(gh.data(), ws->gram, gh.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        for (int q = 0; q < np_; ++q) rep.ortho_max = std::max(rep.ortho_max, std::hypot(gh[2 * q], gh[2 * q + 1]));
+      }
+    }
     if (k > 0) {
       std::vector<cplx> y(g.begin(), g.begin() + k);
       if (k == 1) {
@@ -1691,15 +1716,30 @@ void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart,
           for (int i = 0; i < jj; ++i) y[i] = hsub(y[i], hmul(y[jj], Hm(i, jj)));
         }
       }
+      const bool flexible = !(flags & FG_NONFLEXIBLE) || !M;
       LinComb lcb{};
       for (int i = 0; i < k; ++i) {
-        lcb.v[i] = M ? ws->Z[i] : ws->V[i];
+        lcb.v[i] = flexible && M ? ws->Z[i] : ws->V[i];
         lcb.yv[i] = y[i];
       }
       lcb.kfix = k;
-      lcb.base = x;
-      lcb.out = x;
-      launch_lincomb(lcd, N, lcb, gate_always());
+      if (flexible) {  // x + Z[:k]^T y
+        lcb.base = x;
+        lcb.out = x;
+        launch_lincomb(lcd, N, lcb, gate_always());
+      } else {  // x + M(V[:k]^T y)   (helmadr/krylov.py:222-223)
+        lcb.base = nullptr;
+        lcb.out = ws->t;
+        launch_lincomb(lcd, N, lcb, gate_always());
+        M->apply(ws->t, ws->w);
+        LinComb add{};
+        add.v[0] = ws->w;
+        add.yv[0] = mk(1.0, 0.0);
+        add.kfix = 1;
+        add.base = x;
+        add.out = x;
+        launch_lincomb(lcd, N, add, gate_always());
+      }
     }
     rnorm = resid_norm(x, ws->r);
     if (broke) break;

@@ -202,12 +202,17 @@ struct Report {
   int note = 0;
   double bnorm = 0, final_relres = 0, wall_time = 0;
   double device_time = 0;  // CUDA events on the library stream around the solve
+  double ortho_max = 0;    // max |<v_i, v_j>|, i != j, over the restart cycles (collect_diagnostics)
   std::vector<double> history;
 };
 
+enum : int { FG_NONFLEXIBLE = 1, FG_DIAGNOSTICS = 2 };
+
 // x = fgmres(A, b, x0, M) on device pointers (x0 may be null)
+// flags: FG_NONFLEXIBLE (x += M(V[:k]^T y), helmadr/krylov.py:222-223), FG_DIAGNOSTICS (ortho_max,
+// helmadr/krylov.py:214-217)
 void fgmres(Op& A, Hier* M, const cplx* b, const cplx* x0, cplx* x, int restart, int maxiter, double tol,
-            Report& rep);
+            Report& rep, int flags = 0);
 // Jacobi-GMRES relaxation of arbitrary length on one operator (public gmres_relax)
 void gmres_relax(Op& A, const cplx* b, const cplx* x, cplx* xo, int steps);
 

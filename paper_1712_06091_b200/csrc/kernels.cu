@@ -1603,6 +1603,113 @@ void launch_phase(cudaStream_t s, long n, const cplx* q, const double* tau, doub
   k_phase<<<blocks, 256, 0, s>>>(n, q, tau, omega, sign, out);
 }
 
+// ---------------------------------------------------------------------------
+// tau_derivatives (helmadr/eikonal.py:180-226) with the distance factor of
+// AnalyticBase (helmadr/eikonal.py:15-36): tau = tau0*tau1, grad(tau), lap(tau) from
+// tau1 by the chain rule, every expression in the reference's (numpy) order, so the
+// fields are bit-identical to the reference's on the same tau1 (tests).
+// ---------------------------------------------------------------------------
+// np.hypot on this image = glibc 2.39 __hypot (sysdeps/ieee754/dbl-64/e_hypot.c, the
+// non-FMA kernel of Borges' correction); grid offsets never reach its huge/tiny
+// scaling branches (|e| is 0 or >= one grid step).
+__device__ __forceinline__ double glibc_hypot(double x, double y) {
+  x = fabs(x);
+  y = fabs(y);
+  const double ax = x < y ? y : x, ay = x < y ? x : y;
+  if (ay <= ax * 0x1p-54) return ax + ay;
+  double h = sqrt(ax * ax + ay * ay), t1, t2;
+  if (h <= 2.0 * ay) {
+    const double d = h - ay;
+    t1 = ax * (2.0 * d - ax);
+    t2 = (d - 2.0 * (ax - ay)) * d;
+  } else {
+    const double d = h - ax;
+    t1 = 2.0 * d * (ax - 2.0 * ay);
+    t2 = (4.0 * d - ay) * ay + d * d;
+  }
+  return h - (t1 + t2) / (2.0 * h);
+}
+
+struct TauGeom {
+  int dim;
+  int n[3];
+  double h[3], L[3];
+  int src[3];
+};
+
+// first difference along one axis: central inside, one-sided first order at the ends
+// (helmadr/eikonal.py:180-188); t(d) = tau1 at offset d along the axis
+__device__ __forceinline__ double tau_d1(const double* t, long k, long st, int i, int n, double h) {
+  if (i == 0) return (t[k + st] - t[k]) / h;
+  if (i == n - 1) return (t[k] - t[k - st]) / h;
+  return (t[k + st] - t[k - st]) / (2.0 * h);
+}
+// second difference: 3-point inside, one-sided 4-point at the ends (helmadr/eikonal.py:191-201)
+__device__ __forceinline__ double tau_d2(const double* t, long k, long st, int i, int n, double h) {
+  const double hh = h * h;
+  if (i == 0) return (2.0 * t[k] - 5.0 * t[k + st] + 4.0 * t[k + 2 * st] - t[k + 3 * st]) / hh;
+  if (i == n - 1) return (2.0 * t[k] - 5.0 * t[k - st] + 4.0 * t[k - 2 * st] - t[k - 3 * st]) / hh;
+  return (t[k + st] - 2.0 * t[k] + t[k - st]) / hh;
+}
+
+__global__ void __launch_bounds__(256) k_tau_derivs(TauGeom g, const double* __restrict__ tau1,
+                                                      double* __restrict__ tau, double* __restrict__ gr0,
+                                                      double* __restrict__ gr1, double* __restrict__ gr2,
+                                                      double* __restrict__ lap) {
+  const int n1 = g.n[0], n2 = g.n[1], n3 = g.dim == 3 ? g.n[2] : 1;
+  const long n = (long)n1 * n2 * n3;
+  const long st[3] = {(long)n2 * n3, (long)n3, 1};
+  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    const int i[3] = {(int)(k / st[0]), (int)((k / n3) % n2), (int)(k % n3)};
+    double e[3], a[3];
+    // x = np.linspace(0, L, n): i * step, the last node exactly L; source position i_s * h
+    for (int ax = 0; ax < g.dim; ++ax) {
+      const double x = i[ax] == g.n[ax] - 1 ? g.L[ax] : (double)i[ax] * g.h[ax];
+      e[ax] = x - (double)g.src[ax] * g.h[ax];
+      a[ax] = tau_d1(tau1, k, st[ax], i[ax], g.n[ax], g.h[ax]);
+    }
+    const double t1 = tau1[k];
+    const bool at_src = i[0] == g.src[0] && i[1] == g.src[1] && (g.dim == 2 || i[2] == g.src[2]);
+    double r, l0;
+    if (g.dim == 2) {
+      r = glibc_hypot(e[0], e[1]);  // AnalyticBase: tau0 = hypot, lap(tau0) = 1/r
+      l0 = r > 0 ? 1.0 / r : 0.0;
+    } else {  // per-axis generalisation: lap(tau0) = (d - 1)/r = 2/r
+      r = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+      l0 = r > 0 ? 2.0 / r : 0.0;
+    }
+    double lap1 = tau_d2(tau1, k, st[0], i[0], n1, g.h[0]) + tau_d2(tau1, k, st[1], i[1], n2, g.h[1]);
+    if (g.dim == 3) lap1 = lap1 + tau_d2(tau1, k, st[2], i[2], n3, g.h[2]);
+    double s = (r > 0 ? e[0] / r : 0.0) * a[0] + (r > 0 ? e[1] / r : 0.0) * a[1];
+    if (g.dim == 3) s = s + (r > 0 ? e[2] / r : 0.0) * a[2];
+    double* gr[3] = {gr0, gr1, gr2};
+    for (int ax = 0; ax < g.dim; ++ax) {
+      const double gax = r > 0 ? e[ax] / r : 0.0;
+      gr[ax][k] = at_src ? 0.0 : r * a[ax] + t1 * gax;
+    }
+    lap[k] = at_src ? 2.0 * t1 : t1 * l0 + 2.0 * s + r * lap1;
+    if (tau) tau[k] = r * t1;
+  }
+}
+
+void launch_tau_derivs(cudaStream_t s, int dim, const int* n, const double* h, const double* L, const int* src,
+                       const double* tau1, double* tau, double* const* grads, double* lap) {
+  TauGeom g{};
+  g.dim = dim;
+  for (int a = 0; a < 3; ++a) {
+    g.n[a] = a < dim ? n[a] : 1;
+    g.h[a] = a < dim ? h[a] : 1.0;
+    g.L[a] = a < dim ? L[a] : 0.0;
+    g.src[a] = a < dim ? src[a] : 0;
+  }
+  const long N = (long)g.n[0] * g.n[1] * g.n[2];
+  ++g_launch_count;
+  int blocks = (int)((N + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) return;
+  k_tau_derivs<<<blocks, 256, 0, s>>>(g, tau1, tau, grads[0], grads[1], dim == 3 ? grads[2] : nullptr, lap);
+}
+
 struct PairTab {
   int pos_a[HADR_MAX_OFS], pos_b[HADR_MAX_OFS], bit[HADR_MAX_OFS];
   int nslot;

@@ -18,10 +18,32 @@ extern long g_cl_max_n;  // single-cluster reductions (in-kernel epilogue) up to
 // n1 global planes; every pointer handed to a kernel points at the first OWNED
 // point, halo planes sit at negative / past-the-end offsets, and coefficient
 // planes are `pstride` apart.  Single GPU: p0 = 0, n1own = n1, pstride = N.
+// Standard 2D offset sets in ascending (d1, d2) order, known at compile time to the
+// cluster engine's fast stencil loops (StencilDev::std2d names the set an operator has).
+// 21: the 5x5 box minus its corners (coarse Galerkin operators of upwind fine operators);
+// 9: the plus of radius 2 (fine upwind/blend operators); 5: the plus of radius 1.
+struct Std2D {
+  template <int NO>
+  __host__ __device__ static constexpr int d1(int o) {
+    constexpr int a21[21] = {-2, -2, -2, -1, -1, -1, -1, -1, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2};
+    constexpr int a9[9] = {-2, -1, 0, 0, 0, 0, 0, 1, 2};
+    constexpr int a5[5] = {-1, 0, 0, 0, 1};
+    return NO == 21 ? a21[o] : NO == 9 ? a9[o] : a5[o];
+  }
+  template <int NO>
+  __host__ __device__ static constexpr int d2(int o) {
+    constexpr int a21[21] = {-1, 0, 1, -2, -1, 0, 1, 2, -2, -1, 0, 1, 2, -2, -1, 0, 1, 2, -1, 0, 1};
+    constexpr int a9[9] = {0, 0, -2, -1, 0, 1, 2, 0, 0};
+    constexpr int a5[5] = {0, -1, 0, 1, 0};
+    return NO == 21 ? a21[o] : NO == 9 ? a9[o] : a5[o];
+  }
+};
+
 struct StencilDev {
   int n1, n2, n3;
   int nofs;
   int p0, n1own;
+  int std2d;  // 2D operator whose offsets are exactly the Std2D set of this size (21 / 9 / 5), else 0
   long pstride;
   int8_t d1[HADR_MAX_OFS];
   int8_t d2[HADR_MAX_OFS];
@@ -206,6 +228,9 @@ void launch_class_classify(cudaStream_t s, const StencilDev& A, int ncls, const 
 void launch_class_fill(cudaStream_t s, const StencilDev& A, const uint16_t* ccode, const int* cnsl_dev,
                        const int* otab_dev, int nsl, cplx* ccoef, long cstr);
 void launch_phase(cudaStream_t s, long n, const cplx* q, const double* tau, double omega, int sign, cplx* out);
+// tau = tau0 tau1, grad(tau) (dim planes), lap(tau) from tau1 (helmadr/eikonal.py:15-36, 180-226); tau may be null
+void launch_tau_derivs(cudaStream_t s, int dim, const int* n, const double* h, const double* L, const int* src,
+                       const double* tau1, double* tau, double* const* grads, double* lap);
 void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, int n3c, unsigned long long* mask,
                      const int* slot_of, cplx* coef_c, int q0 = 0, int nq = -1, long cstride = -1);
 

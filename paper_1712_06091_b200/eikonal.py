@@ -64,21 +64,40 @@ def fast_march(medium, grid, source, order="second") -> np.ndarray:
     return tau1
 
 
+def _tau_fields_device(grid, src_index, tau1):
+    """(tau, [grad per axis], lap) of tau = tau0*tau1 formed on the device (hadr_tau_derivatives)."""
+    sh = tuple(int(v) for v in grid.shape)
+    dim = len(sh)
+    Ls = tuple(float(v) for v in getattr(grid, "Ls", (grid.L1, grid.L2)))
+    t1 = np.ascontiguousarray(np.asarray(tau1, dtype=np.float64))
+    if t1.shape != sh:
+        raise ValueError(f"tau1 has shape {t1.shape}, grid is {sh}")
+    n = np.asarray(sh, dtype=np.int32)
+    L = np.asarray(Ls, dtype=np.float64)
+    s = np.asarray(tuple(src_index), dtype=np.int32)
+    tau = np.empty(sh)
+    grads = np.empty((dim,) + sh)
+    lap = np.empty(sh)
+    _lib.check(_lib.lib().hadr_tau_derivatives(dim, _lib.cbuf(n), _lib.cbuf(L), _lib.cbuf(s), _lib.cbuf(t1),
+                                               _lib.cbuf(tau), _lib.cbuf(grads), _lib.cbuf(lap), 0))
+    return tau, [grads[a] for a in range(dim)], lap
+
+
 def tau_derivatives(tau1: np.ndarray, base, grid):
-    """helmadr/eikonal.py:204-226 (2D): ((grad1, grad2), lap) of tau = tau0 * tau1."""
-    from .workloads import travel_time_from_tau1
+    """helmadr/eikonal.py:180-226 on the device: ((grad1, grad2[, grad3]), lap) of
+    tau = tau0 * tau1 (bit-identical to the reference's numpy arithmetic)."""
+    _, grads, lap = _tau_fields_device(grid, base.source.index if hasattr(base.source, "index")
+                                       else (base.source.i1, base.source.i2), tau1)
+    return tuple(grads), lap
 
-    tt = travel_time_from_tau1(grid, base.source, tau1)
-    return (tt.grad1, tt.grad2), tt.lap
 
-
-def compute_travel_time(medium, grid, source, order="second") -> TravelTime:
-    """helmadr/eikonal.py:229-239: fast_march + tau_derivatives, with fm_time."""
-    from .workloads import travel_time_from_tau1, travel_time_nd
+def compute_travel_time(medium, grid, source, order="second"):
+    """helmadr/eikonal.py:229-239: fast_march (host, timed as fm_time), then the
+    derivative fields of tau_derivatives — formed on the device where the solve needs
+    them (``DeviceTravelTime``), so only tau1 is copied to the GPU."""
+    from .fields import DeviceTravelTime
 
     t0 = time.perf_counter()
     tau1 = fast_march(medium, grid, source, order)
     fm_time = time.perf_counter() - t0
-    tt = travel_time_from_tau1(grid, source, tau1) if grid.dim == 2 else travel_time_nd(grid, source, tau1)
-    tt.fm_time = fm_time
-    return tt
+    return DeviceTravelTime(grid, source, tau1, fm_time)

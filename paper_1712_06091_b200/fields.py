@@ -238,6 +238,74 @@ class TravelTime:
         return s
 
 
+class _SourceOnly:
+    """``base`` of a DeviceTravelTime: the source (the distance factor lives on the device)."""
+
+    def __init__(self, source):
+        self.source = source
+
+
+class DeviceTravelTime:
+    """A TravelTime given by tau1 alone: tau = tau0*tau1, grad(tau) and lap(tau) are formed
+    on the device (``hadr_tau_derivatives``, helmadr/eikonal.py:180-226) — inside the solve
+    by the drivers, so only tau1 crosses the host link (8 B/dof instead of the 32-40 B/dof
+    of tau, the gradients and the Laplacian).  Reading ``tau`` / ``grad1`` / ``lap`` / ...
+    on the host forms them on the device once and copies them back (same values)."""
+
+    def __init__(self, grid, source, tau1, fm_time: float = 0.0):
+        source.validate(grid)
+        tau1 = np.asarray(tau1)
+        if tau1.shape != tuple(grid.shape):
+            raise ValueError(f"tau1 has shape {tau1.shape}, grid is {tuple(grid.shape)}")
+        self.grid = grid
+        self.source = source
+        self.tau1 = tau1
+        self.base = _SourceOnly(source)
+        self.fm_time = fm_time
+        self._host = None
+
+    device_derivatives = True
+
+    def _fields(self):
+        if self._host is None:
+            from .eikonal import _tau_fields_device
+
+            self._host = _tau_fields_device(self.grid, self.source.index, self.tau1)
+        return self._host
+
+    @property
+    def tau(self):
+        return self._fields()[0]
+
+    @property
+    def grads(self):
+        return list(self._fields()[1])
+
+    @property
+    def grad1(self):
+        return self._fields()[1][0]
+
+    @property
+    def grad2(self):
+        return self._fields()[1][1]
+
+    @property
+    def grad3(self):
+        g = self._fields()[1]
+        return g[2] if len(g) > 2 else None
+
+    @property
+    def lap(self):
+        return self._fields()[2]
+
+    @property
+    def grad_sq(self) -> np.ndarray:
+        s = self.grad1**2 + self.grad2**2
+        if self.grad3 is not None:
+            s = s + self.grad3**2
+        return s
+
+
 def point_source(grid, source) -> np.ndarray:
     """1/(h1 h2 [h3]) at the source node (helmadr/grid.py:128-136)."""
     source.validate(grid)

@@ -13,7 +13,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import HadrReport, as_c128, cbuf, check
-from .stencil import StencilOperator, as_operator
+from .stencil import StencilOperator, as_operator  # noqa: F401
 
 
 @dataclass
@@ -59,33 +59,48 @@ class SolveReport:
 _NOTES = {0: "", 1: "numerical breakdown: non-finite Arnoldi vector"}
 
 
-def _grid_of(A, b=None):
-    if isinstance(A, StencilOperator):
-        return A.grid_shape
-    raise TypeError("a scipy matrix has no grid; wrap it with StencilOperator.from_csr(A, (n1, n2))")
+def grid_of(A, grid=None):
+    """The structured grid a device stencil needs for ``A``: the operator's own grid, an
+    explicit ``grid`` (shape tuple or object with ``.shape``), or — for a plain scipy
+    matrix, the reference's documented argument type — the square (n = m^2) or cubic
+    (n = m^3) grid its size implies.  Anything else must name its grid."""
+    if grid is not None:
+        return tuple(grid.shape) if hasattr(grid, "shape") and not isinstance(grid, tuple) else tuple(grid)
+    g = getattr(A, "grid_shape", None)
+    if g is not None:
+        return tuple(g)
+    n = int(A.shape[0])
+    m = int(round(n ** 0.5))
+    if m * m == n:
+        return (m, m)
+    m = int(round(n ** (1.0 / 3.0)))
+    if m * m * m == n:
+        return (m, m, m)
+    raise ValueError(f"cannot infer the grid of a {A.shape} operator (not m^2 or m^3 points): pass grid=(n1, n2[, n3])"
+                     " or wrap it with StencilOperator.from_csr(A, grid)")
 
 
-def spmv(A, x) -> np.ndarray:
+def spmv(A, x, grid=None) -> np.ndarray:
     """y = A x with an explicit dimension check (helmadr/krylov.py:60-65)."""
     x = np.asarray(x)
     if A.shape[1] != x.shape[0]:
         raise ValueError(f"dimension mismatch: operator {A.shape}, vector {x.shape}")
-    op = as_operator(A, getattr(A, "grid_shape", None))
+    op = as_operator(A, grid_of(A, grid))
     return op.matvec(x)
 
 
-def jacobi_apply(A, r) -> np.ndarray:
+def jacobi_apply(A, r, grid=None) -> np.ndarray:
     """z_j = r_j / A_jj (helmadr/krylov.py:68-73)."""
-    op = as_operator(A, getattr(A, "grid_shape", None))
+    op = as_operator(A, grid_of(A, grid))
     r = as_c128(r, op.shape[0])
     z = np.empty_like(r)
     check(_lib.lib().hadr_op_jacobi(op.handle, cbuf(r), cbuf(z), 0))
     return z
 
 
-def gmres_relax(A, b, x, steps: int) -> np.ndarray:
+def gmres_relax(A, b, x, steps: int, grid=None) -> np.ndarray:
     """Fixed-length Jacobi-preconditioned GMRES from x (helmadr/krylov.py:82-119)."""
-    op = as_operator(A, getattr(A, "grid_shape", None))
+    op = as_operator(A, grid_of(A, grid))
     n = op.shape[0]
     b = as_c128(b, n)
     x = as_c128(x, n)
@@ -104,6 +119,7 @@ def _report_from(rep: HadrReport, hist: np.ndarray) -> SolveReport:
         final_relres=float(rep.final_relres),
         note=_NOTES.get(int(rep.note), "breakdown"),
         device_time=float(rep.device_time),
+        ortho_max=float(rep.ortho_max),
     )
 
 
@@ -117,12 +133,10 @@ def fgmres(A, b, x0=None, precond=None, cfg: KrylovConfig | None = None):
     from .multigrid import KCyclePreconditioner  # local: multigrid imports krylov
 
     cfg = cfg or KrylovConfig()
-    if not cfg.flexible:
-        raise ValueError("the K-cycle is a varying preconditioner: only flexible GMRES is supported")
     grid = getattr(A, "grid_shape", None)
     if grid is None and isinstance(precond, KCyclePreconditioner):
         grid = precond.hier.shapes[0]  # a scipy A on the hierarchy's finest grid
-    op = as_operator(A, grid)
+    op = as_operator(A, grid_of(A, grid))
     n = op.shape[0]
     b = as_c128(b, n)
     x0a = None if x0 is None else as_c128(x0, n)
@@ -134,13 +148,19 @@ def fgmres(A, b, x0=None, precond=None, cfg: KrylovConfig | None = None):
         raise TypeError("precond must be None or make_kcycle_preconditioner(hier) (device K-cycle)")
     x = np.empty_like(b)
     rep = HadrReport()
-    cap = cfg.maxiter + 2
+    cap = max(int(cfg.maxiter), 0) + 2
     hist = np.zeros(cap)
     check(
-        _lib.lib().hadr_fgmres(op.handle, hh, cbuf(b), None if x0a is None else cbuf(x0a), int(cfg.restart),
-                               int(cfg.maxiter), float(cfg.tol), cbuf(x), C.byref(rep), cbuf(hist), cap, 0)
+        _lib.lib().hadr_fgmres_ex(op.handle, hh, cbuf(b), None if x0a is None else cbuf(x0a), int(cfg.restart),
+                                  int(cfg.maxiter), float(cfg.tol), _flags(cfg), cbuf(x), C.byref(rep), cbuf(hist),
+                                  cap, 0)
     )
     return x, _report_from(rep, hist)
+
+
+def _flags(cfg: KrylovConfig) -> int:
+    """KrylovConfig switches -> hadr_fgmres_ex flags (include/hadr.h)."""
+    return (0 if cfg.flexible else 1) | (2 if cfg.collect_diagnostics else 0)
 
 
 def fgmres_device(A, b_ptr: int, x_ptr: int, precond=None, cfg: KrylovConfig | None = None, x0_ptr: int | None = None):
@@ -150,12 +170,12 @@ def fgmres_device(A, b_ptr: int, x_ptr: int, precond=None, cfg: KrylovConfig | N
     op = as_operator(A, getattr(A, "grid_shape", None))
     hh = None if precond is None else precond.hier.handle
     rep = HadrReport()
-    cap = cfg.maxiter + 2
+    cap = max(int(cfg.maxiter), 0) + 2
     hist = np.zeros(cap)
     check(
-        _lib.lib().hadr_fgmres(op.handle, hh, C.c_void_p(b_ptr), None if x0_ptr is None else C.c_void_p(x0_ptr),
-                               int(cfg.restart), int(cfg.maxiter), float(cfg.tol), C.c_void_p(x_ptr), C.byref(rep),
-                               cbuf(hist), cap, 1)
+        _lib.lib().hadr_fgmres_ex(op.handle, hh, C.c_void_p(b_ptr), None if x0_ptr is None else C.c_void_p(x0_ptr),
+                                  int(cfg.restart), int(cfg.maxiter), float(cfg.tol), _flags(cfg), C.c_void_p(x_ptr),
+                                  C.byref(rep), cbuf(hist), cap, 1)
     )
     return _report_from(rep, hist)
 

@@ -51,9 +51,22 @@ def coarsenable_levels(shape, max_levels: int):
 
 
 class MGHierarchy:
-    """Per-level device operators + K-cycle workspace (helmadr/multigrid.py:58-95)."""
+    """Per-level device operators + K-cycle workspace (helmadr/multigrid.py:58-95).
 
-    def __init__(self, handle, keepalive=(), coarse_steps=COARSE_GMRES_STEPS, coarse_tol=COARSE_FGMRES_TOL):
+    Constructed either as the reference does, ``MGHierarchy(ops=[...], prols=[...],
+    shapes=[...], inv_diags=[], coarse_steps=10, coarse_tol=0.1)`` with per-level
+    operators (scipy matrices or StencilOperators, finest first; the device keeps its
+    own copies), or from a device hierarchy handle (``build_hierarchy``).
+    ``prols`` must be the bilinear/trilinear prolongations of ``build_prolongation``
+    (the device applies them matrix-free) and ``inv_diags``, when given, 1 / diag of
+    each level (the device recomputes them bit-exactly); anything else raises."""
+
+    def __init__(self, ops=None, prols=None, shapes=None, inv_diags=None, coarse_steps=COARSE_GMRES_STEPS,
+                 coarse_tol=COARSE_FGMRES_TOL, *, handle=None, keepalive=()):
+        if handle is None:
+            if ops is None:
+                raise TypeError("MGHierarchy needs ops (with prols and shapes) or a device handle")
+            handle, keepalive = _hier_handle_from_levels(ops, prols, shapes, inv_diags, coarse_steps, coarse_tol)
         self._h = handle
         self._keep = tuple(keepalive)
         self.coarse_steps = coarse_steps
@@ -101,6 +114,49 @@ class MGHierarchy:
         return "\n".join(lines)
 
 
+def _hier_handle_from_levels(ops, prols, shapes, inv_diags, coarse_steps, coarse_tol):
+    """Device hierarchy for the reference constructor MGHierarchy(ops, prols, shapes, ...)."""
+    ops = list(ops)
+    if shapes is None:
+        shapes = [getattr(A, "grid_shape", None) for A in ops]
+        if any(s_ is None for s_ in shapes):
+            raise ValueError("scipy level operators need `shapes`")
+    shapes = [tuple(int(v) for v in s_) for s_ in shapes]
+    if len(shapes) != len(ops):
+        raise ValueError(f"{len(ops)} operators but {len(shapes)} shapes")
+    for l, (A, s_) in enumerate(zip(ops, shapes)):
+        if A.shape[0] != int(np.prod(s_)):
+            raise ValueError(f"level {l + 1}: operator {A.shape} does not match grid {s_}")
+        if l + 1 < len(shapes) and tuple((n - 1) // 2 + 1 for n in s_) != shapes[l + 1]:
+            raise ValueError(f"level {l + 2}: grid {shapes[l + 1]} is not the coarsening of {s_}")
+    if prols is not None:
+        prols = list(prols)
+        if len(prols) != len(ops) - 1:
+            raise ValueError(f"{len(ops)} levels need {len(ops) - 1} prolongations, got {len(prols)}")
+        for l, P in enumerate(prols):
+            if tuple(P.shape) != (int(np.prod(shapes[l])), int(np.prod(shapes[l + 1]))):
+                raise ValueError(f"prolongation {l + 1} has shape {P.shape}")
+            if isinstance(P, Prolongation):
+                continue
+            ref = Prolongation(shapes[l]).tocsr()
+            Pc = P.tocsr() if hasattr(P, "tocsr") else None
+            if Pc is None or (Pc != ref).nnz:
+                raise ValueError(f"prolongation {l + 1} is not build_prolongation({shapes[l]}): the device applies "
+                                 "the bilinear/trilinear P matrix-free")
+    dev = [as_operator(A, shapes[i]) for i, A in enumerate(ops)]
+    if inv_diags:
+        for l, (A, d) in enumerate(zip(dev, inv_diags)):
+            dg = A.diagonal()
+            if np.any(dg == 0):
+                raise ValueError("hierarchy operator has zero diagonal entries")
+            if not np.array_equal(np.asarray(d), 1.0 / dg):
+                raise ValueError(f"inv_diags[{l}] is not 1 / diag(ops[{l}])")
+    arr = (C.c_void_p * len(dev))(*[d.handle.value for d in dev])
+    h = C.c_void_p()
+    check(_lib.lib().hadr_hier_from_ops(len(dev), arr, int(coarse_steps), float(coarse_tol), C.byref(h)))
+    return h, tuple(dev)
+
+
 def build_hierarchy(A0, grid, max_levels: int = 5, coarse_steps: int = COARSE_GMRES_STEPS,
                     coarse_tol: float = COARSE_FGMRES_TOL) -> MGHierarchy:
     """Chain of Galerkin operators on the device (helmadr/multigrid.py:113-129)."""
@@ -116,20 +172,14 @@ def build_hierarchy(A0, grid, max_levels: int = 5, coarse_steps: int = COARSE_GM
     h = C.c_void_p()
     check(_lib.lib().hadr_hier_create(fine.handle, int(max_levels), int(coarse_steps), float(coarse_tol),
                                       C.byref(h)))
-    return MGHierarchy(h, keepalive=(fine,), coarse_steps=coarse_steps, coarse_tol=coarse_tol)
+    return MGHierarchy(handle=h, keepalive=(fine,), coarse_steps=coarse_steps, coarse_tol=coarse_tol)
 
 
 def hierarchy_from_ops(ops, coarse_steps: int = COARSE_GMRES_STEPS, coarse_tol: float = COARSE_FGMRES_TOL,
                        shapes=None) -> MGHierarchy:
     """MGHierarchy(ops=...) from given per-level operators (finest first), e.g. the
     reference's own CSR hierarchy for bit-exact operator parity."""
-    if shapes is None and not all(isinstance(A, StencilOperator) for A in ops):
-        raise ValueError("scipy level operators need `shapes`")
-    dev = [as_operator(A, None if shapes is None else shapes[i]) for i, A in enumerate(ops)]
-    arr = (C.c_void_p * len(dev))(*[d.handle.value for d in dev])
-    h = C.c_void_p()
-    check(_lib.lib().hadr_hier_from_ops(len(dev), arr, int(coarse_steps), float(coarse_tol), C.byref(h)))
-    return MGHierarchy(h, keepalive=tuple(dev), coarse_steps=coarse_steps, coarse_tol=coarse_tol)
+    return MGHierarchy(ops=ops, prols=None, shapes=shapes, coarse_steps=coarse_steps, coarse_tol=coarse_tol)
 
 
 def k_cycle(hier: MGHierarchy, level: int, b, x, stats: dict | None = None) -> np.ndarray:

@@ -180,3 +180,18 @@ def rhs_transform(q: np.ndarray, tt, omega: float, direction: str) -> np.ndarray
 def max_nnz_per_row(A) -> int:
     csr = as_operator(A).tocsr()
     return int(np.diff(csr.indptr).max())
+
+
+def export_operator_coo(A, path: str) -> None:
+    """Debug dump: one 'row col re im' line per stored entry (helmadr/operators.py:281-286).
+
+    The device operator is exported to canonical CSR (rows ascending, columns ascending
+    within a row), the order the reference's ``A.tocoo()`` of a canonical CSR has.  A
+    structured stencil stores no explicit zeros, so an entry the reference kept as an
+    explicit 0 (e.g. cancelling duplicate COO terms) has no line here."""
+    if isinstance(A, StencilOperator):
+        A = A.tocsr()
+    coo = A.tocoo()
+    with open(path, "w", encoding="ascii") as fh:
+        for r, c, v in zip(coo.row, coo.col, coo.data):
+            fh.write(f"{r} {c} {v.real!r} {v.imag!r}\n")

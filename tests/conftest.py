@@ -47,9 +47,13 @@ def oracle_problem(wl):
     from oracle import hadr_oracle as O
 
     g = wl.grid
-    return O.Problem(g.n1, g.n2, g.h1, g.h2, wl.omega, (wl.source.i1, wl.source.i2),
-                     wl.medium.kappa_sq, wl.medium.gamma, wl.tt.tau, wl.tt.grad1,
-                     wl.tt.grad2, wl.tt.lap, wl.bc)
+    src = (wl.source.i1, wl.source.i2)
+    if getattr(wl.tt, "device_derivatives", False):  # tau1 only: the checker forms the fields itself
+        gr1, gr2, lap, tau = O.tau_fields(wl.tt.tau1, g.L1, g.L2, src)
+    else:
+        gr1, gr2, lap, tau = wl.tt.grad1, wl.tt.grad2, wl.tt.lap, wl.tt.tau
+    return O.Problem(g.n1, g.n2, g.h1, g.h2, wl.omega, src, wl.medium.kappa_sq, wl.medium.gamma, tau, gr1, gr2, lap,
+                     wl.bc)
 
 
 @pytest.fixture(scope="session")

@@ -18,6 +18,7 @@ import numpy as np
 import pytest
 
 from conftest import csr_from, oracle_problem
+from parity_util import protocol_bar, self_floor
 
 pytestmark = pytest.mark.gpu
 
@@ -335,27 +336,69 @@ def test_device_assembly_helmholtz_shift_similarity(hadr, g33):
     assert (abs(Ar.tocsr() - csr_from(g33, "Aresc"))).max() == 0
 
 
+def _oracle_strategies(wl, tol):
+    """The oracle's three strategies on a workload (the checker): name -> solve() -> result."""
+    from oracle import hadr_oracle as O
+
+    p = oracle_problem(wl)
+    H = O.helm_of(p)
+    q = O.delta_source(p.n1, p.n2, p.h1, p.h2, p.src)
+    return {
+        "upwind": lambda: O.solve_upwind(p, tol=tol, maxiter=1000)[1],
+        "standard": lambda: O.solve_sl(H, q, p, tol=tol, maxiter=1000)[0],
+        "central": lambda: O.solve_central(p, tol=tol, maxiter=1000)[0],
+    }
+
+
+def _gpu_strategy(hadr, wl, name, tol):
+    """The public drivers (device assembly, hierarchy and FGMRES) -> (result, report)."""
+    from paper_1712_06091_b200 import drivers, fields, operators
+
+    if name == "upwind":
+        cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=tol, max_iter=1000)
+        u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
+        assert np.allclose(np.abs(u), np.abs(a))
+        return a, rep
+    if name == "standard":
+        cfg = drivers.StrategyConfig(strategy="standard_sl", tol=tol, max_iter=1000)
+        H = operators.assemble_helmholtz(wl.medium, wl.grid, wl.omega, wl.bc)
+        return drivers.solve_standard(H, fields.point_source(wl.grid, wl.source), wl.medium, wl.omega, cfg)
+    cfg = drivers.StrategyConfig(strategy="adr_central_two_stage", tol=tol, max_iter=1000)
+    u, a, rep = drivers.solve_adr_central(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
+    return u, rep
+
+
 @pytest.mark.parametrize("case", ["g33", "g65", "gcfg1"])
-def test_drivers_end_to_end(hadr, case, request):
-    from paper_1712_06091_b200 import drivers, fields, operators, workloads
+@pytest.mark.parametrize("strategy", ["upwind", "standard", "central"])
+def test_drivers_end_to_end(hadr, case, strategy, request):
+    """The public drivers (device assembly -> hierarchy -> FGMRES) vs the reference's
+    own solves (golden vectors), at the parity protocol's bar: iterations within +-1,
+    relative L2 <= max(1e-8, 3x the oracle self-floor measured here on the same inputs)."""
+    from oracle import hadr_oracle as O
+    from paper_1712_06091_b200 import workloads
 
     g = request.getfixturevalue(case)
     wl = {"g33": lambda: workloads.cfg1(33), "g65": lambda: workloads.cfg2(65),
           "gcfg1": lambda: workloads.cfg1(129)}[case]()
-    cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=1e-6, max_iter=1000)
-    u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
-    assert rep.converged and abs(rep.iterations - int(g["upwind_iterations"])) <= 1
-    assert rel(a, g["upwind_a"]) <= 1e-6
-    assert np.allclose(np.abs(u), np.abs(a))
-    cfg = drivers.StrategyConfig(strategy="standard_sl", tol=1e-6, max_iter=1000)
-    H = operators.assemble_helmholtz(wl.medium, wl.grid, wl.omega, wl.bc)
-    u, rep = drivers.solve_standard(H, fields.point_source(wl.grid, wl.source), wl.medium, wl.omega, cfg)
-    assert rep.converged and abs(rep.iterations - int(g["standard_iterations"])) <= 1
-    assert rel(u, g["standard_u"]) <= 1e-6
-    cfg = drivers.StrategyConfig(strategy="adr_central_two_stage", tol=1e-6, max_iter=1000)
-    u, a, rep = drivers.solve_adr_central(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
-    assert rep.converged and abs(rep.iterations - int(g["central_iterations"])) <= 1
-    assert rel(u, g["central_u"]) <= 1e-6
+    key = {"upwind": "upwind_a", "standard": "standard_u", "central": "central_u"}[strategy]
+    floor, base = self_floor(O, _oracle_strategies(wl, 1e-6)[strategy])
+    assert np.array_equal(base.reshape(-1), g[key].reshape(-1))  # the checker is the reference here
+    x, rep = _gpu_strategy(hadr, wl, strategy, 1e-6)
+    assert rep.converged and abs(rep.iterations - int(g[strategy + "_iterations"])) <= 1
+    assert rel(x, g[key]) <= protocol_bar(floor), (rel(x, g[key]), floor)
+
+
+@pytest.mark.parametrize("strategy", ["upwind", "standard", "central"])
+def test_drivers_tight_tol_strict(hadr, strategy):
+    """Protocol step 3: at tol 1e-10 the public drivers (device-assembled operators) and
+    the oracle agree to <= 1e-8 strictly (config-2 recipe at 65^2)."""
+    from paper_1712_06091_b200 import workloads
+
+    wl = workloads.cfg2(65)
+    ref = _oracle_strategies(wl, 1e-10)[strategy]()
+    x, rep = _gpu_strategy(hadr, wl, strategy, 1e-10)
+    assert rep.converged
+    assert rel(x, ref) <= 1e-8
 
 
 def test_phase_transforms(hadr):
@@ -380,11 +423,15 @@ def test_drivers_cfg3(hadr, gcfg3):
     travel time) through the public driver."""
     from paper_1712_06091_b200 import drivers, workloads
 
+    from oracle import hadr_oracle as O
+
     wl = workloads.cfg3(65)
+    floor, base = self_floor(O, _oracle_strategies(wl, 1e-6)["upwind"])
+    assert np.array_equal(base, gcfg3["upwind_a"])
     cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=1e-6, max_iter=1000)
     u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
     assert rep.converged and abs(rep.iterations - int(gcfg3["upwind_iterations"])) <= 1
-    assert rel(a, gcfg3["upwind_a"]) <= 1e-6
+    assert rel(a, gcfg3["upwind_a"]) <= protocol_bar(floor), (rel(a, gcfg3["upwind_a"]), floor)
 
 
 @pytest.mark.parametrize("case", ["g65", "gcfg1"])
@@ -473,3 +520,23 @@ def test_full_size_cfg2_properties(hadr):
     assert np.all(np.diff(rep.history) <= 1e-12 * rep.history[0])
     # waveform = amplitude x exp(-i w tau) (helmadr/drivers.py:171-173), |u| = |a|
     np.testing.assert_allclose(np.abs(u), np.abs(a), rtol=1e-13, atol=1e-300)
+
+
+def test_full_size_cfg2_amplitude_vs_oracle(hadr):
+    """The headline workload itself (BASELINE configs[1], 1025^2, the amplitude bench.py
+    times) against the oracle's full solve on the same inputs (about a minute on the host):
+    iterations within +-1, amplitude within max(1e-8, 3x the oracle self-floor).  The floor
+    is measured on the 513^2 instance of the same recipe (six oracle solves at 1025^2 would
+    take ~6 min); it is the floor of the recipe's trajectory, not of the grid size.  Both
+    device execution paths at this size run: graph path on 1025^2/513^2/257^2, cluster
+    engine on 129^2/65^2 — the split bench.py times."""
+    from oracle import hadr_oracle as O
+    from paper_1712_06091_b200 import drivers, workloads
+
+    floor, _ = self_floor(O, _oracle_strategies(workloads.cfg2(513), 1e-6)["upwind"])
+    wl = workloads.cfg2(1025)
+    a_or = _oracle_strategies(wl, 1e-6)["upwind"]()
+    cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=1e-6, max_iter=1000)
+    u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
+    assert rep.converged and abs(rep.iterations - 62) <= 1
+    assert rel(a, a_or) <= protocol_bar(floor), (rel(a, a_or), floor)

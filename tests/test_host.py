@@ -90,3 +90,32 @@ def test_bench_cpu_baseline_helpers_import():
     assert bench.B_OP_2D_UPWIND_C128 == 7726.0
     hbm, src = bench.peaks()
     assert hbm > 1000
+
+
+def test_grid_inference_for_scipy_operators():
+    """spmv / jacobi_apply / gmres_relax accept plain scipy matrices (helmadr/krylov.py:60-88):
+    the grid is the operator's own, an explicit one, or the square / cubic grid its size implies."""
+    import scipy.sparse as sp
+
+    from paper_1712_06091_b200.krylov import grid_of
+
+    assert grid_of(sp.identity(33 * 33, format="csr")) == (33, 33)
+    assert grid_of(sp.identity(9 * 9 * 9, format="csr")) == (27, 27)  # m^2 wins over m^3 (729 = 27^2)
+    assert grid_of(sp.identity(5 * 5 * 5, format="csr")) == (5, 5, 5)
+    assert grid_of(sp.identity(65 * 33, format="csr"), (65, 33)) == (65, 33)
+
+    class G:
+        shape = (65, 33)
+
+    assert grid_of(sp.identity(65 * 33, format="csr"), G()) == (65, 33)
+    with pytest.raises(ValueError):
+        grid_of(sp.identity(65 * 33, format="csr"))
+
+
+def test_krylov_flags():
+    from paper_1712_06091_b200 import KrylovConfig
+    from paper_1712_06091_b200.krylov import _flags
+
+    assert _flags(KrylovConfig()) == 0
+    assert _flags(KrylovConfig(flexible=False)) == 1
+    assert _flags(KrylovConfig(collect_diagnostics=True)) == 2

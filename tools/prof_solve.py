@@ -67,7 +67,7 @@ def ce_breakdown(n=1025, its=1000):
 
     L = _lib.lib()
     _lib.set_option("ce_profile", 1)
-    out = (C.c_ulonglong * 16)()
+    out = (C.c_ulonglong * 32)()
     L.hadr_ce_profile(out, 1)
     sys.argv = [sys.argv[0], "--n", str(n), "--its", str(its), "--warm", "0"]
     main()
@@ -75,8 +75,10 @@ def ce_breakdown(n=1025, its=1000):
     v = list(out)
     f = 1.9e3  # cycles per us
     print(f"CE launches={v[7]} total={v[0]/f:.0f}us")
-    for name, i in (("allreduce", 1), ("epilogue", 3), ("stencil", 5), ("vector ops", 8), ("barriers", 10),
-                    ("transfers", 12), ("relax update", 14)):
+    for name, i in (("allreduce", 1), ("relax control", 3), ("stencil", 5), ("vector ops", 8), ("barriers", 10),
+                    ("transfers", 12), ("relax update", 14), ("stencil big", 16), ("smrelax stage big", 18),
+                    ("smrelax rows big", 20), ("smrelax stage sm", 22), ("smrelax rows sm", 24),
+                    ("allred barrier", 26), ("fg control", 28)):
         print(f"  {name:13s} {v[i]/f:9.0f} us  n={v[i+1]:7d}  {v[i]/max(v[i+1],1)/1.9:7.0f} ns/op")
 
 
