@@ -631,7 +631,7 @@ def engine_roofline(H, L, wl, cfg, its_mean, t_krylov):
     # latency budget: phase counters of CTA 0 over profiled launches (clock64, 1965 MHz)
     from paper_1712_06091_b200 import _lib
 
-    prof = (C.c_ulonglong * 32)()
+    prof = (C.c_ulonglong * 48)()
     _lib.set_option("ce_profile", 1)
     try:
         L.hadr_ce_profile(prof, 1)

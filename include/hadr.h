@@ -140,11 +140,12 @@ void hadr_hier_destroy(hadr_hier h);
  * (mixed precision: K-cycle operators c64, vectors / reductions / outer FGMRES c128) */
 int hadr_set_option(const char* name, double value);
 /* cluster-engine phase counters (enable with hadr_set_option("ce_profile", 1)): cycles seen by CTA 0,
- * 32 entries: [total, allreduce, n, relaxation control, n, stencil, n, launches, vector ops, n, barriers,
+ * 48 entries: [total, allreduce, n, relaxation control, n, stencil, n, launches, vector ops, n, barriers,
  * n, transfers, n, relaxation update, n, stencil on levels > 8192 points, n, shared-memory relaxation
  * staging (> 8192), n, its stencil rows (> 8192), n, staging (small levels), n, stencil rows (small), n,
- * all-reduce cluster-barrier wait, n, inner-FGMRES control, n, 0, 0] */
-int hadr_ce_profile(unsigned long long* out32, int reset);
+ * all-reduce cluster-barrier wait, n, inner-FGMRES control, n, CGS2 step, n, then the CGS2 phases: dots 1, n,
+ * all-reduce 1, n, update 1, n, dots 2, n, all-reduce 2, n, update 2, n, final barrier, n, 0, 0] */
+int hadr_ce_profile(unsigned long long* out48, int reset);
 /* Measurement hook (bench.py roofline): launch the cluster engine `reps` times back to back at
  * hierarchy level `level` (1-based, 2 <= level < n_levels) in its inner-FGMRES(2) entry — one
  * launch = the coarse part of the K-cycle from that level down (helmadr/multigrid.py:153-167)

@@ -611,10 +611,10 @@ int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, 
   });
 }
 
-int hadr_ce_profile(unsigned long long* out32, int reset) {
+int hadr_ce_profile(unsigned long long* out48, int reset) {
   return guarded([&] {
     Ctx::get().sync();
-    if (ce_profile_read(out32, reset)) throw std::runtime_error("ce_profile_read failed");
+    if (ce_profile_read(out48, reset)) throw std::runtime_error("ce_profile_read failed");
   });
 }
 
@@ -623,6 +623,13 @@ int hadr_set_option(const char* name, double value) {
     std::string n(name ? name : "");
     if (n == "ce_profile") {
       g_ce_prof_on = value != 0.0;
+    } else if (n == "ce_cgs2") {
+      g_ce_cgs2 = value != 0.0;
+      for (;;) {  // captured graphs carry the engine's launch flags
+        Hier* h = hier_pool_pop();
+        if (!h) break;
+        delete h;
+      }
     } else if (n == "kcycle_c64") {
       g_kcycle_c64 = value != 0.0;
     } else if (n == "ce_smem_relax") {

@@ -25,6 +25,13 @@ namespace hadr {
 struct CEShared {
   double pslot[2][CE_CTAS][4];  // all-reduce: CTA r's total, pushed here by CTA r (double-buffered)
   double bsum[4 * 32];
+  int ph[CE_THREADS / 32];      // per-warp parity of the all-reduce slot buffers
+  int prof_on;
+  int cgs2;                     // relaxations orthogonalise by CGS2 (two batched reductions per step)
+  alignas(16) double rout[32];  // batched all-reduce: cluster totals (read as complex pairs)
+  double vslot[2][32];          // batched all-reduce: this CTA's partials (read by every CTA)
+  double rin[32];                    // batched all-reduce: this CTA's partials (warp 0)
+  double wpart[CE_THREADS / 32][2];  // per-warp partial sums of the batched dots
   RelaxCtl rc;            // the (single) live relaxation
   FgCtl2 fg[CE_MAXLEV];   // one inner FGMRES(2) per level (nested)
   CELevel lv[CE_MAXLEV];
@@ -32,14 +39,28 @@ struct CEShared {
   double coarse_tol;
 };
 
-struct CEC {
-  unsigned rank, C;
-  long gtid, gstride;
-  int ph;
-  CEShared* S;
-  unsigned long long* prof;      // CTA 0 / thread 0 phase counters (null = off)
-  unsigned long long* prof_ctl;  // CTA 0 / relaxation control thread (blockDim.x - 1): slot 3
-};
+// The engine's state lives in shared memory (ce_S) and special registers only: nothing
+// per thread in local memory.  (A per-thread context struct passed by reference into the
+// __noinline__ phases lived in the stack frame — every access an LDL / generic load, and
+// every cluster barrier invalidates L1 (CCTL.IVALL), so those reloads went to L2.)
+__shared__ CEShared ce_S;
+constexpr int CE_CGS_MAX = 10;  // relaxations up to this length orthogonalise by CGS2 (when on)
+constexpr int CE_CGS_FROM = 4;  // ... from this step on
+
+struct CEC {};  // phase functions keep a context parameter; all state is in ce_S / special registers
+
+__device__ __forceinline__ unsigned ce_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned ce_nctas() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ long ce_gtid() { return (long)blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ long ce_gstride() { return (long)gridDim.x * blockDim.x; }
 
 // Phase profile of the engine (hadr_ce_profile): cycles seen by CTA 0 — thread 0, except
 // slot 3 (relaxation control), owned by the control thread (blockDim.x - 1).  Every slot
@@ -47,14 +68,21 @@ struct CEC {
 // control, 5 stencil, 7 launches, 8 vector ops, 10 barriers, 12 transfers, 14 lincomb,
 // 16 stencil on levels > 8192 points, 18 / 20 shared-memory relaxation staging / stencil
 // rows on levels > 8192 points, 22 / 24 the same on smaller levels, 26 all-reduce cluster-
-// barrier wait, 28 inner-FGMRES control (thread 0).
-constexpr int CE_NPROF = 32;
+// barrier wait, 28 inner-FGMRES control (thread 0), 30 CGS2 orthogonalisation of the relaxations.
+constexpr int CE_NPROF = 48;
 __device__ unsigned long long g_ce_prof[CE_NPROF];
+// CTA 0's thread 0 (and, for slot 3, its control thread) count when profiling is on
+__device__ __forceinline__ unsigned long long* ce_prof() {
+  return (ce_S.prof_on && blockIdx.x == 0 && threadIdx.x == 0) ? g_ce_prof : nullptr;
+}
+__device__ __forceinline__ unsigned long long* ce_prof_ctl() {
+  return (ce_S.prof_on && blockIdx.x == 0 && threadIdx.x == blockDim.x - 1) ? g_ce_prof : nullptr;
+}
 struct CEProfScope {
   unsigned long long* p;
   int slot;
   long long t0;
-  __device__ CEProfScope(const CEC& c, int s) : p(c.prof), slot(s), t0(0) {
+  __device__ CEProfScope(const CEC&, int s) : p(ce_prof()), slot(s), t0(0) {
     if (p) t0 = clock64();
   }
   __device__ CEProfScope(unsigned long long* q, int s) : p(q), slot(s), t0(0) {
@@ -101,13 +129,14 @@ __device__ __forceinline__ void ce_store_remote(double* p, unsigned rank, double
 template <int NV>
 __device__ void ce_allreduce(CEC& c, double (&v)[NV]) {
   CEProfScope prof_(c, 1);
-  CEShared* S = c.S;
+  CEShared* S = &ce_S;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ph = S->ph[wid];
   if (lane == 0) {
 #pragma unroll
     for (int q = 0; q < NV; ++q) S->bsum[q * 32 + wid] = v[q];
@@ -120,7 +149,7 @@ __device__ void ce_allreduce(CEC& c, double (&v)[NV]) {
       double t = lane < nw ? S->bsum[q * 32 + lane] : 0.0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (lane < (int)c.C) ce_store_remote(&S->pslot[c.ph][c.rank][q], lane, t);
+      if (lane < (int)ce_nctas()) ce_store_remote(&S->pslot[ph][ce_rank()][q], lane, t);
     }
   }
   {
@@ -129,12 +158,114 @@ __device__ void ce_allreduce(CEC& c, double (&v)[NV]) {
   }
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
-    double t = lane < (int)c.C ? S->pslot[c.ph][lane][q] : 0.0;
+    double t = lane < (int)ce_nctas() ? S->pslot[ph][lane][q] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
     v[q] = t;
   }
-  c.ph ^= 1;
+  __syncwarp();
+  if (lane == 0) S->ph[wid] = ph ^ 1;
+  __syncwarp();
+}
+
+// Batched all-reduce of the nv (<= 32) CTA partials in ce_S.rin: every CTA ends with the
+// cluster totals in ce_S.rout, lane q of warp 0 adding the 16 CTAs' value q in rank order
+// (identical operations in every CTA: bit-identical totals).
+__device__ __forceinline__ double ce_remote(const double* p, unsigned rank) {
+  unsigned long long in = reinterpret_cast<unsigned long long>(p), out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(in), "r"(rank));
+  return *reinterpret_cast<const volatile double*>(out);
+}
+// Barrier of the worker warps only (all but the CTA's last warp, the relaxation control
+// warp): named barrier 1, so the control thread's Givens update of the previous step is
+// not waited for by the intra-step syncs of the shared-memory relaxation.
+__device__ __forceinline__ void ce_worker_sync() {
+  asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x - 32) : "memory");
+}
+
+// CTA partials of nd complex dots <V_i, w> (i < nd; V_i = V + i * vs) over the CTA's np own
+// points, plus (norm) the real ||w||^2: dot i -> rin[2i], rin[2i+1], the norm -> rin[2 nd].
+// One dot per group of worker warps (the control warp takes none), each warp over a
+// contiguous chunk of the points, lanes strided; the per-warp sums are combined in warp
+// order by thread d < nd(+1) of warp 0: deterministic.  Worker warps only; rin is
+// complete for warp 0 when this returns.
+__device__ __forceinline__ void ce_dots_cta(const cplx* V, long vs, int nd, const cplx* w, long np, bool norm) {
+  CEShared* S = &ce_S;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nww = (blockDim.x >> 5) - 1;  // worker warps
+  const int ndt = nd + (norm ? 1 : 0);
+  const int per = nww / ndt;              // warps per dot (>= 1: nd + 1 <= nww, checked by the caller)
+  if (wid < ndt * per) {
+    const int d = wid / per, part = wid - d * per;
+    const long p0 = np * part / per, p1 = np * (part + 1) / per;
+    double a = 0.0, b = 0.0;
+    if (d < nd) {
+      const cplx* u = V + (long)d * vs;
+      for (long p = p0 + lane; p < p1; p += 32) {
+        const cplx uu = u[p], y = w[p];
+        a += uu.x * y.x + uu.y * y.y;
+        b += uu.x * y.y - uu.y * y.x;
+      }
+    } else {
+      for (long p = p0 + lane; p < p1; p += 32) {
+        const cplx y = w[p];
+        a += y.x * y.x + y.y * y.y;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) {
+      S->wpart[wid][0] = a;
+      S->wpart[wid][1] = b;
+    }
+  }
+  ce_worker_sync();
+  if ((int)threadIdx.x < ndt) {
+    const int d = threadIdx.x;
+    double a = S->wpart[d * per][0], b = S->wpart[d * per][1];
+    for (int q = 1; q < per; ++q) {
+      a += S->wpart[d * per + q][0];
+      b += S->wpart[d * per + q][1];
+    }
+    if (d < nd) {
+      S->rin[2 * d] = a;
+      S->rin[2 * d + 1] = b;
+    } else {
+      S->rin[2 * nd] = a;
+    }
+  }
+}
+
+// Batched cluster all-reduce of the nv (<= 32) CTA partials warp 0 holds in ce_S.rin (from
+// ce_dots_cta): every CTA ends with the totals in ce_S.rout, value q summed over the CTAs in
+// rank order by lane q of warp 0 (identical in every CTA).  All threads take part.
+__device__ void ce_allreduce_cta(CEC& c, int nv) {
+  CEProfScope prof_(c, 1);
+  CEShared* S = &ce_S;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ph = S->ph[wid];
+  __syncwarp();
+  if (wid == 0 && lane < nv) S->vslot[ph][lane] = S->rin[lane];
+  {
+    CEProfScope prof_w_(c, 26);
+    ce_sync();
+  }
+  if (wid == 0 && lane < nv) {
+    double r[CE_CTAS];
+#pragma unroll
+    for (int q = 0; q < CE_CTAS; ++q) r[q] = ce_remote(&S->vslot[ph][lane], q);
+    double t = r[0];
+#pragma unroll
+    for (int q = 1; q < CE_CTAS; ++q) t += r[q];
+    S->rout[lane] = t;
+  }
+  __syncthreads();
+  __syncwarp();
+  if (lane == 0) S->ph[wid] = ph ^ 1;
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
@@ -228,8 +359,8 @@ __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double
   const int n1 = A.n1, n2 = A.n2, n3 = A.n3, nofs = A.nofs;
   const int n23 = n2 * n3;
   const long N = (long)n1 * n23;
-  const int R = (n1 + (int)c.C - 1) / (int)c.C;
-  const int r0 = min(n1, (int)c.rank * R), r1 = min(n1, r0 + R);
+  const int R = (n1 + (int)ce_nctas() - 1) / (int)ce_nctas();
+  const int r0 = min(n1, (int)ce_rank() * R), r1 = min(n1, r0 + R);
   const int t0 = max(0, r0 - 2), t1 = min(n1, r1 + 2);
   const long base = (long)t0 * n23, tn = (long)(t1 - t0) * n23;
   for (long p = threadIdx.x; p < tn; p += blockDim.x) {
@@ -317,7 +448,7 @@ template <int INM, int OUTM, int RED>
 __device__ __noinline__ void ce_stencil(CEC& c, const StencilDev& A, const cplx* x, double s, const cplx* dinv,
                                         cplx* vout, const cplx* b, cplx* y, const cplx* u, double (&red)[3]) {
   CEProfScope prof_(c, 5);
-  CEProfScope prof_big_(A.n1 * A.n2 * A.n3 > 8192 ? c.prof : nullptr, 16);
+  CEProfScope prof_big_(A.n1 * A.n2 * A.n3 > 8192 ? ce_prof() : nullptr, 16);
   red[0] = red[1] = red[2] = 0.0;
   if (A.coef32) {  // mixed precision: complex64-stored operator
     switch (A.nofs) {
@@ -340,7 +471,7 @@ template <int RED>
 __device__ void ce_axpy(CEC& c, long n, cplx* w, cplx h, const cplx* v, const cplx* u, double (&red)[2]) {
   CEProfScope prof_(c, 8);
   red[0] = red[1] = 0.0;
-  for (long k = c.gtid; k < n; k += c.gstride) {
+  for (long k = ce_gtid(); k < n; k += ce_gstride()) {
     const cplx y = csub(ldm(w, k), cmul_np(h, ldm(v, k)));
     w[k] = y;
     if (RED == RED_NORM) {
@@ -356,7 +487,7 @@ __device__ void ce_axpy(CEC& c, long n, cplx* w, cplx h, const cplx* v, const cp
 __device__ void ce_dot(CEC& c, long n, const cplx* u, const cplx* w, double (&red)[2]) {
   CEProfScope prof_(c, 8);
   red[0] = red[1] = 0.0;
-  for (long k = c.gtid; k < n; k += c.gstride) {
+  for (long k = ce_gtid(); k < n; k += ce_gstride()) {
     const cplx uu = ldm(u, k), y = ldm(w, k);
     red[0] += uu.x * y.x + uu.y * y.y;
     red[1] += uu.x * y.y - uu.y * y.x;
@@ -367,7 +498,7 @@ __device__ void ce_dot(CEC& c, long n, const cplx* u, const cplx* w, double (&re
 __device__ double ce_scale(CEC& c, long n, const cplx* in, double s, bool scaled, cplx* out) {
   CEProfScope prof_(c, 8);
   double r = 0.0;
-  for (long k = c.gtid; k < n; k += c.gstride) {
+  for (long k = ce_gtid(); k < n; k += ce_gstride()) {
     cplx y = ldm(in, k);
     if (scaled) y = cscale(y, s);
     if (out) out[k] = y;
@@ -380,7 +511,7 @@ __device__ double ce_scale(CEC& c, long n, const cplx* in, double s, bool scaled
 // Jacobi-GMRES(s) relaxation (helmadr/krylov.py:91-119)
 // ---------------------------------------------------------------------------
 __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, const cplx* x, cplx* xo, int s) {
-  RelaxCtl* R = &c.S->rc;
+  RelaxCtl* R = &ce_S.rc;
   const long n = L.N;
   // the control thread: the CTA's last, whose share of the vector work is the smallest
   // (none at all on the coarsest grids), so the Givens updates run beside the other
@@ -443,7 +574,7 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
       double v[1] = {v2[0]};
       ce_allreduce<1>(c, v);
       if (ctl) {
-        CEProfScope prof_(c.prof_ctl, 3);
+        CEProfScope prof_(ce_prof_ctl(), 3);
         relax_step_sm(R, j, v[0]);
       }
       const double hn = sqrt(v[0]);
@@ -456,7 +587,7 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
   // xo = x + dinv (.) (V[:k]^T y)
   const int k = R->k;
   CEProfScope prof_lc_(c, 14);
-  for (long p = c.gtid; p < n; p += c.gstride) {
+  for (long p = ce_gtid(); p < n; p += ce_gstride()) {
     cplx t = mk(0.0, 0.0);
     for (int i = 0; i < k; ++i) t = cadd(t, cmul_np(ldm(L.V[i], p), R->y[i]));
     t = cmul_np(ldk(L.dinv, p), t);
@@ -536,10 +667,10 @@ __device__ __forceinline__ void sm_stencil_rows(CEC& c, const StencilDev& A, con
 }
 
 __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b, const cplx* x, cplx* xo, int s) {
-  RelaxCtl* R = &c.S->rc;
+  RelaxCtl* R = &ce_S.rc;
   const int n1 = L.A.n1, n23 = L.A.n2 * L.A.n3;
-  const int rows = (n1 + (int)c.C - 1) / (int)c.C;
-  const int r0 = min(n1, (int)c.rank * rows), r1 = min(n1, r0 + rows);
+  const int rows = (n1 + (int)ce_nctas() - 1) / (int)ce_nctas();
+  const int r0 = min(n1, (int)ce_rank() * rows), r1 = min(n1, r0 + rows);
   const int t0 = max(0, r0 - 2), t1 = min(n1, r1 + 2);
   const long np = (long)(r1 - r0) * n23, own0 = (long)r0 * n23;
   const long rs = (long)rows * n23;  // per-buffer stride (same layout in every CTA)
@@ -552,6 +683,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
   const bool ctl = threadIdx.x == blockDim.x - 1;
   const long nwk = blockDim.x - 32;                                   // worker threads
   const long tw = threadIdx.x < nwk ? threadIdx.x : (long)1 << 40;    // this thread's first point (none: ctl warp)
+  const bool cgs2 = ce_S.cgs2 && s <= CE_CGS_MAX && s + 1 <= (int)(blockDim.x >> 5) - 1;
   if (ctl) {
     R->steps = s;
     R->k = 0;
@@ -591,10 +723,13 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
     cplx* wp = wb + (long)((j + 1) % 2) * rs;  // previous Arnoldi vector (step 0: r)
     cplx* w = wb + (long)(j % 2) * rs;
     cplx* Vj = Vb + (long)j * rs;
+    // CGS2 from the 5th step on: two batched all-reduces (~2 us each) replace MGS's j + 2
+    // (~1.7 us each); below that MGS is cheaper (measured)
+    const bool cg = cgs2 && j >= CE_CGS_FROM;
     {
       CEProfScope prof_(c, 5);
       const bool big = (long)n1 * n23 > 8192;
-      CEProfScope prof_st_(c.prof, big ? 18 : 22);
+      CEProfScope prof_st_(ce_prof(), big ? 18 : 22);
       // V[j] = wp * sc (own rows); tile = D^-1 (.) (wp * sc) on rows [t0, t1)
       const long tn = (long)(t1 - t0) * n23;
       for (long q = tw; q < tn; q += nwk) {
@@ -611,11 +746,12 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
         }
         tile[q] = cmul_np(ldk(L.dinv, (long)row * n23 + col), v);
       }
-      __syncthreads();
+      if (threadIdx.x < blockDim.x - 32) ce_worker_sync();  // the control warp neither stages nor applies
       prof_st_.stop();
-      CEProfScope prof_rows_(c.prof, big ? 20 : 24);
+      CEProfScope prof_rows_(ce_prof(), big ? 20 : 24);
       double red[2] = {0.0, 0.0};
       const cplx* V0 = Vb;
+      if (cg) V0 = Vj;  // the epilogue's dot is discarded: batched dots follow
       if (L.A.coef32) {
         if (L.A.nofs == 21)
           sm_stencil_rows<21, true>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk);
@@ -631,10 +767,81 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
           default: sm_stencil_rows<0, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk); break;
         }
       }
-      double v[2] = {red[0], red[1]};
-      ce_allreduce<2>(c, v);
-      hcol = mk(v[0], v[1]);
-      if (ctl) R->H[0 * RMAX + j] = hcol;
+      if (!cg) {
+        double v[2] = {red[0], red[1]};
+        ce_allreduce<2>(c, v);
+        hcol = mk(v[0], v[1]);
+        if (ctl) R->H[0 * RMAX + j] = hcol;
+      }
+    }
+    if (cg) {
+      // CGS2 (two batched projections; algebraically the MGS loop below):
+      // h = V^H w ; w' = w - V h ; c = V^H w', ||w'||^2 ; w'' = w' - V c ;
+      // H[:, j] = h + c ; ||w''||^2 = ||w'||^2 - |c|^2 (c is at rounding level of ||w'||:
+      // no cancellation; an explicit norm when it is not).  Intra-CTA syncs are worker-only.
+      CEProfScope prof_cg_(c, 30);
+      const int nd = j + 1;
+      const cplx* hv = reinterpret_cast<const cplx*>(ce_S.rout);
+      CEProfScope ps1(ce_prof(), 32);
+      if (threadIdx.x < blockDim.x - 32) {  // worker warps
+        ce_worker_sync();  // w of every own point
+        ce_dots_cta(Vb, rs, nd, w, np, false);
+      }
+      ps1.stop();
+      CEProfScope ps2(ce_prof(), 34);
+      ce_allreduce_cta(c, 2 * nd);
+      ps2.stop();
+      CEProfScope ps3(ce_prof(), 36);
+      if (ctl)
+        for (int i = 0; i < nd; ++i) R->H[i * RMAX + j] = hv[i];
+      for (long p = tw; p < np; p += nwk) {
+        cplx y = w[p];
+        for (int i = 0; i < nd; ++i) y = csub(y, cmul_np(hv[i], Vb[(long)i * rs + p]));
+        w[p] = y;
+      }
+      ps3.stop();
+      CEProfScope ps4(ce_prof(), 38);
+      if (threadIdx.x < blockDim.x - 32) {  // worker warps
+        ce_worker_sync();  // w' complete
+        ce_dots_cta(Vb, rs, nd, w, np, true);
+      }
+      ps4.stop();
+      CEProfScope ps5(ce_prof(), 40);
+      ce_allreduce_cta(c, 2 * nd + 1);
+      ps5.stop();
+      CEProfScope ps6(ce_prof(), 42);
+      double cc = 0.0;
+      for (int i = 0; i < nd; ++i) cc += hv[i].x * hv[i].x + hv[i].y * hv[i].y;
+      const double n2 = ce_S.rout[2 * nd];
+      double nn = 0.0;
+      for (long p = tw; p < np; p += nwk) {
+        cplx y = w[p];
+        for (int i = 0; i < nd; ++i) y = csub(y, cmul_np(hv[i], Vb[(long)i * rs + p]));
+        w[p] = y;
+        nn += y.x * y.x + y.y * y.y;
+      }
+      if (ctl)
+        for (int i = 0; i < nd; ++i) R->H[i * RMAX + j] = cadd(R->H[i * RMAX + j], hv[i]);
+      ps6.stop();
+      CEProfScope ps7(ce_prof(), 44);
+      double hn2;
+      if (cc <= 1e-8 * n2) {
+        hn2 = n2 - cc;
+        CE_SYNC(c);  // w'' of every CTA before the neighbours read its halo rows
+      } else {       // heavy cancellation: the explicit norm (its all-reduce is the barrier)
+        double v[1] = {nn};
+        ce_allreduce<1>(c, v);
+        hn2 = v[0];
+      }
+      if (ctl) {  // Givens, least squares (the control thread)
+        CEProfScope prof_(ce_prof_ctl(), 3);
+        relax_step_sm(R, j, hn2);
+      }
+      const double hn = sqrt(hn2);
+      const bool stop = (hn <= kBreakdownEps * beta) || (j + 1 >= s);  // helmadr/krylov.py:113-114
+      cur = stop ? kStopped : j + 1;
+      sc_next = 1.0 / hn;
+      continue;
     }
     for (int i = 0; i < j; ++i) {
       const cplx h = hcol;  // H[i][j], the previous all-reduce
@@ -662,7 +869,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       }
       ce_allreduce<1>(c, v);
       if (ctl) {  // Givens, least squares (the control thread)
-        CEProfScope prof_(c.prof_ctl, 3);
+        CEProfScope prof_(ce_prof_ctl(), 3);
         relax_step_sm(R, j, v[0]);
       }
       const double hn = sqrt(v[0]);
@@ -702,7 +909,7 @@ __device__ __noinline__ void ce_restrict(CEC& c, int n1f, int n2f, int n3f, cons
   const int n1c = (n1f - 1) / 2 + 1, n2c = (n2f - 1) / 2 + 1, n3c = (n3f - 1) / 2 + 1;
   const long Nc = (long)n1c * n2c * n3c;
   const int c3lo = n3f > 1 ? -1 : 0, c3hi = n3f > 1 ? 1 : 0;
-  for (long q = c.gtid; q < Nc; q += c.gstride) {
+  for (long q = ce_gtid(); q < Nc; q += ce_gstride()) {
     const int I1 = (int)(q / ((long)n2c * n3c));
     const int rem = (int)(q - (long)I1 * n2c * n3c);
     const int I2 = rem / n3c, I3 = rem - (rem / n3c) * n3c;
@@ -745,7 +952,7 @@ __device__ __noinline__ void ce_prolong_add(CEC& c, int n1f, int n2f, int n3f, c
   const int n2c = (n2f - 1) / 2 + 1, n3c = (n3f - 1) / 2 + 1;
   const int n23 = n2f * n3f;
   const long Nf = (long)n1f * n23;
-  for (long f = c.gtid; f < Nf; f += c.gstride) {
+  for (long f = ce_gtid(); f < Nf; f += ce_gstride()) {
     const int f1 = (int)(f / n23);
     const int rem = (int)(f - (long)f1 * n23);
     const int f2 = rem / n3f, f3 = rem - (rem / n3f) * n3f;
@@ -842,7 +1049,7 @@ __device__ __noinline__ void ce_arnoldi(CEC& c, FgCtl2* f, const CELevel& L, int
 
 template <int D>
 __device__ void ce_inner(CEC& c, int ci) {
-  CEShared* S = c.S;
+  CEShared* S = &ce_S;
   const CELevel& C = S->lv[ci];
   FgCtl2* f = &S->fg[ci];
   const long n = C.N;
@@ -857,7 +1064,7 @@ __device__ void ce_inner(CEC& c, int ci) {
     __syncthreads();
   }
   if (f->path == FG_ZERO) {
-    for (long p = c.gtid; p < n; p += c.gstride) C.fx[p] = mk(0.0, 0.0);
+    for (long p = ce_gtid(); p < n; p += ce_gstride()) C.fx[p] = mk(0.0, 0.0);
     CE_SYNC(c);
     return;
   }
@@ -868,7 +1075,7 @@ __device__ void ce_inner(CEC& c, int ci) {
   if (f->path == FG_BRK) {  // early exit after iteration 1: x = Z0 y0, r = b - A x
     const int k = f->k;
     const cplx y0 = f->y[0];
-    for (long p = c.gtid; p < n; p += c.gstride)
+    for (long p = ce_gtid(); p < n; p += ce_gstride())
       C.fx[p] = (k >= 1) ? cadd(mk(0.0, 0.0), cmul_np(ldm(C.fZ0, p), y0)) : mk(0.0, 0.0);
     CE_SYNC(c);
     double red[3];
@@ -894,7 +1101,7 @@ __device__ void ce_inner(CEC& c, int ci) {
   if (f->path == FG_FIN) {
     const int k = f->k, cyc = f->cycle;
     const cplx y0 = f->y[0], y1 = f->y[1];
-    for (long p = c.gtid; p < n; p += c.gstride) {
+    for (long p = ce_gtid(); p < n; p += ce_gstride()) {
       cplx out;
       if (cyc == 0) {
         cplx t = mk(0.0, 0.0);
@@ -914,7 +1121,7 @@ __device__ void ce_inner(CEC& c, int ci) {
 template <int D>
 __device__ void ce_kcycle(CEC& c, int l, const cplx* b, cplx* xo) {
   if constexpr (D < CE_MAXLEV) {
-    CEShared* S = c.S;
+    CEShared* S = &ce_S;
     const CELevel& L = S->lv[l];
     const CELevel& C = S->lv[l + 1];
     ce_relax_any(c, L, b, nullptr, xo, L.s);
@@ -940,7 +1147,7 @@ __global__ void __launch_bounds__(CE_THREADS, 1)
                      int prof) {
   pdl_enter();
   if (active && *((volatile const int*)active) == 0) return;
-  __shared__ CEShared S;
+  CEShared& S = ce_S;
   // level descriptors into shared memory
   {
     const int nw = (int)(sizeof(CELevel) * CE_MAXLEV / sizeof(int));
@@ -951,18 +1158,13 @@ __global__ void __launch_bounds__(CE_THREADS, 1)
       S.nlev = d->nlev;
       S.coarse_steps = d->coarse_steps;
       S.coarse_tol = d->coarse_tol;
+      S.prof_on = prof & 1;
+      S.cgs2 = (prof >> 1) & 1;
     }
+    if ((threadIdx.x & 31) == 0) S.ph[threadIdx.x >> 5] = 0;
   }
   __syncthreads();
   CEC c;
-  c.rank = blockIdx.x;
-  c.C = gridDim.x;
-  c.gtid = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  c.gstride = (long)gridDim.x * blockDim.x;
-  c.ph = 0;
-  c.S = &S;
-  c.prof = (prof && blockIdx.x == 0 && threadIdx.x == 0) ? g_ce_prof : nullptr;
-  c.prof_ctl = (prof && blockIdx.x == 0 && threadIdx.x == blockDim.x - 1) ? g_ce_prof : nullptr;
   const long long t_start = clock64();
   if (mode == 0) {
     ce_kcycle<0>(c, l0, b, xo);
@@ -973,9 +1175,9 @@ __global__ void __launch_bounds__(CE_THREADS, 1)
     ce_relax_any(c, C, C.fb, nullptr, C.fx, C.s);
   }
   ce_sync();  // no CTA exits while another may still read its shared memory
-  if (c.prof) {
-    c.prof[0] += clock64() - t_start;
-    c.prof[7] += 1;
+  if (unsigned long long* pr = ce_prof()) {
+    pr[0] += clock64() - t_start;
+    pr[7] += 1;
   }
 }
 
@@ -990,6 +1192,7 @@ int ce_profile_read(unsigned long long* out, int reset) {
 }
 
 int g_ce_prof_on = 0;
+int g_ce_cgs2 = 1;
 
 extern int g_ce_prof_on;
 void launch_cluster_engine(cudaStream_t s, const CEDesc* d, int mode, int l0, const cplx* b, cplx* xo,
@@ -1019,7 +1222,7 @@ void launch_cluster_engine(cudaStream_t s, const CEDesc* d, int mode, int l0, co
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = g_pdl ? 2 : 1;
-  cudaLaunchKernelEx(&cfg, k_cluster_engine, d, mode, l0, b, xo, active, g_ce_prof_on);
+  cudaLaunchKernelEx(&cfg, k_cluster_engine, d, mode, l0, b, xo, active, (g_ce_prof_on ? 1 : 0) | (g_ce_cgs2 ? 2 : 0));
 }
 
 }  // namespace hadr

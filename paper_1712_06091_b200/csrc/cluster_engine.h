@@ -37,6 +37,7 @@ struct CEDesc {
 // phase counters [total cyc, allreduce cyc, n, epilogue cyc, n, stencil cyc, n, launches]
 int ce_profile_read(unsigned long long* out, int reset);
 extern int g_ce_prof_on;
+extern int g_ce_cgs2;  // engine relaxations orthogonalise by CGS2 (batched reductions) instead of MGS
 void launch_cluster_engine(cudaStream_t s, const CEDesc* d, int mode, int l0, const cplx* b, cplx* xo,
                            const int* active, int ctas, size_t tile_bytes);
 // dynamic shared memory for the stencil row tiles of levels with n1 x n2 points

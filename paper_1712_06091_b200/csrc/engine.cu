@@ -888,7 +888,7 @@ size_t Hier::ce_tile(int li) const {
   size_t m = 0;  // the engine touches levels li .. coarsest
   for (int i = li; i < (int)lv.size(); ++i) {
     m = std::max(m, ce_tile_bytes(lv[i].n1, lv[i].n2 * lv[i].n3, CE_CTAS));
-    if (level_smr(lv[i])) m = std::max(m, ce_relax_sm_bytes(lv[i].n1, (long)lv[i].n2 * lv[i].n3, lv[i].s, CE_CTAS));
+    if (lv[i].smr) m = std::max(m, ce_relax_sm_bytes(lv[i].n1, (long)lv[i].n2 * lv[i].n3, lv[i].s, CE_CTAS));
   }
   return m;
 }
@@ -927,6 +927,7 @@ void Hier::alloc_workspace() {
     L.s = (i == nl - 1) ? coarse_steps : (i + 2);  // relax_steps(l) = l + 1 (helmadr/multigrid.py:87-88)
     if (L.s > RMAX) throw ValueError("relaxation length exceeds the device limit (16)");
     L.s = (int)std::min<long>(L.s, L.A->N);
+    L.smr = level_smr(L);  // the engine descriptor and ce_tile() agree for the hierarchy's lifetime
     for (int j = 0; j <= L.s; ++j) L.V[j] = valloc(L);
     L.w[0] = valloc(L);
     L.w[1] = valloc(L);
@@ -965,7 +966,7 @@ void Hier::alloc_workspace() {
       d.dinv = L.dinv;
       d.N = L.N;
       d.s = L.s;
-      d.smr = level_smr(L) ? 1 : 0;
+      d.smr = L.smr ? 1 : 0;
       d.r = L.r;
       for (int j = 0; j <= RMAX; ++j) d.V[j] = L.V[j];
       d.w[0] = L.w[0];
@@ -990,10 +991,17 @@ Hier* hier_pool_pop() {
   return h;
 }
 
+std::vector<long long> hier_option_signature() {
+  return {g_ce_smem_relax, g_ce_max_n, g_cl_max_n, g_stencil_tile, g_relax_split, g_class_compress, g_pair_compress,
+          g_pdl, g_ce_prof_on, g_kcycle_c64, g_ce_cgs2};
+}
+
 void hier_release(Hier* h) {
   if (!h) return;
   auto& pool = hier_pool();
-  if (h->poolable && pool.size() < 4) {
+  // a hierarchy released after an option change (e.g. freed late by the Python GC) carries
+  // descriptors and graphs of the old options: never recycle it
+  if (h->poolable && pool.size() < 4 && h->opt_sig == hier_option_signature()) {
     pool.push_back(h);
     return;
   }
@@ -1031,7 +1039,7 @@ Hier* hier_build(Op* fine, int max_levels, int coarse_steps, double coarse_tol) 
   for (size_t i = 0; i < pool.size(); ++i) {
     Hier* h = pool[i];
     if (h->lv.size() != shapes.size() || h->coarse_steps != coarse_steps || h->coarse_tol != coarse_tol ||
-        h->c64 != (g_kcycle_c64 != 0))
+        h->c64 != (g_kcycle_c64 != 0) || h->opt_sig != hier_option_signature())
       continue;
     bool same = true;
     for (size_t l = 0; l < shapes.size(); ++l)

@@ -127,6 +127,7 @@ struct Level {
   std::vector<int> bounds;   // slab level: every rank's first plane (size + 1 entries)
   const cplx* dinv = nullptr;
   int s = 0;                 // relaxation length at this level
+  bool smr = false;          // its engine relaxation runs out of shared memory (fixed at allocation)
   // K-cycle workspace
   cplx* r = nullptr;
   cplx* V[RMAX + 1] = {nullptr};
@@ -139,8 +140,13 @@ struct Level {
   FgCtl* fctl = nullptr;
 };
 
+// The runtime options a hierarchy's structure and captured graphs depend on (engine
+// split, shared-memory relaxations, stencil paths, launch attributes, profiling).
+std::vector<long long> hier_option_signature();
+
 struct Hier {
   std::vector<Level> lv;
+  std::vector<long long> opt_sig = hier_option_signature();  // options at construction
   bool poolable = false;     // owns copies of every level operator: may be recycled
   bool c64 = false;          // K-cycle operators applied from complex64 storage (mixed precision)
   int coarse_steps = 10;

@@ -224,8 +224,242 @@ __global__ void __launch_bounds__(512, 1) k_bench(int variant, const cplx* __res
   if (chk == 12345.678) out[0] = chk;
 }
 
+// ---- all-reduce floor: push version (as cluster_engine.cu), NV doubles, no work between ----
+struct ARS {
+  double pslot[2][16][4];
+  double bsum[4 * 32];
+};
+__device__ __forceinline__ void st_remote(double* p, unsigned rank, double v) {
+  unsigned long long in = reinterpret_cast<unsigned long long>(p), out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(in), "r"(rank));
+  *reinterpret_cast<volatile double*>(out) = v;
+}
+template <int NV>
+__device__ __forceinline__ void allred(ARS* S, int& ph, double (&v)[NV], int sync_first) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned rank = blockIdx.x, C = gridDim.x;
+  if (sync_first) {
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < NV; ++q) S->bsum[q * 32 + wid] = v[q];
+    __syncthreads();
+    if (wid == 0) {
+      const int nw = blockDim.x >> 5;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        double t = lane < nw ? S->bsum[q * 32 + lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane < (int)C) st_remote(&S->pslot[ph][rank][q], lane, t);
+      }
+    }
+  } else {  // no block barrier: only warp 0 contributes (floor of the cluster part)
+    if (wid == 0)
+#pragma unroll
+      for (int q = 0; q < NV; ++q)
+        if (lane < (int)C) st_remote(&S->pslot[ph][rank][q], lane, v[q]);
+  }
+  csync();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    double t = lane < (int)C ? S->pslot[ph][lane][q] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    v[q] = t;
+  }
+  ph ^= 1;
+}
+// pull version (the engine's round-1 all-reduce): block sum -> own slot -> barrier -> warp 0
+// reads the 16 remote slots -> smem -> __syncthreads
+struct ARP {
+  double slot[2][4];
+  double tot[4];
+  double bsum[4 * 32];
+};
+__device__ __forceinline__ double ld_remote(const double* p, unsigned rank) {
+  unsigned long long in = reinterpret_cast<unsigned long long>(p), out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(in), "r"(rank));
+  return *reinterpret_cast<const volatile double*>(out);
+}
+template <int NV>
+__device__ __forceinline__ void allred_pull(ARP* S, int& ph, double (&v)[NV]) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned C = gridDim.x;
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) S->bsum[q * 32 + wid] = v[q];
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double t = lane < nw ? S->bsum[q * 32 + lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) S->slot[ph][q] = t;
+    }
+  }
+  csync();
+  if (wid == 0) {
+    double t[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) t[q] = lane < (int)C ? ld_remote(&S->slot[ph][q], lane) : 0.0;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t[q] += __shfl_xor_sync(0xffffffffu, t[q], o);
+      if (lane == 0) S->tot[q] = t[q];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = S->tot[q];
+  ph ^= 1;
+}
+
+// st.async version: the pushes land in the remote CTA's slots and complete_tx its mbarrier;
+// no cluster barrier.  WARPS: 0 -> warp 0 pushes the block sum (after __syncthreads);
+// 1 -> every warp pushes its own partial (no block barrier), every warp sums 16 x nw slots.
+struct ARA {
+  double slot[2][16 * 16][4];
+  double bsum[4 * 32];
+  unsigned long long bar[2];
+};
+__device__ __forceinline__ void st_async_f64(double* remote_local_addr, unsigned rank, double v,
+                                             unsigned long long* bar_local) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(remote_local_addr), b = (unsigned)__cvta_generic_to_shared(bar_local);
+  unsigned ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(b), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra), "d"(v), "r"(rb)
+               : "memory");
+}
+template <int NV, int ALLW>
+__device__ __forceinline__ void allred_async(ARA* S, int& k, double (&v)[NV]) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned C = gridDim.x, rank = blockIdx.x;
+  const int ph = k & 1;
+  const unsigned par = (k >> 1) & 1;
+  if (threadIdx.x == 0) {
+    const unsigned bytes = (ALLW ? C * nw : C) * NV * 8;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&S->bar[ph])),
+                 "r"(bytes)
+                 : "memory");
+  }
+  if (ALLW) {
+    if (lane < (int)C)
+#pragma unroll
+      for (int q = 0; q < NV; ++q) st_async_f64(&S->slot[ph][rank * nw + wid][q], lane, v[q], &S->bar[ph]);
+  } else {
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < NV; ++q) S->bsum[q * 32 + wid] = v[q];
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        double t = lane < nw ? S->bsum[q * 32 + lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane < (int)C) st_async_f64(&S->slot[ph][rank][q], lane, t, &S->bar[ph]);
+      }
+    }
+  }
+  asm volatile(
+      "{\n.reg .pred P;\nW: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n@!P bra W;\n}\n" ::"r"(
+          (unsigned)__cvta_generic_to_shared(&S->bar[ph])),
+      "r"(par)
+      : "memory");
+  const int ns = ALLW ? C * nw : C;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    double t = 0.0;
+    for (int i = lane; i < ns; i += 32) t += S->slot[ph][i][q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    v[q] = t;
+  }
+  ++k;
+}
+
+__global__ void __launch_bounds__(512, 1) k_allred(int variant, int reps, double* out) {
+  __shared__ ARS S;
+  __shared__ ARP SP;
+  __shared__ ARA SA;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&SA.bar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  csync();
+  int ph = 0;
+  double v[2] = {threadIdx.x * 1e-3, blockIdx.x * 1.0};
+  for (int r = 0; r < reps; ++r) {
+    if (variant == 0) allred<2>(&S, ph, v, 1);
+    else if (variant == 1) allred<2>(&S, ph, v, 0);
+    else if (variant == 2) csync();
+    else if (variant == 3) allred_pull<2>(&SP, ph, v);
+    else if (variant == 4) allred_async<2, 0>(&SA, ph, v);
+    else allred_async<2, 1>(&SA, ph, v);
+    v[0] *= 0.5;
+    v[1] *= 0.5;
+  }
+  csync();
+  if (v[0] == 12345.678) out[0] = v[1];
+}
+
 int main(int argc, char** argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 129;
+  if (n == 0) {  // all-reduce floor
+    double* o;
+    CK(cudaMalloc(&o, 8));
+    CK(cudaFuncSetAttribute(k_allred, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    const char* names[6] = {"push all-reduce (block sum + DSMEM push + barrier + local sum)",
+                            "warp-0 push only (no __syncthreads)", "cluster barrier alone",
+                            "pull all-reduce (round 1: barrier + remote reads + __syncthreads)",
+                            "st.async + mbarrier, block sum pushed by warp 0",
+                            "st.async + mbarrier, every warp pushes its partial"};
+    for (int v = 0; v < 6; ++v)
+      for (int threads : {512, 256}) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(16);
+        cfg.blockDim = dim3(threads);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 16;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const int reps = 20000;
+        CK(cudaLaunchKernelEx(&cfg, k_allred, v, 100, o));
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0));
+        CK(cudaLaunchKernelEx(&cfg, k_allred, v, reps, o));
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        printf("%s, %d threads: %.3f us\n", names[v], threads, ms * 1e3 / reps);
+      }
+    return 0;
+  }
   const int reps = 200;
   const long N = (long)n * n;
   int d1[NO], d2[NO], q = 0;

@@ -32,7 +32,7 @@ def main():
             _lib.set_option(k, float(v))
     _lib.set_option("ce_profile", 1)  # read when the K-cycle graphs are captured
     drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
-    prof = (C.c_ulonglong * 32)()
+    prof = (C.c_ulonglong * 48)()
     L.hadr_ce_profile(prof, 1)
     u, amp, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
     L.hadr_ce_profile(prof, 0)

@@ -26,7 +26,7 @@ def main():
     from paper_1712_06091_b200.operators import rhs_transform
 
     L = _lib.lib()
-    for opt in ("pdl", "ce_max_n", "kcycle_c64", "stencil_tile", "ce_smem_relax", "cl_max_n"):
+    for opt in ("pdl", "ce_max_n", "kcycle_c64", "stencil_tile", "ce_smem_relax", "cl_max_n", "ce_cgs2"):
         if os.environ.get("HADR_" + opt.upper()) is not None:
             _lib.set_option(opt, float(os.environ["HADR_" + opt.upper()]))
     wl = workloads.by_name(os.environ.get("HADR_WORKLOAD", "cfg2"), args.n)
@@ -67,7 +67,7 @@ def ce_breakdown(n=1025, its=1000):
 
     L = _lib.lib()
     _lib.set_option("ce_profile", 1)
-    out = (C.c_ulonglong * 32)()
+    out = (C.c_ulonglong * 48)()
     L.hadr_ce_profile(out, 1)
     sys.argv = [sys.argv[0], "--n", str(n), "--its", str(its), "--warm", "0"]
     main()
@@ -78,7 +78,9 @@ def ce_breakdown(n=1025, its=1000):
     for name, i in (("allreduce", 1), ("relax control", 3), ("stencil", 5), ("vector ops", 8), ("barriers", 10),
                     ("transfers", 12), ("relax update", 14), ("stencil big", 16), ("smrelax stage big", 18),
                     ("smrelax rows big", 20), ("smrelax stage sm", 22), ("smrelax rows sm", 24),
-                    ("allred barrier", 26), ("fg control", 28)):
+                    ("allred barrier", 26), ("fg control", 28), ("cgs2", 30), ("cg dots1", 32),
+                    ("cg allred1", 34), ("cg update1", 36), ("cg dots2", 38), ("cg allred2", 40),
+                    ("cg update2", 42), ("cg final sync", 44)):
         print(f"  {name:13s} {v[i]/f:9.0f} us  n={v[i+1]:7d}  {v[i]/max(v[i+1],1)/1.9:7.0f} ns/op")
 
 
