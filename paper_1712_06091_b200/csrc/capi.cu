@@ -623,6 +623,13 @@ int hadr_set_option(const char* name, double value) {
     std::string n(name ? name : "");
     if (n == "ce_profile") {
       g_ce_prof_on = value != 0.0;
+    } else if (n == "defer_mgs") {
+      g_defer_mgs = value != 0.0;
+      for (;;) {
+        Hier* h = hier_pool_pop();
+        if (!h) break;
+        delete h;
+      }
     } else if (n == "ce_cgs2") {
       g_ce_cgs2 = value != 0.0;
       for (;;) {  // captured graphs carry the engine's launch flags

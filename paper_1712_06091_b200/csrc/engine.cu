@@ -81,6 +81,8 @@ Ctx& Ctx::get() {
     HADR_CUDA(cudaDeviceGetAttribute(&n->nsm, cudaDevAttrMultiProcessorCount, n->device));
     HADR_CUDA(cudaStreamCreateWithFlags(&n->stream, cudaStreamNonBlocking));
     n->rs.partials = dalloc<double>(4 * 8192);
+    n->rs2.partials = dalloc<double>(4 * 8192);
+    n->rs2.ticket = nullptr;
     n->rs.ticket = dalloc<unsigned>(4);
     HADR_CUDA(cudaMemset(n->rs.ticket, 0, 4 * sizeof(unsigned)));
     n->dscal = dalloc<double>(64);
@@ -877,6 +879,7 @@ Hier::~Hier() {
 }
 
 int g_ce_smem_relax = 1;
+int g_defer_mgs = 1;  // option "defer_mgs": fold the MGS dots' finalize kernels into the next axpy
 
 // the level's relaxation fits the engine's shared memory (ce_relax_sm)
 static bool level_smr(const Level& L) {
@@ -993,7 +996,7 @@ Hier* hier_pool_pop() {
 
 std::vector<long long> hier_option_signature() {
   return {g_ce_smem_relax, g_ce_max_n, g_cl_max_n, g_stencil_tile, g_relax_split, g_class_compress, g_pair_compress,
-          g_pdl, g_ce_prof_on, g_kcycle_c64, g_ce_cgs2};
+          g_pdl, g_ce_prof_on, g_kcycle_c64, g_ce_cgs2, g_defer_mgs};
 }
 
 void hier_release(Hier* h) {
@@ -1228,16 +1231,29 @@ void Hier::emit_relax(Level& L, const cplx* b, const cplx* x, cplx* xo, int s, G
       launch_scale_jac(lc0, L.N, a.x, a.scale, L.dinv, L.V[j], L.z, gj);
       a.x = L.z;
       xchg(L, L.z);
-      launch_stencil(lc0, IN_PLAIN, OUT_APPLY, RED_DOT, a);
-    } else {
+    }
+    // MGS chain: each dot's 1-block finalize is folded into the next axpy (Pend), the
+    // partials alternating between the two scratch buffers
+    Pend pend{};
+    const bool defer = g_defer_mgs && !L.dist;
+    g_defer_out = defer ? &pend : nullptr;
+    if (!L.z) {
       xchg(L, a.x);
       launch_stencil(lc0, IN_SCALE | IN_JAC | IN_WRITEV, OUT_APPLY, j == 0 ? RED_DOT_CENTER : RED_DOT, a);
+    } else {
+      launch_stencil(lc0, IN_PLAIN, OUT_APPLY, RED_DOT, a);
     }
-    for (int i = 0; i < j; ++i)
-      launch_axpy_red(lc0, L.N, w, &rc->H[i * RMAX + j], L.V[i], RED_DOT, L.V[i + 1], gj, c.rs,
-                      epi(EPI_RELAX_H, rc, i + 1, j));
-    launch_axpy_red(lc0, L.N, w, &rc->H[j * RMAX + j], L.V[j], RED_NORM, nullptr, gj, c.rs,
-                    epi(EPI_RELAX_STEP, rc, 0, j));
+    int buf = 0;  // the producer wrote c.rs
+    for (int i = 0; i < j; ++i) {
+      Pend in = pend;
+      pend = Pend{};
+      launch_axpy_red(lc0, L.N, w, &rc->H[i * RMAX + j], L.V[i], RED_DOT, L.V[i + 1], gj, buf ? c.rs : c.rs2,
+                      epi(EPI_RELAX_H, rc, i + 1, j), in);
+      buf ^= 1;
+    }
+    g_defer_out = nullptr;
+    launch_axpy_red(lc0, L.N, w, &rc->H[j * RMAX + j], L.V[j], RED_NORM, nullptr, gj, buf ? c.rs : c.rs2,
+                    epi(EPI_RELAX_STEP, rc, 0, j), pend);
   }
   LinComb lc{};
   for (int j = 0; j < s; ++j) lc.v[j] = L.V[j];

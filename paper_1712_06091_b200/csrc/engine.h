@@ -29,6 +29,7 @@ struct Ctx {
   int nsm = 148;
   cudaStream_t stream = nullptr;
   RedScratch rs{};
+  RedScratch rs2{};          // second partials buffer: a deferred reduction's consumer writes its own here
   double* dscal = nullptr;   // device scalars for host readback
   double* hscal = nullptr;   // pinned mirror
   LaunchCfg lc{};
@@ -179,6 +180,7 @@ extern long g_ce_max_n;  // levels with N <= this run inside the cluster engine 
 extern int g_kcycle_c64; // build hierarchies with complex64 operator storage (mixed-precision K-cycle)
 extern int g_ce_smem_relax;  // engine relaxations out of shared memory where they fit
 extern int g_pair_compress;  // pair-compress fine operators (outer A, hierarchy level 0)
+extern int g_defer_mgs;     // MGS dot finalizes folded into the next axpy (option "defer_mgs")
 extern long g_relax_split;   // 3D levels with at least this many points form D^-1 (s w) once per point
 extern int g_class_compress;  // class-compress coarse graph-path levels: 0 off, 1 3D, 2 2D and 3D
 

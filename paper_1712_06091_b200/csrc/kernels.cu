@@ -229,9 +229,15 @@ __global__ void k_epi_gathered(const double* all, int size, Gate g, Epi e) {
   run_epi(e, t, NV);
 }
 
+Pend* g_defer_out = nullptr;
+
 template <int NV>
 static void launch_finalize(const LaunchCfg& lc, const Geo& geo, Gate g, RedScratch rs, Epi e) {
   if (geo.cluster) return;
+  if (NV == 2 && g_defer_out && !lc.dist) {  // the consumer finishes it (Pend)
+    *g_defer_out = Pend{rs.partials, geo.blocks, e};
+    return;
+  }
   ++g_launch_count;
   if (!lc.dist) {
     launch_k(k_finalize<NV>, 1, kThreads, lc.stream, rs, geo.blocks, g, e);
@@ -829,10 +835,29 @@ void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const Stenc
 template <int RED, int CL>
 __global__ void __launch_bounds__(kThreads) k_axpy_red(long n, cplx* __restrict__ w, const cplx* h,
                                                          const cplx* __restrict__ v, const cplx* __restrict__ u,
-                                                         Gate g, RedScratch rs, Epi e) {
+                                                         Gate g, RedScratch rs, Epi e, Pend in) {
   pdl_enter();
   if (!gate_open(g)) return;
-  const cplx hh = *h;
+  cplx hh;
+  if (in.partials) {  // the deferred finalize of the producer (k_finalize<2>'s exact summation)
+    __shared__ double smf[2 * 32];
+    __shared__ double tot[2];
+    double acc[2] = {0.0, 0.0};
+    for (int b = threadIdx.x; b < in.nblocks; b += blockDim.x) {
+      acc[0] += in.partials[b * 2];
+      acc[1] += in.partials[b * 2 + 1];
+    }
+    block_sum<2>(acc, smf);
+    if (threadIdx.x == 0) {
+      tot[0] = acc[0];
+      tot[1] = acc[1];
+      if (blockIdx.x == 0) run_epi(in.e, acc, 2);
+    }
+    __syncthreads();
+    hh = mk(tot[0], tot[1]);
+  } else {
+    hh = *h;
+  }
   constexpr int NV = (RED == RED_NORM) ? 1 : 2;
   double red[NV];
 #pragma unroll
@@ -853,20 +878,21 @@ __global__ void __launch_bounds__(kThreads) k_axpy_red(long n, cplx* __restrict_
 }
 
 void launch_axpy_red(const LaunchCfg& lc, long n, cplx* w, const cplx* h, const cplx* v, int red, const cplx* u,
-                     Gate g, RedScratch rs, Epi e) {
+                     Gate g, RedScratch rs, Epi e, Pend in) {
   ++g_launch_count;
   const Geo geo = geo_for(lc, n);
+  if (in.partials && (geo.cluster || lc.dist)) throw std::logic_error("a deferred reduction needs a plain grid");
   if (red == RED_NORM) {
     if (geo.cluster)
-      launch_geo(k_axpy_red<RED_NORM, 1>, geo, lc.stream, n, w, h, v, u, g, rs, e);
+      launch_geo(k_axpy_red<RED_NORM, 1>, geo, lc.stream, n, w, h, v, u, g, rs, e, in);
     else
-      launch_geo(k_axpy_red<RED_NORM, 0>, geo, lc.stream, n, w, h, v, u, g, rs, e);
+      launch_geo(k_axpy_red<RED_NORM, 0>, geo, lc.stream, n, w, h, v, u, g, rs, e, in);
     launch_finalize<1>(lc, geo, g, rs, e);
   } else {
     if (geo.cluster)
-      launch_geo(k_axpy_red<RED_DOT, 1>, geo, lc.stream, n, w, h, v, u, g, rs, e);
+      launch_geo(k_axpy_red<RED_DOT, 1>, geo, lc.stream, n, w, h, v, u, g, rs, e, in);
     else
-      launch_geo(k_axpy_red<RED_DOT, 0>, geo, lc.stream, n, w, h, v, u, g, rs, e);
+      launch_geo(k_axpy_red<RED_DOT, 0>, geo, lc.stream, n, w, h, v, u, g, rs, e, in);
     launch_finalize<2>(lc, geo, g, rs, e);
   }
 }

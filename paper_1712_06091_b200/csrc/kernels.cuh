@@ -149,9 +149,22 @@ struct LaunchCfg {
 
 void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const StencilArgs& a);
 
+// A 2-value (complex dot) reduction whose 1-block finalize was not launched: its consumer
+// (the next MGS axpy of the chain) sums the producer's per-block partials itself, with the
+// finalize kernel's exact summation (same thread layout, same order: bit-identical totals
+// in every block), block 0 running the deferred epilogue.  Saves one kernel per link.
+struct Pend {
+  const double* partials = nullptr;  // producer's per-block partials (2 per block); null: none
+  int nblocks = 0;
+  Epi e{};
+};
+// While *g_defer_out is non-null, a 2-value finalize on a plain grid (no cluster, no
+// multi-GPU communicator) is recorded there instead of launched.
+extern Pend* g_defer_out;
+
 // w -= (*h) * v ; then reduce: RED_DOT -> <u, w>, RED_NORM -> ||w||^2
 void launch_axpy_red(const LaunchCfg& lc, long n, cplx* w, const cplx* h, const cplx* v, int red, const cplx* u,
-                     Gate g, RedScratch rs, Epi e);
+                     Gate g, RedScratch rs, Epi e, Pend in = Pend{});
 // reduce <u, w>
 void launch_dot(const LaunchCfg& lc, long n, const cplx* u, const cplx* w, Gate g, RedScratch rs, Epi e);
 // out = in * (*s) (s may be null: copy); red: RED_NORM of out ; out may be null (reduction only)
