@@ -650,9 +650,16 @@ def engine_roofline(H, L, wl, cfg, its_mean, t_krylov):
               "barrier_us_per_launch": v[10] / mhz / nl_, "transfer_us_per_launch": v[12] / mhz / nl_,
               "lincomb_us_per_launch": v[14] / mhz / nl_,
               "note": "clock64 of CTA 0 (thread 0; relaxation control on the last thread), 1965 MHz"}
+    traffic = None
+    try:  # dram__bytes_read.sum + dram__bytes_write.sum of the committed ncu --set full capture
+        with open(os.path.join(REPO, "profiles", "r02_engine_ncu.json")) as f:
+            pr = json.load(f)
+        traffic = (pr["dram_read_MB"] + pr["dram_write_MB"]) * 1e6
+    except Exception:
+        pass
     return {"kernel": f"k_cluster_engine (16-CTA cluster; inner FGMRES(2) at level {entry} "
                       f"{'x'.join(map(str, hier.shapes[entry - 1]))} + K-cycles + coarsest GMRES(10))",
-            "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+            "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
             "peak_source": src, "avg_launch_ms": avg.value, "algorithmic_bytes_per_launch": bytes_launch,
             "launches_per_outer_iteration": launches_per_it,
             "share_of_krylov_time": launches_per_it * its_mean * avg.value * 1e-3 / t_krylov,

@@ -181,6 +181,9 @@ int hadr_dist_info(int* rank, int* size, int* kind);
  * *n_dist_levels leading slab levels out of *n_levels */
 int hadr_dist_plan(int n1, int n2, int n3, int max_levels, int* bounds, int* n_dist_levels, int* n_levels);
 /* pure host helper: split n1 planes into `size` slabs with interior bounds multiples of `align` */
+/* the slab plan hadr_dist_plan would make for `size` ranks (host logic only, no device or
+ * communicator): fine slab bounds (size + 1), levels split in slabs, levels in total */
+int hadr_slab_plan(int n1, int n2, int n3, int max_levels, int size, int* bounds, int* n_dist_levels, int* n_levels);
 int hadr_slab_bounds(int n1, int size, int align, int* bounds /* size + 1 */);
 
 /* tau_derivatives (helmadr/eikonal.py:180-226) with AnalyticBase's distance factor

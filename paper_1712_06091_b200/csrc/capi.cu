@@ -690,6 +690,8 @@ int hadr_set_option(const char* name, double value) {
       }
     } else if (n == "dist_min_planes") {
       g_dist_min_planes = (int)value;
+    } else if (n == "dist_min_work") {
+      g_dist_min_work = value;
     } else if (n == "dist_levels") {
       g_dist_levels = (int)value;
     } else if (n == "ce_max_n") {
@@ -733,6 +735,15 @@ int hadr_dist_info(int* rank, int* size, int* kind) {
 int hadr_dist_plan(int n1, int n2, int n3, int max_levels, int* bounds, int* n_dist_levels, int* n_levels) {
   return guarded([&] {
     const SlabPlan p = slab_plan(n1, n2, n3, max_levels);
+    for (size_t i = 0; i < p.bounds.size(); ++i) bounds[i] = p.bounds[i];
+    *n_dist_levels = p.ndist;
+    *n_levels = p.nlev;
+  });
+}
+
+int hadr_slab_plan(int n1, int n2, int n3, int max_levels, int size, int* bounds, int* n_dist_levels, int* n_levels) {
+  return guarded([&] {
+    const SlabPlan p = slab_plan_for(n1, n2, n3, max_levels, size);
     for (size_t i = 0; i < p.bounds.size(); ++i) bounds[i] = p.bounds[i];
     *n_dist_levels = p.ndist;
     *n_levels = p.nlev;

@@ -175,6 +175,7 @@ void Comm::allreduce_or_u64(unsigned long long* v, int n, cudaStream_t s) {
 Comm* dist_comm() { return g_comm; }
 int g_dist_min_planes = 16;
 int g_dist_levels = 0;
+double g_dist_min_work = 8e6;
 
 static void install(Comm* c) {
   c->red.size = c->size;

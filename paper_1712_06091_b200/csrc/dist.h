@@ -58,6 +58,7 @@ struct Comm {
 Comm* dist_comm();  // null unless a distributed context is active
 extern int g_dist_min_planes;  // a coarse level stays distributed while every slab keeps >= this many planes
 extern int g_dist_levels;      // > 0: distribute exactly this many levels (tests / tuning)
+extern double g_dist_min_work;  // split a coarse level while points x planes >= this x R/(R-1) (cost model)
 int dist_init_nccl(int rank, int size, const char* unique_id /* 128 bytes */);
 int dist_nccl_unique_id(char* out /* 128 bytes */);
 int dist_init_host(int rank, int size, HostAllgather ag, HostSendrecv sr, HostBcast bc);

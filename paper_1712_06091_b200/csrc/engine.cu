@@ -1115,14 +1115,20 @@ static std::vector<int> level_bounds(const std::vector<int>& fine, int l, int n1
   return b;
 }
 
-SlabPlan slab_plan(int n1, int n2, int n3, int max_levels) {
-  Comm* cm = dist_comm();
-  if (!cm) throw ValueError("no distributed context (hadr_dist_init_*)");
+// Which levels to split (cost model in DESIGN.md §7): a coarse level stays
+// distributed while every slab keeps >= dist_min_planes planes and splitting it saves more
+// per reduction-separated step than the collective it adds.  A step at level l moves about
+// N_l S_l x 16 B (S_l: coefficient planes per point, nominal 54 for 3D / 15 for 2D coarse
+// Galerkin operators); splitting saves (1 - 1/R) of that at ~6.5 TB/s, an all-gather or halo
+// exchange over NVLink costs ~20 us, so split while N_l S_l >= dist_min_work R / (R - 1)
+// with dist_min_work = 8e6 (= 20 us x 6.5 TB/s / 16 B).  Config 4 (513^2 x 257): levels
+// 513^2x257, 257^2x129 and 129^2x65 split at 2-8 ranks, 65^2x33 down replicated.
+SlabPlan slab_plan_for(int n1, int n2, int n3, int max_levels, int R) {
   auto shapes = coarsenable_levels(n1, n2, n3, max_levels);
   const int nl = (int)shapes.size();
   if (nl < 2)
     throw ValueError("grid cannot support two multigrid levels ((n_d - 1) must be even with at least 3 coarse nodes)");
-  const int R = cm->size;
+  if (R < 1) throw ValueError("slab plan needs at least one rank");
   for (int nd = nl - 1; nd >= 1; --nd) {
     if (g_dist_levels > 0 && nd != std::min(g_dist_levels, nl - 1)) continue;
     std::vector<int> b = slab_bounds(n1, R, 1 << nd);
@@ -1132,10 +1138,19 @@ SlabPlan slab_plan(int n1, int n2, int n3, int max_levels) {
       const std::vector<int> bl = level_bounds(b, l, shapes[l].n1);
       const int need = l == 0 ? kHalo : std::max(kHalo, g_dist_levels > 0 ? kHalo : g_dist_min_planes);
       for (int r = 0; r < R; ++r) ok = ok && bl[r + 1] - bl[r] >= need;
+      const double pts = (double)shapes[l].n1 * shapes[l].n2 * shapes[l].n3;
+      const double planes = shapes[l].n3 > 1 ? 54.0 : 15.0;
+      if (l > 0 && g_dist_levels <= 0 && R > 1 && pts * planes < g_dist_min_work * R / (R - 1.0)) ok = false;
     }
     if (ok) return SlabPlan{b, nd, nl};
   }
   throw ValueError("grid too small for the requested number of slab ranks");
+}
+
+SlabPlan slab_plan(int n1, int n2, int n3, int max_levels) {
+  Comm* cm = dist_comm();
+  if (!cm) throw ValueError("no distributed context (hadr_dist_init_*)");
+  return slab_plan_for(n1, n2, n3, max_levels, cm->size);
 }
 
 Hier* hier_build_dist(Op* fine, const SlabPlan& plan, int coarse_steps, double coarse_tol) {

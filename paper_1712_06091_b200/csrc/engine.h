@@ -195,6 +195,7 @@ struct SlabPlan {
   int nlev = 0;
 };
 SlabPlan slab_plan(int n1, int n2, int n3, int max_levels);
+SlabPlan slab_plan_for(int n1, int n2, int n3, int max_levels, int ranks);  // host logic only
 // hierarchy over a slab fine operator (every rank calls it collectively)
 Hier* hier_build_dist(Op* fine_slab, const SlabPlan& plan, int coarse_steps, double coarse_tol);
 // slab assembly: rows of this rank's slab (+1 halo row each side) from global host/device fields

@@ -155,3 +155,17 @@ def set_policy(min_planes: int | None = None, levels: int | None = None) -> None
         _lib.set_option("dist_min_planes", min_planes)
     if levels is not None:
         _lib.set_option("dist_levels", levels)
+
+
+def plan_for(shape, levels: int = 5, size: int = 1):
+    """The slab plan ``plan`` would make with ``size`` ranks (host logic, no device):
+    (bounds, n_dist_levels, n_levels).  Coarse levels whose split saves less per step than
+    a collective costs (points x planes < 8e6 x R/(R-1)) or that would keep fewer than
+    dist_min_planes (16) planes per slab are agglomerated (replicated)."""
+    n1, n2 = int(shape[0]), int(shape[1])
+    n3 = int(shape[2]) if len(shape) > 2 else 1
+    b = np.zeros(size + 1, dtype=np.int32)
+    nd, nl = C.c_int(), C.c_int()
+    _lib.check(_lib.load().hadr_slab_plan(n1, n2, n3, int(levels), int(size), b.ctypes.data, C.byref(nd),
+                                          C.byref(nl)))
+    return [int(x) for x in b], nd.value, nl.value

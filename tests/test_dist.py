@@ -166,3 +166,22 @@ def test_bench_slab_watchdog_prints_headline():
         raise RuntimeError("nccl")
 
     assert "nccl" in bench.guarded_slab_run(boom, {}, 2, 0, 60.0)["error"]
+
+
+def test_slab_plan_agglomerates_small_levels():
+    """SURVEY.md §8(e) with the cost model of DESIGN.md §7: split the levels whose per-step
+    bytes saved exceed a collective's cost, agglomerate (replicate) the rest — config 4
+    (513^2 x 257): 513^2x257, 257^2x129 and 129^2x65 split, 65^2x33 down replicated at 2, 4
+    and 8 ranks; config 5 (1025^2 x 513): four levels split at 8 ranks."""
+    sys.path.insert(0, REPO)
+    from paper_1712_06091_b200 import distributed as D
+
+    for R in (2, 4, 8):
+        b, nd, nl = D.plan_for((513, 513, 257), 5, R)
+        assert nl == 5 and nd == 3, (R, nd)
+        assert b[0] == 0 and b[-1] == 513 and len(b) == R + 1
+        assert all((x % 8) == 0 for x in b[:-1])  # slabs nest on the 3 split levels
+    b, nd, nl = D.plan_for((1025, 1025, 513), 5, 8)
+    assert (nd, nl) == (4, 5)
+    b, nd, nl = D.plan_for((65, 65, 33), 5, 2)  # coarse levels too small to pay for a split
+    assert nd == 1
