@@ -623,6 +623,13 @@ int hadr_set_option(const char* name, double value) {
     std::string n(name ? name : "");
     if (n == "ce_profile") {
       g_ce_prof_on = value != 0.0;
+    } else if (n == "ce_smem_coef") {
+      g_ce_smem_coef = value != 0.0;
+      for (;;) {
+        Hier* h = hier_pool_pop();
+        if (!h) break;
+        delete h;
+      }
     } else if (n == "defer_mgs") {
       g_defer_mgs = value != 0.0;
       for (;;) {

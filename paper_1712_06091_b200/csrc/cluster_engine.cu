@@ -320,9 +320,11 @@ extern __shared__ cplx ce_tile[];
 // NO coefficient loads of a point are issued together.  Same accumulation order as
 // csr_matvec (ascending offsets, no FMA): bit-identical to the generic loop.
 // out(k, acc) consumes point k.
-template <int NO, bool C32, class F>
+// cs != null: the coefficients come from the CTA's shared-memory copy of its own rows
+// (plane o at cs + o * css, point k at k - own0).
+template <int NO, bool C32, bool SMC = false, class F>
 __device__ __forceinline__ void ce_rows_std2d(const StencilDev& A, const cplx* tile, int t0, long own0, long own1,
-                                              long tw, long nwk, F&& out) {
+                                              long tw, long nwk, F&& out, const cplx* cs = nullptr, long css = 0) {
   const int n1 = A.n1, n2 = A.n2;
   const long N = (long)n1 * n2;
   const cplx* __restrict__ coef = A.coef;
@@ -332,7 +334,9 @@ __device__ __forceinline__ void ce_rows_std2d(const StencilDev& A, const cplx* t
     cplx cv[NO];
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
-      if constexpr (C32) {
+      if constexpr (SMC) {
+        cv[o] = cs[(long)o * css + (k - own0)];
+      } else if constexpr (C32) {
         const float2 f = __ldg(coef32 + (long)o * N + k);
         cv[o] = make_double2((double)f.x, (double)f.y);
       } else {
@@ -613,20 +617,24 @@ __device__ __forceinline__ cplx ce_remote_c(const cplx* p, unsigned rank) {
 template <int NO, bool C32>
 __device__ __forceinline__ void sm_stencil_rows(CEC& c, const StencilDev& A, const cplx* tile, int r0, int r1,
                                                 int t0, cplx* w, const cplx* v0, double (&red)[2], long tw,
-                                                long nwk) {
+                                                long nwk, const cplx* cs = nullptr, long css = 0) {
   const int n1 = A.n1, n2 = A.n2, n3 = A.n3, nofs = A.nofs;
   const int n23 = n2 * n3;
   const long N = (long)n1 * n23;
   const long own0 = (long)r0 * n23, own1 = (long)r1 * n23;
   if constexpr (NO == 5 || NO == 9 || NO == 21) {
     if (A.std2d == NO) {
-      ce_rows_std2d<NO, C32>(A, tile, t0, own0, own1, tw, nwk, [&](long k, cplx acc) {
+      auto epi = [&](long k, cplx acc) {
         const long p = k - own0;
         w[p] = acc;
         const cplx u = v0[p];
         red[0] += u.x * acc.x + u.y * acc.y;
         red[1] += u.x * acc.y - u.y * acc.x;
-      });
+      };
+      if (!C32 && cs)
+        ce_rows_std2d<NO, C32, true>(A, tile, t0, own0, own1, tw, nwk, epi, cs, css);
+      else
+        ce_rows_std2d<NO, C32, false>(A, tile, t0, own0, own1, tw, nwk, epi);
       return;
     }
   }
@@ -677,6 +685,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
   cplx* tile = ce_tile;                        // (rows + 4) * n23
   cplx* Vb = ce_tile + (long)(rows + 4) * n23;  // V[i] = Vb + i * rs, i <= s
   cplx* wb = Vb + (long)(s + 1) * rs;           // w[0], w[1]
+  cplx* cs = L.smc ? wb + 2 * rs : nullptr;      // the CTA's rows of the coefficient planes (L.smc)
   // the control warp (the CTA's last) takes no share of the vector work: its last thread
   // runs the Givens / least-squares update of each step while the other warps already
   // stage and apply the next step's stencil, so the update is off the critical path
@@ -707,6 +716,11 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       wb[rs + p] = y;  // w[1] = r : the "previous" buffer of step 0
       nn += y.x * y.x + y.y * y.y;
     }
+    if (cs) {  // stage the own rows of the nofs coefficient planes once for the s stencils
+      const long N = (long)n1 * n23;
+      for (int o = 0; o < L.A.nofs; ++o)
+        for (long p = tw; p < np; p += nwk) cs[(long)o * rs + p] = ldk(L.A.coef, (long)o * N + own0 + p);
+    }  // (read after the staging barrier of step 0)
     if (!x) v[0] = nn;
     ce_allreduce<1>(c, v);
     if (ctl) relax_beta(R, v[0]);
@@ -761,9 +775,9 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
           sm_stencil_rows<0, true>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk);
       } else {
         switch (L.A.nofs) {
-          case 5: sm_stencil_rows<5, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk); break;
-          case 9: sm_stencil_rows<9, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk); break;
-          case 21: sm_stencil_rows<21, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk); break;
+          case 5: sm_stencil_rows<5, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk, cs, rs); break;
+          case 9: sm_stencil_rows<9, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk, cs, rs); break;
+          case 21: sm_stencil_rows<21, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk, cs, rs); break;
           default: sm_stencil_rows<0, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk); break;
         }
       }

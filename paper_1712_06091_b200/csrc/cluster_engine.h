@@ -18,6 +18,7 @@ struct CELevel {
   long N;
   int s;    // relaxation length
   int smr;  // 1: the relaxation runs out of shared memory (ce_relax_sm; see ce_relax_sm_bytes)
+  int smc;  // 1: ... and stages the CTA's rows of the coefficient planes there too (ce_relax_smc_bytes)
   cplx* r;
   cplx* V[RMAX + 1];
   cplx* w[2];
@@ -49,6 +50,11 @@ inline size_t ce_tile_bytes(int n1, int n2, int ctas) {
 inline size_t ce_relax_sm_bytes(int n1, long n23, int s, int ctas) {
   const long rows = (n1 + ctas - 1) / ctas;
   return (size_t)(rows * (s + 3) + rows + 4) * n23 * sizeof(cplx);
+}
+// ... plus the CTA's rows of the nofs coefficient planes (complex128)
+inline size_t ce_relax_smc_bytes(int n1, long n23, int s, int nofs, int ctas) {
+  const long rows = (n1 + ctas - 1) / ctas;
+  return ce_relax_sm_bytes(n1, n23, s, ctas) + (size_t)rows * n23 * nofs * sizeof(cplx);
 }
 constexpr size_t CE_SMEM_BUDGET = 190 * 1024;  // dynamic shared memory the engine may request
 

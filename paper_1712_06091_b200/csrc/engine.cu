@@ -886,12 +886,22 @@ static bool level_smr(const Level& L) {
   return g_ce_smem_relax && !L.dist &&
          ce_relax_sm_bytes(L.n1, (long)L.n2 * L.n3, L.s, CE_CTAS) <= CE_SMEM_BUDGET;
 }
+int g_ce_smem_coef = 1;  // option "ce_smem_coef": stage a fitting level's coefficient rows in shared memory
+// ... and its coefficient rows fit beside it (the standard 2D complex128 stencils, whose
+// fast loop reads them: the coarsest 65^2 level of config 2 — 20 stencils per engine launch)
+static bool level_smc(const Level& L) {
+  const StencilDev A = L.A->dev();
+  return g_ce_smem_coef && level_smr(L) && A.std2d && !A.coef32 &&
+         ce_relax_smc_bytes(L.n1, (long)L.n2 * L.n3, L.s, A.nofs, CE_CTAS) <= CE_SMEM_BUDGET;
+}
 
 size_t Hier::ce_tile(int li) const {
   size_t m = 0;  // the engine touches levels li .. coarsest
   for (int i = li; i < (int)lv.size(); ++i) {
     m = std::max(m, ce_tile_bytes(lv[i].n1, lv[i].n2 * lv[i].n3, CE_CTAS));
     if (lv[i].smr) m = std::max(m, ce_relax_sm_bytes(lv[i].n1, (long)lv[i].n2 * lv[i].n3, lv[i].s, CE_CTAS));
+    if (lv[i].smc)
+      m = std::max(m, ce_relax_smc_bytes(lv[i].n1, (long)lv[i].n2 * lv[i].n3, lv[i].s, lv[i].A->nofs, CE_CTAS));
   }
   return m;
 }
@@ -931,6 +941,7 @@ void Hier::alloc_workspace() {
     if (L.s > RMAX) throw ValueError("relaxation length exceeds the device limit (16)");
     L.s = (int)std::min<long>(L.s, L.A->N);
     L.smr = level_smr(L);  // the engine descriptor and ce_tile() agree for the hierarchy's lifetime
+    L.smc = level_smc(L);
     for (int j = 0; j <= L.s; ++j) L.V[j] = valloc(L);
     L.w[0] = valloc(L);
     L.w[1] = valloc(L);
@@ -970,6 +981,7 @@ void Hier::alloc_workspace() {
       d.N = L.N;
       d.s = L.s;
       d.smr = L.smr ? 1 : 0;
+      d.smc = L.smc ? 1 : 0;
       d.r = L.r;
       for (int j = 0; j <= RMAX; ++j) d.V[j] = L.V[j];
       d.w[0] = L.w[0];
@@ -995,7 +1007,7 @@ Hier* hier_pool_pop() {
 }
 
 std::vector<long long> hier_option_signature() {
-  return {g_ce_smem_relax, g_ce_max_n, g_cl_max_n, g_stencil_tile, g_relax_split, g_class_compress, g_pair_compress,
+  return {g_ce_smem_relax, g_ce_smem_coef, g_ce_max_n, g_cl_max_n, g_stencil_tile, g_relax_split, g_class_compress, g_pair_compress,
           g_pdl, g_ce_prof_on, g_kcycle_c64, g_ce_cgs2, g_defer_mgs};
 }
 

@@ -129,6 +129,7 @@ struct Level {
   const cplx* dinv = nullptr;
   int s = 0;                 // relaxation length at this level
   bool smr = false;          // its engine relaxation runs out of shared memory (fixed at allocation)
+  bool smc = false;          // ... with its coefficient rows staged there too
   // K-cycle workspace
   cplx* r = nullptr;
   cplx* V[RMAX + 1] = {nullptr};
@@ -180,6 +181,7 @@ extern long g_ce_max_n;  // levels with N <= this run inside the cluster engine 
 extern int g_kcycle_c64; // build hierarchies with complex64 operator storage (mixed-precision K-cycle)
 extern int g_ce_smem_relax;  // engine relaxations out of shared memory where they fit
 extern int g_pair_compress;  // pair-compress fine operators (outer A, hierarchy level 0)
+extern int g_ce_smem_coef;   // option "ce_smem_coef"
 extern int g_defer_mgs;     // MGS dot finalizes folded into the next axpy (option "defer_mgs")
 extern long g_relax_split;   // 3D levels with at least this many points form D^-1 (s w) once per point
 extern int g_class_compress;  // class-compress coarse graph-path levels: 0 off, 1 3D, 2 2D and 3D
