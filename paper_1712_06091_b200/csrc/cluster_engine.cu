@@ -1,5 +1,5 @@
 // Cluster engine: the coarse part of the K-cycle as ONE persistent kernel on
-// one thread-block cluster (16 CTAs x 512 threads, non-portable cluster size).
+// one thread-block cluster (16 CTAs x 384 threads, non-portable cluster size).
 //
 // Why: on the coarse grids (<= ~32k points) every Krylov/multigrid operation
 // is latency-bound.  As separate kernels each op costs ~5 us (launch + a chain

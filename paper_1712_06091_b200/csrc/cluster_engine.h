@@ -6,7 +6,7 @@ namespace hadr {
 
 constexpr int CE_MAXLEV = 6;      // levels a single engine launch may span
 #ifndef HADR_CE_THREADS
-#define HADR_CE_THREADS 512
+#define HADR_CE_THREADS 384  // 11 worker warps + the control warp; 168 registers per thread (512: 128, spills)
 #endif
 constexpr int CE_THREADS = HADR_CE_THREADS;  // threads per CTA
 constexpr int CE_CTAS = 16;       // CTAs in the (single, non-portable) cluster
