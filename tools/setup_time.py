@@ -12,8 +12,13 @@ def main():
     ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--n", type=int, default=513)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--opt", action="append", default=[], help="name=value runtime option")
     a = ap.parse_args()
-    from paper_1712_06091_b200 import drivers, workloads
+    from paper_1712_06091_b200 import _lib, drivers, workloads
+
+    for kv in a.opt:
+        k, v = kv.split("=")
+        _lib.set_option(k, float(v))
 
     wl = workloads.by_name(a.workload, a.n)
     cfg = drivers.StrategyConfig(strategy="adr_upwind_blend", tol=1e-6, max_iter=1)
