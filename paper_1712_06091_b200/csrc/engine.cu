@@ -960,6 +960,8 @@ void Hier::alloc_workspace() {
       L.fr = valloc(L);
       L.fctl = dalloc<FgCtl>(1);
       HADR_CUDA(cudaMemset(L.fctl, 0, sizeof(FgCtl)));
+      // the inner FGMRES(2) tolerance is fixed per hierarchy: set once (fg_init resets the rest)
+      HADR_CUDA(cudaMemcpy(&L.fctl->tol, &coarse_tol, sizeof(double), cudaMemcpyHostToDevice));
     }
   }
   kact = dalloc<int>(nl + 1);
@@ -1220,7 +1222,6 @@ void Hier::emit_relax(Level& L, const cplx* b, const cplx* x, cplx* xo, int s, G
   Ctx& c = Ctx::get();
   const LaunchCfg& lc0 = lcf(L);
   const StencilDev A = L.A->dev();
-  launch_relax_init(c.stream, L.rctl, s, g);
   const cplx* r = b;
   if (x) {
     xchg(L, x);
@@ -1231,11 +1232,11 @@ void Hier::emit_relax(Level& L, const cplx* b, const cplx* x, cplx* xo, int s, G
     a.y = L.w[1];
     a.gate = g;
     a.rs = c.rs;
-    a.epi = epi(EPI_RELAX_BETA, L.rctl);
+    a.epi = epi(EPI_RELAX_BETA, L.rctl, 0, s);  // the epilogue also initialises the control block
     launch_stencil(lc0, IN_PLAIN, OUT_RESID, RED_NORM, a);
     r = L.w[1];
   } else {
-    launch_scale(lc0, L.N, b, nullptr, nullptr, RED_NORM, g, c.rs, epi(EPI_RELAX_BETA, L.rctl));
+    launch_scale(lc0, L.N, b, nullptr, nullptr, RED_NORM, g, c.rs, epi(EPI_RELAX_BETA, L.rctl, 0, s));
   }
   RelaxCtl* rc = L.rctl;
   for (int j = 0; j < s; ++j) {
@@ -1367,7 +1368,6 @@ void Hier::emit_inner(int ci, Gate g, bool count) {
   const LaunchCfg& lcc = lcf(C);
   int* act = kact + ci;
   const unsigned bA = 1u << FG_A, bC = 1u << FG_CONT, bB = 1u << FG_BRK, bR = 1u << FG_RST;
-  launch_fg_setup(c.stream, f, coarse_tol, g);
   launch_scale(lcc, n, C.fb, nullptr, nullptr, RED_NORM, g, c.rs, epi(EPI_FG_INIT, f));
   const Gate gA = gate_var(g.active, &f->path, bA);
   launch_scale(lcc, n, C.fb, &f->inv_r, C.fV0, 0, gA, c.rs, epi_none());

@@ -21,9 +21,14 @@ __device__ __noinline__ void run_epi(const Epi& e, const double* t, int nv) {
     case EPI_STORE:
       for (int q = 0; q < nv; ++q) e.out[q] = t[q];
       break;
-    case EPI_RELAX_BETA:
-      relax_beta((RelaxCtl*)e.ctl, t[0]);
+    case EPI_RELAX_BETA: {  // the relaxation's start: steps (e.j), k, cur, then beta (helmadr/krylov.py:95-97)
+      RelaxCtl* c = (RelaxCtl*)e.ctl;
+      c->steps = e.j;
+      c->k = 0;
+      c->cur = kStopped;
+      relax_beta(c, t[0]);
       break;
+    }
     case EPI_RELAX_H:
       ((RelaxCtl*)e.ctl)->H[e.i * RMAX + e.j] = mk(t[0], t[1]);
       break;

@@ -119,3 +119,37 @@ def test_krylov_flags():
     assert _flags(KrylovConfig()) == 0
     assert _flags(KrylovConfig(flexible=False)) == 1
     assert _flags(KrylovConfig(collect_diagnostics=True)) == 2
+
+
+def test_bench_op_stream_model_reproduces_survey_b_op():
+    """bench.py's algorithmic-bytes model (the reference's op stream, SURVEY.md §8(d)
+    counting) reproduces SURVEY's B_op for config 2 (7,726 B/dof/iteration) within 1%, and
+    gives the cluster engine's per-launch bytes (inner FGMRES(2) at 129^2 with everything
+    below) that the bench line's roofline uses."""
+    import sys
+
+    sys.path.insert(0, REPO)
+    import bench
+
+    Ns = [1025 ** 2, 513 ** 2, 257 ** 2, 129 ** 2, 65 ** 2]
+    S = [7.0, 14.96, 14.91, 14.82, 14.64]
+    lev, inner = bench.op_stream_model(Ns, S, 7.0)
+    assert abs(sum(lev) / Ns[0] - 7726.0) / 7726.0 < 0.01
+    # 4 engine launches per outer iteration carry levels 4-5's bytes
+    assert abs(4 * inner(3) - (lev[3] + lev[4])) / (lev[3] + lev[4]) < 0.02
+
+
+def test_bench_arms_share_the_config_dict():
+    """Both bench arms print the same `config` (the driver compares them)."""
+    import argparse
+    import sys
+
+    sys.path.insert(0, REPO)
+    import bench
+    from paper_1712_06091_b200 import workloads
+
+    wl = workloads.cfg2(65)
+    a = argparse.Namespace(tol=1e-6)
+    c1, c2 = bench.bench_config(wl, a, 1), bench.bench_config(wl, a, 1)
+    assert c1 == c2 and c1["grid"] == [65, 65] and c1["tol"] == 1e-6
+    assert "outer_iterations" not in c1 and "t_setup_ms" not in c1
