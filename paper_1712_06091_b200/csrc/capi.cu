@@ -630,6 +630,15 @@ int hadr_set_option(const char* name, double value) {
         if (!h) break;
         delete h;
       }
+    } else if (n == "mid_ppt" || n == "mid_max_n" || n == "mid_min_n") {
+      if (n == "mid_ppt") g_mid_ppt = (int)value;
+      if (n == "mid_min_n") g_mid_min_n = (long)value;
+      if (n == "mid_max_n") g_mid_max_n = (long)value;
+      for (;;) {
+        Hier* h = hier_pool_pop();
+        if (!h) break;
+        delete h;
+      }
     } else if (n == "defer_mgs") {
       g_defer_mgs = value != 0.0;
       for (;;) {

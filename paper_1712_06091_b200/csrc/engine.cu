@@ -911,7 +911,7 @@ bool Hier::use_ce(int li) const {
          (int)lv.size() <= CE_MAXLEV && ce_tile(li) <= 200 * 1024;
 }
 
-const LaunchCfg& Hier::lcf(const Level& L) const { return L.dist ? dlc : Ctx::get().lc; }
+const LaunchCfg& Hier::lcf(const Level& L) const { return L.dist ? dlc : L.lc; }
 
 void Hier::xchg(const Level& L, const cplx* v) const {
   if (L.dist) dist_comm()->halo((void*)v, (size_t)L.n2 * L.n3 * sizeof(cplx), L.nown, kHalo, Ctx::get().stream);
@@ -941,6 +941,8 @@ void Hier::alloc_workspace() {
     if (L.s > RMAX) throw ValueError("relaxation length exceeds the device limit (16)");
     L.s = (int)std::min<long>(L.s, L.A->N);
     L.smr = level_smr(L);  // the engine descriptor and ce_tile() agree for the hierarchy's lifetime
+    L.lc = Ctx::get().lc;
+    if (L.n3 == 1 && L.N > g_mid_min_n && L.N <= g_mid_max_n) L.lc.ppt = g_mid_ppt;
     L.smc = level_smc(L);
     for (int j = 0; j <= L.s; ++j) L.V[j] = valloc(L);
     L.w[0] = valloc(L);
@@ -1010,7 +1012,7 @@ Hier* hier_pool_pop() {
 
 std::vector<long long> hier_option_signature() {
   return {g_ce_smem_relax, g_ce_smem_coef, g_ce_max_n, g_cl_max_n, g_stencil_tile, g_relax_split, g_class_compress, g_pair_compress,
-          g_pdl, g_ce_prof_on, g_kcycle_c64, g_ce_cgs2, g_defer_mgs};
+          g_pdl, g_ce_prof_on, g_kcycle_c64, g_ce_cgs2, g_defer_mgs, g_mid_ppt, g_mid_min_n, g_mid_max_n};
 }
 
 void hier_release(Hier* h) {

@@ -129,6 +129,7 @@ struct Level {
   const cplx* dinv = nullptr;
   int s = 0;                 // relaxation length at this level
   bool smr = false;          // its engine relaxation runs out of shared memory (fixed at allocation)
+  LaunchCfg lc{};            // single-GPU launch config of the level's kernels (points per thread)
   bool smc = false;          // ... with its coefficient rows staged there too
   // K-cycle workspace
   cplx* r = nullptr;

@@ -151,6 +151,18 @@ struct Geo {
   int cluster;  // 0: plain grid
 };
 
+// Points per thread of the grid-stride vector / stencil kernels (LaunchCfg::ppt, set per
+// hierarchy level): 2 on 2D levels of 70k-300k points (config 2's 513^2: -3% per solve;
+// 257^2, the fine level and 3D levels lose or break even, 3-8 points per thread lose).
+int g_mid_ppt = 2;          // option "mid_ppt"
+long g_mid_min_n = 70000;   // option "mid_min_n"
+long g_mid_max_n = 300000;  // option "mid_max_n"
+
+static long blocks_of(const LaunchCfg& lc, long n) {
+  const long ppt = lc.ppt > 1 ? lc.ppt : 1;
+  return (n + kThreads * ppt - 1) / (kThreads * ppt);
+}
+
 static Geo geo_for(const LaunchCfg& lc, long n) {
   long b = (n + kThreads - 1) / kThreads;
   if (n <= g_cl_max_n && !lc.dist) {  // distributed sums finish through the communicator
@@ -158,12 +170,13 @@ static Geo geo_for(const LaunchCfg& lc, long n) {
     if (b < 1) b = 1;
     return Geo{(int)b, (int)b};
   }
+  b = blocks_of(lc, n);
   if (b > lc.max_blocks) b = lc.max_blocks;
   return Geo{(int)b, 0};
 }
 
 static int blocks_for(const LaunchCfg& lc, long n) {
-  long b = (n + kThreads - 1) / kThreads;
+  long b = blocks_of(lc, n);
   if (b > lc.max_blocks) b = lc.max_blocks;
   if (b < 1) b = 1;
   return (int)b;

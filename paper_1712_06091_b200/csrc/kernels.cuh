@@ -5,7 +5,10 @@
 namespace hadr {
 
 extern long long g_launch_count;
-extern int g_pdl;  // programmatic dependent launch of the solve-phase kernels
+extern int g_pdl;
+extern int g_mid_ppt;    // points per thread of a 2D level's kernels with mid_min_n < N <= mid_max_n
+extern long g_mid_max_n;
+extern long g_mid_min_n;  // programmatic dependent launch of the solve-phase kernels
 extern int g_stencil_tile;
 extern long g_cl_max_n;  // single-cluster reductions (in-kernel epilogue) up to this many points  // shared-memory tiled stencil kernel on the graph path
 
@@ -145,6 +148,7 @@ struct LaunchCfg {
   cudaStream_t stream;
   int max_blocks;                  // grid cap (multiple of the SM count)
   const DistRed* dist = nullptr;   // non-null: reductions are completed across the slab ranks
+  int ppt = 1;                     // points per thread of the level's grid-stride kernels
 };
 
 void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const StencilArgs& a);
