@@ -1514,6 +1514,7 @@ void gmres_relax(Op& A, const cplx* b, const cplx* x, cplx* xo, int steps) {
   L.N = A.N;
   L.dinv = A.inv_diag();
   L.s = (int)std::min<long>(std::max(steps, 0), A.N);
+  L.lc = c.lc;
   for (int j = 0; j <= L.s; ++j) L.V[j] = dalloc<cplx>(L.N);
   L.w[0] = dalloc<cplx>(L.N);
   L.w[1] = dalloc<cplx>(L.N);
