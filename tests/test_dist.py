@@ -66,6 +66,20 @@ def test_reference_arm_under_torchrun():
     assert rec["e2e"]["h2d_bytes_per_step"] == 0
 
 
+def test_bench_gpus_flag_self_launches():
+    """`python bench.py --gpus 2` without torchrun re-launches itself as 2 ranks (one JSON
+    line from rank 0 with n_gpus 2); a WORLD_SIZE that contradicts --gpus is refused."""
+    cmd = [sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--size", "33", "--steps", "1",
+           "--warmup", "0", "--ref-its", "2"]
+    out = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1 and json.loads(lines[0])["n_gpus"] == 2
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    bad = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=120, env=env)
+    assert bad.returncode != 0 and "WORLD_SIZE" in (bad.stderr + bad.stdout)
+
+
 # ---------------------------------------------------------------------------
 # multi-GPU slab decomposition: host logic (no device)
 # ---------------------------------------------------------------------------

@@ -174,16 +174,38 @@ def test_galerkin_device(hadr, case, request):
         assert err <= 1e-12 * abs(ref).max(), (l, err)
 
 
-@pytest.fixture(params=["cluster", "cluster_gmem", "graph"])
+@pytest.fixture(params=["cluster", "cluster_mgs", "cluster_gmem", "graph"])
 def engine(request, hadr):
     """Run a test with the coarse levels in the single-cluster engine (default: relaxations
-    out of shared memory where they fit), in the engine with global-memory relaxations,
+    out of shared memory where they fit, CGS2 from their 5th step), in the engine with the
+    reference's MGS throughout (ce_cgs2 = 0), in the engine with global-memory relaxations,
     and with every operation as its own kernel (ce_max_n = 0)."""
     hadr._lib.set_option("ce_max_n", 0 if request.param == "graph" else 32768)
     hadr._lib.set_option("ce_smem_relax", 0 if request.param == "cluster_gmem" else 1)
+    hadr._lib.set_option("ce_cgs2", 0 if request.param == "cluster_mgs" else 1)
     yield request.param
     hadr._lib.set_option("ce_max_n", 32768)
     hadr._lib.set_option("ce_smem_relax", 1)
+    hadr._lib.set_option("ce_cgs2", 1)
+
+
+def test_engine_smem_coefficients_identical(hadr, g65):
+    """The coarsest relaxation reading its coefficient rows from shared memory (ce_smem_coef)
+    computes exactly what it computes from global memory."""
+    n = int(g65["n_levels"])
+    shapes = [tuple(s) for s in g65["shapes"]]
+    ops = [csr_from(g65, f"lev{l}") for l in range(n)]
+    b = g65["rnd_b"]
+    out = {}
+    try:
+        for on in (0, 1):
+            hadr._lib.set_option("ce_smem_coef", on)
+            H = hadr.hierarchy_from_ops(ops, shapes=shapes)
+            out[on] = hadr.make_kcycle_preconditioner(H)(b)
+    finally:
+        hadr._lib.set_option("ce_smem_coef", 1)
+    assert np.array_equal(out[0], out[1])
+    assert rel(out[1], g65["kcycle"]) <= 1e-12
 
 
 @pytest.mark.parametrize("case", ["g33", "g65"])
