@@ -271,8 +271,9 @@ __device__ void ce_allreduce_cta(CEC& c, int nv) {
 // ---------------------------------------------------------------------------
 // vector operations (same element formulas as kernels.cu)
 // ---------------------------------------------------------------------------
-// Stencil on a row-slab partition: CTA r owns rows [r0, r1) of the level grid.
-// The (transformed) input rows [r0-2, r1+2) are staged once in shared memory,
+// Stencil on a point partition: CTA r owns points [r ppc, (r+1) ppc) of the level grid
+// (ce_ppc).  The (transformed) input points within StencilDev::halo of them (the largest
+// linear displacement of the offsets) are staged once in shared memory,
 // so every neighbour is an LDS instead of an L2 round trip; D^-1 and the scale
 // are applied once per point (same values as applying them per neighbour).
 // Class-compressed row (StencilDev::ccode, kernels.cu stencil_cc; 3D engine levels): the
@@ -320,10 +321,10 @@ extern __shared__ cplx ce_tile[];
 // NO coefficient loads of a point are issued together.  Same accumulation order as
 // csr_matvec (ascending offsets, no FMA): bit-identical to the generic loop.
 // out(k, acc) consumes point k.
-// cs != null: the coefficients come from the CTA's shared-memory copy of its own rows
+// cs != null: the coefficients come from the CTA's shared-memory copy of its own points
 // (plane o at cs + o * css, point k at k - own0).
 template <int NO, bool C32, bool SMC = false, class F>
-__device__ __forceinline__ void ce_rows_std2d(const StencilDev& A, const cplx* tile, int t0, long own0, long own1,
+__device__ __forceinline__ void ce_rows_std2d(const StencilDev& A, const cplx* tile, long tb, long own0, long own1,
                                               long tw, long nwk, F&& out, const cplx* cs = nullptr, long css = 0) {
   const int n1 = A.n1, n2 = A.n2;
   const long N = (long)n1 * n2;
@@ -348,7 +349,7 @@ __device__ __forceinline__ void ce_rows_std2d(const StencilDev& A, const cplx* t
     for (int o = 0; o < NO; ++o) {
       const int j1 = i1 + Std2D::d1<NO>(o), j2 = i2 + Std2D::d2<NO>(o);
       const bool ok = j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2;
-      const cplx v = tile[ok ? (long)(j1 - t0) * n2 + j2 : 0];
+      const cplx v = tile[ok ? (long)j1 * n2 + j2 - tb : 0];
       const cplx t = cadd(acc, cmul_sp(cv[o], v));
       acc = ok ? t : acc;
     }
@@ -363,10 +364,9 @@ __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double
   const int n1 = A.n1, n2 = A.n2, n3 = A.n3, nofs = A.nofs;
   const int n23 = n2 * n3;
   const long N = (long)n1 * n23;
-  const int R = (n1 + (int)ce_nctas() - 1) / (int)ce_nctas();
-  const int r0 = min(n1, (int)ce_rank() * R), r1 = min(n1, r0 + R);
-  const int t0 = max(0, r0 - 2), t1 = min(n1, r1 + 2);
-  const long base = (long)t0 * n23, tn = (long)(t1 - t0) * n23;
+  const long ppc = (N + ce_nctas() - 1) / ce_nctas();
+  const long own0 = min(N, (long)ce_rank() * ppc), own1 = min(N, own0 + ppc);
+  const long base = max(0L, own0 - A.halo), tn = own1 > own0 ? min(N, own1 + A.halo) - base : 0;
   for (long p = threadIdx.x; p < tn; p += blockDim.x) {
     cplx v = ldm(x, base + p);
     if (INM & IN_SCALE) v = cscale(v, s);
@@ -374,10 +374,9 @@ __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double
     ce_tile[p] = v;
   }
   __syncthreads();
-  const long own1 = (long)r1 * n23;
   if constexpr (NO == 5 || NO == 9 || NO == 21) {
     if (A.std2d == NO) {
-      ce_rows_std2d<NO, C32>(A, ce_tile, t0, (long)r0 * n23, own1, threadIdx.x, blockDim.x, [&](long k, cplx acc) {
+      ce_rows_std2d<NO, C32>(A, ce_tile, base, own0, own1, threadIdx.x, blockDim.x, [&](long k, cplx acc) {
         cplx vc = mk(0.0, 0.0);
         if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) {
           vc = ldm(x, k);
@@ -398,7 +397,7 @@ __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double
       return;
     }
   }
-  for (long k = (long)r0 * n23 + threadIdx.x; k < own1; k += blockDim.x) {
+  for (long k = own0 + threadIdx.x; k < own1; k += blockDim.x) {
     const int i1 = (int)(k / n23);
     const int rem = (int)(k - (long)i1 * n23);
     const int i2 = rem / n3, i3 = rem - (rem / n3) * n3;
@@ -424,7 +423,7 @@ __device__ void ce_stencil_no(CEC& c, const StencilDev& A, const cplx* x, double
         const int oo = o < nofs ? o : 0;
         const int j1 = i1 + A.d1[oo], j2 = i2 + A.d2[oo], j3 = i3 + A.d3[oo];
         const bool ok = o < nofs && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2 && j3 >= 0 && j3 < n3;
-        const cplx v = ce_tile[ok ? ((long)(j1 - t0) * n2 + j2) * n3 + j3 : 0];
+        const cplx v = ce_tile[ok ? ((long)j1 * n2 + j2) * n3 + j3 - base : 0];
         const cplx t = cadd(acc, cmul_sp(cv[q], v));
         acc = ok ? t : acc;
       }
@@ -602,8 +601,8 @@ __device__ __noinline__ void ce_relax(CEC& c, const CELevel& L, const cplx* b, c
 
 // ---------------------------------------------------------------------------
 // The same relaxation with every vector of it in shared memory: CTA r keeps its
-// own rows of the basis V[0..s] and of the Arnoldi vector w (double-buffered);
-// the stencil input tile takes its halo rows from the neighbouring CTAs' w over
+// own points of the basis V[0..s] and of the Arnoldi vector w (double-buffered);
+// the stencil input tile takes its halo points from the neighbouring CTAs' w over
 // DSMEM.  Only the right-hand side, the starting guess and the result touch
 // global memory.  Element formulas are those of ce_relax (the reductions sum in
 // a different order: rounding-level differences only).
@@ -615,13 +614,12 @@ __device__ __forceinline__ cplx ce_remote_c(const cplx* p, unsigned rank) {
 }
 
 template <int NO, bool C32>
-__device__ __forceinline__ void sm_stencil_rows(CEC& c, const StencilDev& A, const cplx* tile, int r0, int r1,
-                                                int t0, cplx* w, const cplx* v0, double (&red)[2], long tw,
+__device__ __forceinline__ void sm_stencil_rows(CEC& c, const StencilDev& A, const cplx* tile, long own0, long own1,
+                                                long tb, cplx* w, const cplx* v0, double (&red)[2], long tw,
                                                 long nwk, const cplx* cs = nullptr, long css = 0) {
   const int n1 = A.n1, n2 = A.n2, n3 = A.n3, nofs = A.nofs;
   const int n23 = n2 * n3;
   const long N = (long)n1 * n23;
-  const long own0 = (long)r0 * n23, own1 = (long)r1 * n23;
   if constexpr (NO == 5 || NO == 9 || NO == 21) {
     if (A.std2d == NO) {
       auto epi = [&](long k, cplx acc) {
@@ -632,9 +630,9 @@ __device__ __forceinline__ void sm_stencil_rows(CEC& c, const StencilDev& A, con
         red[1] += u.x * acc.y - u.y * acc.x;
       };
       if (!C32 && cs)
-        ce_rows_std2d<NO, C32, true>(A, tile, t0, own0, own1, tw, nwk, epi, cs, css);
+        ce_rows_std2d<NO, C32, true>(A, tile, tb, own0, own1, tw, nwk, epi, cs, css);
       else
-        ce_rows_std2d<NO, C32, false>(A, tile, t0, own0, own1, tw, nwk, epi);
+        ce_rows_std2d<NO, C32, false>(A, tile, tb, own0, own1, tw, nwk, epi);
       return;
     }
   }
@@ -645,7 +643,7 @@ __device__ __forceinline__ void sm_stencil_rows(CEC& c, const StencilDev& A, con
     cplx acc = mk(0.0, 0.0);
     constexpr int CH = NO > 0 ? NO : 9;
     const int nch = (NO == 0 && A.ccode) ? 0 : NO > 0 ? 1 : (nofs + CH - 1) / CH;
-    if (NO == 0 && A.ccode) acc = ce_cc_row<C32>(A, tile, k, (long)t0 * n23, i1, i2, i3, n1, n2, n3);
+    if (NO == 0 && A.ccode) acc = ce_cc_row<C32>(A, tile, k, tb, i1, i2, i3, n1, n2, n3);
     for (int ch = 0; ch < nch; ++ch) {
       const int o0 = ch * CH;
       cplx cv[CH];
@@ -661,7 +659,7 @@ __device__ __forceinline__ void sm_stencil_rows(CEC& c, const StencilDev& A, con
         const int oo = o < nofs ? o : 0;
         const int j1 = i1 + A.d1[oo], j2 = i2 + A.d2[oo], j3 = i3 + A.d3[oo];
         const bool ok = o < nofs && j1 >= 0 && j1 < n1 && j2 >= 0 && j2 < n2 && j3 >= 0 && j3 < n3;
-        const cplx v = tile[ok ? ((long)(j1 - t0) * n2 + j2) * n3 + j3 : 0];
+        const cplx v = tile[ok ? ((long)j1 * n2 + j2) * n3 + j3 - tb : 0];
         const cplx t = cadd(acc, cmul_sp(cv[q], v));
         acc = ok ? t : acc;
       }
@@ -676,16 +674,14 @@ __device__ __forceinline__ void sm_stencil_rows(CEC& c, const StencilDev& A, con
 
 __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b, const cplx* x, cplx* xo, int s) {
   RelaxCtl* R = &ce_S.rc;
-  const int n1 = L.A.n1, n23 = L.A.n2 * L.A.n3;
-  const int rows = (n1 + (int)ce_nctas() - 1) / (int)ce_nctas();
-  const int r0 = min(n1, (int)ce_rank() * rows), r1 = min(n1, r0 + rows);
-  const int t0 = max(0, r0 - 2), t1 = min(n1, r1 + 2);
-  const long np = (long)(r1 - r0) * n23, own0 = (long)r0 * n23;
-  const long rs = (long)rows * n23;  // per-buffer stride (same layout in every CTA)
-  cplx* tile = ce_tile;                        // (rows + 4) * n23
-  cplx* Vb = ce_tile + (long)(rows + 4) * n23;  // V[i] = Vb + i * rs, i <= s
-  cplx* wb = Vb + (long)(s + 1) * rs;           // w[0], w[1]
-  cplx* cs = L.smc ? wb + 2 * rs : nullptr;      // the CTA's rows of the coefficient planes (L.smc)
+  const long N = (long)L.A.n1 * L.A.n2 * L.A.n3;
+  const long rs = (N + ce_nctas() - 1) / ce_nctas();  // points per CTA = per-buffer stride (ce_ppc)
+  const long own0 = min(N, (long)ce_rank() * rs), own1 = min(N, own0 + rs), np = own1 - own0;
+  const long tb = max(0L, own0 - L.A.halo), tn = np > 0 ? min(N, own1 + L.A.halo) - tb : 0;
+  cplx* tile = ce_tile;                          // tn <= rs + 2 halo points
+  cplx* Vb = ce_tile + rs + 2L * L.A.halo;       // V[i] = Vb + i * rs, i <= s
+  cplx* wb = Vb + (long)(s + 1) * rs;            // w[0], w[1]
+  cplx* cs = L.smc ? wb + 2 * rs : nullptr;      // the CTA's points of the coefficient planes (L.smc)
   // the control warp (the CTA's last) takes no share of the vector work: its last thread
   // runs the Givens / least-squares update of each step while the other warps already
   // stage and apply the next step's stencil, so the update is off the critical path
@@ -708,7 +704,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       double red[3];
       ce_stencil<IN_PLAIN, OUT_RESID, RED_NORM>(c, L.A, x, 1.0, nullptr, nullptr, b, L.w[1], nullptr, red);
       v[0] = red[0];
-      src = L.w[1];  // written by this CTA's own rows (row partition of ce_stencil)
+      src = L.w[1];  // written by this CTA's own points (the point partition of ce_stencil)
     }
     double nn = 0.0;
     for (long p = tw; p < np; p += nwk) {
@@ -716,8 +712,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       wb[rs + p] = y;  // w[1] = r : the "previous" buffer of step 0
       nn += y.x * y.x + y.y * y.y;
     }
-    if (cs) {  // stage the own rows of the nofs coefficient planes once for the s stencils
-      const long N = (long)n1 * n23;
+    if (cs) {  // stage the own points of the nofs coefficient planes once for the s stencils
       for (int o = 0; o < L.A.nofs; ++o)
         for (long p = tw; p < np; p += nwk) cs[(long)o * rs + p] = ldk(L.A.coef, (long)o * N + own0 + p);
     }  // (read after the staging barrier of step 0)
@@ -742,23 +737,21 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
     const bool cg = cgs2 && j >= CE_CGS_FROM;
     {
       CEProfScope prof_(c, 5);
-      const bool big = (long)n1 * n23 > 8192;
+      const bool big = N > 8192;
       CEProfScope prof_st_(ce_prof(), big ? 18 : 22);
-      // V[j] = wp * sc (own rows); tile = D^-1 (.) (wp * sc) on rows [t0, t1)
-      const long tn = (long)(t1 - t0) * n23;
+      // V[j] = wp * sc (own points); tile = D^-1 (.) (wp * sc) on points [tb, tb + tn)
       for (long q = tw; q < tn; q += nwk) {
-        const int row = t0 + (int)(q / n23);
-        const long col = q - (long)(row - t0) * n23;
+        const long g = tb + q;
         cplx v;
-        if (row >= r0 && row < r1) {
-          v = cscale(wp[(long)(row - r0) * n23 + col], sc);
-          Vj[(long)(row - r0) * n23 + col] = v;
-        } else {  // halo row owned by a neighbouring CTA: its previous w over DSMEM
-          const int owner = row / rows;
-          const cplx* rw = wb + (long)((j + 1) % 2) * rs + (long)(row - owner * rows) * n23 + col;
+        if (g >= own0 && g < own1) {
+          v = cscale(wp[g - own0], sc);
+          Vj[g - own0] = v;
+        } else {  // halo point owned by another CTA: its previous w over DSMEM
+          const unsigned owner = (unsigned)(g / rs);
+          const cplx* rw = wb + (long)((j + 1) % 2) * rs + (g - (long)owner * rs);
           v = cscale(ce_remote_c(rw, owner), sc);
         }
-        tile[q] = cmul_np(ldk(L.dinv, (long)row * n23 + col), v);
+        tile[q] = cmul_np(ldk(L.dinv, g), v);
       }
       if (threadIdx.x < blockDim.x - 32) ce_worker_sync();  // the control warp neither stages nor applies
       prof_st_.stop();
@@ -768,17 +761,17 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       if (cg) V0 = Vj;  // the epilogue's dot is discarded: batched dots follow
       if (L.A.coef32) {
         if (L.A.nofs == 21)
-          sm_stencil_rows<21, true>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk);
+          sm_stencil_rows<21, true>(c, L.A, tile, own0, own1, tb, w, V0, red, tw, nwk);
         else if (L.A.nofs == 9)
-          sm_stencil_rows<9, true>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk);
+          sm_stencil_rows<9, true>(c, L.A, tile, own0, own1, tb, w, V0, red, tw, nwk);
         else
-          sm_stencil_rows<0, true>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk);
+          sm_stencil_rows<0, true>(c, L.A, tile, own0, own1, tb, w, V0, red, tw, nwk);
       } else {
         switch (L.A.nofs) {
-          case 5: sm_stencil_rows<5, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk, cs, rs); break;
-          case 9: sm_stencil_rows<9, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk, cs, rs); break;
-          case 21: sm_stencil_rows<21, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk, cs, rs); break;
-          default: sm_stencil_rows<0, false>(c, L.A, tile, r0, r1, t0, w, V0, red, tw, nwk); break;
+          case 5: sm_stencil_rows<5, false>(c, L.A, tile, own0, own1, tb, w, V0, red, tw, nwk, cs, rs); break;
+          case 9: sm_stencil_rows<9, false>(c, L.A, tile, own0, own1, tb, w, V0, red, tw, nwk, cs, rs); break;
+          case 21: sm_stencil_rows<21, false>(c, L.A, tile, own0, own1, tb, w, V0, red, tw, nwk, cs, rs); break;
+          default: sm_stencil_rows<0, false>(c, L.A, tile, own0, own1, tb, w, V0, red, tw, nwk); break;
         }
       }
       if (!cg) {
@@ -841,7 +834,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
       double hn2;
       if (cc <= 1e-8 * n2) {
         hn2 = n2 - cc;
-        CE_SYNC(c);  // w'' of every CTA before the neighbours read its halo rows
+        CE_SYNC(c);  // w'' of every CTA before the neighbours read its halo points
       } else {       // heavy cancellation: the explicit norm (its all-reduce is the barrier)
         double v[1] = {nn};
         ce_allreduce<1>(c, v);
@@ -893,7 +886,7 @@ __device__ __noinline__ void ce_relax_sm(CEC& c, const CELevel& L, const cplx* b
     }
   }
   __syncthreads();  // the control thread's y / k
-  // xo = x + dinv (.) (V[:k]^T y)   (own rows)
+  // xo = x + dinv (.) (V[:k]^T y)   (own points)
   const int k = R->k;
   {
     CEProfScope prof_lc_(c, 14);

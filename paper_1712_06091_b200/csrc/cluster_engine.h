@@ -41,20 +41,22 @@ extern int g_ce_prof_on;
 extern int g_ce_cgs2;  // engine relaxations orthogonalise by CGS2 (batched reductions) instead of MGS
 void launch_cluster_engine(cudaStream_t s, const CEDesc* d, int mode, int l0, const cplx* b, cplx* xo,
                            const int* active, int ctas, size_t tile_bytes);
-// dynamic shared memory for the stencil row tiles of levels with n1 x n2 points
-inline size_t ce_tile_bytes(int n1, int n2, int ctas) {
-  return (size_t)((n1 + ctas - 1) / ctas + 4) * n2 * sizeof(cplx);
+// The engine partitions a level of N points by POINTS: CTA r owns [r ppc, (r+1) ppc),
+// ppc = ceil(N / ctas) (a row partition left 129^2 at 9 rows = 1161 points on most CTAs
+// against a mean of 1040); a stencil's input tile adds `halo` points on each side.
+inline long ce_ppc(long N, int ctas) { return (N + ctas - 1) / ctas; }
+// dynamic shared memory for the stencil input tile of a level
+inline size_t ce_tile_bytes(long N, int halo, int ctas) {
+  return (size_t)(ce_ppc(N, ctas) + 2L * halo) * sizeof(cplx);
 }
-// shared-memory relaxation of a level with n1 rows of n23 points and s steps: per CTA the
-// input tile (rows + 4 halo rows), the basis V[0..s] and two w buffers of its own rows
-inline size_t ce_relax_sm_bytes(int n1, long n23, int s, int ctas) {
-  const long rows = (n1 + ctas - 1) / ctas;
-  return (size_t)(rows * (s + 3) + rows + 4) * n23 * sizeof(cplx);
+// shared-memory relaxation with s steps: per CTA the input tile, the basis V[0..s] and two
+// w buffers of its own points
+inline size_t ce_relax_sm_bytes(long N, int halo, int s, int ctas) {
+  return ce_tile_bytes(N, halo, ctas) + (size_t)ce_ppc(N, ctas) * (s + 3) * sizeof(cplx);
 }
-// ... plus the CTA's rows of the nofs coefficient planes (complex128)
-inline size_t ce_relax_smc_bytes(int n1, long n23, int s, int nofs, int ctas) {
-  const long rows = (n1 + ctas - 1) / ctas;
-  return ce_relax_sm_bytes(n1, n23, s, ctas) + (size_t)rows * n23 * nofs * sizeof(cplx);
+// ... plus the CTA's points of the nofs coefficient planes (complex128)
+inline size_t ce_relax_smc_bytes(long N, int halo, int s, int nofs, int ctas) {
+  return ce_relax_sm_bytes(N, halo, s, ctas) + (size_t)ce_ppc(N, ctas) * nofs * sizeof(cplx);
 }
 constexpr size_t CE_SMEM_BUDGET = 190 * 1024;  // dynamic shared memory the engine may request
 

@@ -315,6 +315,9 @@ StencilDev Op::dev() const {
     s.d2[o] = d2[o];
     s.d3[o] = d3[o];
   }
+  s.halo = 0;
+  for (int o = 0; o < nofs; ++o)
+    s.halo = std::max(s.halo, std::abs((d1[o] * n2 + d2[o]) * n3 + d3[o]));
   s.std2d = 0;
   if (n3 == 1 && (nofs == 21 || nofs == 9 || nofs == 5)) {
     bool same = true;
@@ -884,7 +887,7 @@ int g_defer_mgs = 1;  // option "defer_mgs": fold the MGS dots' finalize kernels
 // the level's relaxation fits the engine's shared memory (ce_relax_sm)
 static bool level_smr(const Level& L) {
   return g_ce_smem_relax && !L.dist &&
-         ce_relax_sm_bytes(L.n1, (long)L.n2 * L.n3, L.s, CE_CTAS) <= CE_SMEM_BUDGET;
+         ce_relax_sm_bytes(L.N, L.A->dev().halo, L.s, CE_CTAS) <= CE_SMEM_BUDGET;
 }
 int g_ce_smem_coef = 1;  // option "ce_smem_coef": stage a fitting level's coefficient rows in shared memory
 // ... and its coefficient rows fit beside it (the standard 2D complex128 stencils, whose
@@ -892,16 +895,16 @@ int g_ce_smem_coef = 1;  // option "ce_smem_coef": stage a fitting level's coeff
 static bool level_smc(const Level& L) {
   const StencilDev A = L.A->dev();
   return g_ce_smem_coef && level_smr(L) && A.std2d && !A.coef32 &&
-         ce_relax_smc_bytes(L.n1, (long)L.n2 * L.n3, L.s, A.nofs, CE_CTAS) <= CE_SMEM_BUDGET;
+         ce_relax_smc_bytes(L.N, A.halo, L.s, A.nofs, CE_CTAS) <= CE_SMEM_BUDGET;
 }
 
 size_t Hier::ce_tile(int li) const {
   size_t m = 0;  // the engine touches levels li .. coarsest
   for (int i = li; i < (int)lv.size(); ++i) {
-    m = std::max(m, ce_tile_bytes(lv[i].n1, lv[i].n2 * lv[i].n3, CE_CTAS));
-    if (lv[i].smr) m = std::max(m, ce_relax_sm_bytes(lv[i].n1, (long)lv[i].n2 * lv[i].n3, lv[i].s, CE_CTAS));
-    if (lv[i].smc)
-      m = std::max(m, ce_relax_smc_bytes(lv[i].n1, (long)lv[i].n2 * lv[i].n3, lv[i].s, lv[i].A->nofs, CE_CTAS));
+    const int h = lv[i].A->dev().halo;
+    m = std::max(m, ce_tile_bytes(lv[i].N, h, CE_CTAS));
+    if (lv[i].smr) m = std::max(m, ce_relax_sm_bytes(lv[i].N, h, lv[i].s, CE_CTAS));
+    if (lv[i].smc) m = std::max(m, ce_relax_smc_bytes(lv[i].N, h, lv[i].s, lv[i].A->nofs, CE_CTAS));
   }
   return m;
 }

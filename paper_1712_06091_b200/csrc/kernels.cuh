@@ -47,6 +47,7 @@ struct StencilDev {
   int nofs;
   int p0, n1own;
   int std2d;  // 2D operator whose offsets are exactly the Std2D set of this size (21 / 9 / 5), else 0
+  int halo;   // max |linear displacement| of the offsets (the engine's point-partition halo)
   long pstride;
   int8_t d1[HADR_MAX_OFS];
   int8_t d2[HADR_MAX_OFS];
