@@ -153,7 +153,9 @@ int hadr_ce_profile(unsigned long long* out48, int reset);
 int hadr_ce_bench(hadr_hier h, int level, int reps, double* avg_ms);
 /* microbenchmark of the stencil kernel K1 on device vectors x, y: `reps` back-to-back launches timed
  * with CUDA events on the library stream; variant 0 = y = A x, 1 = the relaxation's fused
- * y = A(D^-1 s x) + basis write + <V0, y>.  *avg_ms = mean launch duration (incl. any finalize). */
+ * y = A(D^-1 s x) + basis write + <V0, y>, 2 = y = A x + <u, y>, 3 = the split relaxation step of large
+ * 3D levels (V = s x, z = D^-1 V in one kernel, then y = A z + <u, y>).  *avg_ms = mean duration of one
+ * such step (incl. any finalize). */
 int hadr_op_bench(hadr_op op, const double* x, double* y, int reps, int variant, double* avg_ms);
 /* number of kernels this library has launched so far (graph launches add their kernel nodes) */
 long long hadr_launch_count(void);

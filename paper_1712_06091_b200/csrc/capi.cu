@@ -570,6 +570,7 @@ int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, 
     cplx* yd = (cplx*)y;
     cplx* vtmp = dalloc<cplx>(op->N);
     cplx* utmp = dalloc<cplx>(op->N);  // dot partner V0: its own stream, as in the relaxation
+    cplx* ztmp = variant == 3 ? dalloc<cplx>(op->N) : nullptr;
     HADR_CUDA(cudaMemsetAsync(utmp, 0, op->N * sizeof(cplx), c.stream));
     double* sc = c.dscal + 56;
     const double one = 1.0;
@@ -584,6 +585,16 @@ int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, 
       if (variant == 0) {  // y = A x
         a.epi = epi_none();
         launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_NONE, a);
+      } else if (variant == 2) {  // y = A x, <u, y> (the split relaxation's stencil)
+        a.u = utmp;
+        a.epi = epi_store(c.dscal);
+        launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_DOT, a);
+      } else if (variant == 3) {  // split relaxation step: V = s x, z = D^-1 V, then y = A z, <u, y>
+        launch_scale_jac(c.lc, op->N, xd, sc, op->inv_diag(), vtmp, ztmp, gate_always());
+        a.x = ztmp;
+        a.u = utmp;
+        a.epi = epi_store(c.dscal);
+        launch_stencil(c.lc, IN_PLAIN, OUT_APPLY, RED_DOT, a);
       } else {             // relaxation Arnoldi input: y = A (D^-1 (s x)), V = s x, <V0, y>
         a.scale = sc;
         a.dinv = op->inv_diag();
@@ -608,6 +619,7 @@ int hadr_op_bench(hadr_op h, const double* x, double* y, int reps, int variant, 
     cudaEventDestroy(e1);
     dfree(vtmp);
     dfree(utmp);
+    if (ztmp) dfree(ztmp);
   });
 }
 
@@ -671,6 +683,16 @@ int hadr_set_option(const char* name, double value) {
       }
     } else if (n == "stencil_tile") {
       g_stencil_tile = (int)value;
+      for (;;) {
+        Hier* h = hier_pool_pop();
+        if (!h) break;
+        delete h;
+      }
+    } else if (n == "stencil_march" || n == "march_min_n") {
+      if (n == "stencil_march")
+        g_stencil_march = (int)value;
+      else
+        g_march_min_n = (long)value;
       for (;;) {
         Hier* h = hier_pool_pop();
         if (!h) break;

@@ -719,6 +719,315 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_tile(StencilArgs a, Til
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// K1 marching (3D fine level, pair-compressed plus-radius-2 operator, plain input):
+// a block owns a column tile of ty x tx points of the (axis 1, axis 2) plane and
+// marches along axis 0 through a chunk of planes.  The input's plane tiles (2-point
+// halo on axes 1 and 2) land in a ring of 6 shared-memory slots by row-wise bulk
+// asynchronous copies (cp.async.bulk -> UBLKCP; one "full" mbarrier per slot counts the
+// bytes), issued by a dedicated producer warp that runs ahead of the arithmetic as far
+// as the ring allows; the compute warps hand a slot back through its "empty" mbarrier
+// (one arrival per warp), so there is no block-wide barrier in the loop.  Every input
+// element comes from DRAM once per sweep (plus the tile halo, ~1.4x of 16 of the ~210 B
+// per point) instead of once per axis-0 neighbour plane that has left L2 (ncu: 20.2 GB
+// per 513^2 x 257 sweep for the flat kernel, 15.2 GB here; layout 14.1 GB).  The ten
+// coefficient planes stream from HBM straight into registers, once.  Arithmetic and
+// accumulation order are stencil_pc's: bit-identical outputs.
+// ---------------------------------------------------------------------------
+struct MarchCfg {
+  int nty, ntx, nch;  // tiles along axis 1 / axis 2, chunks of planes
+  int pc;             // planes per chunk
+  int pitch, slot;    // shared-memory row pitch and slot size (elements)
+};
+#ifndef HADR_MARCH_THREADS
+#define HADR_MARCH_THREADS 480  // compute threads (one point of the tile each); + 1 producer warp
+#endif
+#ifndef HADR_MARCH_PPT
+#define HADR_MARCH_PPT 1
+#endif
+#ifndef HADR_MARCH_MIN_BLOCKS
+#define HADR_MARCH_MIN_BLOCKS 1
+#endif
+constexpr int kMarchRing = 6;
+constexpr int kMarchPpt = HADR_MARCH_PPT;
+constexpr int kMarchThreads = HADR_MARCH_THREADS;
+constexpr int kMarchBlock = kMarchThreads + 32;
+constexpr int kMarchWarps = kMarchThreads / 32;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+template <int OUTM, int RED, bool C32>
+__global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_march(StencilArgs a, MarchCfg m) {
+  pdl_enter();
+  if (!gate_open(a.gate)) return;
+  extern __shared__ __align__(128) unsigned char march_smem[];
+  __shared__ __align__(8) unsigned long long full[kMarchRing], empty[kMarchRing];
+  cplx* ring = reinterpret_cast<cplx*>(march_smem);
+  using Lay = PcLayout<13>;
+  constexpr int NS = Lay::NS;
+  constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & RED_DOT) ? 2 : 0);
+  const int n1 = a.A.n1, n2 = a.A.n2, n3 = a.A.n3, n1own = a.A.n1own, p0 = a.A.p0;
+  const long n23 = (long)n2 * n3;
+  int item = blockIdx.x;
+  const int bx = item % m.ntx;
+  item /= m.ntx;
+  const int by = item % m.nty;
+  const int bc = item / m.nty;
+  const int Y0 = (int)((long)by * n2 / m.nty), Y1 = (int)((long)(by + 1) * n2 / m.nty);
+  const int X0 = (int)((long)bx * n3 / m.ntx), X1 = (int)((long)(bx + 1) * n3 / m.ntx);
+  const int P0 = bc * m.pc, P1 = (P0 + m.pc < n1own) ? P0 + m.pc : n1own;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < kMarchRing; ++s) {
+      mbar_init(smem_u32(&full[s]), 1u);
+      mbar_init(smem_u32(&empty[s]), (unsigned)kMarchWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double red[NV > 0 ? NV : 1];
+#pragma unroll
+  for (int q = 0; q < (NV > 0 ? NV : 1); ++q) red[q] = 0.0;
+  if (wid == kMarchWarps) {
+    // ---- producer warp: plane q (owned-relative; halo planes at q < 0 and q >= n1own) -> slot
+    // (q - (P0 - 2)) % ring; a slot's barriers complete one phase per plane it carries ----
+    const int ys = Y0 - 2 > 0 ? Y0 - 2 : 0, ye = Y1 + 2 < n2 ? Y1 + 2 : n2;
+    const int xs = X0 - 2 > 0 ? X0 - 2 : 0, xe = X1 + 2 < n3 ? X1 + 2 : n3;
+    const int nrows = ye - ys;
+    const unsigned rowbytes = (unsigned)(xe - xs) * (unsigned)sizeof(cplx);
+    for (int q = P0 - 2; q <= P1 + 1; ++q) {
+      const int r = q - (P0 - 2), s = r % kMarchRing, use = r / kMarchRing;
+      if (use > 0) mbar_wait(smem_u32(&empty[s]), (unsigned)(use - 1) & 1u);  // the compute warps left the slot
+      const bool valid = q + p0 >= 0 && q + p0 < n1;
+      const unsigned bar = smem_u32(&full[s]);
+      if (lane == 0) {
+        if (valid)
+          mbar_expect_tx(bar, (unsigned)nrows * rowbytes);
+        else
+          mbar_arrive(bar);
+      }
+      __syncwarp();
+      if (valid) {
+        const cplx* src = a.x + (long)q * n23 + xs;
+        const unsigned dst = smem_u32(ring + (long)s * m.slot + (xs - (X0 - 2)));
+        for (int rr = lane; rr < nrows; rr += 32)
+          bulk_g2s(dst + (unsigned)((ys + rr - (Y0 - 2)) * m.pitch) * (unsigned)sizeof(cplx),
+                   src + (long)(ys + rr) * n3, rowbytes, bar);
+      }
+    }
+  } else {
+    // ---- compute warps ----
+    const long ps = a.A.pstr;
+    const int ty = Y1 - Y0, tx = X1 - X0;
+    int sidx[kMarchPpt];
+    int krel[kMarchPpt];
+    bool act[kMarchPpt];
+    unsigned okm[kMarchPpt];  // bit (axis - 1) * 5 + (delta + 2): in-grid neighbour along axes 1, 2
+#pragma unroll
+    for (int t = 0; t < kMarchPpt; ++t) {
+      const int e = threadIdx.x + t * kMarchThreads;
+      act[t] = e < ty * tx;
+      const int py = act[t] ? e / tx : 0, px = act[t] ? e - py * tx : 0;
+      const int i2 = Y0 + py, i3 = X0 + px;
+      sidx[t] = (py + 2) * m.pitch + (px + 2);
+      krel[t] = i2 * n3 + i3;
+      unsigned mk_ = 0;
+#pragma unroll
+      for (int d = -2; d <= 2; ++d) {
+        if ((unsigned)(i2 + d) < (unsigned)n2) mk_ |= 1u << (d + 2);
+        if ((unsigned)(i3 + d) < (unsigned)n3) mk_ |= 1u << (5 + d + 2);
+      }
+      okm[t] = mk_;
+    }
+    for (int r = 0; r < 4; ++r) mbar_wait(smem_u32(&full[r]), 0u);  // planes P0 - 2 .. P0 + 1
+    for (int p = P0; p < P1; ++p) {
+      // the unit's global loads (10 coefficients, pair code, rhs / dot partner) go out first
+      cplx cv[kMarchPpt][NS], bk[kMarchPpt], uk[kMarchPpt];
+      unsigned code[kMarchPpt];
+#pragma unroll
+      for (int t = 0; t < kMarchPpt; ++t) {
+        if (!act[t]) continue;
+        const long k = (long)p * n23 + krel[t];
+        code[t] = __ldg(a.A.pcode + k);
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          if constexpr (C32) {
+            const float2 c = __ldg(a.A.pcoef32 + (long)q * ps + k);
+            cv[t][q] = make_double2((double)c.x, (double)c.y);
+          } else {
+            cv[t][q] = ldc(a.A.pcoef, (long)q * ps + k);
+          }
+        }
+        if (OUTM == OUT_RESID) bk[t] = ldc(a.b, k);
+        if (RED & RED_DOT) uk[t] = ldc(a.u, k);
+      }
+      const int r2 = p - P0 + 4;  // plane p + 2
+      mbar_wait(smem_u32(&full[r2 % kMarchRing]), (unsigned)(r2 / kMarchRing) & 1u);
+      const cplx* pl[5];  // slots of planes p - 2 .. p + 2
+#pragma unroll
+      for (int d = 0; d < 5; ++d) pl[d] = ring + (long)((p - P0 + d) % kMarchRing) * m.slot;
+      unsigned ok0 = 0;  // bit (delta + 2): in-grid plane along axis 0
+#pragma unroll
+      for (int d = -2; d <= 2; ++d)
+        if ((unsigned)(p + p0 + d) < (unsigned)n1) ok0 |= 1u << (d + 2);
+#pragma unroll
+      for (int t = 0; t < kMarchPpt; ++t) {
+        if (!act[t]) continue;
+        const long k = (long)p * n23 + krel[t];
+        cplx tv[NS];
+        bool ok[NS];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          const int ax = Lay::axis(q);
+          int dl = Lay::delta(q);
+          if (Lay::plus_pos(q) >= 0) dl = ((code[t] >> Lay::pair(Lay::first_pos(q))) & 1u) ? 2 : -2;
+          cplx v;
+          if (ax < 0) {
+            ok[q] = true;
+            v = pl[2][sidx[t]];
+          } else if (ax == 0) {
+            ok[q] = (ok0 >> (dl + 2)) & 1u;
+            // (a select between the two candidate slots, not a runtime index into pl[])
+            const cplx* ps0 = Lay::plus_pos(q) >= 0 ? (dl > 0 ? pl[4] : pl[0]) : pl[Lay::delta(q) + 2];
+            v = ps0[sidx[t]];
+          } else if (ax == 1) {
+            ok[q] = (okm[t] >> (dl + 2)) & 1u;
+            v = pl[2][sidx[t] + dl * m.pitch];
+          } else {
+            ok[q] = (okm[t] >> (5 + dl + 2)) & 1u;
+            v = pl[2][sidx[t] + dl];
+          }
+          tv[q] = cmul_sp(cv[t][q], v);
+        }
+        cplx acc = mk(0.0, 0.0);
+#pragma unroll
+        for (int pp = 0; pp < 13; ++pp) {
+          const int q = Lay::slot(pp);
+          bool live = ok[q];
+          if (Lay::pair(pp) >= 0) {
+            const unsigned member = (Lay::plus_pos(q) == pp) ? 1u : 0u;
+            live = live && ((code[t] >> Lay::pair(pp)) & 1u) == member;
+          }
+          const cplx tt = cadd(acc, tv[q]);
+          acc = live ? tt : acc;
+        }
+        const cplx y = (OUTM == OUT_RESID) ? csub(bk[t], acc) : acc;
+        a.y[k] = y;
+        if (RED & RED_NORM) red[0] += y.x * y.x + y.y * y.y;
+        if (RED & RED_DOT) {
+          constexpr int o = (RED & RED_NORM) ? 1 : 0;
+          red[o] += uk[t].x * y.x + uk[t].y * y.y;
+          red[o + 1] += uk[t].x * y.y - uk[t].y * y.x;
+        }
+      }
+      __syncwarp();  // every lane's reads of plane p - 2 are done: hand its slot back
+      if (lane == 0) mbar_arrive(smem_u32(&empty[(p - P0) % kMarchRing]));
+    }
+  }
+  if constexpr (NV > 0) {
+    double v[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v[q] = red[q];
+    finish<NV, 0>(v, a.rs, a.epi);
+  }
+}
+
+int g_stencil_march = 1;          // option "stencil_march": 0 off, 1 policy (large 3D fine levels), 2 always
+long g_march_min_n = 2000000;     // option "march_min_n": policy threshold (owned points)
+
+static bool march_cfg(const StencilDev& A, MarchCfg& m, int& blocks, size_t& smem) {
+  if (!A.pcode || A.nofs != 13 || A.n3 < 2 || A.n1own < 1) return false;
+  m.ntx = (A.n3 + 33) / 34;
+  const int txmax = (A.n3 + m.ntx - 1) / m.ntx;
+  int tymax = (kMarchThreads * kMarchPpt) / txmax;
+  if (tymax > A.n2) tymax = A.n2;
+  m.nty = (A.n2 + tymax - 1) / tymax;
+  tymax = (A.n2 + m.nty - 1) / m.nty;
+  const long cols = (long)m.ntx * m.nty;
+  long nch = (148L * HADR_MARCH_MIN_BLOCKS * 4 + cols - 1) / cols;  // >= 4 waves of blocks
+  if (nch > A.n1own / 8) nch = A.n1own / 8;                          // chunks of >= 8 planes
+  if (nch < 1) nch = 1;
+  if (cols * nch > 8192) nch = 8192 / cols;                          // reduction scratch: 8192 blocks
+  if (nch < 1) return false;
+  m.pc = (int)((A.n1own + nch - 1) / nch);
+  m.nch = (A.n1own + m.pc - 1) / m.pc;
+  m.pitch = txmax + 4;
+  m.slot = (tymax + 4) * m.pitch;
+  blocks = (int)(cols * m.nch);
+  smem = (size_t)kMarchRing * m.slot * sizeof(cplx);
+  return smem <= 200 * 1024;
+}
+
+template <int OUTM, int RED, bool C32>
+static void launch_march_t(const LaunchCfg& lc, const StencilArgs& a, const MarchCfg& m, int blocks, size_t smem) {
+  static size_t enabled = 0;
+  if (smem > enabled) {
+    cudaFuncSetAttribute(k_stencil_march<OUTM, RED, C32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    enabled = smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kMarchBlock);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = lc.stream;
+  cudaLaunchAttribute at[1];
+  cfg.numAttrs = pdl_attr(at);
+  cfg.attrs = at;
+  cudaLaunchKernelEx(&cfg, k_stencil_march<OUTM, RED, C32>, a, m);
+  constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & RED_DOT) ? 2 : 0);
+  if constexpr (NV > 0) launch_finalize<NV>(lc, Geo{blocks, 0}, a.gate, a.rs, a.epi);
+}
+
+// true when the marching kernel took the launch
+static bool launch_march(const LaunchCfg& lc, int outm, int red, const StencilArgs& a) {
+  MarchCfg m{};
+  int blocks = 0;
+  size_t smem = 0;
+  if (!march_cfg(a.A, m, blocks, smem)) return false;
+  const bool c32 = a.A.pcoef32 != nullptr;
+#define HADR_MCASE(O, R)                                      \
+  if (outm == (O) && red == (R)) {                            \
+    if (c32)                                                  \
+      launch_march_t<O, R, true>(lc, a, m, blocks, smem);     \
+    else                                                      \
+      launch_march_t<O, R, false>(lc, a, m, blocks, smem);    \
+    return true;                                              \
+  }
+  HADR_MCASE(OUT_APPLY, RED_NONE)
+  HADR_MCASE(OUT_APPLY, RED_NORM | RED_DOT)
+  HADR_MCASE(OUT_APPLY, RED_DOT)
+  HADR_MCASE(OUT_RESID, RED_NONE)
+  HADR_MCASE(OUT_RESID, RED_NORM)
+#undef HADR_MCASE
+  return false;
+}
+
 int g_stencil_tile = 1;  // option "stencil_tile": 0 off, 1 policy (2D wide stencils), 2 always
 
 template <int INM, int OUTM, int RED, int NO>
@@ -797,6 +1106,10 @@ void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const Stenc
   const long N = (long)a.A.n1own * a.A.n2 * a.A.n3;  // points computed (owned slab)
   const Geo geo = red ? geo_for(lc, N) : Geo{blocks_for(lc, N), 0};
   constexpr int J = IN_SCALE | IN_JAC | IN_WRITEV;
+  // 3D pair-compressed fine level, plain input: the plane-marching bulk-copy kernel
+  if (g_stencil_march && inm == IN_PLAIN && a.A.pcode && a.A.nofs == 13 && !geo.cluster &&
+      (g_stencil_march > 1 || N >= g_march_min_n) && launch_march(lc, outm, red, a))
+    return;
   // tiled kernel where it measured faster (B200): 2D operators with wide (Galerkin)
   // stencils; the 3D and 9-point fine-level sweeps keep the flat kernel, whose
   // neighbour re-reads L1 already absorbs (tools/prof_solve.py A/B)

@@ -10,6 +10,8 @@ extern int g_mid_ppt;    // points per thread of a 2D level's kernels with mid_m
 extern long g_mid_max_n;
 extern long g_mid_min_n;  // programmatic dependent launch of the solve-phase kernels
 extern int g_stencil_tile;
+extern int g_stencil_march;   // plane-marching bulk-copy kernel on 3D pair-compressed fine levels
+extern long g_march_min_n;
 extern long g_cl_max_n;  // single-cluster reductions (in-kernel epilogue) up to this many points  // shared-memory tiled stencil kernel on the graph path
 
 // Structured 2D/3D stencil in union-offset, plane-major layout (2D: n3 = 1, d3 = 0):

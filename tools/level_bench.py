@@ -21,6 +21,9 @@ def main():
     ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--n", type=int, default=513)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--levels", type=int, default=99, help="bench the first N levels only")
+    ap.add_argument("--variants", default="0,1", help="hadr_op_bench variants (0 apply, 1 fused relaxation input, "
+                    "2 apply + dot, 3 split relaxation step: scale/Jacobi kernel + apply + dot)")
     a, extra = ap.parse_known_args()
     import torch
 
@@ -38,16 +41,16 @@ def main():
     del H1
     hier = multigrid.build_hierarchy(B, g.shape, 5)
     out = []
-    for lev, op in enumerate(hier.ops):
+    for lev, op in enumerate(hier.ops[: a.levels]):
         N = op.shape[0]
         x = torch.randn(N, dtype=torch.complex128, device="cuda")
         y = torch.empty_like(x)
         nnz = op.nnz if N * len(op.offsets) <= 2e8 else float('nan')  # export is host-side
-        for var in (0, 1):
+        for var in [int(v) for v in a.variants.split(",")]:
             ms = C.c_double()
             _lib.check(L.hadr_op_bench(op.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), a.reps, var,
                                        C.byref(ms)))
-            per = 5 if var == 1 else 2
+            per = {0: 2, 1: 5, 2: 3, 3: 9}[var]  # vector streams of 16 B per point
             planes = op.storage_slots or len(op.offsets)
             lay = (planes + per) * N * 16
             alg = (nnz + per * N) * 16
