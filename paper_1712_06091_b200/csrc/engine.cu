@@ -951,7 +951,8 @@ void Hier::alloc_workspace() {
     L.w[0] = valloc(L);
     L.w[1] = valloc(L);
     L.r = valloc(L);
-    if (g_relax_split > 0 && L.n3 > 1 && L.N >= g_relax_split) L.z = valloc(L);
+    // (not where the marching kernel runs: it applies D^-1 (s w) to its shared-memory input tiles)
+    if (g_relax_split > 0 && L.n3 > 1 && L.N >= g_relax_split && !march_takes(L.A->dev())) L.z = valloc(L);
     L.rctl = dalloc<RelaxCtl>(1);
     HADR_CUDA(cudaMemset(L.rctl, 0, sizeof(RelaxCtl)));
     if (i >= 1) {

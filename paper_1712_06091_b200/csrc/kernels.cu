@@ -781,16 +781,19 @@ __device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned
                : "memory");
 }
 
-template <int OUTM, int RED, bool C32>
+template <int INM, int OUTM, int RED, bool C32>
 __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_march(StencilArgs a, MarchCfg m) {
   pdl_enter();
   if (!gate_open(a.gate)) return;
   extern __shared__ __align__(128) unsigned char march_smem[];
   __shared__ __align__(8) unsigned long long full[kMarchRing], empty[kMarchRing];
   cplx* ring = reinterpret_cast<cplx*>(march_smem);
+  // relaxation input (IN_JAC): D^-1 tiles in a second ring, the transform D^-1 (.) (s x) applied per read
+  constexpr bool JAC = (INM & IN_JAC) != 0;
+  const long dofs = (long)kMarchRing * m.slot;  // D^-1 ring offset (elements)
   using Lay = PcLayout<13>;
   constexpr int NS = Lay::NS;
-  constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & RED_DOT) ? 2 : 0);
+  constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & (RED_DOT | RED_DOT_CENTER)) ? 2 : 0);
   const int n1 = a.A.n1, n2 = a.A.n2, n3 = a.A.n3, n1own = a.A.n1own, p0 = a.A.p0;
   const long n23 = (long)n2 * n3;
   int item = blockIdx.x;
@@ -828,7 +831,7 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
       const unsigned bar = smem_u32(&full[s]);
       if (lane == 0) {
         if (valid)
-          mbar_expect_tx(bar, (unsigned)nrows * rowbytes);
+          mbar_expect_tx(bar, (unsigned)nrows * rowbytes * (JAC ? 2u : 1u));
         else
           mbar_arrive(bar);
       }
@@ -839,11 +842,19 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
         for (int rr = lane; rr < nrows; rr += 32)
           bulk_g2s(dst + (unsigned)((ys + rr - (Y0 - 2)) * m.pitch) * (unsigned)sizeof(cplx),
                    src + (long)(ys + rr) * n3, rowbytes, bar);
+        if constexpr (JAC) {
+          const cplx* dsrc = a.dinv + (long)q * n23 + xs;
+          const unsigned ddst = dst + (unsigned)dofs * (unsigned)sizeof(cplx);
+          for (int rr = lane; rr < nrows; rr += 32)
+            bulk_g2s(ddst + (unsigned)((ys + rr - (Y0 - 2)) * m.pitch) * (unsigned)sizeof(cplx),
+                     dsrc + (long)(ys + rr) * n3, rowbytes, bar);
+        }
       }
     }
   } else {
     // ---- compute warps ----
     const long ps = a.A.pstr;
+    const double sc = (INM & IN_SCALE) ? *a.scale : 1.0;
     const int ty = Y1 - Y0, tx = X1 - X0;
     int sidx[kMarchPpt];
     int krel[kMarchPpt];
@@ -902,27 +913,31 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
         const long k = (long)p * n23 + krel[t];
         cplx tv[NS];
         bool ok[NS];
+        cplx xc[kMarchPpt];  // the centre's raw input
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
           const int ax = Lay::axis(q);
           int dl = Lay::delta(q);
           if (Lay::plus_pos(q) >= 0) dl = ((code[t] >> Lay::pair(Lay::first_pos(q))) & 1u) ? 2 : -2;
-          cplx v;
+          const cplx* src;
           if (ax < 0) {
             ok[q] = true;
-            v = pl[2][sidx[t]];
+            src = pl[2] + sidx[t];
           } else if (ax == 0) {
             ok[q] = (ok0 >> (dl + 2)) & 1u;
             // (a select between the two candidate slots, not a runtime index into pl[])
-            const cplx* ps0 = Lay::plus_pos(q) >= 0 ? (dl > 0 ? pl[4] : pl[0]) : pl[Lay::delta(q) + 2];
-            v = ps0[sidx[t]];
+            src = (Lay::plus_pos(q) >= 0 ? (dl > 0 ? pl[4] : pl[0]) : pl[Lay::delta(q) + 2]) + sidx[t];
           } else if (ax == 1) {
             ok[q] = (okm[t] >> (dl + 2)) & 1u;
-            v = pl[2][sidx[t] + dl * m.pitch];
+            src = pl[2] + sidx[t] + dl * m.pitch;
           } else {
             ok[q] = (okm[t] >> (5 + dl + 2)) & 1u;
-            v = pl[2][sidx[t] + dl];
+            src = pl[2] + sidx[t] + dl;
           }
+          cplx v = *src;
+          if (INM & IN_SCALE) v = cscale(v, sc);
+          if constexpr (JAC) v = cmul_np(src[dofs], v);
+          if (ax < 0) xc[t] = *src;
           tv[q] = cmul_sp(cv[t][q], v);
         }
         cplx acc = mk(0.0, 0.0);
@@ -937,13 +952,20 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
           const cplx tt = cadd(acc, tv[q]);
           acc = live ? tt : acc;
         }
+        cplx vc = mk(0.0, 0.0);
+        if ((INM & IN_WRITEV) || (RED & RED_DOT_CENTER)) {
+          vc = xc[t];
+          if (INM & IN_SCALE) vc = cscale(vc, sc);
+          if (INM & IN_WRITEV) a.vout[k] = vc;
+        }
         const cplx y = (OUTM == OUT_RESID) ? csub(bk[t], acc) : acc;
         a.y[k] = y;
         if (RED & RED_NORM) red[0] += y.x * y.x + y.y * y.y;
-        if (RED & RED_DOT) {
+        if (RED & (RED_DOT | RED_DOT_CENTER)) {
+          const cplx u = (RED & RED_DOT_CENTER) ? vc : uk[t];
           constexpr int o = (RED & RED_NORM) ? 1 : 0;
-          red[o] += uk[t].x * y.x + uk[t].y * y.y;
-          red[o + 1] += uk[t].x * y.y - uk[t].y * y.x;
+          red[o] += u.x * y.x + u.y * y.y;
+          red[o + 1] += u.x * y.y - u.y * y.x;
         }
       }
       __syncwarp();  // every lane's reads of plane p - 2 are done: hand its slot back
@@ -961,7 +983,13 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
 int g_stencil_march = 1;          // option "stencil_march": 0 off, 1 policy (large 3D fine levels), 2 always
 long g_march_min_n = 2000000;     // option "march_min_n": policy threshold (owned points)
 
-static bool march_cfg(const StencilDev& A, MarchCfg& m, int& blocks, size_t& smem) {
+// the marching kernel's policy: a pair-compressed 3D plus-radius-2 operator of >= march_min_n owned points
+bool march_takes(const StencilDev& A) {
+  if (!g_stencil_march || !A.pcode || A.nofs != 13 || A.n3 < 2) return false;
+  return g_stencil_march > 1 || (long)A.n1own * A.n2 * A.n3 >= g_march_min_n;
+}
+
+static bool march_cfg(const StencilDev& A, bool jac, MarchCfg& m, int& blocks, size_t& smem) {
   if (!A.pcode || A.nofs != 13 || A.n3 < 2 || A.n1own < 1) return false;
   m.ntx = (A.n3 + 33) / 34;
   const int txmax = (A.n3 + m.ntx - 1) / m.ntx;
@@ -980,15 +1008,15 @@ static bool march_cfg(const StencilDev& A, MarchCfg& m, int& blocks, size_t& sme
   m.pitch = txmax + 4;
   m.slot = (tymax + 4) * m.pitch;
   blocks = (int)(cols * m.nch);
-  smem = (size_t)kMarchRing * m.slot * sizeof(cplx);
+  smem = (size_t)kMarchRing * m.slot * sizeof(cplx) * (jac ? 2 : 1);
   return smem <= 200 * 1024;
 }
 
-template <int OUTM, int RED, bool C32>
+template <int INM, int OUTM, int RED, bool C32>
 static void launch_march_t(const LaunchCfg& lc, const StencilArgs& a, const MarchCfg& m, int blocks, size_t smem) {
   static size_t enabled = 0;
   if (smem > enabled) {
-    cudaFuncSetAttribute(k_stencil_march<OUTM, RED, C32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_stencil_march<INM, OUTM, RED, C32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     enabled = smem;
   }
   cudaLaunchConfig_t cfg{};
@@ -999,31 +1027,34 @@ static void launch_march_t(const LaunchCfg& lc, const StencilArgs& a, const Marc
   cudaLaunchAttribute at[1];
   cfg.numAttrs = pdl_attr(at);
   cfg.attrs = at;
-  cudaLaunchKernelEx(&cfg, k_stencil_march<OUTM, RED, C32>, a, m);
-  constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & RED_DOT) ? 2 : 0);
+  cudaLaunchKernelEx(&cfg, k_stencil_march<INM, OUTM, RED, C32>, a, m);
+  constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & (RED_DOT | RED_DOT_CENTER)) ? 2 : 0);
   if constexpr (NV > 0) launch_finalize<NV>(lc, Geo{blocks, 0}, a.gate, a.rs, a.epi);
 }
 
 // true when the marching kernel took the launch
-static bool launch_march(const LaunchCfg& lc, int outm, int red, const StencilArgs& a) {
+static bool launch_march(const LaunchCfg& lc, int inm, int outm, int red, const StencilArgs& a) {
   MarchCfg m{};
   int blocks = 0;
   size_t smem = 0;
-  if (!march_cfg(a.A, m, blocks, smem)) return false;
+  if (!march_cfg(a.A, (inm & IN_JAC) != 0, m, blocks, smem)) return false;
   const bool c32 = a.A.pcoef32 != nullptr;
-#define HADR_MCASE(O, R)                                      \
-  if (outm == (O) && red == (R)) {                            \
-    if (c32)                                                  \
-      launch_march_t<O, R, true>(lc, a, m, blocks, smem);     \
-    else                                                      \
-      launch_march_t<O, R, false>(lc, a, m, blocks, smem);    \
-    return true;                                              \
+  constexpr int J = IN_SCALE | IN_JAC | IN_WRITEV;
+#define HADR_MCASE(I, O, R)                                      \
+  if (inm == (I) && outm == (O) && red == (R)) {                 \
+    if (c32)                                                     \
+      launch_march_t<I, O, R, true>(lc, a, m, blocks, smem);     \
+    else                                                         \
+      launch_march_t<I, O, R, false>(lc, a, m, blocks, smem);    \
+    return true;                                                 \
   }
-  HADR_MCASE(OUT_APPLY, RED_NONE)
-  HADR_MCASE(OUT_APPLY, RED_NORM | RED_DOT)
-  HADR_MCASE(OUT_APPLY, RED_DOT)
-  HADR_MCASE(OUT_RESID, RED_NONE)
-  HADR_MCASE(OUT_RESID, RED_NORM)
+  HADR_MCASE(IN_PLAIN, OUT_APPLY, RED_NONE)
+  HADR_MCASE(IN_PLAIN, OUT_APPLY, RED_NORM | RED_DOT)
+  HADR_MCASE(IN_PLAIN, OUT_APPLY, RED_DOT)
+  HADR_MCASE(IN_PLAIN, OUT_RESID, RED_NONE)
+  HADR_MCASE(IN_PLAIN, OUT_RESID, RED_NORM)
+  HADR_MCASE(J, OUT_APPLY, RED_DOT_CENTER)
+  HADR_MCASE(J, OUT_APPLY, RED_DOT)
 #undef HADR_MCASE
   return false;
 }
@@ -1107,9 +1138,7 @@ void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const Stenc
   const Geo geo = red ? geo_for(lc, N) : Geo{blocks_for(lc, N), 0};
   constexpr int J = IN_SCALE | IN_JAC | IN_WRITEV;
   // 3D pair-compressed fine level, plain input: the plane-marching bulk-copy kernel
-  if (g_stencil_march && inm == IN_PLAIN && a.A.pcode && a.A.nofs == 13 && !geo.cluster &&
-      (g_stencil_march > 1 || N >= g_march_min_n) && launch_march(lc, outm, red, a))
-    return;
+  if (march_takes(a.A) && !geo.cluster && launch_march(lc, inm, outm, red, a)) return;
   // tiled kernel where it measured faster (B200): 2D operators with wide (Galerkin)
   // stencils; the 3D and 9-point fine-level sweeps keep the flat kernel, whose
   // neighbour re-reads L1 already absorbs (tools/prof_solve.py A/B)

@@ -12,6 +12,8 @@ extern long g_mid_min_n;  // programmatic dependent launch of the solve-phase ke
 extern int g_stencil_tile;
 extern int g_stencil_march;   // plane-marching bulk-copy kernel on 3D pair-compressed fine levels
 extern long g_march_min_n;
+struct StencilDev;
+bool march_takes(const StencilDev& A);  // launch_stencil runs the marching kernel on this operator
 extern long g_cl_max_n;  // single-cluster reductions (in-kernel epilogue) up to this many points  // shared-memory tiled stencil kernel on the graph path
 
 // Structured 2D/3D stencil in union-offset, plane-major layout (2D: n3 = 1, d3 = 0):
