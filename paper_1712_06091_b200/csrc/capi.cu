@@ -688,11 +688,13 @@ int hadr_set_option(const char* name, double value) {
         if (!h) break;
         delete h;
       }
-    } else if (n == "stencil_march" || n == "march_min_n") {
+    } else if (n == "stencil_march" || n == "march_min_n" || n == "march_min_n2d") {
       if (n == "stencil_march")
         g_stencil_march = (int)value;
-      else
+      else if (n == "march_min_n")
         g_march_min_n = (long)value;
+      else
+        g_march_min_n2d = (long)value;
       for (;;) {
         Hier* h = hier_pool_pop();
         if (!h) break;

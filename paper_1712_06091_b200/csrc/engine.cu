@@ -1017,7 +1017,7 @@ Hier* hier_pool_pop() {
 std::vector<long long> hier_option_signature() {
   return {g_ce_smem_relax, g_ce_smem_coef, g_ce_max_n, g_cl_max_n, g_stencil_tile, g_relax_split, g_class_compress, g_pair_compress,
           g_pdl, g_ce_prof_on, g_kcycle_c64, g_ce_cgs2, g_defer_mgs, g_mid_ppt, g_mid_min_n, g_mid_max_n,
-          g_stencil_march, g_march_min_n};
+          g_stencil_march, g_march_min_n, g_march_min_n2d};
 }
 
 void hier_release(Hier* h) {

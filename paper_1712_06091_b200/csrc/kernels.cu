@@ -739,6 +739,7 @@ struct MarchCfg {
   int nty, ntx, nch;  // tiles along axis 1 / axis 2, chunks of planes
   int pc;             // planes per chunk
   int pitch, slot;    // shared-memory row pitch and slot size (elements)
+  int hy;             // halo rows of a slot along axis 1 (3D: 2; 2D, where a plane is one grid row: 0)
 };
 #ifndef HADR_MARCH_THREADS
 #define HADR_MARCH_THREADS 480  // compute threads (one point of the tile each); + 1 producer warp
@@ -781,7 +782,9 @@ __device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned
                : "memory");
 }
 
-template <int INM, int OUTM, int RED, bool C32>
+// NO = 13: 3D (planes along axis 0, tiles over axes 1 x 2).  NO = 9: 2D — the grid (n1, n2) is marched as
+// (n1, 1, n2): a plane is one grid row, a tile a row segment of up to one point per compute thread.
+template <int NO, int INM, int OUTM, int RED, bool C32>
 __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_march(StencilArgs a, MarchCfg m) {
   pdl_enter();
   if (!gate_open(a.gate)) return;
@@ -791,10 +794,11 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
   // relaxation input (IN_JAC): D^-1 tiles in a second ring, the transform D^-1 (.) (s x) applied per read
   constexpr bool JAC = (INM & IN_JAC) != 0;
   const long dofs = (long)kMarchRing * m.slot;  // D^-1 ring offset (elements)
-  using Lay = PcLayout<13>;
+  using Lay = PcLayout<NO>;
   constexpr int NS = Lay::NS;
+  constexpr bool D2 = NO == 9;
   constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & (RED_DOT | RED_DOT_CENTER)) ? 2 : 0);
-  const int n1 = a.A.n1, n2 = a.A.n2, n3 = a.A.n3, n1own = a.A.n1own, p0 = a.A.p0;
+  const int n1 = a.A.n1, n2 = D2 ? 1 : a.A.n2, n3 = D2 ? a.A.n2 : a.A.n3, n1own = a.A.n1own, p0 = a.A.p0;
   const long n23 = (long)n2 * n3;
   int item = blockIdx.x;
   const int bx = item % m.ntx;
@@ -820,7 +824,7 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
   if (wid == kMarchWarps) {
     // ---- producer warp: plane q (owned-relative; halo planes at q < 0 and q >= n1own) -> slot
     // (q - (P0 - 2)) % ring; a slot's barriers complete one phase per plane it carries ----
-    const int ys = Y0 - 2 > 0 ? Y0 - 2 : 0, ye = Y1 + 2 < n2 ? Y1 + 2 : n2;
+    const int ys = Y0 - m.hy > 0 ? Y0 - m.hy : 0, ye = Y1 + m.hy < n2 ? Y1 + m.hy : n2;
     const int xs = X0 - 2 > 0 ? X0 - 2 : 0, xe = X1 + 2 < n3 ? X1 + 2 : n3;
     const int nrows = ye - ys;
     const unsigned rowbytes = (unsigned)(xe - xs) * (unsigned)sizeof(cplx);
@@ -840,13 +844,13 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
         const cplx* src = a.x + (long)q * n23 + xs;
         const unsigned dst = smem_u32(ring + (long)s * m.slot + (xs - (X0 - 2)));
         for (int rr = lane; rr < nrows; rr += 32)
-          bulk_g2s(dst + (unsigned)((ys + rr - (Y0 - 2)) * m.pitch) * (unsigned)sizeof(cplx),
+          bulk_g2s(dst + (unsigned)((ys + rr - (Y0 - m.hy)) * m.pitch) * (unsigned)sizeof(cplx),
                    src + (long)(ys + rr) * n3, rowbytes, bar);
         if constexpr (JAC) {
           const cplx* dsrc = a.dinv + (long)q * n23 + xs;
           const unsigned ddst = dst + (unsigned)dofs * (unsigned)sizeof(cplx);
           for (int rr = lane; rr < nrows; rr += 32)
-            bulk_g2s(ddst + (unsigned)((ys + rr - (Y0 - 2)) * m.pitch) * (unsigned)sizeof(cplx),
+            bulk_g2s(ddst + (unsigned)((ys + rr - (Y0 - m.hy)) * m.pitch) * (unsigned)sizeof(cplx),
                      dsrc + (long)(ys + rr) * n3, rowbytes, bar);
         }
       }
@@ -866,7 +870,7 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
       act[t] = e < ty * tx;
       const int py = act[t] ? e / tx : 0, px = act[t] ? e - py * tx : 0;
       const int i2 = Y0 + py, i3 = X0 + px;
-      sidx[t] = (py + 2) * m.pitch + (px + 2);
+      sidx[t] = (py + m.hy) * m.pitch + (px + 2);
       krel[t] = i2 * n3 + i3;
       unsigned mk_ = 0;
 #pragma unroll
@@ -916,7 +920,7 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
         cplx xc[kMarchPpt];  // the centre's raw input
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
-          const int ax = Lay::axis(q);
+          const int ax = (D2 && Lay::axis(q) == 1) ? 2 : Lay::axis(q);  // 2D: the in-row axis is the tile's x
           int dl = Lay::delta(q);
           if (Lay::plus_pos(q) >= 0) dl = ((code[t] >> Lay::pair(Lay::first_pos(q))) & 1u) ? 2 : -2;
           const cplx* src;
@@ -942,7 +946,7 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
         }
         cplx acc = mk(0.0, 0.0);
 #pragma unroll
-        for (int pp = 0; pp < 13; ++pp) {
+        for (int pp = 0; pp < NO; ++pp) {
           const int q = Lay::slot(pp);
           bool live = ok[q];
           if (Lay::pair(pp) >= 0) {
@@ -980,23 +984,31 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
   }
 }
 
-int g_stencil_march = 1;          // option "stencil_march": 0 off, 1 policy (large 3D fine levels), 2 always
-long g_march_min_n = 2000000;     // option "march_min_n": policy threshold (owned points)
+int g_stencil_march = 1;          // option "stencil_march": 0 off, 1 policy (large fine levels), 2 always
+long g_march_min_n = 2000000;     // option "march_min_n": policy threshold, 3D (owned points)
+long g_march_min_n2d = 1L << 40;  // option "march_min_n2d": policy threshold, 2D
 
-// the marching kernel's policy: a pair-compressed 3D plus-radius-2 operator of >= march_min_n owned points
+// the marching kernel's policy: a pair-compressed plus-radius-2 operator (3D 13 / 2D 9 offsets) of at least
+// march_min_n / march_min_n2d owned points
 bool march_takes(const StencilDev& A) {
-  if (!g_stencil_march || !A.pcode || A.nofs != 13 || A.n3 < 2) return false;
-  return g_stencil_march > 1 || (long)A.n1own * A.n2 * A.n3 >= g_march_min_n;
+  if (!g_stencil_march || !A.pcode) return false;
+  const bool d3 = A.nofs == 13 && A.n3 >= 2, d2 = A.nofs == 9 && A.n3 == 1;
+  if (!d3 && !d2) return false;
+  return g_stencil_march > 1 || (long)A.n1own * A.n2 * A.n3 >= (d3 ? g_march_min_n : g_march_min_n2d);
 }
 
 static bool march_cfg(const StencilDev& A, bool jac, MarchCfg& m, int& blocks, size_t& smem) {
-  if (!A.pcode || A.nofs != 13 || A.n3 < 2 || A.n1own < 1) return false;
-  m.ntx = (A.n3 + 33) / 34;
-  const int txmax = (A.n3 + m.ntx - 1) / m.ntx;
+  const bool d3 = A.nofs == 13 && A.n3 >= 2, d2 = A.nofs == 9 && A.n3 == 1;
+  if (!A.pcode || (!d3 && !d2) || A.n1own < 1) return false;
+  const int nY = d3 ? A.n2 : 1, nX = d3 ? A.n3 : A.n2;  // tile axes (2D: a plane is one row)
+  const int txcap = d3 ? 34 : kMarchThreads * kMarchPpt;
+  m.hy = d3 ? 2 : 0;
+  m.ntx = (nX + txcap - 1) / txcap;
+  const int txmax = (nX + m.ntx - 1) / m.ntx;
   int tymax = (kMarchThreads * kMarchPpt) / txmax;
-  if (tymax > A.n2) tymax = A.n2;
-  m.nty = (A.n2 + tymax - 1) / tymax;
-  tymax = (A.n2 + m.nty - 1) / m.nty;
+  if (tymax > nY) tymax = nY;
+  m.nty = (nY + tymax - 1) / tymax;
+  tymax = (nY + m.nty - 1) / m.nty;
   const long cols = (long)m.ntx * m.nty;
   long nch = (148L * HADR_MARCH_MIN_BLOCKS * 4 + cols - 1) / cols;  // >= 4 waves of blocks
   if (nch > A.n1own / 8) nch = A.n1own / 8;                          // chunks of >= 8 planes
@@ -1006,17 +1018,17 @@ static bool march_cfg(const StencilDev& A, bool jac, MarchCfg& m, int& blocks, s
   m.pc = (int)((A.n1own + nch - 1) / nch);
   m.nch = (A.n1own + m.pc - 1) / m.pc;
   m.pitch = txmax + 4;
-  m.slot = (tymax + 4) * m.pitch;
+  m.slot = (tymax + 2 * m.hy) * m.pitch;
   blocks = (int)(cols * m.nch);
   smem = (size_t)kMarchRing * m.slot * sizeof(cplx) * (jac ? 2 : 1);
   return smem <= 200 * 1024;
 }
 
-template <int INM, int OUTM, int RED, bool C32>
+template <int NO, int INM, int OUTM, int RED, bool C32>
 static void launch_march_t(const LaunchCfg& lc, const StencilArgs& a, const MarchCfg& m, int blocks, size_t smem) {
   static size_t enabled = 0;
   if (smem > enabled) {
-    cudaFuncSetAttribute(k_stencil_march<INM, OUTM, RED, C32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_stencil_march<NO, INM, OUTM, RED, C32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     enabled = smem;
   }
   cudaLaunchConfig_t cfg{};
@@ -1027,7 +1039,7 @@ static void launch_march_t(const LaunchCfg& lc, const StencilArgs& a, const Marc
   cudaLaunchAttribute at[1];
   cfg.numAttrs = pdl_attr(at);
   cfg.attrs = at;
-  cudaLaunchKernelEx(&cfg, k_stencil_march<INM, OUTM, RED, C32>, a, m);
+  cudaLaunchKernelEx(&cfg, k_stencil_march<NO, INM, OUTM, RED, C32>, a, m);
   constexpr int NV = ((RED & RED_NORM) ? 1 : 0) + ((RED & (RED_DOT | RED_DOT_CENTER)) ? 2 : 0);
   if constexpr (NV > 0) launch_finalize<NV>(lc, Geo{blocks, 0}, a.gate, a.rs, a.epi);
 }
@@ -1042,10 +1054,17 @@ static bool launch_march(const LaunchCfg& lc, int inm, int outm, int red, const 
   constexpr int J = IN_SCALE | IN_JAC | IN_WRITEV;
 #define HADR_MCASE(I, O, R)                                      \
   if (inm == (I) && outm == (O) && red == (R)) {                 \
-    if (c32)                                                     \
-      launch_march_t<I, O, R, true>(lc, a, m, blocks, smem);     \
-    else                                                         \
-      launch_march_t<I, O, R, false>(lc, a, m, blocks, smem);    \
+    if (a.A.nofs == 13) {                                        \
+      if (c32)                                                   \
+        launch_march_t<13, I, O, R, true>(lc, a, m, blocks, smem);  \
+      else                                                       \
+        launch_march_t<13, I, O, R, false>(lc, a, m, blocks, smem); \
+    } else {                                                     \
+      if (c32)                                                   \
+        launch_march_t<9, I, O, R, true>(lc, a, m, blocks, smem);   \
+      else                                                       \
+        launch_march_t<9, I, O, R, false>(lc, a, m, blocks, smem);  \
+    }                                                            \
     return true;                                                 \
   }
   HADR_MCASE(IN_PLAIN, OUT_APPLY, RED_NONE)

@@ -11,7 +11,7 @@ extern long g_mid_max_n;
 extern long g_mid_min_n;  // programmatic dependent launch of the solve-phase kernels
 extern int g_stencil_tile;
 extern int g_stencil_march;   // plane-marching bulk-copy kernel on 3D pair-compressed fine levels
-extern long g_march_min_n;
+extern long g_march_min_n, g_march_min_n2d;
 struct StencilDev;
 bool march_takes(const StencilDev& A);  // launch_stencil runs the marching kernel on this operator
 extern long g_cl_max_n;  // single-cluster reductions (in-kernel epilogue) up to this many points  // shared-memory tiled stencil kernel on the graph path

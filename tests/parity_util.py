@@ -51,3 +51,39 @@ def self_floor(mod, solve, levels=5):
 
 def protocol_bar(floor):
     return max(1e-8, 3.0 * floor)
+
+
+def plus2_operator(shape, rng):
+    """Random operator on the plus-radius-2 union of a 2D / 3D grid (9 / 13 offsets, sorted):
+    one of the two +-2 entries of every axis zeroed per row (the upwind pair property).
+    Out-of-grid entries are zero for the +-2 pairs but left non-zero for the +-1 offsets — a
+    kernel must skip them by position, not rely on a zero coefficient.
+    Returns (offsets, planes, csr)."""
+    import scipy.sparse as sp
+
+    dim = len(shape)
+    N = int(np.prod(shape))
+    offs = sorted([(0,) * dim] + [tuple(d if a == ax else 0 for a in range(dim)) for ax in range(dim)
+                                  for d in (-2, -1, 1, 2)])
+    idx = np.meshgrid(*[np.arange(n) for n in shape], indexing="ij")
+    strides = [int(np.prod(shape[a + 1:])) for a in range(dim)]
+    coef = rng.standard_normal((len(offs), N)) + 1j * rng.standard_normal((len(offs), N))
+    side = rng.integers(0, 2, size=(dim, N))
+    rows, cols, vals = [], [], []
+    k = np.arange(N)
+    for o, d in enumerate(offs):
+        ok = np.ones(shape, dtype=bool)
+        for ax in range(dim):
+            ok &= (idx[ax] + d[ax] >= 0) & (idx[ax] + d[ax] < shape[ax])
+        ok = ok.ravel()
+        present = ok.copy()
+        for ax in range(dim):
+            if abs(d[ax]) == 2:
+                present &= side[ax] == (1 if d[ax] > 0 else 0)
+        if max(abs(x) for x in d) != 1:
+            coef[o, ~present] = 0.0
+        rows.append(k[present])
+        cols.append((k + sum(d[ax] * strides[ax] for ax in range(dim)))[present])
+        vals.append(coef[o, present])
+    A = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(N, N))
+    return offs, coef, A

@@ -27,6 +27,8 @@ CASES = [
     (2, ["--case", "cfg4:65", "--backend", "host", "--levels", "2", "--c64", "1"]),  # mixed precision
     (2, ["--case", "cfg3:65", "--backend", "host", "--levels", "2"]),     # Neumann top, non-square, FM tau
     (2, ["--case", "cfg4:33", "--backend", "host", "--levels", "2", "--opt", "relax_split=1000"]),  # split relax, z halos
+    (2, ["--case", "cfg4:33", "--backend", "host", "--levels", "2", "--opt", "stencil_march=2"]),   # marching kernel on slabs
+    (3, ["--case", "cfg4:65", "--backend", "host", "--levels", "2", "--opt", "stencil_march=2"]),   # ... uneven slabs, chunks
 ]
 
 
