@@ -1707,16 +1707,8 @@ void launch_similarity(cudaStream_t s, const StencilDev& A, cplx* out, const cpl
 // Pass 2: write the compacted planes (slot_of maps box slot -> plane).
 // Slabs: coarse planes [q0, q0 + nq) are produced (coef_c points at plane q0, planes cstride apart); the fine
 // coefficients are read relative to Af.p0 with plane stride Af.pstride (one halo plane below is read).
-__global__ void __launch_bounds__(128) k_galerkin(StencilDev Af, int n1c, int n2c, int n3c, int q0, int nq, long cstride,
-                                                   unsigned long long* mask, const int* slot_of, cplx* coef_c) {
-  // One coarse point per thread.  The 125 coarse offsets are produced in five groups, one per
-  // axis-0 coarse offset D1: a group's 25 accumulators (400 B per thread, 50 KB per block) stay
-  // in L1, where the earlier single pass over all 125 (2000 B per thread) streamed its local
-  // memory through DRAM (ncu: 157 GB per 513^2 x 257 level against 25 GB of operator bytes).
-  // Every group walks the same (fine point, fine offset, parent) loop nest and keeps the terms
-  // whose axis-0 parent offset is its D1, so each coefficient is summed in the same order as
-  // before: bit-identical coarse operators.  The fine coefficients are re-read per group from
-  // L1 / L2.
+__global__ void k_galerkin(StencilDev Af, int n1c, int n2c, int n3c, int q0, int nq, long cstride,
+                           unsigned long long* mask, const int* slot_of, cplx* coef_c) {
   const int n1f = Af.n1, n2f = Af.n2, n3f = Af.n3;
   const long Nf = Af.pstride, Nc = (long)nq * n2c * n3c;
   const long fbase = (long)Af.p0 * n2f * n3f;
@@ -1726,58 +1718,44 @@ __global__ void __launch_bounds__(128) k_galerkin(StencilDev Af, int n1c, int n2
     int I1, I2, I3;
     decomp3(c, n2c, n3c, I1, I2, I3);
     I1 += q0;
-    for (int D1 = -2; D1 <= 2; ++D1) {
-      cplx acc[25];
-#pragma unroll
-      for (int q = 0; q < 25; ++q) acc[q] = mk(0.0, 0.0);
-      for (int a = -1; a <= 1; ++a) {
-        const int f1 = 2 * I1 + a;
-        if (f1 < 0 || f1 >= n1f) continue;
-        for (int b = -1; b <= 1; ++b) {
-          const int f2 = 2 * I2 + b;
-          if (f2 < 0 || f2 >= n2f) continue;
-          for (int cc = c3lo; cc <= c3hi; ++cc) {
-            const int f3 = 2 * I3 + cc;
-            if (f3 < 0 || f3 >= n3f) continue;
-            const double wf = (a == 0 ? 1.0 : 0.5) * (b == 0 ? 1.0 : 0.5) * (cc == 0 ? 1.0 : 0.5);
-            const long f = ((long)f1 * n2f + f2) * n3f + f3 - fbase;
-            for (int o = 0; o < Af.nofs; ++o) {
-              const int g1 = f1 + Af.d1[o];
-              if (g1 < 0 || g1 >= n1f) continue;
-              int p1[2];
-              double v1;
-              const int m1n = parents(g1, p1, v1);
-              // the axis-0 parents of g1 that belong to this group (at most one: they are adjacent)
-              int x1 = -1;
-              if (p1[0] - I1 == D1) x1 = 0;
-              else if (m1n == 2 && p1[1] - I1 == D1) x1 = 1;
-              if (x1 < 0) continue;
-              const int g2 = f2 + Af.d2[o], g3 = f3 + Af.d3[o];
-              if (g2 < 0 || g2 >= n2f || g3 < 0 || g3 >= n3f) continue;
-              const cplx cf = Af.coef[(long)o * Nf + f];
-              if (cf.x == 0.0 && cf.y == 0.0) continue;
-              const cplx wc = mk(wf * cf.x, wf * cf.y);
-              int p2[2], p3[2];
-              double v2, v3;
-              const int m2n = parents(g2, p2, v2), m3n = parents(g3, p3, v3);
+    cplx acc[125];
+    for (int q = 0; q < 125; ++q) acc[q] = mk(0.0, 0.0);
+    for (int a = -1; a <= 1; ++a) {
+      const int f1 = 2 * I1 + a;
+      if (f1 < 0 || f1 >= n1f) continue;
+      for (int b = -1; b <= 1; ++b) {
+        const int f2 = 2 * I2 + b;
+        if (f2 < 0 || f2 >= n2f) continue;
+        for (int cc = c3lo; cc <= c3hi; ++cc) {
+          const int f3 = 2 * I3 + cc;
+          if (f3 < 0 || f3 >= n3f) continue;
+          const double wf = (a == 0 ? 1.0 : 0.5) * (b == 0 ? 1.0 : 0.5) * (cc == 0 ? 1.0 : 0.5);
+          const long f = ((long)f1 * n2f + f2) * n3f + f3 - fbase;
+          for (int o = 0; o < Af.nofs; ++o) {
+            const int g1 = f1 + Af.d1[o], g2 = f2 + Af.d2[o], g3 = f3 + Af.d3[o];
+            if (g1 < 0 || g1 >= n1f || g2 < 0 || g2 >= n2f || g3 < 0 || g3 >= n3f) continue;
+            const cplx cf = Af.coef[(long)o * Nf + f];
+            if (cf.x == 0.0 && cf.y == 0.0) continue;
+            const cplx wc = mk(wf * cf.x, wf * cf.y);
+            int p1[2], p2[2], p3[2];
+            double v1, v2, v3;
+            const int m1n = parents(g1, p1, v1), m2n = parents(g2, p2, v2), m3n = parents(g3, p3, v3);
+            for (int x = 0; x < m1n; ++x)
               for (int y = 0; y < m2n; ++y)
                 for (int z = 0; z < m3n; ++z) {
-                  const int sl = (p2[y] - I2 + 2) * 5 + (p3[z] - I3 + 2);
+                  const int sl = slot125(p1[x] - I1, p2[y] - I2, p3[z] - I3);
                   const double pw = v1 * v2 * v3;
                   acc[sl] = cadd(acc[sl], mk(pw * wc.x, pw * wc.y));
                 }
-            }
           }
         }
       }
-#pragma unroll 1
-      for (int q = 0; q < 25; ++q) {
-        const int s125 = (D1 + 2) * 25 + q;
-        if (acc[q].x != 0.0 || acc[q].y != 0.0) {
-          if (s125 < 64) m0 |= 1ull << s125; else m1 |= 1ull << (s125 - 64);
-        }
-        if (coef_c && slot_of[s125] >= 0) coef_c[(long)slot_of[s125] * cstride + c] = acc[q];
+    }
+    for (int q = 0; q < 125; ++q) {
+      if (acc[q].x != 0.0 || acc[q].y != 0.0) {
+        if (q < 64) m0 |= 1ull << q; else m1 |= 1ull << (q - 64);
       }
+      if (coef_c && slot_of[q] >= 0) coef_c[(long)slot_of[q] * cstride + c] = acc[q];
     }
   }
   if (mask) {
@@ -1785,7 +1763,6 @@ __global__ void __launch_bounds__(128) k_galerkin(StencilDev Af, int n1c, int n2
     if (m1) atomicOr(mask + 1, m1);
   }
 }
-
 void launch_galerkin(cudaStream_t s, const StencilDev& Af, int n1c, int n2c, int n3c, unsigned long long* mask,
                      const int* slot_of, cplx* coef_c, int q0, int nq, long cstride) {
   ++g_launch_count;
