@@ -133,14 +133,23 @@ def load(path: str = LIB_PATH):
     return lib
 
 
-def lib():
-    """The library with a CUDA device initialised (raises if none)."""
-    global _initialised
+_device = None  # the CUDA device the library was bound to (hadr_init binds once)
+
+
+def lib(device=None):
+    """The library with a CUDA device initialised (raises if none).  The first call binds the
+    device (`device`, else HADR_DEVICE, else 0); a later call that names a different device
+    raises instead of silently staying on the first one."""
+    global _initialised, _device
     L = load()
     if not _initialised:
-        dev = int(os.environ.get("HADR_DEVICE", "0"))
+        dev = int(device) if device is not None else int(os.environ.get("HADR_DEVICE", "0"))
         check(L.hadr_init(dev))
         _initialised = True
+        _device = dev
+    elif device is not None and int(device) != _device:
+        raise RuntimeError(f"libhadr is already bound to CUDA device {_device}; cannot rebind to {int(device)} "
+                           "(call distributed.init() before any other library call)")
     return L
 
 

@@ -100,8 +100,8 @@ def init(backend: str = "auto", group=None) -> str:
         backend = "nccl" if ndev >= size else "host"
     if backend == "nccl":
         local = int(os.environ.get("LOCAL_RANK", rank))
-        os.environ.setdefault("HADR_DEVICE", str(local))
-        L = _lib.lib()
+        dev = int(os.environ.get("HADR_DEVICE", local))
+        L = _lib.lib(dev)  # binds the device now; raises if the library already sits on another one
         uid = C.create_string_buffer(128)
         if rank == 0:
             _lib.check(L.hadr_dist_nccl_id(uid))
