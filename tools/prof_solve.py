@@ -56,6 +56,12 @@ def main():
         solve(args.its)
     k0 = L.hadr_launch_count()
     t = solve(args.its)
+    if os.environ.get("HADR_PRINT_MEM"):  # device memory held with the hierarchy pooled (nvidia-smi, MiB)
+        import subprocess
+
+        used = subprocess.run(["nvidia-smi", "--query-gpu=memory.used", "--format=csv,noheader,nounits"],
+                              capture_output=True, text=True).stdout.split()[0]
+        print(f"device memory in use after the solve: {used} MiB")
     print(f"profiled solve: its={rep.iterations} device_time={t*1e3:.3f} ms kernels={L.hadr_launch_count()-k0}")
 
 
