@@ -376,6 +376,25 @@ struct PcLayout<13> {
   }
 };
 
+// The 3D plus of radius 1 (7 offsets in sorted order: (-1,0,0) (0,-1,0) (0,0,-1) centre (0,0,1) (0,1,0)
+// (1,0,0)) in the same terms, for the marching kernel: one slot per offset, no pairs, union planes.
+template <>
+struct PcLayout<7> {
+  static constexpr int NS = 7;
+  __host__ __device__ static constexpr int slot(int p) { return p; }
+  __host__ __device__ static constexpr int pair(int) { return -1; }
+  __host__ __device__ static constexpr int plus_pos(int) { return -1; }
+  __host__ __device__ static constexpr int first_pos(int q) { return q; }
+  __host__ __device__ static constexpr int axis(int q) {
+    constexpr int t[7] = {0, 1, 2, -1, 2, 1, 0};
+    return t[q];
+  }
+  __host__ __device__ static constexpr int delta(int q) {
+    constexpr int t[7] = {-1, -1, -1, 0, 1, 1, 1};
+    return t[q];
+  }
+};
+
 // Coefficient planes are read exactly once per sweep: stream them with an L2
 // evict-first policy (and no L1 allocation) so they do not push the stencil input's
 // neighbour rows (x, D^-1) out of L2.  Measured on B200: the 2D fine sweep gains
@@ -857,7 +876,8 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
     }
   } else {
     // ---- compute warps ----
-    const long ps = a.A.pstr;
+    constexpr bool UNION = NO == 7;  // the 7-point operator streams its union planes (nothing to compress)
+    const long ps = UNION ? a.A.pstride : a.A.pstr;
     const double sc = (INM & IN_SCALE) ? *a.scale : 1.0;
     const int ty = Y1 - Y0, tx = X1 - X0;
     int sidx[kMarchPpt];
@@ -889,14 +909,14 @@ __global__ void __launch_bounds__(kMarchBlock, HADR_MARCH_MIN_BLOCKS) k_stencil_
       for (int t = 0; t < kMarchPpt; ++t) {
         if (!act[t]) continue;
         const long k = (long)p * n23 + krel[t];
-        code[t] = __ldg(a.A.pcode + k);
+        code[t] = UNION ? 0u : (unsigned)__ldg(a.A.pcode + k);
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
           if constexpr (C32) {
-            const float2 c = __ldg(a.A.pcoef32 + (long)q * ps + k);
+            const float2 c = __ldg((UNION ? a.A.coef32 : a.A.pcoef32) + (long)q * ps + k);
             cv[t][q] = make_double2((double)c.x, (double)c.y);
           } else {
-            cv[t][q] = ldc(a.A.pcoef, (long)q * ps + k);
+            cv[t][q] = ldc(UNION ? a.A.coef : a.A.pcoef, (long)q * ps + k);
           }
         }
         if (OUTM == OUT_RESID) bk[t] = ldc(a.b, k);
@@ -990,16 +1010,28 @@ long g_march_min_n2d = 1L << 40;  // option "march_min_n2d": policy threshold, 2
 
 // the marching kernel's policy: a pair-compressed plus-radius-2 operator (3D 13 / 2D 9 offsets) of at least
 // march_min_n / march_min_n2d owned points
+static bool is_plus1_3d(const StencilDev& A) {  // exactly the 3D plus of radius 1, in PcLayout<7>'s order
+  if (A.nofs != 7 || A.n3 < 2) return false;
+  using Lay = PcLayout<7>;
+  for (int q = 0; q < 7; ++q) {
+    const int d[3] = {A.d1[q], A.d2[q], A.d3[q]};
+    for (int ax = 0; ax < 3; ++ax)
+      if (d[ax] != (Lay::axis(q) == ax ? Lay::delta(q) : 0)) return false;
+  }
+  return true;
+}
+
 bool march_takes(const StencilDev& A) {
-  if (!g_stencil_march || !A.pcode) return false;
-  const bool d3 = A.nofs == 13 && A.n3 >= 2, d2 = A.nofs == 9 && A.n3 == 1;
+  if (!g_stencil_march) return false;
+  const bool d7 = is_plus1_3d(A);
+  const bool d3 = (A.pcode && A.nofs == 13 && A.n3 >= 2) || d7, d2 = A.pcode && A.nofs == 9 && A.n3 == 1;
   if (!d3 && !d2) return false;
   return g_stencil_march > 1 || (long)A.n1own * A.n2 * A.n3 >= (d3 ? g_march_min_n : g_march_min_n2d);
 }
 
 static bool march_cfg(const StencilDev& A, bool jac, MarchCfg& m, int& blocks, size_t& smem) {
-  const bool d3 = A.nofs == 13 && A.n3 >= 2, d2 = A.nofs == 9 && A.n3 == 1;
-  if (!A.pcode || (!d3 && !d2) || A.n1own < 1) return false;
+  const bool d3 = (A.pcode && A.nofs == 13 && A.n3 >= 2) || is_plus1_3d(A), d2 = A.pcode && A.nofs == 9 && A.n3 == 1;
+  if ((!d3 && !d2) || A.n1own < 1) return false;
   const int nY = d3 ? A.n2 : 1, nX = d3 ? A.n3 : A.n2;  // tile axes (2D: a plane is one row)
   const int txcap = d3 ? 34 : kMarchThreads * kMarchPpt;
   m.hy = d3 ? 2 : 0;
@@ -1050,7 +1082,7 @@ static bool launch_march(const LaunchCfg& lc, int inm, int outm, int red, const 
   int blocks = 0;
   size_t smem = 0;
   if (!march_cfg(a.A, (inm & IN_JAC) != 0, m, blocks, smem)) return false;
-  const bool c32 = a.A.pcoef32 != nullptr;
+  const bool c32 = a.A.nofs == 7 ? a.A.coef32 != nullptr : a.A.pcoef32 != nullptr;
   constexpr int J = IN_SCALE | IN_JAC | IN_WRITEV;
 #define HADR_MCASE(I, O, R)                                      \
   if (inm == (I) && outm == (O) && red == (R)) {                 \
@@ -1059,6 +1091,11 @@ static bool launch_march(const LaunchCfg& lc, int inm, int outm, int red, const 
         launch_march_t<13, I, O, R, true>(lc, a, m, blocks, smem);  \
       else                                                       \
         launch_march_t<13, I, O, R, false>(lc, a, m, blocks, smem); \
+    } else if (a.A.nofs == 7) {                                  \
+      if (c32)                                                   \
+        launch_march_t<7, I, O, R, true>(lc, a, m, blocks, smem);   \
+      else                                                       \
+        launch_march_t<7, I, O, R, false>(lc, a, m, blocks, smem);  \
     } else {                                                     \
       if (c32)                                                   \
         launch_march_t<9, I, O, R, true>(lc, a, m, blocks, smem);   \

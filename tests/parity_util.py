@@ -87,3 +87,28 @@ def plus2_operator(shape, rng):
         vals.append(coef[o, present])
     A = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(N, N))
     return offs, coef, A
+
+
+def plus1_operator(shape, rng):
+    """Random operator on the 3D plus of radius 1 (7 offsets, sorted); out-of-grid entries are
+    left non-zero in the planes (a kernel must skip them by position).  Returns (offsets,
+    planes, csr)."""
+    import scipy.sparse as sp
+
+    N = int(np.prod(shape))
+    offs = sorted([(0, 0, 0)] + [tuple(d if a == ax else 0 for a in range(3)) for ax in range(3) for d in (-1, 1)])
+    idx = np.meshgrid(*[np.arange(n) for n in shape], indexing="ij")
+    strides = [shape[1] * shape[2], shape[2], 1]
+    coef = rng.standard_normal((7, N)) + 1j * rng.standard_normal((7, N))
+    rows, cols, vals = [], [], []
+    k = np.arange(N)
+    for o, d in enumerate(offs):
+        ok = np.ones(shape, dtype=bool)
+        for ax in range(3):
+            ok &= (idx[ax] + d[ax] >= 0) & (idx[ax] + d[ax] < shape[ax])
+        ok = ok.ravel()
+        rows.append(k[ok])
+        cols.append((k + sum(d[ax] * strides[ax] for ax in range(3)))[ok])
+        vals.append(coef[o, ok])
+    A = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(N, N))
+    return offs, coef, A
