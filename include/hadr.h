@@ -187,6 +187,12 @@ int hadr_dist_plan(int n1, int n2, int n3, int max_levels, int* bounds, int* n_d
  * communicator): fine slab bounds (size + 1), levels split in slabs, levels in total */
 int hadr_slab_plan(int n1, int n2, int n3, int max_levels, int size, int* bounds, int* n_dist_levels, int* n_levels);
 int hadr_slab_bounds(int n1, int size, int align, int* bounds /* size + 1 */);
+/* pure host helper: the tiling the plane-marching stencil kernel (k_stencil_march; replaces csr_matvec on
+ * large 3D fine levels, helmadr/krylov.py:60-65) uses for an owned slab of n1own x n2 x n3 points (n3 = 1:
+ * 2D, marched row by row): out10 = {tiles along axis 1, tiles along axis 2, plane chunks, planes per chunk,
+ * shared-memory row pitch, slot elements, halo rows, thread blocks, dynamic shared-memory bytes (jac: with
+ * the D^-1 ring), points-per-tile cap}.  Tile t of n along an axis covers [t*n/nt, (t+1)*n/nt). */
+int hadr_march_plan(int n1own, int n2, int n3, int jac, int* out10);
 
 /* tau_derivatives (helmadr/eikonal.py:180-226) with AnalyticBase's distance factor
  * (helmadr/eikonal.py:15-36; 3D: the per-axis generalisation, lap(tau0) = 2/r): from tau1 on the

@@ -29,7 +29,7 @@ EXPORTS = (
     "hadr_dist_nccl_id", "hadr_dist_init_nccl", "hadr_dist_init_host", "hadr_dist_finalize", "hadr_dist_info",
     "hadr_dist_plan", "hadr_slab_bounds", "hadr_fast_march", "hadr_phase_transform", "hadr_op_storage",
     "hadr_relative_error", "hadr_memset", "hadr_fgmres_ex",
-    "hadr_tau_derivatives", "hadr_ce_bench", "hadr_slab_plan",
+    "hadr_tau_derivatives", "hadr_ce_bench", "hadr_slab_plan", "hadr_march_plan",
 )
 
 # host-communicator callbacks (include/hadr.h hadr_host_*)
@@ -101,6 +101,7 @@ _SIGS = {
     "hadr_dist_plan": (_i, [_i, _i, _i, _i, _vp, C.POINTER(_i), C.POINTER(_i)]),
     "hadr_slab_bounds": (_i, [_i, _i, _i, _vp]),
     "hadr_slab_plan": (_i, [_i, _i, _i, _i, _i, _vp, C.POINTER(_i), C.POINTER(_i)]),
+    "hadr_march_plan": (_i, [_i, _i, _i, _i, _vp]),
     "hadr_fast_march": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, C.POINTER(C.c_longlong)]),
     "hadr_phase_transform": (_i, [C.c_longlong, _vp, _vp, _d, _i, _vp, _i]),
     "hadr_op_storage": (_i, [_vp, C.POINTER(_i), C.POINTER(C.c_longlong)]),

@@ -790,6 +790,12 @@ int hadr_slab_plan(int n1, int n2, int n3, int max_levels, int size, int* bounds
   });
 }
 
+int hadr_march_plan(int n1own, int n2, int n3, int jac, int* out10) {
+  return guarded([&] {
+    if (!march_plan(n1own, n2, n3, jac, out10)) throw ValueError("the marching kernel declines this shape");
+  });
+}
+
 int hadr_slab_bounds(int n1, int size, int align, int* bounds) {
   return guarded([&] {
     const std::vector<int> b = slab_bounds(n1, size, align);

@@ -1029,10 +1029,11 @@ bool march_takes(const StencilDev& A) {
   return g_stencil_march > 1 || (long)A.n1own * A.n2 * A.n3 >= (d3 ? g_march_min_n : g_march_min_n2d);
 }
 
-static bool march_cfg(const StencilDev& A, bool jac, MarchCfg& m, int& blocks, size_t& smem) {
-  const bool d3 = (A.pcode && A.nofs == 13 && A.n3 >= 2) || is_plus1_3d(A), d2 = A.pcode && A.nofs == 9 && A.n3 == 1;
-  if ((!d3 && !d2) || A.n1own < 1) return false;
-  const int nY = d3 ? A.n2 : 1, nX = d3 ? A.n3 : A.n2;  // tile axes (2D: a plane is one row)
+// Tiling of the marching kernel (host logic; hadr_march_plan exposes it to the CPU tests): the
+// (axis 1, axis 2) plane in nty x ntx near-equal tiles of at most one point per compute thread,
+// axis 0 in nch chunks of pc planes.  d3 = false: a 2D grid marched as (n1, 1, n2).
+static bool march_dims(bool d3, int n1own, int nY, int nX, bool jac, MarchCfg& m, int& blocks, size_t& smem) {
+  if (n1own < 1 || nY < 1 || nX < 1) return false;
   const int txcap = d3 ? 34 : kMarchThreads * kMarchPpt;
   m.hy = d3 ? 2 : 0;
   m.ntx = (nX + txcap - 1) / txcap;
@@ -1043,17 +1044,34 @@ static bool march_cfg(const StencilDev& A, bool jac, MarchCfg& m, int& blocks, s
   tymax = (nY + m.nty - 1) / m.nty;
   const long cols = (long)m.ntx * m.nty;
   long nch = (148L * HADR_MARCH_MIN_BLOCKS * 4 + cols - 1) / cols;  // >= 4 waves of blocks
-  if (nch > A.n1own / 8) nch = A.n1own / 8;                          // chunks of >= 8 planes
+  if (nch > n1own / 8) nch = n1own / 8;                              // chunks of >= 8 planes
   if (nch < 1) nch = 1;
   if (cols * nch > 8192) nch = 8192 / cols;                          // reduction scratch: 8192 blocks
   if (nch < 1) return false;
-  m.pc = (int)((A.n1own + nch - 1) / nch);
-  m.nch = (A.n1own + m.pc - 1) / m.pc;
+  m.pc = (int)((n1own + nch - 1) / nch);
+  m.nch = (n1own + m.pc - 1) / m.pc;
   m.pitch = txmax + 4;
   m.slot = (tymax + 2 * m.hy) * m.pitch;
   blocks = (int)(cols * m.nch);
   smem = (size_t)kMarchRing * m.slot * sizeof(cplx) * (jac ? 2 : 1);
   return smem <= 200 * 1024;
+}
+
+static bool march_cfg(const StencilDev& A, bool jac, MarchCfg& m, int& blocks, size_t& smem) {
+  const bool d3 = (A.pcode && A.nofs == 13 && A.n3 >= 2) || is_plus1_3d(A), d2 = A.pcode && A.nofs == 9 && A.n3 == 1;
+  if (!d3 && !d2) return false;
+  return march_dims(d3, A.n1own, d3 ? A.n2 : 1, d3 ? A.n3 : A.n2, jac, m, blocks, smem);
+}
+
+bool march_plan(int n1own, int n2, int n3, int jac, int* out) {
+  MarchCfg m{};
+  int blocks = 0;
+  size_t smem = 0;
+  const bool d3 = n3 > 1;
+  if (!march_dims(d3, n1own, d3 ? n2 : 1, d3 ? n3 : n2, jac != 0, m, blocks, smem)) return false;
+  const int v[10] = {m.nty, m.ntx, m.nch, m.pc, m.pitch, m.slot, m.hy, blocks, (int)smem, kMarchThreads * kMarchPpt};
+  for (int i = 0; i < 10; ++i) out[i] = v[i];
+  return true;
 }
 
 template <int NO, int INM, int OUTM, int RED, bool C32>

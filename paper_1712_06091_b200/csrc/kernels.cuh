@@ -13,7 +13,10 @@ extern int g_stencil_tile;
 extern int g_stencil_march;   // plane-marching bulk-copy kernel on 3D pair-compressed fine levels
 extern long g_march_min_n, g_march_min_n2d;
 struct StencilDev;
-bool march_takes(const StencilDev& A);  // launch_stencil runs the marching kernel on this operator
+bool march_takes(const StencilDev& A);
+// the marching kernel's tiling of an (n1own, n2, n3) slab (n3 = 1: 2D): out[10] = {nty, ntx, nch, pc, pitch,
+// slot, hy, blocks, smem bytes, points per tile cap}; false when the kernel declines the shape
+bool march_plan(int n1own, int n2, int n3, int jac, int* out);  // launch_stencil runs the marching kernel on this operator
 extern long g_cl_max_n;  // single-cluster reductions (in-kernel epilogue) up to this many points  // shared-memory tiled stencil kernel on the graph path
 
 // Structured 2D/3D stencil in union-offset, plane-major layout (2D: n3 = 1, d3 = 0):

@@ -153,3 +153,40 @@ def test_bench_arms_share_the_config_dict():
     c1, c2 = bench.bench_config(wl, a, 1), bench.bench_config(wl, a, 1)
     assert c1 == c2 and c1["grid"] == [65, 65] and c1["tol"] == 1e-6
     assert "outer_iterations" not in c1 and "t_setup_ms" not in c1
+
+
+@pytest.mark.parametrize("shape", [(513, 513, 257), (65, 513, 257), (129, 1025, 513), (257, 257, 129), (33, 16, 35),
+                                   (9, 7, 6), (40, 31, 129), (4097, 2049, 1), (37, 1300, 1), (9, 7, 1)])
+@pytest.mark.parametrize("jac", [0, 1])
+def test_march_plan_covers_the_slab(shape, jac):
+    """Host logic of the plane-marching stencil kernel (hadr_march_plan, no device): its tiles and
+    plane chunks cover every owned point exactly once, a tile holds at most one point per compute
+    thread, the ring fits shared memory and the reduction scratch (8192 blocks) is respected —
+    on the BASELINE grids (config 4, an 8-rank slab of it, a slab of config 5), ragged 3D grids
+    and 2D grids (marched row by row)."""
+    import ctypes as C
+
+    from paper_1712_06091_b200 import _lib
+
+    L = _lib.load()
+    out = (C.c_int * 10)()
+    n1, n2, n3 = shape
+    assert L.hadr_march_plan(n1, n2, n3, jac, out) == 0, L.hadr_last_error()
+    nty, ntx, nch, pc, pitch, slot, hy, blocks, smem, cap = list(out)
+    d3 = n3 > 1
+    nY, nX = (n2, n3) if d3 else (1, n2)
+    assert blocks == nty * ntx * nch <= 8192
+    assert smem == 6 * slot * 16 * (2 if jac else 1) <= 200 * 1024
+    cover = np.zeros((nY, nX), dtype=np.int32)
+    for ty in range(nty):
+        y0, y1 = ty * nY // nty, (ty + 1) * nY // nty
+        for tx in range(ntx):
+            x0, x1 = tx * nX // ntx, (tx + 1) * nX // ntx
+            assert 0 < (y1 - y0) * (x1 - x0) <= cap
+            assert x1 - x0 + 4 <= pitch and (y1 - y0 + 2 * hy) * pitch <= slot
+            cover[y0:y1, x0:x1] += 1
+    assert (cover == 1).all()
+    planes = np.zeros(n1, dtype=np.int32)
+    for c in range(nch):
+        planes[c * pc:min((c + 1) * pc, n1)] += 1
+    assert (planes == 1).all() and (nch - 1) * pc < n1
