@@ -740,7 +740,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_tile(StencilArgs a, Til
 
 
 // ---------------------------------------------------------------------------
-// K1 marching (3D fine level, pair-compressed plus-radius-2 operator, plain input):
+// K1 marching (3D fine levels: the pair-compressed plus-radius-2 operator — 13 offsets, 10 slot
+// planes — and the 7-point plus of radius 1 from its union planes; every variant of K1: plain
+// input or the relaxation's D^-1 (s x) from a second ring of D^-1 tiles, apply / residual,
+// fused dot / norm; a 2D instantiation marches a grid row by row):
 // a block owns a column tile of ty x tx points of the (axis 1, axis 2) plane and
 // marches along axis 0 through a chunk of planes.  The input's plane tiles (2-point
 // halo on axes 1 and 2) land in a ring of 6 shared-memory slots by row-wise bulk
