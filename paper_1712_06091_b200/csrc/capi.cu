@@ -688,6 +688,13 @@ int hadr_set_option(const char* name, double value) {
         if (!h) break;
         delete h;
       }
+    } else if (n == "ce_max_n3d" || n == "cl_max_n3d") {
+      (n == "ce_max_n3d" ? g_ce_max_n3d : g_cl_max_n3d) = (long)value;
+      for (;;) {
+        Hier* h = hier_pool_pop();
+        if (!h) break;
+        delete h;
+      }
     } else if (n == "stencil_march" || n == "march_min_n" || n == "march_min_n2d") {
       if (n == "stencil_march")
         g_stencil_march = (int)value;

@@ -165,7 +165,8 @@ static long blocks_of(const LaunchCfg& lc, long n) {
 
 static Geo geo_for(const LaunchCfg& lc, long n) {
   long b = (n + kThreads - 1) / kThreads;
-  if (n <= g_cl_max_n && !lc.dist) {  // distributed sums finish through the communicator
+  const long clmax = lc.cl_max_n >= 0 && lc.cl_max_n < g_cl_max_n ? lc.cl_max_n : g_cl_max_n;  // per-level cap
+  if (n <= clmax && !lc.dist) {  // distributed sums finish through the communicator
     if (b > kClusterMaxCTAs) b = kClusterMaxCTAs;
     if (b < 1) b = 1;
     return Geo{(int)b, (int)b};

@@ -157,6 +157,7 @@ struct LaunchCfg {
   int max_blocks;                  // grid cap (multiple of the SM count)
   const DistRed* dist = nullptr;   // non-null: reductions are completed across the slab ranks
   int ppt = 1;                     // points per thread of the level's grid-stride kernels
+  long cl_max_n = -1;              // >= 0: the level's own single-cluster limit (min with option cl_max_n)
 };
 
 void launch_stencil(const LaunchCfg& lc, int inm, int outm, int red, const StencilArgs& a);
