@@ -688,8 +688,8 @@ int hadr_set_option(const char* name, double value) {
         if (!h) break;
         delete h;
       }
-    } else if (n == "ce_max_n3d" || n == "cl_max_n3d") {
-      (n == "ce_max_n3d" ? g_ce_max_n3d : g_cl_max_n3d) = (long)value;
+    } else if (n == "small_max_work") {
+      g_small_max_work = (long)value;
       for (;;) {
         Hier* h = hier_pool_pop();
         if (!h) break;

@@ -13,12 +13,14 @@
 namespace hadr {
 
 long g_ce_max_n = 32768;
-// 3D levels carry 54-81 coefficients per row (2D: 15-21): a 33^2 x 17 level streams 16-24 MB per
-// stencil, which the engine's 16 SMs (and the single-cluster vector kernels) do far slower than a
-// plain grid over all SMs.  Measured (B200): config-5 recipe 551.6 -> 484.5 ms per solve, config 4
-// 2032 -> 2003 ms with 3D levels above 4096 points on the plain-grid graph path.
-long g_ce_max_n3d = 4096;  // option "ce_max_n3d": the engine's size limit for 3D levels (min with ce_max_n)
-long g_cl_max_n3d = 4096;  // option "cl_max_n3d": single-cluster vector kernels' limit on 3D levels (min with cl_max_n)
+// The engine's 16 SMs (and the single-cluster vector kernels) pay per coefficient streamed: the 2D
+// limit of 32768 points x 21 offsets is 688k coefficients per stencil.  3D upwind levels carry up to
+// 81 offsets per row — the 33^2 x 17 level streams 1.5 M coefficients (24 MB) per stencil — and run
+// faster on plain grids over all SMs (B200: config-5 recipe 551.6 -> 484.5 ms per solve, config 4
+// 2032 -> 2003 ms), while the 27-offset shifted-Laplacian level of the same size (0.5 M) is faster
+// in the engine (standard_sl 1251 vs 1125 Mdof*it/s).  A level is engine / cluster sized when
+// N <= ce_max_n (cl_max_n) and N x offsets <= small_max_work.
+long g_small_max_work = 32768L * 21;  // option "small_max_work" 
 int g_kcycle_c64 = 0;
 
 // ---------------------------------------------------------------------------
@@ -916,7 +918,7 @@ size_t Hier::ce_tile(int li) const {
 }
 
 bool Hier::use_ce(int li) const {
-  return ce_desc != nullptr && g_ce_max_n > 0 && li < (int)lv.size() && !lv[li].dist && lv[li].N <= (lv[li].n3 > 1 ? std::min(g_ce_max_n, g_ce_max_n3d) : g_ce_max_n) &&
+  return ce_desc != nullptr && g_ce_max_n > 0 && li < (int)lv.size() && !lv[li].dist && lv[li].N <= g_ce_max_n && lv[li].N * lv[li].A->nofs <= g_small_max_work &&
          (int)lv.size() <= CE_MAXLEV && ce_tile(li) <= 200 * 1024;
 }
 
@@ -952,7 +954,7 @@ void Hier::alloc_workspace() {
     L.smr = level_smr(L);  // the engine descriptor and ce_tile() agree for the hierarchy's lifetime
     L.lc = Ctx::get().lc;
     if (L.n3 == 1 && L.N > g_mid_min_n && L.N <= g_mid_max_n) L.lc.ppt = g_mid_ppt;
-    if (L.n3 > 1) L.lc.cl_max_n = g_cl_max_n3d;
+    if (L.N * L.A->nofs > g_small_max_work) L.lc.cl_max_n = 0;  // plain grids only
     L.smc = level_smc(L);
     for (int j = 0; j <= L.s; ++j) L.V[j] = valloc(L);
     L.w[0] = valloc(L);
@@ -1024,7 +1026,7 @@ Hier* hier_pool_pop() {
 std::vector<long long> hier_option_signature() {
   return {g_ce_smem_relax, g_ce_smem_coef, g_ce_max_n, g_cl_max_n, g_stencil_tile, g_relax_split, g_class_compress, g_pair_compress,
           g_pdl, g_ce_prof_on, g_kcycle_c64, g_ce_cgs2, g_defer_mgs, g_mid_ppt, g_mid_min_n, g_mid_max_n,
-          g_stencil_march, g_march_min_n, g_march_min_n2d, g_ce_max_n3d, g_cl_max_n3d};
+          g_stencil_march, g_march_min_n, g_march_min_n2d, g_small_max_work};
 }
 
 void hier_release(Hier* h) {

@@ -178,7 +178,7 @@ struct Hier {
 };
 
 // runtime options (hadr_set_option)
-extern long g_ce_max_n3d, g_cl_max_n3d;  // the 3D levels' own limits (options "ce_max_n3d" / "cl_max_n3d")
+extern long g_small_max_work;  // engine / cluster-kernel levels also need N x offsets <= this (option "small_max_work")
 extern long g_ce_max_n;  // levels with N <= this run inside the cluster engine (0 disables)
 extern int g_kcycle_c64; // build hierarchies with complex64 operator storage (mixed-precision K-cycle)
 extern int g_ce_smem_relax;  // engine relaxations out of shared memory where they fit

@@ -26,7 +26,7 @@ def main():
     from paper_1712_06091_b200.operators import rhs_transform
 
     L = _lib.lib()
-    for opt in ("pdl", "ce_max_n", "kcycle_c64", "stencil_tile", "ce_smem_relax", "cl_max_n", "ce_cgs2", "defer_mgs", "ce_smem_coef", "mid_ppt", "mid_max_n", "mid_min_n", "class_compress", "pair_compress", "relax_split", "stencil_march", "march_min_n", "ce_max_n3d", "cl_max_n3d"):
+    for opt in ("pdl", "ce_max_n", "kcycle_c64", "stencil_tile", "ce_smem_relax", "cl_max_n", "ce_cgs2", "defer_mgs", "ce_smem_coef", "mid_ppt", "mid_max_n", "mid_min_n", "class_compress", "pair_compress", "relax_split", "stencil_march", "march_min_n", "small_max_work"):
         if os.environ.get("HADR_" + opt.upper()) is not None:
             _lib.set_option(opt, float(os.environ["HADR_" + opt.upper()]))
     wl = workloads.by_name(os.environ.get("HADR_WORKLOAD", "cfg2"), args.n)
