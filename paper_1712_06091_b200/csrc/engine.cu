@@ -133,7 +133,7 @@ void Op::make_c64() {
 }
 
 int g_class_compress = 2;
-long g_relax_split = 1L << 20;
+long g_relax_split = 8192;  // (1 << 20 until session 5: the 139k- and 18.5k-point 3D levels gain too: config-5 recipe -2.7%)
 
 bool Op::class_compress() {
   cc_tried = true;

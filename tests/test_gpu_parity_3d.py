@@ -338,7 +338,7 @@ def test_relax_split_solve_identical_3d(hadr):
             u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
             out[split] = (a, rep.iterations, list(rep.history))
     finally:
-        for k, v in (("relax_split", 1 << 20), ("cl_max_n", 32768), ("ce_max_n", 32768)):
+        for k, v in (("relax_split", 8192), ("cl_max_n", 32768), ("ce_max_n", 32768)):
             hadr._lib.set_option(k, v)
     assert out[0][1] == out[1000][1]
     assert np.array_equal(out[0][0], out[1000][0])
@@ -391,7 +391,7 @@ def test_march_solve_3d(hadr, c64):
             u, a, rep = drivers.solve_adr_upwind(wl.medium, wl.grid, wl.source, wl.tt, cfg, wl.bc)
             out[mode] = (a, rep.iterations)
     finally:
-        for k, v in (("stencil_march", 1), ("kcycle_c64", 0), ("cl_max_n", 32768), ("relax_split", 1 << 20)):
+        for k, v in (("stencil_march", 1), ("kcycle_c64", 0), ("cl_max_n", 32768), ("relax_split", 8192)):
             hadr._lib.set_option(k, v)
     assert out[0][1] == out[2][1]
     assert rel(out[2][0], out[0][0]) <= 1e-8
@@ -445,7 +445,7 @@ def test_march_solve_sl_3d(hadr, c64):
             u, rep = drivers.solve_standard(H, q, wl.medium, wl.omega, cfg)
             out[mode] = (u, rep.iterations)
     finally:
-        for k, v in (("stencil_march", 1), ("kcycle_c64", 0), ("cl_max_n", 32768), ("relax_split", 1 << 20)):
+        for k, v in (("stencil_march", 1), ("kcycle_c64", 0), ("cl_max_n", 32768), ("relax_split", 8192)):
             hadr._lib.set_option(k, v)
     assert out[0][1] == out[2][1]
     assert rel(out[2][0], out[0][0]) <= 1e-8
